@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark of the XFBQ hot path on B200.
+
+Workload (BASELINE.json metric / configs[3]): exhaustive top-100 over 10M x 256-d 4-bit codes,
+10k queries, synthetic unit-norm data.  A "step" is one pass of the hot path over the whole
+query batch: quantize queries -> fused XOR/POPC scan + top-K over the (sharded) database ->
+[all-gather + merge when N > 1] -> keys.
+
+    python bench.py --gpus N --steps K --warmup W            # our arm (torchrun for N > 1)
+    python bench.py --impl reference --gpus N --steps K ...   # CPU arm: the reference algorithm
+                                                              # (oracle C port, all host threads)
+
+Prints ONE JSON line (rank 0).  `value` = whole-job QPS with inputs resident in HBM, `e2e` = QPS
+through the public API with host query buffers (H2D + D2H inside the timed region), `roofline`
+= the scan kernel against the measured HBM peak, `cpu_baseline` = the CPU port timed on this
+box's cores on a bounded sample.  Multi-GPU: the database is row-sharded (total fixed ->
+"strong" scaling), one all-gather of [nq, k] keys + a merge kernel per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "QPS, exhaustive top-100 over 10M x 256-d 4-bit codes"
+CHUNK = 1_000_000  # rows per generated chunk; chunk c of the global corpus uses seed 4000 + c
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=10_000_000)
+    ap.add_argument("--dim", type=int, default=256)
+    ap.add_argument("--doc-bits", type=int, default=4)
+    ap.add_argument("--query-bits", type=int, default=4)
+    ap.add_argument("--nq", type=int, default=10_000)
+    ap.add_argument("--k", type=int, default=100)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the cpu_baseline leg")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip recall / single-query extras")
+    return ap.parse_args()
+
+
+def workload_name(a):
+    return (f"synthetic unit-norm {a.n}x{a.dim}-d, {a.doc_bits}-bit docs x {a.query_bits}-bit queries, "
+            f"{a.nq} queries, top-{a.k}")
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = Path(f"/tmp/xfbq_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200", "-i", str(self.gpu)],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if sm:
+            out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), reasons=sorted(reasons), samples=len(sm))
+        try:
+            self.path.unlink()
+        except OSError:
+            pass
+        return out
+
+
+# ------------------------------------------------------------------------------------ corpus
+def gen_chunk_gpu(torch, c, rows, dim):
+    g = torch.Generator(device="cuda").manual_seed(4000 + c)
+    x = torch.randn((rows, dim), generator=g, device="cuda", dtype=torch.float32)
+    return x / x.norm(dim=1, keepdim=True)
+
+
+def gen_rows_gpu(torch, lo, hi, n, dim):
+    """Rows [lo, hi) of the global synthetic corpus (identical for every sharding)."""
+    out = torch.empty((hi - lo, dim), dtype=torch.float32, device="cuda")
+    c = lo // CHUNK
+    while c * CHUNK < hi:
+        c_lo, c_hi = c * CHUNK, min(n, (c + 1) * CHUNK)
+        x = gen_chunk_gpu(torch, c, c_hi - c_lo, dim)
+        a, b = max(lo, c_lo), min(hi, c_hi)
+        out[a - lo:b - lo] = x[a - c_lo:b - c_lo]
+        c += 1
+    return out
+
+
+def gen_queries(nq, dim):
+    rng = np.random.Generator(np.random.PCG64(4001))
+    q = rng.normal(0.0, 1.0 / np.sqrt(dim), size=(nq, dim))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    return q.astype(np.float32)
+
+
+# ------------------------------------------------------------------------------------ ours
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2008_02002_b200 as xb
+    from paper_2008_02002_b200 import _native, search as xsearch
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if world != a.gpus and rank == 0:
+        print(f"warning: --gpus {a.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- build this rank's shard
+    lo, hi = xb.shard_bounds(a.n, world, rank)
+    head = gen_chunk_gpu(torch, 0, min(CHUNK, a.n), a.dim)[:100_000].cpu().numpy()
+    scale = xb.estimate_scale(head, 0.98)
+    params = xb.QuantParams(dim=a.dim, scale=scale, doc_bits=a.doc_bits, query_bits=a.query_bits)
+    docs = gen_rows_gpu(torch, lo, hi, a.n, a.dim)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    shard = xb.ShardedIndex.build(docs, params, n_total=a.n, row_offset=lo, world=world, rank=rank)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    packed2 = xb.quantize_matrix(docs, a.doc_bits, scale)  # quantizer kernel alone (no validation passes)
+    ev1.record(); torch.cuda.synchronize()
+    quant_ms = ev0.elapsed_time(ev1)
+    del packed2
+
+    q_host = gen_queries(a.nq, a.dim)
+    q_pinned = torch.from_numpy(q_host).pin_memory()
+    q_dev = q_pinned.cuda()
+
+    index = shard.local
+    db_bytes_local = index.packed.nbytes                      # algorithmic bytes of this rank's shard
+    db_bytes_total = a.n * a.doc_bits * ((a.dim + 63) // 64) * 8
+
+    # ---- extras that need the float originals (N = 1 only): recall@K vs float cosine
+    recall = None
+    if world == 1 and not a.no_extras:
+        nr = min(64, a.nq)
+        keys = shard.search_keys(q_dev[:nr], a.k)
+        ids_q = (keys & 0xFFFFFFFF)
+        sims = q_dev[:nr] @ docs.T                           # float32 cosine (unit rows)
+        ids_f = torch.topk(sims, min(a.k, a.n), dim=1).indices
+        hit = 0
+        for r in range(nr):
+            hit += int(torch.isin(ids_q[r], ids_f[r]).sum())
+        recall = hit / float(nr * min(a.k, a.n))
+        del sims, ids_f
+    del docs
+    torch.cuda.empty_cache()
+
+    plan = (np.zeros(6, dtype=np.int32))
+    _native.check(_native.lib().xfbq_scan_plan(index.n, a.dim, a.doc_bits, min(a.nq, xsearch._QUERY_BATCH),
+                                               a.query_bits, min(a.k, index.n), plan.ctypes.data))
+
+    def step_device():
+        return shard.search_keys(q_dev, a.k)
+
+    def step_e2e():
+        return shard.search(q_pinned, a.k)
+
+    sampler = ClockSampler(local_rank)
+    # ---- device-resident timing
+    for _ in range(a.warmup):
+        step_device()
+    barrier()
+    if rank == 0:
+        sampler.start()
+    xsearch.SCAN_EVENTS = []
+    launches0 = _native.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.steps):
+        step_device()
+    e1.record()
+    barrier()
+    launches = _native.launch_count() - launches0
+    scan_events, xsearch.SCAN_EVENTS = xsearch.SCAN_EVENTS, None
+    ms_step = max_over_ranks(e0.elapsed_time(e1) / a.steps)
+    scan_ms = [s.elapsed_time(e) for s, e in scan_events]
+    scan_ms_avg = sum(scan_ms) / len(scan_ms)
+
+    # ---- end-to-end through the public API with host buffers
+    for _ in range(max(1, a.warmup - 1)):
+        step_e2e()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        res = step_e2e()
+    barrier()
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / a.steps)
+    clocks = sampler.stop() if rank == 0 else None
+
+    # ---- small-batch regime: single-query latency and achieved HBM bandwidth
+    single = None
+    if not a.no_extras:
+        single = {}
+        for nq1 in (1, 4, 16):
+            for _ in range(3):
+                shard.search_keys(q_dev[:nq1], a.k)
+            barrier()
+            reps = 20
+            e0.record()
+            for r in range(reps):
+                shard.search_keys(q_dev[r * nq1:(r + 1) * nq1], a.k)
+            e1.record()
+            barrier()
+            ms = max_over_ranks(e0.elapsed_time(e1) / reps)
+            single[f"nq{nq1}"] = {"latency_us": round(ms * 1e3, 1), "qps": round(nq1 / ms * 1e3, 1),
+                                  "db_scan_GBps": round(db_bytes_total / ms / 1e6, 1)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = peaks()
+    scans_per_launch = int(plan[1]) * (min(a.nq, xsearch._QUERY_BATCH) / min(a.nq, xsearch._QUERY_BATCH))
+    launches_per_step = -(-a.nq // xsearch._QUERY_BATCH)
+    q_tiles_total = sum(-(-min(xsearch._QUERY_BATCH, a.nq - q0) // int(plan[0])) for q0 in range(0, a.nq, xsearch._QUERY_BATCH))
+    algo_bytes_per_launch = db_bytes_local * q_tiles_total / launches_per_step
+    achieved = algo_bytes_per_launch / (scan_ms_avg * 1e-3) / 1e9
+    popc32 = index.n * a.nq * a.doc_bits * a.query_bits * ((a.dim + 31) // 32)
+    sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    popc_peak = 16 * 148 * sm_mhz * 1e6
+    out = {
+        "metric": METRIC, "value": round(a.nq / ms_step * 1e3, 2), "unit": "queries/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32 (XOR/POPC on packed bit planes; u64 keys)",
+        "data": "synthetic",
+        "config": {"workload": workload_name(a), "n": a.n, "dim": a.dim, "doc_bits": a.doc_bits,
+                   "query_bits": a.query_bits, "nq": a.nq, "k": a.k,
+                   "sharding": f"rows/{world}" if world > 1 else "none",
+                   "l2": "inputs larger than L2 (packed DB %.0f MB per GPU streamed every scan)" % (db_bytes_local / 1e6),
+                   "plan": {"queries_per_tile": int(plan[0]), "query_tiles": int(plan[1]), "doc_splits": int(plan[2]),
+                            "cand_capacity": int(plan[3]), "specialised_kernel": bool(plan[4]), "smem_bytes": int(plan[5])}},
+        "e2e": {"value": round(a.nq / e2e_ms * 1e3, 2), "unit": "queries/s", "ms_per_step": round(e2e_ms, 3),
+                "h2d_bytes_per_step": int(q_pinned.numel() * 4), "d2h_bytes_per_step": int(a.nq * min(a.k, a.n) * 8)},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "roofline": {"bound": "hbm", "kernel": "scan_topk_kernel (+ partial-result merge)", "achieved": round(achieved, 1),
+                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "peak_source": peak_src, "launch_ms": round(scan_ms_avg, 3),
+                     "algorithmic_bytes_per_launch": int(algo_bytes_per_launch),
+                     "note": "one launch scans the shard once per query tile; large batches are integer-pipe bound"},
+        "integer_pipe": {"popc32_per_step": int(popc32), "achieved_Gpopc_per_s": round(popc32 / (scan_ms_avg * launches_per_step * 1e-3) / 1e9, 1),
+                         "peak_Gpopc_per_s": round(popc_peak / 1e9, 1), "peak_basis": "16 POPC/clk/SM x 148 SMs x median SM clock",
+                         "frac": round(popc32 / (scan_ms_avg * launches_per_step * 1e-3) / popc_peak, 4)},
+        "small_batch": single,
+        "recall_at_k_vs_float_cosine": recall,
+        "build": {"rows_per_s": round((hi - lo) / build_s, 1), "seconds": round(build_s, 3),
+                  "quantize_kernel_ms": round(quant_ms, 3),
+                  "quantize_read_GBps": round((hi - lo) * a.dim * 4 / (quant_ms * 1e-3) / 1e9, 1)},
+    }
+    del scans_per_launch
+    if world == 1 and not a.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline_from_index(a, index, q_host, res)
+    print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline_from_index(a, index, q_host, gpu_result):
+    """The oracle C port (reference pass structure, threads over queries) on this box's host
+    cores, full n, a bounded number of the same queries; also cross-checks the GPU answer."""
+    from oracle import xfbq_oracle as xo
+    planes = index.packed.planes
+    cores = xo.c_max_threads()
+    scale = index.params.scale
+    qp = xo.c_quantize_matrix(q_host.astype(np.float64), a.query_bits, scale).transpose(2, 0, 1)
+    t0 = time.perf_counter()
+    xo.c_search(planes, qp[:1], a.k, threads=1)
+    one = time.perf_counter() - t0
+    nq_cpu = int(max(cores, min(a.nq, a.cpu_seconds * cores / max(one, 1e-6))))
+    nq_cpu = min(nq_cpu, a.nq, 4096)
+    t0 = time.perf_counter()
+    d, i = xo.c_search(planes, qp[:nq_cpu], a.k, threads=cores)
+    dt = time.perf_counter() - t0
+    scores, ids = gpu_result
+    parity = bool(np.array_equal(d, scores[:nq_cpu].astype(np.uint64)) and np.array_equal(i, ids[:nq_cpu]))
+    return {"value": round(nq_cpu / dt, 3), "unit": "queries/s", "cores": cores, "kind": "port",
+            "sample": f"first {nq_cpu} of the {a.nq} queries at full n={a.n} (oracle/xfbq_oracle.c, OpenMP over queries)",
+            "single_thread_ms_per_query": round(one * 1e3, 2), "gpu_matches_cpu_on_sample": parity}
+
+
+# ------------------------------------------------------------------------------------ reference arm
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    from oracle import xfbq_oracle as xo
+    cores = xo.c_max_threads()
+    torch.set_num_threads(cores)
+    W64 = (a.dim + 63) // 64
+    planes = np.empty((a.doc_bits, W64, a.n), dtype=np.uint64)
+    scale = None
+    for c in range(-(-a.n // CHUNK)):
+        lo, hi = c * CHUNK, min(a.n, (c + 1) * CHUNK)
+        g = torch.Generator().manual_seed(4000 + c)
+        x = torch.randn((hi - lo, a.dim), generator=g, dtype=torch.float32)
+        x = (x / x.norm(dim=1, keepdim=True)).numpy()
+        if scale is None:
+            scale = xo.estimate_scale(x[:100_000], 0.98)
+        planes[:, :, lo:hi] = xo.c_quantize_matrix(x, a.doc_bits, scale)
+    q_host = gen_queries(a.nq, a.dim)
+    qp = xo.c_quantize_matrix(q_host.astype(np.float64), a.query_bits, scale).transpose(2, 0, 1)
+    t0 = time.perf_counter()
+    xo.c_search(planes, qp[:1], a.k, threads=1)
+    one = time.perf_counter() - t0
+    # a step = a bounded sample of the batch: enough queries for ~cpu_seconds/ (steps+warmup) of work
+    per_step = max(cores, int(a.cpu_seconds * 4 / (a.steps + a.warmup) * cores / max(one, 1e-6)))
+    per_step = min(per_step, a.nq)
+    for w in range(a.warmup):
+        xo.c_search(planes, qp[:per_step], a.k, threads=cores)
+    t0 = time.perf_counter()
+    for s in range(a.steps):
+        xo.c_search(planes, qp[:per_step], a.k, threads=cores)
+    dt = (time.perf_counter() - t0) / a.steps
+    qps = per_step / dt
+    sample = (f"each step = first {per_step} of the {a.nq} queries at full n={a.n}, all {cores} host threads "
+              f"(oracle/xfbq_oracle.c: reference pass structure _kernels.py:56-69 + (dist,id) top-k)")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(qps, 3), "unit": "queries/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64 (XOR/POPCNT on packed bit planes)", "data": "synthetic",
+        "config": {"workload": workload_name(a), "n": a.n, "dim": a.dim, "doc_bits": a.doc_bits,
+                   "query_bits": a.query_bits, "nq": a.nq, "k": a.k},
+        "cpu_baseline": {"value": round(qps, 3), "unit": "queries/s", "cores": cores, "kind": "port", "sample": sample,
+                         "single_thread_ms_per_query": round(one * 1e3, 2)},
+        "e2e": {"value": round(qps, 3), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)

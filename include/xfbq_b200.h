@@ -1,0 +1,145 @@
+/*
+ * xfbq_b200.h -- C ABI of the B200-native XFBQ hot path (libxfbq_b200.so).
+ *
+ * The reference (arXiv 2008.02002 package `xfbq`, pure Python) has no FFI; its
+ * narrowest swap point is the callable `batch_distances_kernel(doc_planes,
+ * query_planes, out)` (pkg/src/xfbq/_kernels.py:71-75).  The entry points below
+ * are what a binding for the hot path quantize -> pack -> XOR/POPC scan ->
+ * top-K -> merge would call; each cites the reference code it replaces.
+ * INTEGRATION.md shows the ctypes stub a maintainer of the reference would add.
+ *
+ * Conventions
+ *   - every pointer named *_dev is a CUDA device pointer owned by the caller; the
+ *     library never allocates or frees device memory and keeps no global state
+ *     besides a thread-local error string;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = default stream); all
+ *     work is enqueued asynchronously on it, calls are re-entrant per
+ *     (stream, workspace);
+ *   - return value: 0 = ok, nonzero = error (XFBQ_E_*), message via
+ *     xfbq_last_error() (thread-local, valid until the next failing call);
+ *   - no exceptions cross the boundary, no torch types appear in signatures.
+ *
+ * Device layouts
+ *   bundle layout (database codes): documents are grouped in bundles of 32
+ *     ("32-doc warp bundles"); C = ceil(dim/128) 128-bit chunks per
+ *     plane; element (bundle b, plane i, chunk c, lane l) is one 16-byte word
+ *     at index ((b*width + i)*C + c)*32 + l holding dims [128c, 128c+128) of
+ *     bit-plane i of document 32b+l, little-endian bit order (dimension k ->
+ *     bit k%32 of 32-bit word (k%128)/32), identical bit numbering to the
+ *     reference's uint64 words (bitplane.py:1-9).  Padding dims and padding
+ *     documents are all-zero bits.  Size: xfbq_db_bytes().
+ *   query layout: uint32 [nq][width][4*C], same bit numbering, zero padded.
+ *   keys: uint64 (distance << 32) | global_row_id ; ascending key order is the
+ *     reference's ranking (distance asc, row id asc; search.py:129-131).
+ *     Unused slots hold UINT64_MAX.
+ */
+#ifndef XFBQ_B200_H
+#define XFBQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XFBQ_ABI_VERSION 1
+
+#define XFBQ_OK 0
+#define XFBQ_E_INVALID 1     /* argument violates a precondition (InvalidInputError) */
+#define XFBQ_E_CUDA 2        /* CUDA runtime error */
+#define XFBQ_E_UNSUPPORTED 3 /* shape outside what the kernels implement */
+
+#define XFBQ_MAX_WIDTH 8     /* quant.py:20 MAX_WIDTH */
+#define XFBQ_MAX_K 4096      /* largest k one scan pass selects */
+
+int xfbq_abi_version(void);
+const char *xfbq_last_error(void);
+
+/* bitplane.py:29-30 words_needed, in 128-bit chunks */
+int64_t xfbq_chunks128(int64_t dim);
+/* bytes of the bundle layout for n documents (n rounded up to 32) */
+int64_t xfbq_db_bytes(int64_t n, int64_t dim, int width);
+/* bytes of the query layout */
+int64_t xfbq_query_bytes(int64_t nq, int64_t dim, int width);
+/* distance.py:25-29 distance_upper_bound */
+int64_t xfbq_distance_upper_bound(int64_t dim, int width_x, int width_y);
+
+/*
+ * Quantizer + bit-plane packer: replaces quantize_matrix (bitplane.py:225-233) =
+ * widen to float64, multiply by `scale`, quantize_values (quant.py:138-148),
+ * _pack_code_matrix (bitplane.py:151-163).  x_dev is row-major (n, dim) with
+ * leading dimension ld (elements).  *nonfinite_dev (device uint64, caller
+ * zeroes it) is incremented by the number of non-finite scaled values; the
+ * reference raises InvalidInputError when that is nonzero (quant.py:142-143).
+ * Output: bundle layout.
+ */
+int xfbq_quantize_pack_f32(const float *x_dev, int64_t n, int64_t dim, int64_t ld, double scale,
+                           int width, void *db_out_dev, uint64_t *nonfinite_dev, void *stream);
+int xfbq_quantize_pack_f64(const double *x_dev, int64_t n, int64_t dim, int64_t ld, double scale,
+                           int width, void *db_out_dev, uint64_t *nonfinite_dev, void *stream);
+/* Same arithmetic for queries (quantize_vector, bitplane.py:214-222); output: query layout. */
+int xfbq_quantize_queries_f32(const float *q_dev, int64_t nq, int64_t dim, int64_t ld,
+                              double scale, int width, uint32_t *q_out_dev,
+                              uint64_t *nonfinite_dev, void *stream);
+int xfbq_quantize_queries_f64(const double *q_dev, int64_t nq, int64_t dim, int64_t ld,
+                              double scale, int width, uint32_t *q_out_dev,
+                              uint64_t *nonfinite_dev, void *stream);
+
+/*
+ * Layout conversion between the reference's PackedMatrix.planes
+ * ((width, ceil(dim/64), n) uint64, bitplane.py:79-81) and the bundle layout.
+ */
+int xfbq_planes_to_bundles(const uint64_t *planes_dev, int64_t n, int64_t dim, int width,
+                           void *db_out_dev, void *stream);
+int xfbq_bundles_to_planes(const void *db_dev, int64_t n, int64_t dim, int width,
+                           uint64_t *planes_out_dev, void *stream);
+
+/*
+ * batch_distances (distance.py:44-62 -> _kernels.py:56-69): distances from one
+ * packed query (query layout, nq = 1) to every document; out_dev is uint64[n].
+ */
+int xfbq_batch_distances(const void *db_dev, int64_t n, int64_t dim, int doc_bits,
+                         const uint32_t *q_dev, int query_bits, uint64_t *out_dev, void *stream);
+
+/*
+ * Fused scan + top-K: for each of nq queries the k smallest keys
+ * (distance << 32 | row_offset + row) over the n documents, ascending, written
+ * to keys_out_dev[nq][k] (slots beyond min(k, n) hold UINT64_MAX).  No score
+ * matrix is materialised.  Replaces, per query, batch_distances + the
+ * no-originals ranking of k_select (search.py:206-216, :159-172, :129-131).
+ * workspace_dev must hold xfbq_scan_workspace_bytes(...) bytes.
+ * 1 <= k <= XFBQ_MAX_K;  row_offset + n <= 2^32.
+ */
+int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int doc_bits, int64_t nq,
+                                  int query_bits, int k);
+/* Launch plan xfbq_scan_topk will use on the current device, for reporting:
+ * plan_out[0] = queries per CTA tile, [1] = query tiles, [2] = document splits (partial results
+ * merged afterwards), [3] = candidate-list capacity per query, [4] = 1 if a width/dim-specialised
+ * kernel is used, [5] = dynamic shared memory bytes per CTA. */
+int xfbq_scan_plan(int64_t n, int64_t dim, int doc_bits, int64_t nq, int query_bits, int k,
+                   int32_t plan_out[6]);
+int xfbq_scan_topk(const void *db_dev, int64_t n, int64_t dim, int doc_bits,
+                   const uint32_t *q_dev, int64_t nq, int query_bits, int k, int64_t row_offset,
+                   uint64_t *keys_out_dev, void *workspace_dev, int64_t workspace_bytes,
+                   void *stream);
+
+/*
+ * Merge `parts` partial results keys_in_dev[parts][nq][k] (each row ascending,
+ * UINT64_MAX padded) into keys_out_dev[nq][k]: the exchange step after the
+ * per-GPU scans (no reference code; semantics of search.py:129-131: total order
+ * on (distance, id), so the result is independent of the partition).
+ */
+int xfbq_merge_topk(const uint64_t *keys_in_dev, int parts, int64_t nq, int k,
+                    uint64_t *keys_out_dev, void *stream);
+
+/* Split keys into int64 distances and int64 row ids (-1 / -1 for empty slots). */
+int xfbq_unpack_keys(const uint64_t *keys_dev, int64_t count, int64_t *dist_out_dev,
+                     int64_t *id_out_dev, void *stream);
+
+/* Number of kernels this library has launched in the calling process (for bench accounting). */
+int64_t xfbq_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XFBQ_B200_H */

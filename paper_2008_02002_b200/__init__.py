@@ -1,0 +1,24 @@
+"""paper_2008_02002_b200 -- B200-native drop-in for the hot path of the `xfbq` reference
+(arXiv 2008.02002): quantize -> bit-plane pack -> XOR/POPC scan with fused top-K -> merge.
+
+Same names as the reference package facade (/root/reference/pkg/src/xfbq/__init__.py:95-160)
+for everything on that path, plus the batched `search`.  All compute runs in hand-written
+sm_100a kernels behind the C ABI in include/xfbq_b200.h; there is no CPU fallback.
+"""
+from .bitplane import (PackedMatrix, PackedVector, pack_matrix, quantize_matrix, quantize_queries,
+                       quantize_vector, unpack_matrix, words_needed)
+from .distance import (batch_distances, decode_inner_product, decode_inner_product_values,
+                       distance_upper_bound)
+from .errors import DimensionMismatchError, InvalidInputError, NativeLibraryError, XfbqError
+from .index import Index, QuantParams, build_index, estimate_scale
+from .sharded import ShardedIndex, shard_bounds
+from .search import SearchRequest, SearchResult, k_select, search, search_device
+
+__version__ = "0.1.0"
+__all__ = [
+    "DimensionMismatchError", "Index", "InvalidInputError", "NativeLibraryError", "PackedMatrix",
+    "PackedVector", "QuantParams", "SearchRequest", "SearchResult", "XfbqError", "batch_distances",
+    "build_index", "decode_inner_product", "decode_inner_product_values", "distance_upper_bound",
+    "estimate_scale", "k_select", "pack_matrix", "quantize_matrix", "quantize_queries",
+    "quantize_vector", "search", "search_device", "ShardedIndex", "shard_bounds", "unpack_matrix", "words_needed",
+]

@@ -1,0 +1,317 @@
+"""Packed bit-plane containers and the GPU quantizer front end.
+
+Mirrors the reference's `bitplane.py` surface (/root/reference/pkg/src/xfbq/bitplane.py):
+`PackedVector`, `PackedMatrix`, `quantize_vector`, `quantize_matrix`, `pack_matrix`,
+`unpack_matrix`, `words_needed`.  A `PackedMatrix` here owns the codes in HBM in the
+bundle layout (include/xfbq_b200.h); the reference's word-major `(width, words, n)`
+uint64 array is available through `.planes` (converted on the GPU, copied to the host on
+first use, read-only like the reference's, bitplane.py:98).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from .errors import InvalidInputError
+
+WORD_BITS = 64
+MAX_WIDTH = 8
+_ROW_CHUNK = 1 << 20  # rows staged per host->device copy when quantizing host matrices
+
+
+def check_width(width) -> int:
+    """quant.py:23-31."""
+    w = int(width)
+    if w < 1 or w > MAX_WIDTH:
+        raise InvalidInputError(f"bit width must be in 1..{MAX_WIDTH}, got {width}")
+    return w
+
+
+def words_needed(dim: int) -> int:
+    """bitplane.py:29-30."""
+    return (int(dim) + WORD_BITS - 1) // WORD_BITS
+
+
+def _padding_ok(planes: np.ndarray, dim: int) -> bool:
+    """bitplane.py:33-46: bits past `dim` in the last word must be zero."""
+    if dim == 0 or planes.size == 0 or dim % WORD_BITS == 0:
+        return True
+    mask = np.uint64((1 << (dim % WORD_BITS)) - 1)
+    last = planes[:, -1] if planes.ndim == 2 else planes[:, -1, :]
+    return not np.any(last & ~mask)
+
+
+def _stream_ptr(torch):
+    return torch.cuda.current_stream().cuda_stream
+
+
+class PackedVector:
+    """One quantized vector as ``(width, words)`` uint64 bit-planes (bitplane.py:49-76)."""
+
+    __slots__ = ("planes", "dim")
+
+    def __init__(self, planes, dim: int):
+        planes = np.ascontiguousarray(planes, dtype=np.uint64)
+        if planes.ndim != 2:
+            raise InvalidInputError("planes must be a (width, words) array")
+        check_width(planes.shape[0])
+        if dim < 0 or planes.shape[1] != words_needed(dim):
+            raise InvalidInputError(
+                f"expected {words_needed(dim)} words per plane for dim {dim}, got {planes.shape[1]}")
+        if not _padding_ok(planes, dim):
+            raise InvalidInputError("nonzero padding bits past the true dimension")
+        planes.setflags(write=False)
+        object.__setattr__(self, "planes", planes)
+        object.__setattr__(self, "dim", int(dim))
+
+    def __setattr__(self, key, value):  # frozen, like the reference dataclass
+        raise AttributeError("PackedVector is immutable")
+
+    @property
+    def width(self) -> int:
+        return self.planes.shape[0]
+
+    @property
+    def nbytes(self) -> int:
+        return self.planes.nbytes
+
+    def device_words(self):
+        """Query layout uint32 [1][width][4C] on the current CUDA device."""
+        torch = _native.require_cuda()
+        C = (self.dim + 127) // 128
+        host = np.zeros((self.width, 2 * C), dtype=np.uint64)
+        host[:, : self.planes.shape[1]] = self.planes
+        return torch.from_numpy(host.view(np.int64).reshape(1, -1)).cuda()
+
+
+class PackedMatrix:
+    """n quantized vectors; codes live in HBM in the bundle layout.
+
+    Reference surface (bitplane.py:79-122): ``planes`` (word-major ``(width, words, n)``
+    uint64, read-only), ``dim``, ``width``, ``count``, ``nbytes``, ``row(k)``,
+    ``to_row_major()``, ``from_row_major()``.
+    """
+
+    def __init__(self, planes=None, dim: int | None = None, *, _codes=None, _count=None, _width=None):
+        if dim is None:
+            raise InvalidInputError("dim is required")
+        self._dim = int(dim)
+        self._planes = None
+        if _codes is not None:  # device path (quantizer output)
+            self._codes, self._count, self._width = _codes, int(_count), int(_width)
+            return
+        planes = np.ascontiguousarray(planes, dtype=np.uint64)
+        if planes.ndim != 3:
+            raise InvalidInputError("planes must be a (width, words, n) array")
+        check_width(planes.shape[0])
+        if self._dim < 0 or planes.shape[1] != words_needed(self._dim):
+            raise InvalidInputError(
+                f"expected {words_needed(self._dim)} words per plane for dim {self._dim}, got {planes.shape[1]}")
+        if not _padding_ok(planes, self._dim):
+            raise InvalidInputError("nonzero padding bits past the true dimension")
+        if self._dim < 1:
+            raise InvalidInputError("dim must be >= 1 for a device-resident matrix")
+        planes.setflags(write=False)
+        self._planes = planes
+        self._width, self._count = planes.shape[0], planes.shape[2]
+        torch = _native.require_cuda()
+        L = _native.lib()
+        self._codes = torch.empty(max(int(L.xfbq_db_bytes(self._count, self._dim, self._width)), 16),
+                                  dtype=torch.uint8, device="cuda")
+        if self._count:
+            dev = torch.from_numpy(planes.view(np.int64)).cuda()
+            _native.check(L.xfbq_planes_to_bundles(dev.data_ptr(), self._count, self._dim, self._width,
+                                                   self._codes.data_ptr(), _stream_ptr(torch)))
+            torch.cuda.current_stream().synchronize()
+
+    # ---- reference surface
+    @property
+    def dim(self) -> int:
+        return self._dim
+
+    @property
+    def width(self) -> int:
+        return self._width
+
+    @property
+    def count(self) -> int:
+        return self._count
+
+    @property
+    def nbytes(self) -> int:
+        """Algorithmic size = the reference's planes.nbytes (bitplane.py:109-110)."""
+        return self._width * words_needed(self._dim) * 8 * self._count
+
+    @property
+    def device_nbytes(self) -> int:
+        return int(self._codes.numel())
+
+    @property
+    def codes(self):
+        """torch.uint8 device buffer holding the bundle layout."""
+        return self._codes
+
+    @property
+    def planes(self) -> np.ndarray:
+        if self._planes is None:
+            torch = _native.require_cuda()
+            L = _native.lib()
+            W64 = words_needed(self._dim)
+            with torch.cuda.device(self._codes.device):
+                out = torch.zeros((self._width, W64, self._count), dtype=torch.int64, device=self._codes.device)
+                if self._count:
+                    _native.check(L.xfbq_bundles_to_planes(self._codes.data_ptr(), self._count, self._dim,
+                                                           self._width, out.data_ptr(), _stream_ptr(torch)))
+                host = out.cpu().numpy().view(np.uint64)
+            host.setflags(write=False)
+            self._planes = host
+        return self._planes
+
+    def row(self, k: int) -> PackedVector:
+        return PackedVector(np.ascontiguousarray(self.planes[:, :, k]), self._dim)
+
+    def to_row_major(self) -> np.ndarray:
+        return np.ascontiguousarray(self.planes.transpose(2, 0, 1))
+
+    @classmethod
+    def from_row_major(cls, rows, dim: int) -> "PackedMatrix":
+        rows = np.asarray(rows, dtype=np.uint64)
+        return cls(np.ascontiguousarray(rows.transpose(1, 2, 0)), dim)
+
+
+def _as_float_matrix(values):
+    """Host array as float32 or float64 without changing any value (the reference widens
+    everything to float64, bitplane.py:229; float32 -> float64 is exact so float32 input is
+    widened inside the kernel instead)."""
+    a = np.asarray(values)
+    if a.dtype == np.float32:
+        return np.ascontiguousarray(a)
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def quantize_to_device(values, width: int, scale: float, queries: bool):
+    """Run the quantizer kernel.  `values`: host array or CUDA tensor, (n, dim) f32/f64.
+    Returns (device buffer, n, dim).  Raises InvalidInputError on non-finite scaled values
+    (quant.py:142-143) exactly as the reference does."""
+    torch = _native.require_cuda()
+    L = _native.lib()
+    width = check_width(width)
+    scale = float(scale)
+    on_device = _is_torch(values)
+    if on_device:
+        if values.dtype not in (torch.float32, torch.float64):
+            values = values.to(torch.float64)
+        if not values.is_cuda:
+            values = values.cuda()
+        if values.stride(-1) != 1:
+            values = values.contiguous()
+        n, dim = values.shape
+    else:
+        values = _as_float_matrix(values)
+        n, dim = values.shape
+    if dim < 1:
+        raise InvalidInputError("dim must be >= 1")
+    st = _stream_ptr(torch)
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    if queries:
+        out = torch.empty(max(int(L.xfbq_query_bytes(n, dim, width)), 16) // 4, dtype=torch.int32, device="cuda")
+    else:
+        out = torch.empty(max(int(L.xfbq_db_bytes(n, dim, width)), 16), dtype=torch.uint8, device="cuda")
+    row_bytes_out = int(L.xfbq_query_bytes(1, dim, width)) if queries else None
+
+    def run(chunk, row0):
+        f32 = chunk.dtype == torch.float32
+        if queries:
+            fn = L.xfbq_quantize_queries_f32 if f32 else L.xfbq_quantize_queries_f64
+            dst = out.data_ptr() + row0 * row_bytes_out
+        else:
+            fn = L.xfbq_quantize_pack_f32 if f32 else L.xfbq_quantize_pack_f64
+            dst = out.data_ptr() + int(L.xfbq_db_bytes(row0, dim, width))  # row0 is a multiple of 32
+        _native.check(fn(chunk.data_ptr(), chunk.shape[0], dim, chunk.stride(0), scale, width, dst,
+                         bad.data_ptr(), st))
+
+    if on_device:
+        if n:
+            run(values, 0)
+    else:
+        for row0 in range(0, n, _ROW_CHUNK):
+            chunk = torch.from_numpy(values[row0:row0 + _ROW_CHUNK]).cuda()
+            run(chunk, row0)
+            del chunk
+    if n and int(bad.item()):
+        raise InvalidInputError("cannot quantize non-finite values")
+    return out, n, dim
+
+
+def quantize_matrix(values, width: int, scale: float = 1.0) -> PackedMatrix:
+    """Scale, quantize and pack an (n, dim) float matrix (bitplane.py:225-233) on the GPU."""
+    if scale <= 0:
+        raise InvalidInputError(f"scale must be positive, got {scale}")
+    if not _is_torch(values):
+        values = np.asarray(values)
+    if values.ndim != 2:
+        raise InvalidInputError("quantize_matrix expects an (n, dim) matrix")
+    codes, n, dim = quantize_to_device(values, width, scale, queries=False)
+    return PackedMatrix(None, dim, _codes=codes, _count=n, _width=check_width(width))
+
+
+def quantize_queries(values, width: int, scale: float = 1.0):
+    """Batched query quantizer: (nq, dim) -> device int32 buffer in the query layout."""
+    if scale <= 0:
+        raise InvalidInputError(f"scale must be positive, got {scale}")
+    if values.ndim != 2:
+        raise InvalidInputError("quantize_queries expects an (nq, dim) matrix")
+    out, _, _ = quantize_to_device(values, width, scale, queries=True)
+    return out
+
+
+def quantize_vector(values, width: int, scale: float = 1.0) -> PackedVector:
+    """Scale, quantize and pack one float vector (bitplane.py:214-222) on the GPU."""
+    if scale <= 0:
+        raise InvalidInputError(f"scale must be positive, got {scale}")
+    v = np.asarray(values, dtype=np.float64)
+    if v.ndim != 1:
+        raise InvalidInputError("quantize_vector expects a 1-D vector")
+    width = check_width(width)
+    if v.shape[0] == 0:
+        return PackedVector(np.zeros((width, 0), dtype=np.uint64), 0)
+    out, _, dim = quantize_to_device(v[None, :], width, scale, queries=True)
+    C = (dim + 127) // 128
+    words = out[: width * 4 * C].cpu().numpy().view(np.uint64).reshape(width, 2 * C)
+    return PackedVector(np.ascontiguousarray(words[:, : words_needed(dim)]), dim)
+
+
+def pack_matrix(codes, width: int) -> PackedMatrix:
+    """(n, dim) uint codes -> PackedMatrix (bitplane.py:196-201).  Host bit packing of
+    already-quantized codes is a format conversion, done with numpy and uploaded."""
+    width = check_width(width)
+    arr = np.asarray(codes)
+    if arr.ndim != 2:
+        raise InvalidInputError("pack_matrix expects an (n, dim) code array")
+    if arr.size and int(arr.max()) >= (1 << width):
+        raise InvalidInputError(f"code values exceed {width} bits")
+    arr = arr.astype(np.uint8)
+    n, dim = arr.shape
+    nwords = words_needed(dim)
+    planes = np.zeros((width, n, nwords * 8), dtype=np.uint8)
+    for b in range(width):
+        packed = np.packbits((arr >> b) & 1, axis=1, bitorder="little")
+        planes[b, :, : packed.shape[1]] = packed
+    planes = planes.view("<u8").astype(np.uint64, copy=False)
+    return PackedMatrix(np.ascontiguousarray(planes.transpose(0, 2, 1)), dim)
+
+
+def unpack_matrix(packed: PackedMatrix) -> np.ndarray:
+    """Inverse of pack_matrix: (n, dim) uint8 codes (bitplane.py:204-211)."""
+    planes = packed.planes
+    n, dim = packed.count, packed.dim
+    codes = np.zeros((n, dim), dtype=np.uint8)
+    for b in range(packed.width):
+        words = np.ascontiguousarray(planes[b].T).astype("<u8", copy=False)
+        bits = np.unpackbits(words.view(np.uint8).reshape(n, -1), axis=1, bitorder="little")[:, :dim]
+        codes |= (bits << b).astype(np.uint8)
+    return codes

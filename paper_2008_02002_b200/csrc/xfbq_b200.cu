@@ -1,0 +1,744 @@
+// xfbq_b200.cu -- hand-written sm_100a kernels + C ABI for the XFBQ hot path.
+//
+// quantize -> bit-plane pack -> XOR/POPC scan with fused top-K -> merge.
+// See include/xfbq_b200.h for the ABI contract and the device layouts, DESIGN.md for
+// the roofline of each kernel.  Reference citations are paths under
+// /root/reference/pkg/src/xfbq.
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared -Xcompiler -fPIC
+// (no --use_fast_math: the quantizer depends on IEEE float64 and on denormal inputs).
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <atomic>
+
+#include "../../include/xfbq_b200.h"
+
+#define XFBQ_API extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+constexpr uint64_t KEY_INF = 0xFFFFFFFFFFFFFFFFull;
+constexpr int SCAN_THREADS = 256;  // 8 warps = 8 bundles = 256 documents per step
+constexpr int SCAN_WARPS = SCAN_THREADS / 32;
+
+thread_local char g_err[512] = "";
+std::atomic<int64_t> g_launches{0};
+
+int fail(int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return XFBQ_OK;
+}
+
+inline int64_t chunks128(int64_t dim) { return (dim + 127) / 128; }
+inline int64_t bundles_of(int64_t n) { return (n + 31) / 32; }
+inline bool width_ok(int w) { return w >= 1 && w <= XFBQ_MAX_WIDTH; }
+
+struct DeviceInfo {
+    int sms = 0;
+    int smem_optin = 0;
+};
+
+int device_info(DeviceInfo *info) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+    static thread_local int cached_dev = -1;
+    static thread_local DeviceInfo cached;
+    if (cached_dev != dev) {
+        e = cudaDeviceGetAttribute(&cached.sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess)
+            e = cudaDeviceGetAttribute(&cached.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "cudaDeviceGetAttribute: %s", cudaGetErrorString(e));
+        cached_dev = dev;
+    }
+    *info = cached;
+    return XFBQ_OK;
+}
+
+// ----------------------------------------------------------------------------------------------
+// Quantizer (quant.py:138-148 after bitplane.py:229-232): float64 arithmetic, exactly
+//   t = floor((double(x) * scale) * 2^(w-1));  t = clamp(t, -2^(w-1), 2^(w-1)-1);  code = 2^(w-1)-1-t
+// which equals (hi - clip(2*floor(..)+1, -hi, hi)) / 2 with hi = 2^w - 1.
+// ----------------------------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ unsigned quantize_one(T x, double scale, double half, unsigned long long &bad) {
+    double v = static_cast<double>(x) * scale;      // bitplane.py:232
+    if (!isfinite(v)) { ++bad; return 0u; }         // quant.py:142-143
+    double t = floor(v * half);                     // quant.py:146 (overflow to +-inf saturates below)
+    t = fmin(fmax(t, -half), half - 1.0);           // quant.py:147 clip
+    return static_cast<unsigned>(static_cast<int>(half) - 1 - static_cast<int>(t));
+}
+
+// One warp packs one bundle (32 documents) chunk by chunk: lanes read 32 consecutive
+// dimensions of one row (128 B, coalesced), a ballot per bit-plane yields the packed 32-bit
+// word, words are staged in shared memory and leave as 512-byte coalesced 128-bit stores.
+constexpr int QP_WARPS = 8;
+constexpr int QP_PLANE_STRIDE = 132;  // 32 rows * 4 words + 4 pad words: conflict-free staging
+
+template <typename T>
+__global__ void __launch_bounds__(QP_WARPS * 32)
+quantize_pack_kernel(const T *__restrict__ x, int64_t n, int dim, int64_t ld, double scale, int width,
+                     int C, uint4 *__restrict__ out, unsigned long long *__restrict__ nonfinite) {
+    __shared__ __align__(16) uint32_t stage[QP_WARPS][XFBQ_MAX_WIDTH * QP_PLANE_STRIDE];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double half = static_cast<double>(1 << (width - 1));
+    const int64_t nb = (n + 31) >> 5;
+    unsigned long long bad = 0;
+    uint32_t *st = stage[warp];
+    const int my_plane = lane >> 2, my_t = lane & 3;
+    for (int64_t b = static_cast<int64_t>(blockIdx.x) * QP_WARPS + warp; b < nb;
+         b += static_cast<int64_t>(gridDim.x) * QP_WARPS) {
+        for (int c = 0; c < C; ++c) {
+#pragma unroll 2
+            for (int r = 0; r < 32; ++r) {
+                const int64_t doc = b * 32 + r;
+                T v[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int k = c * 128 + t * 32 + lane;
+                    v[t] = (doc < n && k < dim) ? x[doc * ld + k] : static_cast<T>(0);
+                }
+                uint32_t mine = 0;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int k = c * 128 + t * 32 + lane;
+                    const bool real = (doc < n && k < dim);
+                    const unsigned code = real ? quantize_one<T>(v[t], scale, half, bad) : 0u;
+#pragma unroll
+                    for (int i = 0; i < XFBQ_MAX_WIDTH; ++i) {
+                        if (i < width) {  // warp-uniform
+                            const uint32_t w = __ballot_sync(0xffffffffu, real && ((code >> i) & 1u));
+                            if (lane == i * 4 + t) mine = w;
+                        }
+                    }
+                }
+                if (my_plane < width) st[my_plane * QP_PLANE_STRIDE + r * 4 + my_t] = mine;
+            }
+            __syncwarp();
+            for (int i = 0; i < width; ++i) {
+                const uint4 w = *reinterpret_cast<const uint4 *>(&st[i * QP_PLANE_STRIDE + lane * 4]);
+                out[((b * width + i) * C + c) * 32 + lane] = w;
+            }
+            __syncwarp();
+        }
+    }
+    if (bad) atomicAdd(nonfinite, bad);
+}
+
+// Queries: one warp per query row, output uint32 [nq][width][4C].
+template <typename T>
+__global__ void __launch_bounds__(256)
+quantize_queries_kernel(const T *__restrict__ x, int64_t nq, int dim, int64_t ld, double scale,
+                        int width, int C, uint32_t *__restrict__ out,
+                        unsigned long long *__restrict__ nonfinite) {
+    const int lane = threadIdx.x & 31;
+    const int64_t q = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (q >= nq) return;  // whole warp exits together
+    const double half = static_cast<double>(1 << (width - 1));
+    const int W = 4 * C;
+    unsigned long long bad = 0;
+    for (int t = 0; t < W; ++t) {
+        const int k = t * 32 + lane;
+        const bool real = k < dim;
+        const unsigned code = real ? quantize_one<T>(x[q * ld + k], scale, half, bad) : 0u;
+        for (int i = 0; i < width; ++i) {
+            const uint32_t w = __ballot_sync(0xffffffffu, real && ((code >> i) & 1u));
+            if (lane == i) out[(q * width + i) * W + t] = w;
+        }
+    }
+    if (bad) atomicAdd(nonfinite, bad);
+}
+
+// ----------------------------------------------------------------------------------------------
+// Layout conversion: reference planes (width, W64, n) uint64  <->  bundle layout.
+// ----------------------------------------------------------------------------------------------
+__global__ void planes_to_bundles_kernel(const uint64_t *__restrict__ planes, int64_t n, int W64,
+                                         int width, int C, uint4 *__restrict__ out, int64_t total) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const int lane = static_cast<int>(e & 31);
+    int64_t r = e >> 5;
+    const int c = static_cast<int>(r % C); r /= C;
+    const int i = static_cast<int>(r % width);
+    const int64_t b = r / width;
+    const int64_t doc = b * 32 + lane;
+    uint64_t w0 = 0, w1 = 0;
+    if (doc < n) {
+        if (2 * c < W64) w0 = planes[(static_cast<int64_t>(i) * W64 + 2 * c) * n + doc];
+        if (2 * c + 1 < W64) w1 = planes[(static_cast<int64_t>(i) * W64 + 2 * c + 1) * n + doc];
+    }
+    out[e] = make_uint4(static_cast<uint32_t>(w0), static_cast<uint32_t>(w0 >> 32),
+                        static_cast<uint32_t>(w1), static_cast<uint32_t>(w1 >> 32));
+}
+
+__global__ void bundles_to_planes_kernel(const uint4 *__restrict__ db, int64_t n, int W64, int width,
+                                         int C, uint64_t *__restrict__ planes, int64_t total) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const int lane = static_cast<int>(e & 31);
+    int64_t r = e >> 5;
+    const int c = static_cast<int>(r % C); r /= C;
+    const int i = static_cast<int>(r % width);
+    const int64_t b = r / width;
+    const int64_t doc = b * 32 + lane;
+    if (doc >= n) return;
+    const uint4 w = db[e];
+    if (2 * c < W64)
+        planes[(static_cast<int64_t>(i) * W64 + 2 * c) * n + doc] = static_cast<uint64_t>(w.x) | (static_cast<uint64_t>(w.y) << 32);
+    if (2 * c + 1 < W64)
+        planes[(static_cast<int64_t>(i) * W64 + 2 * c + 1) * n + doc] = static_cast<uint64_t>(w.z) | (static_cast<uint64_t>(w.w) << 32);
+}
+
+// ----------------------------------------------------------------------------------------------
+// Distance arithmetic (_kernels.py:56-69):
+//   d = sum_{i<wd} sum_{j<wq} sum_w popcount(D[i,w] ^ Q[j,w]) << (i+j)
+// grouped by weight class s = i+j so each class is shifted once.
+// ----------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t popc4(const uint4 a, const uint4 b) {
+    return __popc(a.x ^ b.x) + __popc(a.y ^ b.y) + __popc(a.z ^ b.z) + __popc(a.w ^ b.w);
+}
+
+// Generic widths / dims: document words are re-read from global (L1/L2) for every query.
+__device__ __forceinline__ uint32_t distance_generic(const uint4 *__restrict__ doc /* + lane */, int wd, int C,
+                                                     const uint32_t *qs, int wq) {
+    uint32_t d = 0;
+    for (int i = 0; i < wd; ++i)
+        for (int c = 0; c < C; ++c) {
+            const uint4 x = __ldg(doc + (i * C + c) * 32);
+            for (int j = 0; j < wq; ++j) {
+                const uint4 y = *reinterpret_cast<const uint4 *>(qs + (j * C + c) * 4);
+                d += popc4(x, y) << (i + j);
+            }
+        }
+    return d;
+}
+
+template <int WD, int WQ, int C>
+__device__ __forceinline__ uint32_t distance_regs(const uint4 (&x)[WD * C], const uint32_t *qs) {
+    uint32_t acc[WD + WQ - 1];
+#pragma unroll
+    for (int s = 0; s < WD + WQ - 1; ++s) acc[s] = 0;
+#pragma unroll
+    for (int j = 0; j < WQ; ++j)
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const uint4 y = *reinterpret_cast<const uint4 *>(qs + (j * C + c) * 4);  // broadcast LDS.128
+#pragma unroll
+            for (int i = 0; i < WD; ++i) acc[i + j] += popc4(x[i * C + c], y);
+        }
+    uint32_t d = 0;
+#pragma unroll
+    for (int s = 0; s < WD + WQ - 1; ++s) d += acc[s] << s;
+    return d;
+}
+
+__global__ void __launch_bounds__(256)
+batch_distances_kernel(const uint4 *__restrict__ db, int64_t n, int wd, int C,
+                       const uint32_t *__restrict__ q, int wq, uint64_t *__restrict__ out) {
+    extern __shared__ __align__(16) uint32_t qs_dyn[];
+    const int qwords = wq * C * 4;
+    for (int t = threadIdx.x; t < qwords; t += blockDim.x) qs_dyn[t] = q[t];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nb = (n + 31) >> 5;
+    const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t b = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nb; b += warps) {
+        const int64_t doc = b * 32 + lane;
+        const uint32_t d = distance_generic(db + b * wd * C * 32 + lane, wd, C, qs_dyn, wq);
+        if (doc < n) out[doc] = d;
+    }
+}
+
+// ----------------------------------------------------------------------------------------------
+// Top-K selection state of one CTA: per query slot a candidate list in shared memory, a count
+// and a threshold key.  A score enters the list only if its key (distance<<32 | row id) is below
+// the threshold; when a list cannot take another full step (SCAN_THREADS pushes) it is sorted,
+// cut to the k best and the threshold becomes the k-th key (search.py:129-131 order).
+// ----------------------------------------------------------------------------------------------
+__device__ __forceinline__ void bitonic_sort_block(uint64_t *s, int P) {
+    for (int size = 2; size <= P; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
+                const int lo = 2 * t - (t & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t a = s[lo], b = s[hi];
+                if ((a > b) == up) { s[lo] = b; s[hi] = a; }
+            }
+            __syncthreads();
+        }
+}
+
+__device__ __forceinline__ int pow2_ceil(int v) {
+    int p = 2;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+// Block-wide; every thread must call it with the same arguments.
+__device__ void compact_list(uint64_t *list, uint32_t *cnt_p, uint64_t *thr_p, int k) {
+    const int c = static_cast<int>(*cnt_p);
+    const int P = pow2_ceil(c);
+    __syncthreads();  // everyone has read *cnt_p
+    for (int t = c + threadIdx.x; t < P; t += blockDim.x) list[t] = KEY_INF;
+    __syncthreads();
+    bitonic_sort_block(list, P);
+    if (threadIdx.x == 0) {
+        *cnt_p = static_cast<uint32_t>(c < k ? c : k);
+        *thr_p = (c >= k) ? list[k - 1] : KEY_INF;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void push_candidate(bool pass, uint64_t key, uint64_t *list, uint32_t *cnt_p, int lane) {
+    const unsigned m = __ballot_sync(0xffffffffu, pass);
+    if (m == 0) return;
+    const int leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(cnt_p, static_cast<uint32_t>(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (pass) list[base + __popc(m & ((1u << lane) - 1u))] = key;
+}
+
+struct ScanParams {
+    const uint4 *db;
+    int64_t n;
+    int64_t row_offset;
+    const uint32_t *q;
+    uint64_t *out;        // [splits][nq][k]
+    int64_t nq;
+    int64_t split_steps;  // steps (of SCAN_WARPS bundles) per doc split
+    int wd, wq, C;
+    int k, cap, tq;
+};
+
+inline size_t scan_smem_bytes(int tq, int qwords, int cap) {
+    // cand + thr (8B) ; qs must stay 16-byte aligned -> pad thr to even count
+    const size_t thr_slots = (tq + 1) & ~1;
+    return static_cast<size_t>(tq) * cap * 8 + thr_slots * 8 + static_cast<size_t>(tq) * qwords * 4 + static_cast<size_t>(tq) * 4 + 16;
+}
+
+// WD == 0 selects the generic (runtime widths) body.
+template <int WD, int WQ, int CC>
+__global__ void __launch_bounds__(SCAN_THREADS, (WD == 0 ? 1 : 2))
+scan_topk_kernel(const ScanParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int wd = WD ? WD : p.wd, wq = WD ? WQ : p.wq, C = WD ? CC : p.C;
+    const int qwords = wq * C * 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t q0 = static_cast<int64_t>(blockIdx.y) * p.tq;
+    const int tq = static_cast<int>(min(static_cast<int64_t>(p.tq), p.nq - q0));
+    const int thr_slots = (p.tq + 1) & ~1;
+    // carve with the launch-time tq so offsets match scan_smem_bytes
+    uint64_t *cand = reinterpret_cast<uint64_t *>(smem_raw);
+    uint64_t *thr = cand + static_cast<size_t>(p.tq) * p.cap;
+    uint32_t *qs = reinterpret_cast<uint32_t *>(thr + thr_slots);
+    uint32_t *cnt = qs + static_cast<size_t>(p.tq) * qwords;
+
+    for (int t = threadIdx.x; t < tq * qwords; t += SCAN_THREADS) qs[t] = p.q[q0 * qwords + t];
+    for (int t = threadIdx.x; t < tq; t += SCAN_THREADS) { thr[t] = KEY_INF; cnt[t] = 0; }
+    __syncthreads();
+
+    const int64_t nb = (p.n + 31) >> 5;
+    const int64_t step0 = static_cast<int64_t>(blockIdx.x) * p.split_steps;
+    int64_t b_begin = step0 * SCAN_WARPS;
+    int64_t b_end = min(nb, (step0 + p.split_steps) * SCAN_WARPS);
+    const int64_t bundle_words = static_cast<int64_t>(wd) * C * 32;  // uint4 per bundle
+
+    uint4 cur[WD ? WD * CC : 1];
+    uint4 nxt[WD ? WD * CC : 1];
+    if (WD) {
+        const int64_t b = b_begin + warp;
+        if (b < b_end) {
+#pragma unroll
+            for (int e = 0; e < (WD ? WD * CC : 1); ++e) cur[e] = __ldg(p.db + b * bundle_words + e * 32 + lane);
+        }
+    }
+
+    for (int64_t bs = b_begin; bs < b_end; bs += SCAN_WARPS) {
+        const int64_t b = bs + warp;
+        const bool active = b < b_end;
+        if (WD) {
+            const int64_t bn = b + SCAN_WARPS;
+            if (bn < b_end) {
+#pragma unroll
+                for (int e = 0; e < (WD ? WD * CC : 1); ++e) nxt[e] = __ldg(p.db + bn * bundle_words + e * 32 + lane);
+            }
+        }
+        if (active) {  // warp-uniform
+            const int64_t doc = b * 32 + lane;
+            const bool valid = doc < p.n;
+            const uint64_t gid = static_cast<uint64_t>(p.row_offset + doc);
+            const uint4 *dptr = p.db + b * bundle_words + lane;
+            for (int qi = 0; qi < tq; ++qi) {
+                uint32_t d;
+                if (WD) d = distance_regs<(WD ? WD : 1), (WD ? WQ : 1), (WD ? CC : 1)>(cur, qs + qi * qwords);
+                else d = distance_generic(dptr, wd, C, qs + qi * qwords, wq);
+                const uint64_t key = (static_cast<uint64_t>(d) << 32) | gid;
+                const bool pass = valid && key < thr[qi];
+                push_candidate(pass, key, cand + static_cast<size_t>(qi) * p.cap, cnt + qi, lane);
+            }
+        }
+        if (WD) {
+#pragma unroll
+            for (int e = 0; e < (WD ? WD * CC : 1); ++e) cur[e] = nxt[e];
+        }
+        bool need = false;
+        __syncthreads();
+        for (int qi = threadIdx.x; qi < tq; qi += SCAN_THREADS) need |= cnt[qi] > static_cast<uint32_t>(p.cap - SCAN_THREADS);
+        if (__syncthreads_or(need)) {
+            for (int qi = 0; qi < tq; ++qi)
+                if (cnt[qi] > static_cast<uint32_t>(p.cap - SCAN_THREADS))
+                    compact_list(cand + static_cast<size_t>(qi) * p.cap, cnt + qi, thr + qi, p.k);
+        }
+    }
+    __syncthreads();
+    for (int qi = 0; qi < tq; ++qi) {
+        uint64_t *list = cand + static_cast<size_t>(qi) * p.cap;
+        compact_list(list, cnt + qi, thr + qi, p.k);
+        const int c = static_cast<int>(cnt[qi]);
+        uint64_t *dst = p.out + (static_cast<int64_t>(blockIdx.x) * p.nq + q0 + qi) * p.k;
+        for (int t = threadIdx.x; t < p.k; t += SCAN_THREADS) dst[t] = t < c ? list[t] : KEY_INF;
+        __syncthreads();
+    }
+}
+
+// ----------------------------------------------------------------------------------------------
+// Merge: one CTA per query keeps the K2 = pow2 >= k best keys in the lower half of a 2*K2
+// buffer, streams the parts through the upper half and re-sorts.
+// ----------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+merge_topk_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k, int K2,
+                  uint64_t *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t *buf = reinterpret_cast<uint64_t *>(smem_raw);
+    const int64_t q = blockIdx.x;
+    for (int t = threadIdx.x; t < K2; t += blockDim.x) buf[t] = KEY_INF;
+    const int64_t total = static_cast<int64_t>(parts) * k;
+    for (int64_t base = 0; base < total; base += K2) {
+        for (int t = threadIdx.x; t < K2; t += blockDim.x) {
+            const int64_t e = base + t;
+            uint64_t v = KEY_INF;
+            if (e < total) {
+                const int64_t part = e / k, slot = e % k;
+                v = in[(part * nq + q) * k + slot];
+            }
+            buf[K2 + t] = v;
+        }
+        __syncthreads();
+        bitonic_sort_block(buf, 2 * K2);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < k; t += blockDim.x) out[q * k + t] = buf[t];
+}
+
+__global__ void unpack_keys_kernel(const uint64_t *__restrict__ keys, int64_t count,
+                                   int64_t *__restrict__ dist, int64_t *__restrict__ ids) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= count) return;
+    const uint64_t key = keys[e];
+    if (key == KEY_INF) { dist[e] = -1; ids[e] = -1; }
+    else { dist[e] = static_cast<int64_t>(key >> 32); ids[e] = static_cast<int64_t>(key & 0xFFFFFFFFull); }
+}
+
+// ----------------------------------------------------------------------------------------------
+// Host-side planning shared by xfbq_scan_workspace_bytes and xfbq_scan_topk.
+// ----------------------------------------------------------------------------------------------
+struct ScanPlan {
+    int tq = 1, cap = 0, splits = 1, q_tiles = 1;
+    int64_t split_steps = 1;
+    size_t smem = 0;
+    bool fast = false;
+};
+
+typedef void (*ScanKernel)(const ScanParams);
+
+ScanKernel pick_kernel(int wd, int wq, int C) {
+#define XFBQ_CASE(WD_, WQ_, C_) if (wd == WD_ && wq == WQ_ && C == C_) return scan_topk_kernel<WD_, WQ_, C_>;
+    XFBQ_CASE(3, 4, 1) XFBQ_CASE(3, 4, 2) XFBQ_CASE(3, 4, 4)
+    XFBQ_CASE(4, 4, 1) XFBQ_CASE(4, 4, 2) XFBQ_CASE(4, 4, 4)
+#undef XFBQ_CASE
+    return nullptr;
+}
+
+int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    if (!v || !*v) return dflt;
+    return atoi(v);
+}
+
+int make_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, ScanPlan *plan) {
+    DeviceInfo info;
+    if (int rc = device_info(&info)) return rc;
+    const int C = static_cast<int>(chunks128(dim));
+    const int qwords = wq * C * 4;
+    ScanPlan pl;
+    int cap = 2;
+    while (cap < k + SCAN_THREADS) cap <<= 1;
+    pl.cap = cap;
+    pl.fast = pick_kernel(wd, wq, C) != nullptr && env_int("XFBQ_FORCE_GENERIC", 0) == 0;
+    const size_t budget = static_cast<size_t>(info.smem_optin) - 1024;
+    int tq_max = env_int("XFBQ_TQ", 32);
+    if (tq_max < 1) tq_max = 1;
+    int tq = static_cast<int>(nq < tq_max ? nq : tq_max);
+    while (tq > 1 && scan_smem_bytes(tq, qwords, cap) > budget) --tq;
+    if (scan_smem_bytes(tq, qwords, cap) > budget)
+        return fail(XFBQ_E_UNSUPPORTED, "scan needs %zu bytes of shared memory for dim=%lld k=%d, device offers %zu",
+                    scan_smem_bytes(tq, qwords, cap), static_cast<long long>(dim), k, budget);
+    pl.tq = tq;
+    pl.smem = scan_smem_bytes(tq, qwords, cap);
+    pl.q_tiles = static_cast<int>((nq + tq - 1) / tq);
+    const int64_t steps = (bundles_of(n) + SCAN_WARPS - 1) / SCAN_WARPS;
+    // resident CTAs per SM: limited by shared memory (and 2 by launch bounds for the fast kernels)
+    int occ = static_cast<int>((static_cast<size_t>(info.smem_optin) + 1024) / (pl.smem + 1024));
+    const int occ_cap = pl.fast ? 2 : 1;
+    if (occ > occ_cap) occ = occ_cap;
+    if (occ < 1) occ = 1;
+    const int64_t capacity = static_cast<int64_t>(info.sms) * occ;
+    const int64_t want = pl.q_tiles >= capacity ? 4 * capacity : capacity;
+    int64_t splits = (want + pl.q_tiles - 1) / pl.q_tiles;
+    const int forced = env_int("XFBQ_SPLITS", 0);
+    if (forced > 0) splits = forced;
+    if (splits > steps) splits = steps;
+    if (splits < 1) splits = 1;
+    pl.split_steps = (steps + splits - 1) / splits;
+    if (pl.split_steps < 1) pl.split_steps = 1;
+    pl.splits = static_cast<int>((steps + pl.split_steps - 1) / pl.split_steps);
+    if (pl.splits < 1) pl.splits = 1;
+    *plan = pl;
+    return XFBQ_OK;
+}
+
+int launch_merge(const uint64_t *in, int parts, int64_t nq, int k, uint64_t *out, cudaStream_t st) {
+    int K2 = 32;
+    while (K2 < k) K2 <<= 1;
+    const size_t smem = static_cast<size_t>(2) * K2 * 8;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(merge_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "merge smem opt-in: %s", cudaGetErrorString(e));
+    }
+    merge_topk_kernel<<<static_cast<unsigned>(nq), 256, smem, st>>>(in, parts, nq, k, K2, out);
+    return check_launch("merge_topk_kernel");
+}
+
+template <typename T>
+int quantize_pack_impl(const T *x, int64_t n, int64_t dim, int64_t ld, double scale, int width,
+                       void *out, uint64_t *nonfinite, void *stream) {
+    if (!width_ok(width)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d", width);
+    if (!(scale > 0.0)) return fail(XFBQ_E_INVALID, "scale must be positive, got %g", scale);
+    if (n < 0 || dim < 1 || ld < dim) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld ld=%lld", (long long)n, (long long)dim, (long long)ld);
+    if (dim > (1 << 20)) return fail(XFBQ_E_UNSUPPORTED, "dim %lld too large", (long long)dim);
+    if (n == 0) return XFBQ_OK;
+    if (!x || !out || !nonfinite) return fail(XFBQ_E_INVALID, "null pointer");
+    DeviceInfo info;
+    if (int rc = device_info(&info)) return rc;
+    const int64_t nb = bundles_of(n);
+    int64_t blocks = (nb + QP_WARPS - 1) / QP_WARPS;
+    const int64_t max_blocks = static_cast<int64_t>(info.sms) * 8;
+    if (blocks > max_blocks) blocks = max_blocks;
+    quantize_pack_kernel<T><<<static_cast<unsigned>(blocks), QP_WARPS * 32, 0, static_cast<cudaStream_t>(stream)>>>(
+        x, n, static_cast<int>(dim), ld, scale, width, static_cast<int>(chunks128(dim)),
+        static_cast<uint4 *>(out), reinterpret_cast<unsigned long long *>(nonfinite));
+    return check_launch("quantize_pack_kernel");
+}
+
+template <typename T>
+int quantize_queries_impl(const T *x, int64_t nq, int64_t dim, int64_t ld, double scale, int width,
+                          uint32_t *out, uint64_t *nonfinite, void *stream) {
+    if (!width_ok(width)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d", width);
+    if (!(scale > 0.0)) return fail(XFBQ_E_INVALID, "scale must be positive, got %g", scale);
+    if (nq < 0 || dim < 1 || ld < dim) return fail(XFBQ_E_INVALID, "bad shape nq=%lld dim=%lld ld=%lld", (long long)nq, (long long)dim, (long long)ld);
+    if (dim > (1 << 20)) return fail(XFBQ_E_UNSUPPORTED, "dim %lld too large", (long long)dim);
+    if (nq == 0) return XFBQ_OK;
+    if (!x || !out || !nonfinite) return fail(XFBQ_E_INVALID, "null pointer");
+    const int64_t blocks = (nq * 32 + 255) / 256;
+    quantize_queries_kernel<T><<<static_cast<unsigned>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        x, nq, static_cast<int>(dim), ld, scale, width, static_cast<int>(chunks128(dim)), out,
+        reinterpret_cast<unsigned long long *>(nonfinite));
+    return check_launch("quantize_queries_kernel");
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------- C ABI
+XFBQ_API int xfbq_abi_version(void) { return XFBQ_ABI_VERSION; }
+XFBQ_API const char *xfbq_last_error(void) { return g_err; }
+XFBQ_API int64_t xfbq_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+XFBQ_API int64_t xfbq_chunks128(int64_t dim) { return chunks128(dim); }
+
+XFBQ_API int64_t xfbq_db_bytes(int64_t n, int64_t dim, int width) {
+    return bundles_of(n) * width * chunks128(dim) * 32 * 16;
+}
+
+XFBQ_API int64_t xfbq_query_bytes(int64_t nq, int64_t dim, int width) {
+    return nq * width * chunks128(dim) * 16;
+}
+
+XFBQ_API int64_t xfbq_distance_upper_bound(int64_t dim, int wx, int wy) {
+    return dim * static_cast<int64_t>((1 << wx) - 1) * static_cast<int64_t>((1 << wy) - 1);
+}
+
+XFBQ_API int xfbq_quantize_pack_f32(const float *x, int64_t n, int64_t dim, int64_t ld, double scale,
+                                    int width, void *out, uint64_t *nonfinite, void *stream) {
+    return quantize_pack_impl<float>(x, n, dim, ld, scale, width, out, nonfinite, stream);
+}
+
+XFBQ_API int xfbq_quantize_pack_f64(const double *x, int64_t n, int64_t dim, int64_t ld, double scale,
+                                    int width, void *out, uint64_t *nonfinite, void *stream) {
+    return quantize_pack_impl<double>(x, n, dim, ld, scale, width, out, nonfinite, stream);
+}
+
+XFBQ_API int xfbq_quantize_queries_f32(const float *q, int64_t nq, int64_t dim, int64_t ld, double scale,
+                                       int width, uint32_t *out, uint64_t *nonfinite, void *stream) {
+    return quantize_queries_impl<float>(q, nq, dim, ld, scale, width, out, nonfinite, stream);
+}
+
+XFBQ_API int xfbq_quantize_queries_f64(const double *q, int64_t nq, int64_t dim, int64_t ld, double scale,
+                                       int width, uint32_t *out, uint64_t *nonfinite, void *stream) {
+    return quantize_queries_impl<double>(q, nq, dim, ld, scale, width, out, nonfinite, stream);
+}
+
+XFBQ_API int xfbq_planes_to_bundles(const uint64_t *planes, int64_t n, int64_t dim, int width, void *out,
+                                    void *stream) {
+    if (!width_ok(width)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d", width);
+    if (n < 0 || dim < 1) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld", (long long)n, (long long)dim);
+    if (n == 0) return XFBQ_OK;
+    if (!planes || !out) return fail(XFBQ_E_INVALID, "null pointer");
+    const int C = static_cast<int>(chunks128(dim));
+    const int64_t total = bundles_of(n) * width * C * 32;
+    planes_to_bundles_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        planes, n, static_cast<int>((dim + 63) / 64), width, C, static_cast<uint4 *>(out), total);
+    return check_launch("planes_to_bundles_kernel");
+}
+
+XFBQ_API int xfbq_bundles_to_planes(const void *db, int64_t n, int64_t dim, int width, uint64_t *planes,
+                                    void *stream) {
+    if (!width_ok(width)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d", width);
+    if (n < 0 || dim < 1) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld", (long long)n, (long long)dim);
+    if (n == 0) return XFBQ_OK;
+    if (!planes || !db) return fail(XFBQ_E_INVALID, "null pointer");
+    const int C = static_cast<int>(chunks128(dim));
+    const int64_t total = bundles_of(n) * width * C * 32;
+    bundles_to_planes_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4 *>(db), n, static_cast<int>((dim + 63) / 64), width, C, planes, total);
+    return check_launch("bundles_to_planes_kernel");
+}
+
+XFBQ_API int xfbq_batch_distances(const void *db, int64_t n, int64_t dim, int wd, const uint32_t *q, int wq,
+                                  uint64_t *out, void *stream) {
+    if (!width_ok(wd) || !width_ok(wq)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d/%d", wd, wq);
+    if (n < 0 || dim < 1) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld", (long long)n, (long long)dim);
+    if (n == 0) return XFBQ_OK;
+    if (!db || !q || !out) return fail(XFBQ_E_INVALID, "null pointer");
+    DeviceInfo info;
+    if (int rc = device_info(&info)) return rc;
+    const int C = static_cast<int>(chunks128(dim));
+    const size_t smem = static_cast<size_t>(wq) * C * 16;
+    if (smem > 48 * 1024) return fail(XFBQ_E_UNSUPPORTED, "dim %lld too large for batch_distances", (long long)dim);
+    int64_t blocks = (bundles_of(n) + 7) / 8;
+    const int64_t max_blocks = static_cast<int64_t>(info.sms) * 8;
+    if (blocks > max_blocks) blocks = max_blocks;
+    batch_distances_kernel<<<static_cast<unsigned>(blocks), 256, smem, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4 *>(db), n, wd, C, q, wq, out);
+    return check_launch("batch_distances_kernel");
+}
+
+XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k) {
+    if (!width_ok(wd) || !width_ok(wq) || n < 0 || dim < 1 || nq < 0 || k < 1 || k > XFBQ_MAX_K) {
+        fail(XFBQ_E_INVALID, "bad scan shape");
+        return -1;
+    }
+    if (n == 0 || nq == 0) return 0;
+    ScanPlan pl;
+    if (make_plan(n, dim, wd, nq, wq, k, &pl)) return -1;
+    if (pl.splits <= 1) return 0;
+    return static_cast<int64_t>(pl.splits) * nq * k * 8;
+}
+
+XFBQ_API int xfbq_scan_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, int32_t out[6]) {
+    if (!width_ok(wd) || !width_ok(wq) || n < 1 || dim < 1 || nq < 1 || k < 1 || k > XFBQ_MAX_K || !out)
+        return fail(XFBQ_E_INVALID, "bad scan shape");
+    ScanPlan pl;
+    if (int rc = make_plan(n, dim, wd, nq, wq, k, &pl)) return rc;
+    out[0] = pl.tq; out[1] = pl.q_tiles; out[2] = pl.splits; out[3] = pl.cap;
+    out[4] = pl.fast ? 1 : 0; out[5] = static_cast<int32_t>(pl.smem);
+    return XFBQ_OK;
+}
+
+XFBQ_API int xfbq_scan_topk(const void *db, int64_t n, int64_t dim, int wd, const uint32_t *q, int64_t nq,
+                            int wq, int k, int64_t row_offset, uint64_t *keys_out, void *workspace,
+                            int64_t workspace_bytes, void *stream) {
+    if (!width_ok(wd) || !width_ok(wq)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d/%d", wd, wq);
+    if (n < 0 || dim < 1 || nq < 0) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld nq=%lld", (long long)n, (long long)dim, (long long)nq);
+    if (k < 1) return fail(XFBQ_E_INVALID, "k must be >= 1, got %d", k);
+    if (k > XFBQ_MAX_K) return fail(XFBQ_E_UNSUPPORTED, "k=%d exceeds XFBQ_MAX_K=%d", k, XFBQ_MAX_K);
+    if (row_offset < 0 || row_offset + n > (1ll << 32)) return fail(XFBQ_E_UNSUPPORTED, "row ids must fit 32 bits");
+    if (xfbq_distance_upper_bound(dim, wd, wq) >= (1ll << 31)) return fail(XFBQ_E_UNSUPPORTED, "distance range exceeds 31 bits");
+    if (nq == 0) return XFBQ_OK;
+    if (!keys_out) return fail(XFBQ_E_INVALID, "null keys_out");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (n == 0) {
+        cudaError_t e = cudaMemsetAsync(keys_out, 0xFF, static_cast<size_t>(nq) * k * 8, st);
+        if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
+        return XFBQ_OK;
+    }
+    if (!db || !q) return fail(XFBQ_E_INVALID, "null pointer");
+    ScanPlan pl;
+    if (int rc = make_plan(n, dim, wd, nq, wq, k, &pl)) return rc;
+    const int64_t need = pl.splits <= 1 ? 0 : static_cast<int64_t>(pl.splits) * nq * k * 8;
+    if (need > 0 && (!workspace || workspace_bytes < need))
+        return fail(XFBQ_E_INVALID, "workspace too small: need %lld bytes, got %lld", (long long)need, (long long)workspace_bytes);
+    const int C = static_cast<int>(chunks128(dim));
+    ScanKernel kern = pl.fast ? pick_kernel(wd, wq, C) : nullptr;
+    if (!kern) kern = scan_topk_kernel<0, 0, 0>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem));
+    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "scan smem opt-in (%zu bytes): %s", pl.smem, cudaGetErrorString(e));
+    ScanParams p;
+    p.db = static_cast<const uint4 *>(db);
+    p.n = n;
+    p.row_offset = row_offset;
+    p.q = q;
+    p.out = pl.splits <= 1 ? keys_out : static_cast<uint64_t *>(workspace);
+    p.nq = nq;
+    p.split_steps = pl.split_steps;
+    p.wd = wd; p.wq = wq; p.C = C;
+    p.k = k; p.cap = pl.cap; p.tq = pl.tq;
+    dim3 grid(static_cast<unsigned>(pl.splits), static_cast<unsigned>(pl.q_tiles));
+    if (pl.q_tiles > 65535) return fail(XFBQ_E_UNSUPPORTED, "too many query tiles (%d); split the batch", pl.q_tiles);
+    kern<<<grid, SCAN_THREADS, pl.smem, st>>>(p);
+    if (int rc = check_launch("scan_topk_kernel")) return rc;
+    if (pl.splits > 1) return launch_merge(static_cast<const uint64_t *>(workspace), pl.splits, nq, k, keys_out, st);
+    return XFBQ_OK;
+}
+
+XFBQ_API int xfbq_merge_topk(const uint64_t *keys_in, int parts, int64_t nq, int k, uint64_t *keys_out,
+                             void *stream) {
+    if (parts < 1 || nq < 0 || k < 1) return fail(XFBQ_E_INVALID, "bad merge shape parts=%d nq=%lld k=%d", parts, (long long)nq, k);
+    if (k > XFBQ_MAX_K) return fail(XFBQ_E_UNSUPPORTED, "k=%d exceeds XFBQ_MAX_K=%d", k, XFBQ_MAX_K);
+    if (nq == 0) return XFBQ_OK;
+    if (!keys_in || !keys_out) return fail(XFBQ_E_INVALID, "null pointer");
+    return launch_merge(keys_in, parts, nq, k, keys_out, static_cast<cudaStream_t>(stream));
+}
+
+XFBQ_API int xfbq_unpack_keys(const uint64_t *keys, int64_t count, int64_t *dist, int64_t *ids, void *stream) {
+    if (count < 0) return fail(XFBQ_E_INVALID, "negative count");
+    if (count == 0) return XFBQ_OK;
+    if (!keys || !dist || !ids) return fail(XFBQ_E_INVALID, "null pointer");
+    unpack_keys_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(keys, count, dist, ids);
+    return check_launch("unpack_keys_kernel");
+}

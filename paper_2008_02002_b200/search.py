@@ -1,0 +1,210 @@
+"""K-select front end: `k_select` (reference search.py:188-232) and the batched
+`search(index, queries, k) -> (scores, indices)` the north star adds.
+
+`search` is defined as the per-query composition of reference calls:
+    pq = quantize_vector(float64(q), query_bits, scale); d = batch_distances(packed, pq)
+    order = lexsort((arange(n), d))[:min(k, n)]; scores, indices = d[order], order
+and is computed by one fused scan+top-K kernel launch per query batch: no score matrix
+reaches HBM.  Keys are (distance << 32 | row id), so ties resolve to the lower row id
+(search.py:129-131).
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .bitplane import PackedMatrix, _is_torch, _stream_ptr, quantize_queries, quantize_vector
+from .distance import batch_distances_device, decode_inner_product_values, distance_upper_bound
+from .errors import DimensionMismatchError, InvalidInputError
+from .index import Index
+
+MAX_K = 4096          # XFBQ_MAX_K
+_QUERY_BATCH = 16384  # queries per scan launch (bounds grid.y and the partial-result workspace)
+SCAN_EVENTS = None    # bench hook: set to a list to collect (start, end) CUDA events around each scan launch
+
+
+@dataclass(frozen=True)
+class SearchRequest:
+    """search.py:33-51."""
+
+    query: np.ndarray
+    k: int
+    extra_distance: int = 0
+
+    def __post_init__(self):
+        query = np.ascontiguousarray(self.query, dtype=np.float64)
+        object.__setattr__(self, "query", query)
+        if query.ndim != 1:
+            raise InvalidInputError("query must be a 1-D vector")
+        if not np.all(np.isfinite(query)):
+            raise InvalidInputError("query contains non-finite entries")
+        if self.k < 1:
+            raise InvalidInputError(f"k must be >= 1, got {self.k}")
+        if self.extra_distance < 0:
+            raise InvalidInputError(f"extra_distance must be >= 0, got {self.extra_distance}")
+
+
+@dataclass(frozen=True)
+class SearchResult:
+    """search.py:54-67."""
+
+    hits: list
+    candidate_count: int
+    threshold_distance: int
+    approximate: bool = False
+    stage_seconds: dict | None = field(default=None, compare=False)
+
+
+def scan_topk_device(packed: PackedMatrix, qwords, nq: int, query_bits: int, k: int, row_offset: int = 0):
+    """Launch the fused scan+top-K on device-resident query words (query layout).
+    Returns an int64 CUDA tensor [nq, k] holding the uint64 keys bit-for-bit
+    (distance << 32 | row_offset + row; 0xFFFF... for empty slots)."""
+    torch = _native.require_cuda()
+    L = _native.lib()
+    dev = packed.codes.device
+    with torch.cuda.device(dev):
+        keys = torch.empty((nq, k), dtype=torch.int64, device=dev)
+        if nq == 0:
+            return keys
+        C = (packed.dim + 127) // 128
+        words_per_query = query_bits * 4 * C  # int32 elements
+        st = _stream_ptr(torch)
+        for q0 in range(0, nq, _QUERY_BATCH):
+            qn = min(_QUERY_BATCH, nq - q0)
+            ws_bytes = int(L.xfbq_scan_workspace_bytes(packed.count, packed.dim, packed.width, qn, query_bits, k))
+            if ws_bytes < 0:
+                _native.check(_native.E_UNSUPPORTED if k > MAX_K else _native.E_INVALID)
+            ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
+            qptr = qwords.data_ptr() + q0 * words_per_query * 4
+            if SCAN_EVENTS is not None:
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record()
+            _native.check(L.xfbq_scan_topk(packed.codes.data_ptr(), packed.count, packed.dim, packed.width,
+                                           qptr, qn, query_bits, k, int(row_offset),
+                                           keys.data_ptr() + q0 * k * 8, ws.data_ptr(), ws_bytes, st))
+            if SCAN_EVENTS is not None:
+                ev[1].record()
+                SCAN_EVENTS.append(ev)
+            # ws is stream-ordered: the caching allocator reuses it only on this stream
+    return keys
+
+
+def unpack_keys_device(keys):
+    """int64 key tensor -> (distances int64, row ids int64) on the device (-1 for empty slots)."""
+    torch = _native.require_cuda()
+    L = _native.lib()
+    with torch.cuda.device(keys.device):
+        d = torch.empty_like(keys)
+        i = torch.empty_like(keys)
+        _native.check(L.xfbq_unpack_keys(keys.data_ptr(), keys.numel(), d.data_ptr(), i.data_ptr(),
+                                         _stream_ptr(torch)))
+    return d, i
+
+
+def _check_queries(index: Index, queries):
+    if queries.ndim != 2:
+        raise InvalidInputError("queries must be an (nq, dim) matrix")
+    if queries.shape[1] != index.params.dim:
+        raise DimensionMismatchError(f"query dim {queries.shape[1]} != index dim {index.params.dim}")
+
+
+def search_device(index: Index, queries, k: int, row_offset: int = 0):
+    """Batched search returning device tensors (keys int64 [nq, min(k, n)]).
+    `queries`: host array or CUDA tensor (nq, dim), float32/float64."""
+    if k < 1:
+        raise InvalidInputError(f"k must be >= 1, got {k}")
+    if not _is_torch(queries):
+        queries = np.asarray(queries)
+        if queries.dtype != np.float32:
+            queries = np.ascontiguousarray(queries, dtype=np.float64)
+    _check_queries(index, queries)
+    p = index.params
+    kk = min(int(k), index.n)
+    torch = _native.require_cuda()
+    with torch.cuda.device(index.packed.codes.device):
+        if kk == 0 or queries.shape[0] == 0:
+            return torch.empty((queries.shape[0], kk), dtype=torch.int64, device=index.packed.codes.device)
+        qwords = quantize_queries(queries, p.query_bits, p.scale)
+        return scan_topk_device(index.packed, qwords, queries.shape[0], p.query_bits, kk, row_offset)
+
+
+def search(index: Index, queries, k: int):
+    """Exhaustive top-k for a batch of float queries.
+
+    Returns ``(scores, indices)``: int64 arrays [nq, min(k, n)]; ``scores`` are the integer
+    XOR/popcount distances (smaller = more similar), rows ordered by (distance asc, row id
+    asc).  Host arrays (numpy, or pinned/pageable CPU tensors) in -> numpy out, with one H2D
+    copy of the queries and one D2H copy of the results; CUDA tensors in -> CUDA tensors out."""
+    keys = search_device(index, queries, k)
+    d, i = unpack_keys_device(keys)
+    if _is_torch(queries) and queries.is_cuda:
+        return d, i
+    return d.cpu().numpy(), i.cpu().numpy()
+
+
+def _originals_device(index: Index):
+    torch = _native.require_cuda()
+    cached = getattr(index, "_originals_dev", None)
+    if cached is None:
+        o = index.originals
+        cached = o if _is_torch(o) else torch.from_numpy(np.asarray(o)).to(index.packed.codes.device)
+        object.__setattr__(index, "_originals_dev", cached)
+    return cached
+
+
+def k_select(index: Index, request: SearchRequest, collect_timing: bool = False) -> SearchResult:
+    """search.py:188-232, one query.  Without originals the hits come straight from the fused
+    scan+top-K (ranking by quantized similarity, `approximate=True`); with originals the
+    candidates d <= kth + extra are re-ranked by float64 dot products on the device."""
+    p = index.params
+    if request.query.shape[0] != p.dim:
+        raise DimensionMismatchError(f"query dim {request.query.shape[0]} != index dim {p.dim}")
+    timings = {} if collect_timing else None
+    if index.n == 0:
+        return SearchResult(hits=[], candidate_count=0, threshold_distance=0,
+                            approximate=index.originals is None, stage_seconds=timings)
+    torch = _native.require_cuda()
+    sync = torch.cuda.synchronize if collect_timing else (lambda: None)
+    kk = min(request.k, index.n)
+    upper = distance_upper_bound(p.dim, p.doc_bits, p.query_bits)
+
+    t0 = time.perf_counter()
+    packed_query = quantize_vector(request.query, p.query_bits, p.scale)
+    qwords = packed_query.device_words()
+    sync(); t1 = time.perf_counter()
+    dists = batch_distances_device(index.packed, packed_query)          # int64[n] on device
+    keys = scan_topk_device(index.packed, qwords.view(torch.int32), 1, p.query_bits, kk)
+    top_d, top_i = unpack_keys_device(keys)
+    top_d, top_i = top_d[0].cpu().numpy(), top_i[0].cpu().numpy()
+    sync(); t2 = time.perf_counter()
+    threshold = int(top_d[kk - 1]) + int(request.extra_distance)        # search.py:211-213
+    cand_mask = dists <= min(threshold, upper)
+    candidate_count = int(cand_mask.sum())
+    sync(); t3 = time.perf_counter()
+    if index.originals is None:
+        sims = decode_inner_product_values(top_d, p.dim, p.doc_bits, p.query_bits)
+        sims /= p.scale * p.scale                                       # search.py:167-171
+        hits = [(int(i), float(s)) for i, s in zip(top_i, sims)]
+        approximate = True
+    else:
+        cand = torch.nonzero(cand_mask).flatten()
+        rows = _originals_device(index)[cand].to(torch.float64)
+        q64 = torch.from_numpy(request.query).to(rows.device)
+        sims = (rows @ q64).cpu().numpy()                               # search.py:153-157
+        ids = cand.cpu().numpy()
+        order = np.lexsort((ids, -sims))[: request.k]                   # search.py:129-131
+        hits = [(int(ids[i]), float(sims[i])) for i in order]
+        approximate = False
+    sync(); t4 = time.perf_counter()
+    if index.ids is not None:
+        hits = [(int(index.ids[row]), sim) for row, sim in hits]
+    if collect_timing:
+        timings["quantize_query"] = t1 - t0
+        timings["distances"] = t2 - t1
+        timings["histogram_gather"] = t3 - t2
+        timings["refine"] = t4 - t3
+    return SearchResult(hits=hits, candidate_count=candidate_count, threshold_distance=threshold,
+                        approximate=approximate, stage_seconds=timings)

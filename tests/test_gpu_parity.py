@@ -1,0 +1,250 @@
+"""GPU parity tests: the CUDA path (through the Python drop-in API -> ctypes -> C ABI) against
+the golden outputs of the unmodified reference (tests/golden, oracle/gen_golden.py) and against
+the CPU oracle on the same seeded inputs.  Integer/byte/index work: bit-exact.
+
+Reference test citations are paths under /root/reference/pkg/tests.
+"""
+import os
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_2008_02002_b200 as xb
+from oracle import xfbq_oracle as xo
+from tests._golden import SYNTH, load, sha, small_cases, synth_case
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _quiet():
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        yield
+
+
+def _codes_of(packed):
+    return xb.unpack_matrix(packed)
+
+
+# ------------------------------------------------------------------ quantizer (kernel 1)
+def test_quantize_values_golden_f64_all_widths():
+    z = load("quant_values")
+    xs = z["xs64"]
+    for w in range(1, 9):
+        pm = xb.quantize_matrix(xs[None, :], w, 1.0)
+        assert np.array_equal(_codes_of(pm)[0], z[f"codes64_w{w}"]), w
+        # row-major many-rows form too (each value its own row, dim 1)
+        pm = xb.quantize_matrix(xs[:, None], w, 1.0)
+        assert np.array_equal(_codes_of(pm)[:, 0], z[f"codes64_w{w}"]), w
+
+
+def test_quantize_values_golden_f32_scaled():
+    """float32 input widened in-kernel to float64 then scaled (bitplane.py:229-232), including
+    denormals, +-0, saturating values and grid neighbours (test_quant.py:132-143)."""
+    z = load("quant_values")
+    xs = z["xs32"]
+    assert xs.dtype == np.float32
+    for w in range(1, 9):
+        for si, s in enumerate(z["scales"]):
+            pm = xb.quantize_matrix(xs[None, :], w, float(s))
+            assert np.array_equal(_codes_of(pm)[0], z[f"codes32_w{w}_s{si}"]), (w, si)
+
+
+def test_worked_examples():
+    # test_quant.py:74-87 / test_bitplane.py:116-123
+    pv = xb.quantize_vector(np.array([0.3, -0.999]), 3, 1.0)
+    assert [int(pv.planes[b, 0]) for b in (2, 1, 0)] == [0b10, 0b11, 0b10]
+    assert _codes_of(xb.quantize_matrix(np.array([[0.3, 0.0, -0.999]]), 3))[0].tolist() == [0b010, 0b011, 0b111]
+    # test_quant.py:114-118 saturation
+    assert _codes_of(xb.quantize_matrix(np.array([[1.0, 1.5, 100.0]]), 4))[0].tolist() == [0, 0, 0]
+    assert _codes_of(xb.quantize_matrix(np.array([[-1.0, -2.5, -1e9]]), 4))[0].tolist() == [15, 15, 15]
+    z = load("worked")
+    # test_search.py:129-155: distances [20, 17, 26, 17, 23], tie broken by id
+    params = xb.QuantParams(dim=1, scale=1.0, doc_bits=3, query_bits=3)
+    idx = xb.build_index(z["pipeline_values"], params, keep_originals=False)
+    d = xb.batch_distances(idx.packed, xb.quantize_vector(np.array([0.375]), 3, 1.0))
+    assert d.dtype == np.uint64 and d.tolist() == [20, 17, 26, 17, 23]
+    scores, ids = xb.search(idx, np.array([[0.375]]), 2)
+    assert scores.tolist() == [[17, 17]] and ids.tolist() == [[1, 3]]
+    res = xb.k_select(idx, xb.SearchRequest(query=np.array([0.375]), k=2))
+    assert [h[0] for h in res.hits] == [1, 3] and res.approximate
+    assert res.threshold_distance == 17 and res.candidate_count == 2
+    # test_distance.py:30-35  55 / 40
+    x = xb.pack_matrix(np.array([[0b010, 0b010]], dtype=np.uint8), 3)
+    y = xb.pack_matrix(np.array([[0b010, 0b111]], dtype=np.uint8), 3)
+    assert int(xb.batch_distances(x, y.row(0))[0]) == 55
+    assert int(xb.batch_distances(x, x.row(0))[0]) == 40
+
+
+def test_small_cases_everything_bit_exact():
+    """84 ragged cases: dims {1..513} x widths {(3,4),(4,4),(8,8),(1,8),(2,1),(5,3)}: planes,
+    query planes, full distances, top-k (with exact ties), decoded sims, threshold, candidates."""
+    count = 0
+    for c in small_cases():
+        params = xb.QuantParams(dim=c["dim"], scale=c["scale"], doc_bits=c["wd"], query_bits=c["wq"])
+        idx = xb.build_index(c["docs"], params, keep_originals=False)
+        assert np.array_equal(idx.packed.planes, c["planes"]), c["ci"]
+        assert idx.packed.nbytes == c["planes"].nbytes
+        for qi in range(c["nq"]):
+            pq = xb.quantize_vector(c["queries"][qi], c["wq"], c["scale"])
+            assert np.array_equal(pq.planes, c["qplanes"][qi]), (c["ci"], qi)
+            assert np.array_equal(xb.batch_distances(idx.packed, pq), c["full"][qi]), (c["ci"], qi)
+        scores, ids = xb.search(idx, c["queries"], c["k"])
+        assert scores.shape == c["dists"].shape
+        assert np.array_equal(scores.astype(np.uint64), c["dists"]), c["ci"]
+        assert np.array_equal(ids, c["ids"]), c["ci"]
+        res = xb.k_select(idx, xb.SearchRequest(query=c["queries"][0], k=c["k"]))
+        assert [h[0] for h in res.hits] == c["ids"][0].tolist()
+        assert [h[1] for h in res.hits] == c["sims"][0].tolist()
+        assert res.threshold_distance == int(c["thr"][0]) and res.candidate_count == int(c["cand"][0])
+        # a PackedMatrix rebuilt from reference planes scans identically (layout conversion)
+        pm = xb.PackedMatrix(c["planes"], c["dim"])
+        idx2 = xb.Index(params=params, packed=pm, originals=None)
+        s2, i2 = xb.search(idx2, c["queries"], c["k"])
+        assert np.array_equal(s2, scores) and np.array_equal(i2, ids)
+        count += 1
+    assert count == 84
+
+
+@pytest.mark.parametrize("name", SYNTH)
+def test_synthetic_configs_match_reference(name):
+    """Config-shaped synthetic corpora (reference generator, seeds in the fixture): packed planes
+    hash, top-k distances and ids for every query equal the unmodified reference's."""
+    c = synth_case(name)
+    z = c["z"]
+    params = xb.QuantParams(dim=c["dim"], scale=c["scale"], doc_bits=c["wd"], query_bits=c["wq"])
+    idx = xb.build_index(c["docs"], params, keep_originals=False)
+    planes = idx.packed.planes
+    assert sha(planes) == str(z["planes_sha"])
+    assert np.array_equal(planes[:, :, :64], z["planes_head"])
+    scores, ids = xb.search(idx, c["queries"], c["k"])
+    assert np.array_equal(scores.astype(np.uint64), z["dists"])
+    assert np.array_equal(ids, z["ids"])
+    # float64 queries give the same answer (float32 -> float64 is exact)
+    s64, i64 = xb.search(idx, c["queries"].astype(np.float64), c["k"])
+    assert np.array_equal(s64, scores) and np.array_equal(i64, ids)
+    for qi in (0, c["nq"] - 1):
+        res = xb.k_select(idx, xb.SearchRequest(query=c["queries"][qi], k=c["k"]))
+        assert [h[0] for h in res.hits] == z["ids"][qi].tolist()
+        assert [h[1] for h in res.hits] == z["sims"][qi].tolist()
+        assert res.threshold_distance == int(z["thr"][qi]) and res.candidate_count == int(z["cand"][qi])
+
+
+@pytest.mark.parametrize("env", [{"XFBQ_FORCE_GENERIC": "1"}, {"XFBQ_SPLITS": "1"}, {"XFBQ_SPLITS": "7"},
+                                 {"XFBQ_TQ": "1"}, {"XFBQ_TQ": "5", "XFBQ_SPLITS": "3"}])
+def test_scan_plans_agree(env, monkeypatch):
+    """Every launch plan (generic/specialised kernel, query-tile size, document splits) yields the
+    same keys: the order on (distance, id) is total, so the result is partition independent."""
+    c = synth_case("cfg4_40k_256_w4")
+    z = c["z"]
+    params = xb.QuantParams(dim=c["dim"], scale=c["scale"], doc_bits=c["wd"], query_bits=c["wq"])
+    idx = xb.build_index(c["docs"], params, keep_originals=False)
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    scores, ids = xb.search(idx, c["queries"], c["k"])
+    assert np.array_equal(scores.astype(np.uint64), z["dists"]) and np.array_equal(ids, z["ids"])
+
+
+def test_edge_cases():
+    """k > n, empty index, dim mismatch, non-finite, bad scale (test_search.py:205-222,
+    test_distance.py:143-153)."""
+    params = xb.QuantParams(dim=5, scale=1.0, doc_bits=3, query_bits=4)
+    idx = xb.build_index(np.zeros((3, 5), dtype=np.float32), params, keep_originals=False)
+    scores, ids = xb.search(idx, np.zeros((2, 5)), 10)
+    assert scores.shape == (2, 3) and ids.tolist() == [[0, 1, 2], [0, 1, 2]]
+    res = xb.k_select(idx, xb.SearchRequest(query=np.zeros(5), k=10))
+    assert len(res.hits) == 3
+    empty = xb.build_index(np.zeros((0, 5), dtype=np.float32), params, keep_originals=False)
+    assert empty.n == 0
+    s, i = xb.search(empty, np.zeros((2, 5)), 4)
+    assert s.shape == (2, 0)
+    res = xb.k_select(empty, xb.SearchRequest(query=np.zeros(5), k=3))
+    assert res.hits == [] and res.candidate_count == 0 and res.threshold_distance == 0
+    assert xb.batch_distances(empty.packed, xb.quantize_vector(np.zeros(5), 4)).shape == (0,)
+    with pytest.raises(xb.DimensionMismatchError):
+        xb.search(idx, np.zeros((1, 6)), 1)
+    with pytest.raises(xb.DimensionMismatchError):
+        xb.k_select(idx, xb.SearchRequest(query=np.zeros(6), k=1))
+    with pytest.raises(xb.DimensionMismatchError):
+        xb.batch_distances(idx.packed, xb.quantize_vector(np.zeros(6), 4))
+    with pytest.raises(xb.InvalidInputError):
+        xb.batch_distances(idx.packed, xb.quantize_vector(np.zeros(5), 4), out=np.zeros(4, dtype=np.uint64))
+    with pytest.raises(xb.InvalidInputError):
+        xb.build_index(np.array([[0.1, np.inf, 0, 0, 0]], dtype=np.float32), params)
+    with pytest.raises(xb.InvalidInputError):
+        xb.quantize_matrix(np.array([[1e300, 1.0]]), 3, 1e300)  # scaled value overflows to inf
+    with pytest.raises(xb.InvalidInputError):
+        xb.search(idx, np.zeros((1, 5)), 0)
+    with pytest.raises(xb.InvalidInputError):
+        xb.PackedMatrix(np.full((3, 1, 2), 1 << 40, dtype=np.uint64), 5)  # padding bits set
+
+
+def test_k_select_with_originals_and_external_ids():
+    """Full pipeline with float refine (search.py:153-157): same ids as the CPU composition,
+    sims to 1e-12 (float64 summation order differs between BLAS and the GPU)."""
+    c = synth_case("cfg3_50k_200_w4")
+    params = xb.QuantParams(dim=c["dim"], scale=c["scale"], doc_bits=c["wd"], query_bits=c["wq"])
+    ext = np.arange(c["n"], dtype=np.int64) * 3 + 7
+    idx = xb.build_index(c["docs"], params, ids=ext)
+    planes = xo.c_quantize_matrix(c["docs"], c["wd"], c["scale"])
+    docs64 = c["docs"].astype(np.float64)
+    for qi in range(4):
+        q = c["queries"][qi].astype(np.float64)
+        extra = 300
+        res = xb.k_select(idx, xb.SearchRequest(query=q, k=10, extra_distance=extra), collect_timing=True)
+        d = xo.c_batch_distances(planes, xo.np_quantize_vector(q, c["wq"], c["scale"]))
+        thr = int(np.sort(d)[9]) + extra
+        cand = np.flatnonzero(d <= thr)
+        sims = docs64[cand] @ q
+        order = np.lexsort((cand, -sims))[:10]
+        assert res.threshold_distance == thr and res.candidate_count == cand.size and not res.approximate
+        assert [h[0] for h in res.hits] == ext[cand[order]].tolist()
+        assert np.allclose([h[1] for h in res.hits], sims[order], rtol=0, atol=1e-12)
+        assert set(res.stage_seconds) == {"quantize_query", "distances", "histogram_gather", "refine"}
+
+
+def test_merge_topk_kernel_against_numpy():
+    import torch
+    from paper_2008_02002_b200 import _native
+    L = _native.lib()
+    rng = np.random.default_rng(5)
+    for parts, nq, k in [(1, 3, 1), (2, 5, 10), (8, 4, 100), (37, 2, 1000), (300, 3, 100), (3, 2, 4096)]:
+        raw = rng.integers(0, 1 << 40, size=(parts, nq, k), dtype=np.uint64)
+        raw[rng.random(raw.shape) < 0.1] = np.uint64(0xFFFFFFFFFFFFFFFF)
+        raw.sort(axis=2)
+        dev = torch.from_numpy(raw.view(np.int64)).cuda()
+        out = torch.empty((nq, k), dtype=torch.int64, device="cuda")
+        _native.check(L.xfbq_merge_topk(dev.data_ptr(), parts, nq, k, out.data_ptr(), 0))
+        torch.cuda.synchronize()
+        want = np.sort(raw.transpose(1, 0, 2).reshape(nq, parts * k), axis=1)[:, :k]
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), want), (parts, nq, k)
+
+
+def test_large_k_and_sharded_equals_single():
+    """top-1000 (config-5 shaped) and the multi-GPU composition on one device: shards scanned with
+    row offsets then merged equal the single scan equal the reference."""
+    import torch
+    from paper_2008_02002_b200 import _native
+    from paper_2008_02002_b200.search import scan_topk_device, unpack_keys_device
+    c = synth_case("cfg5_20k_512_w4")
+    z = c["z"]
+    params = xb.QuantParams(dim=c["dim"], scale=c["scale"], doc_bits=c["wd"], query_bits=c["wq"])
+    idx = xb.build_index(c["docs"], params, keep_originals=False)
+    scores, ids = xb.search(idx, c["queries"], c["k"])
+    assert np.array_equal(scores.astype(np.uint64), z["dists"]) and np.array_equal(ids, z["ids"])
+    L = _native.lib()
+    G = 3
+    per = -(-c["n"] // G)
+    qwords = xb.quantize_queries(c["queries"], c["wq"], c["scale"])
+    parts = []
+    for g in range(G):
+        lo, hi = g * per, min(c["n"], (g + 1) * per)
+        shard = xb.quantize_matrix(c["docs"][lo:hi], c["wd"], c["scale"])
+        parts.append(scan_topk_device(shard, qwords, c["nq"], c["wq"], c["k"], row_offset=lo))
+    stacked = torch.stack(parts).contiguous()
+    out = torch.empty_like(parts[0])
+    _native.check(L.xfbq_merge_topk(stacked.data_ptr(), G, c["nq"], c["k"], out.data_ptr(), 0))
+    d, i = unpack_keys_device(out)
+    assert np.array_equal(d.cpu().numpy().astype(np.uint64), z["dists"]) and np.array_equal(i.cpu().numpy(), z["ids"])

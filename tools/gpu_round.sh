@@ -1,0 +1,19 @@
+#!/bin/bash
+# One GPU session: smoke, microbench, parity tests, bench, ncu launch list + full capture.
+# Usage (under gpurun): bash tools/gpu_round.sh [stages...]   stages: smoke micro tests bench ncu ncufull
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+STAGES="${@:-smoke micro tests bench ncu ncufull}"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
+for s in $STAGES; do
+  case $s in
+    smoke) timeout 600 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" ;;
+    micro) timeout 120 tools/bin/microbench > gpurun_out/microbench.jsonl 2>&1; echo "micro rc=$?" ;;
+    tests) timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "tests rc=$?"; tail -5 gpurun_out/pytest_gpu.log ;;
+    bench) timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json ;;
+    ncu) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
+           python bench.py --steps 1 --warmup 1 --nq 2048 --no-cpu-baseline --no-extras > gpurun_out/ncu_bench.log 2>&1; echo "ncu rc=$?" ;;
+    ncufull) timeout 900 ncu --set full --clock-control none --import-source on -k regex:scan_topk -c 3 -f -o gpurun_out/prof_scan \
+           python bench.py --steps 1 --warmup 1 --nq 2048 --no-cpu-baseline > gpurun_out/ncufull.log 2>&1; echo "ncufull rc=$?" ;;
+  esac
+done
