@@ -152,7 +152,9 @@ def run_ours(a):
     import torch.distributed as dist
 
     import paper_2008_02002_b200 as xb
-    from paper_2008_02002_b200 import _native, search as xsearch
+    import importlib
+    from paper_2008_02002_b200 import _native
+    xsearch = importlib.import_module("paper_2008_02002_b200.search")
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

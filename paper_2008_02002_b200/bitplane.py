@@ -231,7 +231,8 @@ def quantize_to_device(values, width: int, scale: float, queries: bool):
         else:
             fn = L.xfbq_quantize_pack_f32 if f32 else L.xfbq_quantize_pack_f64
             dst = out.data_ptr() + int(L.xfbq_db_bytes(row0, dim, width))  # row0 is a multiple of 32
-        _native.check(fn(chunk.data_ptr(), chunk.shape[0], dim, chunk.stride(0), scale, width, dst,
+        ld = chunk.stride(0) if chunk.shape[0] > 1 else dim
+        _native.check(fn(chunk.data_ptr(), chunk.shape[0], dim, ld, scale, width, dst,
                          bad.data_ptr(), st))
 
     if on_device:
