@@ -14,6 +14,6 @@ for s in $STAGES; do
     ncu) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
            python bench.py --steps 1 --warmup 1 --nq 2048 --no-cpu-baseline --no-extras > gpurun_out/ncu_bench.log 2>&1; echo "ncu rc=$?" ;;
     ncufull) timeout 900 ncu --set full --clock-control none --import-source on -k regex:scan_topk -c 3 -f -o gpurun_out/prof_scan \
-           python bench.py --steps 1 --warmup 1 --nq 2048 --no-cpu-baseline > gpurun_out/ncufull.log 2>&1; echo "ncufull rc=$?" ;;
+           python bench.py --steps 1 --warmup 1 --nq 512 --no-cpu-baseline > gpurun_out/ncufull.log 2>&1; echo "ncufull rc=$?" ;;
   esac
 done
