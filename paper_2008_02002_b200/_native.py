@@ -46,7 +46,7 @@ def _nvcc() -> str | None:
 def needs_build() -> bool:
     if not LIB.exists():
         return True
-    newest = max(SRC.stat().st_mtime, HEADER.stat().st_mtime)
+    newest = max([HEADER.stat().st_mtime] + [f.stat().st_mtime for f in SRC.parent.glob("*.cu*")])
     return LIB.stat().st_mtime < newest
 
 

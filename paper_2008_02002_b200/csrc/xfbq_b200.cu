@@ -447,6 +447,53 @@ merge_topk_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k,
     for (int t = threadIdx.x; t < k; t += blockDim.x) out[q * k + t] = buf[t];
 }
 
+// Tree merge: one CTA per (group of up to G parts, query).  Every part row is sorted, so two
+// rows A, B of length K2 reduce to the K2 smallest of their union by c_i = min(A_i, B_{K2-1-i})
+// (a bitonic sequence) followed by log2(K2) bitonic-merge stages; log2(G) rounds leave the answer
+// in row 0.  Far fewer barrier stages than re-sorting, so single-query latency stays small.
+__global__ void __launch_bounds__(512)
+merge_tree_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k, int K2, int G,
+                  uint64_t *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t *buf = reinterpret_cast<uint64_t *>(smem_raw);
+    const int64_t q = blockIdx.y;
+    const int p0 = blockIdx.x * G;
+    int rows = min(G, parts - p0);
+    int active = 1;
+    while (active < rows) active <<= 1;
+    for (int idx = threadIdx.x; idx < active * K2; idx += blockDim.x) {
+        const int r = idx / K2, i = idx - r * K2;
+        buf[idx] = (r < rows && i < k) ? in[((static_cast<int64_t>(p0) + r) * nq + q) * k + i] : KEY_INF;
+    }
+    __syncthreads();
+    while (active > 1) {
+        const int half = active >> 1;
+        for (int idx = threadIdx.x; idx < half * K2; idx += blockDim.x) {
+            const int r = idx / K2, i = idx - r * K2;
+            const uint64_t a = buf[r * K2 + i], b = buf[(r + half) * K2 + (K2 - 1 - i)];
+            buf[r * K2 + i] = a < b ? a : b;
+        }
+        __syncthreads();
+        for (int stride = K2 >> 1; stride > 0; stride >>= 1) {
+            for (int idx = threadIdx.x; idx < half * (K2 >> 1); idx += blockDim.x) {
+                const int r = idx / (K2 >> 1), t = idx - r * (K2 >> 1);
+                const int lo = r * K2 + 2 * t - (t & (stride - 1));
+                const int hi = lo + stride;
+                const uint64_t a = buf[lo], b = buf[hi];
+                if (a > b) { buf[lo] = b; buf[hi] = a; }
+            }
+            __syncthreads();
+        }
+        active = half;
+    }
+    uint64_t *dst = out + (static_cast<int64_t>(blockIdx.x) * nq + q) * k;
+    for (int i = threadIdx.x; i < k; i += blockDim.x) dst[i] = buf[i];
+}
+
+}  // namespace
+#include "xfbq_mma.cuh"
+namespace {
+
 __global__ void unpack_keys_kernel(const uint64_t *__restrict__ keys, int64_t count,
                                    int64_t *__restrict__ dist, int64_t *__restrict__ ids) {
     const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -524,9 +571,24 @@ int make_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, ScanPla
     return XFBQ_OK;
 }
 
-int launch_merge(const uint64_t *in, int parts, int64_t nq, int k, uint64_t *out, cudaStream_t st) {
+int merge_k2(int k) {
     int K2 = 32;
     while (K2 < k) K2 <<= 1;
+    return K2;
+}
+
+// Parts one tree-merge CTA can hold in shared memory (power of two), 0 if K2 is too large.
+int merge_group(int k) {
+    const int K2 = merge_k2(k);
+    int G = (160 * 1024) / (K2 * 8);
+    if (G < 2) return 0;
+    int p = 2;
+    while (p * 2 <= G && p * 2 <= 256) p <<= 1;
+    return p;
+}
+
+int launch_merge_stream(const uint64_t *in, int parts, int64_t nq, int k, uint64_t *out, cudaStream_t st) {
+    const int K2 = merge_k2(k);
     const size_t smem = static_cast<size_t>(2) * K2 * 8;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(merge_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -534,6 +596,123 @@ int launch_merge(const uint64_t *in, int parts, int64_t nq, int k, uint64_t *out
     }
     merge_topk_kernel<<<static_cast<unsigned>(nq), 256, smem, st>>>(in, parts, nq, k, K2, out);
     return check_launch("merge_topk_kernel");
+}
+
+// Number of intermediate rows-of-parts buffers a multi-level tree merge needs (elements of
+// [groups][nq][k] each); scratch must hold merge_scratch_parts(parts, k) * nq * k keys.
+int64_t merge_scratch_parts(int parts, int k) {
+    const int G = merge_group(k);
+    if (G == 0 || parts <= G) return 0;
+    const int64_t l1 = (parts + G - 1) / G;
+    const int64_t l2 = (l1 + G - 1) / G;
+    return l1 + (l1 > G ? l2 : 0);
+}
+
+int launch_merge(const uint64_t *in, int parts, int64_t nq, int k, uint64_t *out, uint64_t *scratch,
+                 cudaStream_t st) {
+    const int G = merge_group(k);
+    if (nq > 65535 || G == 0 || (parts > G && !scratch)) return launch_merge_stream(in, parts, nq, k, out, st);
+    const int K2 = merge_k2(k);
+    uint64_t *bufs[2] = {scratch, scratch ? scratch + ((parts + G - 1) / G) * nq * k : nullptr};
+    int level = 0;
+    while (true) {
+        const int groups = (parts + G - 1) / G;
+        int rows = parts < G ? parts : G, active = 1;
+        while (active < rows) active <<= 1;
+        const size_t smem = static_cast<size_t>(active) * K2 * 8;
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(merge_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "merge smem opt-in: %s", cudaGetErrorString(e));
+        }
+        uint64_t *dst = groups == 1 ? out : bufs[level & 1];
+        if (groups > 1 && level >= 2) return fail(XFBQ_E_UNSUPPORTED, "merge depth exceeded (parts=%d)", parts);
+        int threads = active * K2 / 2;
+        threads = threads < 64 ? 64 : (threads > 512 ? 512 : threads);
+        merge_tree_kernel<<<dim3(static_cast<unsigned>(groups), static_cast<unsigned>(nq)), threads, smem, st>>>(in, parts, nq, k, K2, G, dst);
+        if (int rc = check_launch("merge_tree_kernel")) return rc;
+        if (groups == 1) return XFBQ_OK;
+        in = dst;
+        parts = groups;
+        ++level;
+    }
+}
+
+// ----------------------------------------------------------------------------------------------
+// Integer-MMA engine planning (kernels in xfbq_mma.cuh).
+// ----------------------------------------------------------------------------------------------
+struct MmaPlan {
+    bool ok = false;
+    int MT = 2, NT = 2, QPW = 32, QW = 8, DW = 1, groups = 1, splits = 1, cap = 0, parts = 1;
+    int64_t total_iters = 0, iters_per_split = 0, nq_pad = 0;
+    size_t smem = 0;
+    // workspace layout (byte offsets) and size
+    size_t off_qop = 0, off_qconst = 0, off_lists = 0, off_parts = 0, off_mscratch = 0, bytes = 0;
+};
+
+typedef void (*MmaKernel)(const mma::Params);
+
+MmaKernel pick_mma_kernel(int wd, int C) {
+#define XFBQ_MMA_CASE(WD_, C_, MT_, NT_) if (wd == WD_ && C == C_) return mma::scan_kernel<WD_, C_, MT_, NT_>;
+    XFBQ_MMA_CASE(1, 1, 2, 2) XFBQ_MMA_CASE(2, 1, 2, 2) XFBQ_MMA_CASE(3, 1, 2, 2) XFBQ_MMA_CASE(4, 1, 2, 2)
+    XFBQ_MMA_CASE(1, 2, 2, 2) XFBQ_MMA_CASE(2, 2, 2, 2) XFBQ_MMA_CASE(3, 2, 2, 2) XFBQ_MMA_CASE(4, 2, 2, 2)
+    XFBQ_MMA_CASE(1, 4, 1, 1) XFBQ_MMA_CASE(2, 4, 1, 1) XFBQ_MMA_CASE(3, 4, 1, 1) XFBQ_MMA_CASE(4, 4, 1, 1)
+#undef XFBQ_MMA_CASE
+    return nullptr;
+}
+
+inline size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
+
+int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, MmaPlan *plan) {
+    MmaPlan pl;
+    const int C = static_cast<int>(chunks128(dim));
+    const char *eng = getenv("XFBQ_ENGINE");
+    const bool forced_popc = eng && strcmp(eng, "popc") == 0;
+    if (forced_popc || wd > 4 || wq > 7 || !(C == 1 || C == 2 || C == 4) || k > 1024 || nq < 1 || n < 1 ||
+        env_int("XFBQ_FORCE_GENERIC", 0)) {
+        *plan = pl;
+        return XFBQ_OK;
+    }
+    DeviceInfo info;
+    if (int rc = device_info(&info)) return rc;
+    pl.ok = true;
+    pl.MT = C == 4 ? 1 : 2;
+    pl.NT = C == 4 ? 1 : 2;
+    pl.QPW = 16 * pl.MT;
+    int cap = 64;
+    while (cap < 2 * k) cap <<= 1;
+    pl.cap = cap;
+    const int64_t qwt = (nq + pl.QPW - 1) / pl.QPW;
+    if (qwt >= mma::WARPS) {
+        pl.QW = mma::WARPS; pl.DW = 1;
+        pl.groups = static_cast<int>((qwt + mma::WARPS - 1) / mma::WARPS);
+    } else {
+        int qw = 1;
+        while (qw < qwt) qw <<= 1;
+        pl.QW = qw; pl.DW = mma::WARPS / qw; pl.groups = 1;
+    }
+    pl.nq_pad = static_cast<int64_t>(pl.groups) * pl.QW * pl.QPW;
+    const int tile = 8 * pl.NT;
+    pl.total_iters = bundles_of(n) * 32 / tile;
+    const int64_t target = pl.groups == 1 ? info.sms : 3ll * info.sms;
+    int64_t splits = pl.groups >= target ? 1 : (target + pl.groups / 2) / pl.groups;
+    const int forced = env_int("XFBQ_SPLITS", 0);
+    if (forced > 0) splits = forced;
+    const int64_t min_iters = static_cast<int64_t>(pl.DW) * 8;
+    if (splits > pl.total_iters / min_iters) splits = pl.total_iters / min_iters;
+    if (splits < 1) splits = 1;
+    pl.iters_per_split = (pl.total_iters + splits - 1) / splits;
+    pl.splits = static_cast<int>((pl.total_iters + pl.iters_per_split - 1) / pl.iters_per_split);
+    pl.parts = pl.splits * pl.DW;
+    pl.smem = static_cast<size_t>(mma::WARPS) * cap * 8;
+    size_t off = 0;
+    pl.off_qop = off; off = align256(off + static_cast<size_t>(pl.nq_pad) * 32 * C * 4);
+    pl.off_qconst = off; off = align256(off + static_cast<size_t>(pl.nq_pad) * 4);
+    pl.off_lists = off; off = align256(off + static_cast<size_t>(pl.groups) * pl.splits * mma::WARPS * pl.QPW * cap * 8);
+    pl.off_parts = off; off = align256(off + (pl.parts > 1 ? static_cast<size_t>(pl.parts) * nq * k * 8 : 0));
+    pl.off_mscratch = off; off = align256(off + static_cast<size_t>(merge_scratch_parts(pl.parts, k)) * nq * k * 8);
+    pl.bytes = off;
+    *plan = pl;
+    return XFBQ_OK;
 }
 
 template <typename T>
@@ -664,15 +843,25 @@ XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64
         return -1;
     }
     if (n == 0 || nq == 0) return 0;
+    MmaPlan mp;
+    if (make_mma_plan(n, dim, wd, nq, wq, k, &mp)) return -1;
+    if (mp.ok) return static_cast<int64_t>(mp.bytes);
     ScanPlan pl;
     if (make_plan(n, dim, wd, nq, wq, k, &pl)) return -1;
     if (pl.splits <= 1) return 0;
-    return static_cast<int64_t>(pl.splits) * nq * k * 8;
+    return static_cast<int64_t>(pl.splits + merge_scratch_parts(pl.splits, k)) * nq * k * 8;
 }
 
 XFBQ_API int xfbq_scan_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, int32_t out[6]) {
     if (!width_ok(wd) || !width_ok(wq) || n < 1 || dim < 1 || nq < 1 || k < 1 || k > XFBQ_MAX_K || !out)
         return fail(XFBQ_E_INVALID, "bad scan shape");
+    MmaPlan mp;
+    if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, &mp)) return rc;
+    if (mp.ok) {  // integer-MMA engine: tile = queries per CTA
+        out[0] = mp.QW * mp.QPW; out[1] = mp.groups; out[2] = mp.parts; out[3] = mp.cap;
+        out[4] = 2; out[5] = static_cast<int32_t>(mp.smem);
+        return XFBQ_OK;
+    }
     ScanPlan pl;
     if (int rc = make_plan(n, dim, wd, nq, wq, k, &pl)) return rc;
     out[0] = pl.tq; out[1] = pl.q_tiles; out[2] = pl.splits; out[3] = pl.cap;
@@ -698,9 +887,40 @@ XFBQ_API int xfbq_scan_topk(const void *db, int64_t n, int64_t dim, int wd, cons
         return XFBQ_OK;
     }
     if (!db || !q) return fail(XFBQ_E_INVALID, "null pointer");
+    MmaPlan mp;
+    if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, &mp)) return rc;
+    if (mp.ok) {
+        if (!workspace || workspace_bytes < static_cast<int64_t>(mp.bytes))
+            return fail(XFBQ_E_INVALID, "workspace too small: need %zu bytes, got %lld", mp.bytes, (long long)workspace_bytes);
+        const int C = static_cast<int>(chunks128(dim));
+        unsigned char *ws = static_cast<unsigned char *>(workspace);
+        uint32_t *qop = reinterpret_cast<uint32_t *>(ws + mp.off_qop);
+        int32_t *qconst = reinterpret_cast<int32_t *>(ws + mp.off_qconst);
+        mma::prep_queries_kernel<<<static_cast<unsigned>((mp.nq_pad * 32 + 255) / 256), 256, 0, st>>>(
+            q, nq, mp.nq_pad, static_cast<int>(dim), wq, wd, C, qop, qconst);
+        if (int rc = check_launch("prep_queries_kernel")) return rc;
+        MmaKernel kern = pick_mma_kernel(wd, C);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(mp.smem));
+        if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "mma scan smem opt-in (%zu bytes): %s", mp.smem, cudaGetErrorString(e));
+        mma::Params p;
+        p.db = static_cast<const uint32_t *>(db);
+        p.n = n; p.row_offset = row_offset;
+        p.qop = qop; p.qconst = qconst;
+        p.lists = reinterpret_cast<uint64_t *>(ws + mp.off_lists);
+        p.out = mp.parts > 1 ? reinterpret_cast<uint64_t *>(ws + mp.off_parts) : keys_out;
+        p.nq = nq;
+        p.total_iters = mp.total_iters; p.iters_per_split = mp.iters_per_split;
+        p.k = k; p.cap = mp.cap; p.QW = mp.QW; p.DW = mp.DW;
+        if (mp.groups > 65535) return fail(XFBQ_E_UNSUPPORTED, "too many query groups (%d); split the batch", mp.groups);
+        kern<<<dim3(static_cast<unsigned>(mp.splits), static_cast<unsigned>(mp.groups)), mma::THREADS, mp.smem, st>>>(p);
+        if (int rc = check_launch("mma::scan_kernel")) return rc;
+        if (mp.parts > 1)
+            return launch_merge(p.out, mp.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + mp.off_mscratch), st);
+        return XFBQ_OK;
+    }
     ScanPlan pl;
     if (int rc = make_plan(n, dim, wd, nq, wq, k, &pl)) return rc;
-    const int64_t need = pl.splits <= 1 ? 0 : static_cast<int64_t>(pl.splits) * nq * k * 8;
+    const int64_t need = pl.splits <= 1 ? 0 : static_cast<int64_t>(pl.splits + merge_scratch_parts(pl.splits, k)) * nq * k * 8;
     if (need > 0 && (!workspace || workspace_bytes < need))
         return fail(XFBQ_E_INVALID, "workspace too small: need %lld bytes, got %lld", (long long)need, (long long)workspace_bytes);
     const int C = static_cast<int>(chunks128(dim));
@@ -722,7 +942,9 @@ XFBQ_API int xfbq_scan_topk(const void *db, int64_t n, int64_t dim, int wd, cons
     if (pl.q_tiles > 65535) return fail(XFBQ_E_UNSUPPORTED, "too many query tiles (%d); split the batch", pl.q_tiles);
     kern<<<grid, SCAN_THREADS, pl.smem, st>>>(p);
     if (int rc = check_launch("scan_topk_kernel")) return rc;
-    if (pl.splits > 1) return launch_merge(static_cast<const uint64_t *>(workspace), pl.splits, nq, k, keys_out, st);
+    if (pl.splits > 1)
+        return launch_merge(static_cast<const uint64_t *>(workspace), pl.splits, nq, k, keys_out,
+                            static_cast<uint64_t *>(workspace) + static_cast<int64_t>(pl.splits) * nq * k, st);
     return XFBQ_OK;
 }
 
@@ -732,7 +954,7 @@ XFBQ_API int xfbq_merge_topk(const uint64_t *keys_in, int parts, int64_t nq, int
     if (k > XFBQ_MAX_K) return fail(XFBQ_E_UNSUPPORTED, "k=%d exceeds XFBQ_MAX_K=%d", k, XFBQ_MAX_K);
     if (nq == 0) return XFBQ_OK;
     if (!keys_in || !keys_out) return fail(XFBQ_E_INVALID, "null pointer");
-    return launch_merge(keys_in, parts, nq, k, keys_out, static_cast<cudaStream_t>(stream));
+    return launch_merge(keys_in, parts, nq, k, keys_out, nullptr, static_cast<cudaStream_t>(stream));
 }
 
 XFBQ_API int xfbq_unpack_keys(const uint64_t *keys, int64_t count, int64_t *dist, int64_t *ids, void *stream) {

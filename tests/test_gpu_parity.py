@@ -133,7 +133,8 @@ def test_synthetic_configs_match_reference(name):
 
 
 @pytest.mark.parametrize("env", [{"XFBQ_FORCE_GENERIC": "1"}, {"XFBQ_SPLITS": "1"}, {"XFBQ_SPLITS": "7"},
-                                 {"XFBQ_TQ": "1"}, {"XFBQ_TQ": "5", "XFBQ_SPLITS": "3"}])
+                                 {"XFBQ_ENGINE": "popc"}, {"XFBQ_ENGINE": "popc", "XFBQ_TQ": "1"},
+                                 {"XFBQ_ENGINE": "popc", "XFBQ_TQ": "5", "XFBQ_SPLITS": "3"}])
 def test_scan_plans_agree(env, monkeypatch):
     """Every launch plan (generic/specialised kernel, query-tile size, document splits) yields the
     same keys: the order on (distance, id) is total, so the result is partition independent."""
@@ -145,6 +146,22 @@ def test_scan_plans_agree(env, monkeypatch):
         monkeypatch.setenv(key, val)
     scores, ids = xb.search(idx, c["queries"], c["k"])
     assert np.array_equal(scores.astype(np.uint64), z["dists"]) and np.array_equal(ids, z["ids"])
+
+
+@pytest.mark.parametrize("name,nq,k", [("cfg4_40k_256_w4", 700, 100), ("cfg2_60k_128_w3", 300, 10),
+                                       ("cfg3_50k_200_w4", 520, 33), ("cfg5_20k_512_w4", 150, 1000)])
+def test_batch_mode_many_queries(name, nq, k):
+    """Enough queries to fill whole CTAs of the batch plan (8 query warps per CTA, several query
+    groups, several document splits); every query checked against the CPU oracle."""
+    c = synth_case(name)
+    params = xb.QuantParams(dim=c["dim"], scale=c["scale"], doc_bits=c["wd"], query_bits=c["wq"])
+    idx = xb.build_index(c["docs"], params, keep_originals=False)
+    queries = xo.synthetic_unit_rows(nq, c["dim"], 777)
+    scores, ids = xb.search(idx, queries, k)
+    planes = xo.c_quantize_matrix(c["docs"], c["wd"], c["scale"])
+    qp = xo.c_quantize_matrix(queries.astype(np.float64), c["wq"], c["scale"]).transpose(2, 0, 1)
+    want_d, want_i = xo.c_search(planes, qp, k)
+    assert np.array_equal(scores.astype(np.uint64), want_d) and np.array_equal(ids, want_i)
 
 
 def test_edge_cases():
