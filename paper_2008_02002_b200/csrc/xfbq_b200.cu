@@ -640,13 +640,18 @@ int launch_merge(const uint64_t *in, int parts, int64_t nq, int k, uint64_t *out
 // ----------------------------------------------------------------------------------------------
 // Integer-MMA engine planning (kernels in xfbq_mma.cuh).
 // ----------------------------------------------------------------------------------------------
+struct MmaShape {  // launch geometry of one mma::scan_kernel launch over n documents
+    int MT = 2, NT = 2, QPW = 32, QW = 8, DW = 1, groups = 1, grid = 1, slots = 1, parts = 1, cap = 0;
+    int64_t stages = 0, nq_pad = 0, n_pad = 0;
+    size_t smem = 0, lists_bytes = 0, parts_bytes = 0, mscratch_bytes = 0;
+};
+
 struct MmaPlan {
     bool ok = false;
-    int MT = 2, NT = 2, QPW = 32, QW = 8, DW = 1, groups = 1, splits = 1, cap = 0, parts = 1;
-    int64_t total_iters = 0, iters_per_split = 0, nq_pad = 0;
-    size_t smem = 0;
-    // workspace layout (byte offsets) and size
-    size_t off_qop = 0, off_qconst = 0, off_lists = 0, off_parts = 0, off_mscratch = 0, bytes = 0;
+    MmaShape main, pre;      // pre: sample scan that seeds the thresholds (small batches only)
+    int64_t sample = 0;      // documents in the sample scan, 0 = none
+    size_t off_qop = 0, off_qconst = 0, off_tau = 0, off_prekeys = 0, off_lists = 0, off_parts = 0,
+           off_mscratch = 0, bytes = 0;
 };
 
 typedef void (*MmaKernel)(const mma::Params);
@@ -662,6 +667,53 @@ MmaKernel pick_mma_kernel(int wd, int C) {
 
 inline size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
 
+void mma_shape(int64_t n, int C, int64_t nq, int k, int sms, MmaShape *out) {
+    MmaShape sh;
+    sh.MT = C == 4 ? 1 : 2;
+    sh.NT = C == 4 ? 1 : 2;
+    sh.QPW = 16 * sh.MT;
+    int cap = 64;
+    while (cap < 2 * k) cap <<= 1;
+    sh.cap = cap;
+    const int64_t qwt = (nq + sh.QPW - 1) / sh.QPW;
+    if (qwt >= mma::WARPS) {
+        sh.QW = mma::WARPS; sh.DW = 1;
+        sh.groups = static_cast<int>((qwt + mma::WARPS - 1) / mma::WARPS);
+    } else {
+        int qw = 1;
+        while (qw < qwt) qw <<= 1;
+        sh.QW = qw; sh.DW = mma::WARPS / qw; sh.groups = 1;
+    }
+    sh.nq_pad = static_cast<int64_t>(sh.groups) * sh.QW * sh.QPW;
+    sh.n_pad = bundles_of(n) * 32;
+    const int64_t stage_docs = static_cast<int64_t>(mma::STAGE_ITERS) * 8 * sh.NT;
+    sh.stages = (sh.n_pad + stage_docs - 1) / stage_docs;
+    const int64_t W = static_cast<int64_t>(sh.groups) * sh.stages;
+    int64_t grid = env_int("XFBQ_GRID", 0) > 0 ? env_int("XFBQ_GRID", 0) : sms;
+    if (grid > W) grid = W;
+    sh.grid = static_cast<int>(grid);
+    // part slots: the largest number of CTA ranges [c*W/G, (c+1)*W/G) overlapping one group
+    int slots = 1;
+    for (int gr = 0; gr < sh.groups; ++gr) {
+        const int64_t lo = static_cast<int64_t>(gr) * sh.stages, hi = lo + sh.stages;  // [lo, hi)
+        int64_t c_first = lo * grid / W;
+        while (c_first > 0 && c_first * W / grid > lo) --c_first;
+        while ((c_first + 1) * W / grid <= lo) ++c_first;
+        int64_t c_last = (hi - 1) * grid / W;
+        while (c_last > 0 && c_last * W / grid > hi - 1) --c_last;
+        while ((c_last + 1) * W / grid <= hi - 1) ++c_last;
+        if (c_last - c_first + 1 > slots) slots = static_cast<int>(c_last - c_first + 1);
+    }
+    sh.slots = slots;
+    sh.parts = slots * sh.DW;
+    const int WPL = sh.NT * C * 8;
+    sh.smem = static_cast<size_t>(2) * mma::STAGE_ITERS * WPL * 32 * 4 + static_cast<size_t>(mma::WARPS) * cap * 8 + mma::WARPS * 32 * 4;
+    sh.lists_bytes = static_cast<size_t>(sh.grid) * mma::WARPS * sh.QPW * cap * 8;
+    sh.parts_bytes = sh.parts > 1 ? static_cast<size_t>(sh.parts) * nq * k * 8 : 0;
+    sh.mscratch_bytes = static_cast<size_t>(merge_scratch_parts(sh.parts, k)) * nq * k * 8;
+    *out = sh;
+}
+
 int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, MmaPlan *plan) {
     MmaPlan pl;
     const int C = static_cast<int>(chunks128(dim));
@@ -675,43 +727,52 @@ int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, Mma
     DeviceInfo info;
     if (int rc = device_info(&info)) return rc;
     pl.ok = true;
-    pl.MT = C == 4 ? 1 : 2;
-    pl.NT = C == 4 ? 1 : 2;
-    pl.QPW = 16 * pl.MT;
-    int cap = 64;
-    while (cap < 2 * k) cap <<= 1;
-    pl.cap = cap;
-    const int64_t qwt = (nq + pl.QPW - 1) / pl.QPW;
-    if (qwt >= mma::WARPS) {
-        pl.QW = mma::WARPS; pl.DW = 1;
-        pl.groups = static_cast<int>((qwt + mma::WARPS - 1) / mma::WARPS);
-    } else {
-        int qw = 1;
-        while (qw < qwt) qw <<= 1;
-        pl.QW = qw; pl.DW = mma::WARPS / qw; pl.groups = 1;
-    }
-    pl.nq_pad = static_cast<int64_t>(pl.groups) * pl.QW * pl.QPW;
-    const int tile = 8 * pl.NT;
-    pl.total_iters = bundles_of(n) * 32 / tile;
-    const int64_t target = pl.groups == 1 ? info.sms : 3ll * info.sms;
-    int64_t splits = pl.groups >= target ? 1 : (target + pl.groups / 2) / pl.groups;
-    const int forced = env_int("XFBQ_SPLITS", 0);
-    if (forced > 0) splits = forced;
-    const int64_t min_iters = static_cast<int64_t>(pl.DW) * 8;
-    if (splits > pl.total_iters / min_iters) splits = pl.total_iters / min_iters;
-    if (splits < 1) splits = 1;
-    pl.iters_per_split = (pl.total_iters + splits - 1) / splits;
-    pl.splits = static_cast<int>((pl.total_iters + pl.iters_per_split - 1) / pl.iters_per_split);
-    pl.parts = pl.splits * pl.DW;
-    pl.smem = static_cast<size_t>(mma::WARPS) * cap * 8;
+    mma_shape(n, C, nq, k, info.sms, &pl.main);
+    // Small batches split the documents over every warp of the chip, so each candidate list sees
+    // few documents and its own threshold tightens slowly; a sample scan of the first S documents
+    // gives all of them a threshold of selectivity ~k/S up front.
+    int64_t sample = env_int("XFBQ_SAMPLE", -1);
+    if (sample < 0) sample = (pl.main.groups == 1 && pl.main.DW > 1) ? 32768 : 0;
+    if (sample > 0 && (n < 16 * sample || sample < 4 * k)) sample = 0;
+    pl.sample = sample;
+    if (sample) mma_shape(sample, C, nq, k, info.sms, &pl.pre);
     size_t off = 0;
-    pl.off_qop = off; off = align256(off + static_cast<size_t>(pl.nq_pad) * 32 * C * 4);
-    pl.off_qconst = off; off = align256(off + static_cast<size_t>(pl.nq_pad) * 4);
-    pl.off_lists = off; off = align256(off + static_cast<size_t>(pl.groups) * pl.splits * mma::WARPS * pl.QPW * cap * 8);
-    pl.off_parts = off; off = align256(off + (pl.parts > 1 ? static_cast<size_t>(pl.parts) * nq * k * 8 : 0));
-    pl.off_mscratch = off; off = align256(off + static_cast<size_t>(merge_scratch_parts(pl.parts, k)) * nq * k * 8);
+    pl.off_qop = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 32 * C * 4);
+    pl.off_qconst = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 4);
+    pl.off_tau = off; off = align256(off + (sample ? static_cast<size_t>(nq) * 4 : 0));
+    pl.off_prekeys = off; off = align256(off + (sample ? static_cast<size_t>(nq) * k * 8 : 0));
+    pl.off_lists = off; off = align256(off + (pl.main.lists_bytes > pl.pre.lists_bytes ? pl.main.lists_bytes : pl.pre.lists_bytes));
+    pl.off_parts = off; off = align256(off + (pl.main.parts_bytes > pl.pre.parts_bytes ? pl.main.parts_bytes : pl.pre.parts_bytes));
+    pl.off_mscratch = off; off = align256(off + (pl.main.mscratch_bytes > pl.pre.mscratch_bytes ? pl.main.mscratch_bytes : pl.pre.mscratch_bytes));
     pl.bytes = off;
     *plan = pl;
+    return XFBQ_OK;
+}
+
+// One scan launch (+ merge of its part slots) over the first n documents of db.
+int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const void *db, int64_t n, int wd, int C,
+                 int64_t nq, int k, int64_t row_offset, const int32_t *tau_init, uint64_t *keys_out, cudaStream_t st) {
+    MmaKernel kern = pick_mma_kernel(wd, C);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh.smem));
+    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "mma scan smem opt-in (%zu bytes): %s", sh.smem, cudaGetErrorString(e));
+    mma::Params p;
+    p.db = static_cast<const uint32_t *>(db);
+    p.n = n; p.n_pad = sh.n_pad; p.row_offset = row_offset;
+    p.qop = reinterpret_cast<const uint32_t *>(ws + pl.off_qop);
+    p.qconst = reinterpret_cast<const int32_t *>(ws + pl.off_qconst);
+    p.tau_init = tau_init;
+    p.lists = reinterpret_cast<uint64_t *>(ws + pl.off_lists);
+    p.out = sh.parts > 1 ? reinterpret_cast<uint64_t *>(ws + pl.off_parts) : keys_out;
+    p.nq = nq; p.stages = sh.stages; p.groups = sh.groups;
+    p.k = k; p.cap = sh.cap; p.QW = sh.QW; p.DW = sh.DW;
+    if (sh.parts > 1) {  // slots a group does not use stay KEY_INF
+        e = cudaMemsetAsync(p.out, 0xFF, sh.parts_bytes, st);
+        if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
+    }
+    kern<<<static_cast<unsigned>(sh.grid), mma::THREADS, sh.smem, st>>>(p);
+    if (int rc = check_launch("mma::scan_kernel")) return rc;
+    if (sh.parts > 1)
+        return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st);
     return XFBQ_OK;
 }
 
@@ -858,8 +919,8 @@ XFBQ_API int xfbq_scan_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, 
     MmaPlan mp;
     if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, &mp)) return rc;
     if (mp.ok) {  // integer-MMA engine: tile = queries per CTA
-        out[0] = mp.QW * mp.QPW; out[1] = mp.groups; out[2] = mp.parts; out[3] = mp.cap;
-        out[4] = 2; out[5] = static_cast<int32_t>(mp.smem);
+        out[0] = mp.main.QW * mp.main.QPW; out[1] = mp.main.groups; out[2] = mp.main.parts; out[3] = mp.main.cap;
+        out[4] = 2; out[5] = static_cast<int32_t>(mp.main.smem);
         return XFBQ_OK;
     }
     ScanPlan pl;
@@ -896,27 +957,19 @@ XFBQ_API int xfbq_scan_topk(const void *db, int64_t n, int64_t dim, int wd, cons
         unsigned char *ws = static_cast<unsigned char *>(workspace);
         uint32_t *qop = reinterpret_cast<uint32_t *>(ws + mp.off_qop);
         int32_t *qconst = reinterpret_cast<int32_t *>(ws + mp.off_qconst);
-        mma::prep_queries_kernel<<<static_cast<unsigned>((mp.nq_pad * 32 + 255) / 256), 256, 0, st>>>(
-            q, nq, mp.nq_pad, static_cast<int>(dim), wq, wd, C, qop, qconst);
+        mma::prep_queries_kernel<<<static_cast<unsigned>((mp.main.nq_pad * 32 + 255) / 256), 256, 0, st>>>(
+            q, nq, mp.main.nq_pad, static_cast<int>(dim), wq, wd, C, qop, qconst);
         if (int rc = check_launch("prep_queries_kernel")) return rc;
-        MmaKernel kern = pick_mma_kernel(wd, C);
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(mp.smem));
-        if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "mma scan smem opt-in (%zu bytes): %s", mp.smem, cudaGetErrorString(e));
-        mma::Params p;
-        p.db = static_cast<const uint32_t *>(db);
-        p.n = n; p.row_offset = row_offset;
-        p.qop = qop; p.qconst = qconst;
-        p.lists = reinterpret_cast<uint64_t *>(ws + mp.off_lists);
-        p.out = mp.parts > 1 ? reinterpret_cast<uint64_t *>(ws + mp.off_parts) : keys_out;
-        p.nq = nq;
-        p.total_iters = mp.total_iters; p.iters_per_split = mp.iters_per_split;
-        p.k = k; p.cap = mp.cap; p.QW = mp.QW; p.DW = mp.DW;
-        if (mp.groups > 65535) return fail(XFBQ_E_UNSUPPORTED, "too many query groups (%d); split the batch", mp.groups);
-        kern<<<dim3(static_cast<unsigned>(mp.splits), static_cast<unsigned>(mp.groups)), mma::THREADS, mp.smem, st>>>(p);
-        if (int rc = check_launch("mma::scan_kernel")) return rc;
-        if (mp.parts > 1)
-            return launch_merge(p.out, mp.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + mp.off_mscratch), st);
-        return XFBQ_OK;
+        const int32_t *tau_init = nullptr;
+        if (mp.sample) {
+            uint64_t *prekeys = reinterpret_cast<uint64_t *>(ws + mp.off_prekeys);
+            int32_t *tau = reinterpret_cast<int32_t *>(ws + mp.off_tau);
+            if (int rc = run_mma_scan(mp.pre, mp, ws, db, mp.sample, wd, C, nq, k, row_offset, nullptr, prekeys, st)) return rc;
+            mma::tau_from_keys_kernel<<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(prekeys, qconst, nq, k, tau);
+            if (int rc = check_launch("tau_from_keys_kernel")) return rc;
+            tau_init = tau;
+        }
+        return run_mma_scan(mp.main, mp, ws, db, n, wd, C, nq, k, row_offset, tau_init, keys_out, st);
     }
     ScanPlan pl;
     if (int rc = make_plan(n, dim, wd, nq, wq, k, &pl)) return rc;

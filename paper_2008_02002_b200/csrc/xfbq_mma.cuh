@@ -9,16 +9,22 @@
 // ~60x faster than the POPC pipe can popcount the 16 plane pairs (profiles/microbench_r1.jsonl:
 // XU/POPC 4.5 T lane-ops/s vs IMMA 568 T MAC/s).  Results are bit-identical to the POPC form.
 //
-// Data flow per warp (no block-level synchronisation anywhere):
-//   * queries: 16*MT query rows live in registers as A fragments (s8 weights 2y-Aq, laid out by
-//     mma_prep_queries_kernel in exactly the K-order the document side produces);
-//   * documents: 8-doc tiles are read straight from the bit-plane bundle layout (one 128-byte
-//     line per plane chunk per tile), transposed in registers from bit planes to one byte per
-//     dimension (4x4 bit-block transpose by delta swaps + nibble split) and used as B fragments;
-//   * selection: the accumulator is initialised to -tau_q, so "distance <= threshold" is the
-//     sign bit of the result; one AND-reduction + vote per 8*NT x 16*MT scores decides whether
-//     the (rare) slow path runs, which appends (distance<<32 | row id) keys to a warp-private
-//     candidate list, compacted by a warp-level bitonic sort when full (search.py:129-131 order).
+// Data flow of one CTA (8 warps), per stage of 8 iterations x TILE = 8*NT documents:
+//   * queries: 16*MT query rows per warp live in registers as A fragments (s8 weights 2y-Aq,
+//     laid out by prep_queries_kernel in exactly the K-order the document side produces);
+//   * documents: warp w reads iteration w of the stage straight from the bit-plane bundle layout
+//     (one 128-byte line per plane chunk per 8-doc tile), transposes it in registers from bit
+//     planes to one byte per dimension (4x4 bit-block transpose by delta swaps + nibble split)
+//     and stores the B fragments to a double-buffered shared-memory stage, so a tile is
+//     transposed once per CTA however many query warps consume it;
+//   * every (query-warp, doc-warp) consumes its iterations of the stage: 8 LDS.128 + MT*NT*4C
+//     IMMAs; the accumulator is initialised to -tau_q, so "distance <= threshold" is the sign
+//     bit of the result and one AND-reduction + vote per TILE x 16*MT scores decides whether the
+//     (rare) slow path runs; there, lanes append (distance<<32 | row id) keys to the warp's
+//     candidate lists in parallel (shared-memory counters), and rows that could overflow in the
+//     next iteration are compacted by a warp-level bitonic sort (search.py:129-131 order);
+//   * work = groups x stages is linearised and cut into gridDim.x equal ranges, so every CTA
+//     scans the same number of stages and a query group is split over as few CTAs as possible.
 #pragma once
 
 namespace mma {
@@ -27,24 +33,29 @@ constexpr int WARPS = 8;
 constexpr int THREADS = WARPS * 32;
 constexpr int TAU_OPEN = -(1 << 30);  // threshold that lets every score through (no list yet)
 
+constexpr int STAGE_ITERS = WARPS;    // iterations per stage: one produced by each warp
+
 struct Params {
-    const uint32_t *db;     // bundle layout viewed as 32-bit words
-    int64_t n;              // real documents
+    const uint32_t *db;       // bundle layout viewed as 32-bit words
+    int64_t n;                // real documents
+    int64_t n_pad;            // documents the buffer holds (multiple of 32)
     int64_t row_offset;
-    const uint32_t *qop;    // [nq_pad][4C k-steps][4 t][2] words of 4 s8 weights
-    const int32_t *qconst;  // [nq_pad] Dq = Ad * sum(y)
-    uint64_t *lists;        // [ctas * WARPS][16*MT][cap] candidate lists
-    uint64_t *out;          // [parts][nq][k]
+    const uint32_t *qop;      // [nq_pad/16][4C k-steps][32 lanes][4] A fragments (s8 weights)
+    const int32_t *qconst;    // [nq_pad] Dq = Ad * sum(y)
+    const int32_t *tau_init;  // [nq] initial thresholds (acc domain) or nullptr
+    uint64_t *lists;          // [gridDim.x * WARPS][16*MT][cap] candidate lists
+    uint64_t *out;            // [slots * DW][nq][k], pre-filled with KEY_INF
     int64_t nq;
-    int64_t total_iters;    // ceil(n_pad / (8*NT))
-    int64_t iters_per_split;
+    int64_t stages;           // ceil(n_pad / (STAGE_ITERS * TILE))
+    int groups;               // query groups of QW * 16*MT queries
     int k, cap, QW, DW;
 };
 
 // ------------------------------------------------------------------------------ query operand
 // One warp per (padded) query row: bit-plane query words -> s8 weights 2*y - Aq in MMA K-order,
 // and Dq = Ad * sum_k y_k.  Operand word ow = (s*4 + t)*2 + hi holds bytes j=0..3 for dimension
-//   dim = 32C*t + 32*(s>>2) + 8*j + (s&3) + 4*hi.
+//   dim = 32C*t + 32*(s>>2) + 8*j + (s&3) + 4*hi; words are stored in mma A-fragment order so a
+// lane fetches the four registers of one (16-row tile, k-step) with a single 128-bit load.
 __global__ void __launch_bounds__(256)
 prep_queries_kernel(const uint32_t *__restrict__ q, int64_t nq, int64_t nq_pad, int dim, int wq, int wd,
                     int C, uint32_t *__restrict__ qop, int32_t *__restrict__ qconst) {
@@ -71,7 +82,10 @@ prep_queries_kernel(const uint32_t *__restrict__ q, int64_t nq, int64_t nq_pad, 
                 packed |= (static_cast<uint32_t>(w) & 0xFFu) << (8 * j);
             }
         }
-        qop[row * (32 * C) + ow] = packed;
+        // fragment order: 16-row tile, k-step, lane (g = row%8, t), register (a0..a3 = half + 2*hi)
+        const int64_t tile = row >> 4;
+        const int rr = static_cast<int>(row & 15);
+        qop[((tile * (4 * C) + s) * 32 + (rr & 7) * 4 + t) * 4 + (rr >> 3) + 2 * hi] = packed;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sy += __shfl_xor_sync(0xffffffffu, sy, o);
@@ -146,17 +160,16 @@ __device__ __forceinline__ void warp_bitonic(uint64_t *s, int P, int lane) {
 
 // Per-lane selection state: lane l owns query row l of the warp.
 struct LaneState {
-    uint64_t thr_key;  // k-th best key so far (KEY_INF until k candidates exist)
-    int dq;            // Dq
-    int tau;           // pass iff acc >= tau  (tau = Dq - distance(thr_key))
-    int count;         // entries in this row's list
+    int dq;   // Dq = Ad * sum(y) of the row's query
+    int tau;  // pass iff acc >= tau  (tau = Dq - distance of the k-th best key so far)
 };
 
-// Sort list row `ql` (cnt entries) through the scratch, keep the k best, refresh the threshold.
-// Warp-uniform arguments.  Returns the new count; writes the new -tau to *negtau_out.
-__device__ __forceinline__ int compact_row(uint64_t *list_row, uint64_t *scratch, int cnt, int k, int ql,
-                                           int lane, LaneState &st, int *negtau_out) {
+// Sort list row `ql` through the warp's scratch, keep the k best, refresh the row's threshold.
+// Warp-uniform call.  Returns -tau of the row (for the per-lane accumulator bias copies).
+__device__ __forceinline__ int compact_row(uint64_t *list_row, uint64_t *scratch, int *cnt_p, int k, int ql,
+                                           int lane, LaneState &st) {
     __syncwarp();
+    const int cnt = *cnt_p;
     int P = 2;
     while (P < cnt) P <<= 1;
     for (int i = lane; i < P; i += 32) scratch[i] = i < cnt ? __ldcg(list_row + i) : KEY_INF;
@@ -164,181 +177,233 @@ __device__ __forceinline__ int compact_row(uint64_t *list_row, uint64_t *scratch
     warp_bitonic(scratch, P, lane);
     const int keep = cnt < k ? cnt : k;
     for (int i = lane; i < keep; i += 32) list_row[i] = scratch[i];
-    const uint64_t new_thr = cnt >= k ? scratch[k - 1] : KEY_INF;
+    const uint64_t kth = cnt >= k ? scratch[k - 1] : KEY_INF;
     __syncwarp();
     if (lane == ql) {
-        st.thr_key = new_thr;
-        st.count = keep;
-        if (cnt >= k) st.tau = st.dq - static_cast<int>(new_thr >> 32);
+        *cnt_p = keep;
+        if (cnt >= k) st.tau = st.dq - static_cast<int>(kth >> 32);
     }
-    *negtau_out = -__shfl_sync(0xffffffffu, st.tau, ql);
-    return keep;
+    __syncwarp();
+    return -__shfl_sync(0xffffffffu, st.tau, ql);
 }
 
 template <int WD, int C, int MT, int NT>
 __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int QPW = 16 * MT;   // query rows per warp
-    constexpr int KS = 4 * C;      // k-steps of 32 dims
-    constexpr int TILE = 8 * NT;   // documents per iteration
+    constexpr int QPW = 16 * MT;        // query rows per warp
+    constexpr int KS = 4 * C;           // k-steps of 32 dims
+    constexpr int TILE = 8 * NT;        // documents per iteration
+    constexpr int WPL = NT * C * 8;     // B-fragment words per lane per iteration
+    constexpr int RCH = WPL / 4;        // 16-byte chunks per lane per iteration
+    constexpr int STAGE_WORDS = STAGE_ITERS * WPL * 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int qw = warp % p.QW, dw = warp / p.QW;
-    const int64_t q0 = (static_cast<int64_t>(blockIdx.y) * p.QW + qw) * QPW;
-    if (q0 >= p.nq) return;  // no block-level synchronisation in this kernel
-    uint64_t *scratch = reinterpret_cast<uint64_t *>(smem_raw) + static_cast<size_t>(warp) * p.cap;
-    const int64_t cta = static_cast<int64_t>(blockIdx.y) * gridDim.x + blockIdx.x;
-    uint64_t *lists = p.lists + (cta * WARPS + warp) * QPW * static_cast<int64_t>(p.cap);
 
-    // ---- A fragments: this warp's query rows, resident for the whole scan
-    uint32_t a[MT][KS][4];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int s = 0; s < KS; ++s) {
-            const uint2 r0 = __ldg(reinterpret_cast<const uint2 *>(p.qop + ((q0 + 16 * mt + g) * KS + s) * 8 + t * 2));
-            const uint2 r1 = __ldg(reinterpret_cast<const uint2 *>(p.qop + ((q0 + 16 * mt + g + 8) * KS + s) * 8 + t * 2));
-            a[mt][s][0] = r0.x; a[mt][s][1] = r1.x; a[mt][s][2] = r0.y; a[mt][s][3] = r1.y;
-        }
+    // shared memory: [2 stages of B fragments][per-warp sort scratch][per-warp row counters]
+    uint4 *stage_mem = reinterpret_cast<uint4 *>(smem_raw);
+    uint64_t *scratch = reinterpret_cast<uint64_t *>(smem_raw + 2 * STAGE_WORDS * 4) + static_cast<size_t>(warp) * p.cap;
+    int *cnt_s = reinterpret_cast<int *>(smem_raw + 2 * STAGE_WORDS * 4 + static_cast<size_t>(WARPS) * p.cap * 8) + warp * 32;
+    uint64_t *lists = p.lists + (static_cast<int64_t>(blockIdx.x) * WARPS + warp) * QPW * static_cast<int64_t>(p.cap);
 
-    // ---- selection state: lane l <-> query row l
-    LaneState st;
-    {
-        const int64_t myq = q0 + lane;
-        const bool valid = lane < QPW && myq < p.nq;
-        st.dq = valid ? p.qconst[myq] : 0;
-        st.tau = valid ? TAU_OPEN : 1;  // rows without a query: acc = 0 < 1 never passes
-        st.thr_key = KEY_INF;
-        st.count = 0;
-    }
-    int negtau[MT][2];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-        negtau[mt][0] = -__shfl_sync(0xffffffffu, st.tau, 16 * mt + g);
-        negtau[mt][1] = -__shfl_sync(0xffffffffu, st.tau, 16 * mt + g + 8);
-    }
-
-    const int64_t it_begin = static_cast<int64_t>(blockIdx.x) * p.iters_per_split;
-    const int64_t it_end = min(p.total_iters, it_begin + p.iters_per_split);
+    // ---- this CTA's share of the linearised (group, stage) work
+    const int64_t T = p.stages;
+    const int64_t W = static_cast<int64_t>(p.groups) * T;
+    const int64_t G = gridDim.x;
+    const int64_t lin_begin = static_cast<int64_t>(blockIdx.x) * W / G;
+    const int64_t lin_end = (static_cast<int64_t>(blockIdx.x) + 1) * W / G;
 
     // lane (g, t) of tile nt reads, for every plane, the C words [C*t, C*t+C) of document 8*nt+g
     auto tile_ptr = [&](int64_t it, int nt, int i) -> const uint32_t * {
         const int64_t doc = it * TILE + 8 * nt + g;
         const int64_t b = doc >> 5;
         const int dl = static_cast<int>(doc & 31);
-        const int word = C * t;  // first word of the quarter within the plane's 4C words
+        const int word = C * t;
         return p.db + ((((b * WD + i) * C + (word >> 2)) * 32 + dl) << 2) + (word & 3);
     };
-
     uint32_t pw[NT][WD][C];
-    int64_t it = it_begin + dw;
-    if (it < it_end) {
+    auto load_raw = [&](int64_t stage) {  // this warp's iteration of `stage` -> pw
+        const int64_t it = stage * STAGE_ITERS + warp;
+        const bool ok = (it + 1) * TILE <= p.n_pad;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-            for (int i = 0; i < WD; ++i) load_quarter<C>(tile_ptr(it, nt, i), pw[nt][i]);
-    }
-
-    for (; it < it_end; it += p.DW) {
-        // ---- bit planes -> byte operands for this iteration
-        uint32_t bw[NT][C][8];
+            for (int i = 0; i < WD; ++i) {
+                if (ok) load_quarter<C>(tile_ptr(it, nt, i), pw[nt][i]);
+                else {
+#pragma unroll
+                    for (int h = 0; h < C; ++h) pw[nt][i][h] = 0u;
+                }
+            }
+    };
+    auto produce = [&](int buf) {  // pw -> byte operands -> stage buffer, slot = this warp's iteration
+        uint4 *dst = stage_mem + (static_cast<size_t>(buf) * STAGE_ITERS + warp) * (RCH * 32) + lane;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int h = 0; h < C; ++h) {
-                uint32_t pin[4];
+                uint32_t pin[4], bw[8];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) pin[i] = i < WD ? pw[nt][i < WD ? i : 0][h] : 0u;
-                planes_to_bytes<WD>(pin, bw[nt][h]);
+                planes_to_bytes<WD>(pin, bw);
+                const int r = (nt * C + h) * 2;
+                dst[r * 32] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+                dst[(r + 1) * 32] = make_uint4(bw[4], bw[5], bw[6], bw[7]);
             }
-        // ---- prefetch the next iteration's plane words
-        const int64_t itn = it + p.DW;
-        if (itn < it_end) {
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int i = 0; i < WD; ++i) load_quarter<C>(tile_ptr(itn, nt, i), pw[nt][i]);
-        }
-        // ---- acc' = sum_k x_k (2 y_k - Aq) - tau   (k-step s uses quarter words 2s, 2s+1)
-        int c[MT][NT][4];
-#pragma unroll
-        for (int s = 0; s < KS; ++s)
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {
-                    const uint32_t b0 = bw[nt][s >> 2][2 * (s & 3)], b1 = bw[nt][s >> 2][2 * (s & 3) + 1];
-                    if (s == 0) imma(c[mt][nt], a[mt][s], b0, b1, negtau[mt][0], negtau[mt][0], negtau[mt][1], negtau[mt][1]);
-                    else imma(c[mt][nt], a[mt][s], b0, b1, c[mt][nt][0], c[mt][nt][1], c[mt][nt][2], c[mt][nt][3]);
-                }
-        // ---- any score with acc' >= 0 ?  (sign bit of the AND of all results is clear)
-        int all = -1;
+    };
+
+    for (int64_t lin = lin_begin; lin < lin_end;) {
+        const int gr = static_cast<int>(lin / T);
+        const int64_t s_begin = lin - static_cast<int64_t>(gr) * T;
+        const int64_t s_end = min(T, s_begin + (lin_end - lin));
+        lin += s_end - s_begin;
+        // part slot of this segment: CTAs overlapping group gr are numbered from the first one
+        int64_t c_first = (static_cast<int64_t>(gr) * T * G) / W;
+        while (c_first > 0 && c_first * W / G > static_cast<int64_t>(gr) * T) --c_first;
+        while ((c_first + 1) * W / G <= static_cast<int64_t>(gr) * T) ++c_first;
+        const int64_t part = (static_cast<int64_t>(blockIdx.x) - c_first) * p.DW + dw;
+
+        const int64_t q0 = (static_cast<int64_t>(gr) * p.QW + qw) * QPW;
+        const bool has_q = q0 < p.nq;  // warp-uniform; warps without queries still produce stages
+
+        // ---- A fragments: this warp's query rows, resident for the whole segment
+        uint32_t a[MT][KS][4];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) all &= c[mt][nt][0] & c[mt][nt][1] & c[mt][nt][2] & c[mt][nt][3];
-        if (__any_sync(0xffffffffu, all >= 0)) {
-            // slow path: hits are handled one at a time with warp-uniform control flow.  The scores
-            // of this iteration were biased with the thresholds in force when it started, so a
-            // compaction in here must not change how they are decoded.
-            const int tau_iter = st.tau;
+            for (int s = 0; s < KS; ++s) {
+                uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                if (has_q) v = __ldg(reinterpret_cast<const uint4 *>(p.qop) + (((q0 >> 4) + mt) * KS + s) * 32 + lane);
+                a[mt][s][0] = v.x; a[mt][s][1] = v.y; a[mt][s][2] = v.z; a[mt][s][3] = v.w;
+            }
+        // ---- selection state: lane l <-> query row l
+        LaneState st;
+        {
+            const int64_t myq = q0 + lane;
+            const bool valid = has_q && lane < QPW && myq < p.nq;
+            st.dq = valid ? p.qconst[myq] : 0;
+            st.tau = valid ? (p.tau_init ? max(TAU_OPEN, p.tau_init[myq]) : TAU_OPEN) : 1;  // no query: acc = 0 < 1
+            cnt_s[lane] = 0;
+        }
+        int negtau[MT][2], dqrow[MT][2];
 #pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt)
+            for (int hf = 0; hf < 2; ++hf) {
+                negtau[mt][hf] = -__shfl_sync(0xffffffffu, st.tau, 16 * mt + g + 8 * hf);
+                dqrow[mt][hf] = __shfl_sync(0xffffffffu, st.dq, 16 * mt + g + 8 * hf);
+            }
+
+        // ---- prologue: stage s_begin into buffer 0, raw words of stage s_begin+1 in flight
+        load_raw(s_begin);
+        produce(0);
+        if (s_begin + 1 < s_end) load_raw(s_begin + 1);
+        __syncthreads();
+
+        for (int64_t s = s_begin; s < s_end; ++s) {
+            const int buf = static_cast<int>((s - s_begin) & 1);
+            if (s + 1 < s_end) {
+                produce(buf ^ 1);
+                if (s + 2 < s_end) load_raw(s + 2);
+            }
+            if (has_q) {
+                for (int i = dw; i < STAGE_ITERS; i += p.DW) {
+                    const int64_t it = s * STAGE_ITERS + i;
+                    if ((it + 1) * TILE > p.n_pad) break;
+                    const uint4 *src = stage_mem + (static_cast<size_t>(buf) * STAGE_ITERS + i) * (RCH * 32) + lane;
+                    uint32_t bw[WPL];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        unsigned m = __ballot_sync(0xffffffffu, c[mt][nt][j] >= 0);
-                        while (m) {
-                            const int L = __ffs(m) - 1;
-                            m &= m - 1;
-                            const int accp = __shfl_sync(0xffffffffu, c[mt][nt][j], L);
-                            const int ql = 16 * mt + (L >> 2) + 8 * (j >> 1);
-                            const int64_t doc = it * TILE + 8 * nt + 2 * (L & 3) + (j & 1);
-                            const int tau_q = __shfl_sync(0xffffffffu, tau_iter, ql);
-                            const int dq_q = __shfl_sync(0xffffffffu, st.dq, ql);
-                            const uint64_t thr = shfl_u64(st.thr_key, ql);
-                            const uint32_t dist = static_cast<uint32_t>(dq_q - (accp + tau_q));
-                            const uint64_t key = (static_cast<uint64_t>(dist) << 32) | static_cast<uint64_t>(p.row_offset + doc);
-                            if (doc < p.n && key < thr) {
-                                int cnt = __shfl_sync(0xffffffffu, st.count, ql);
-                                uint64_t *row = lists + static_cast<int64_t>(ql) * p.cap;
-                                if (lane == 0) row[cnt] = key;
-                                ++cnt;
-                                if (cnt == p.cap) {
-                                    int nv;
-                                    cnt = compact_row(row, scratch, cnt, p.k, ql, lane, st, &nv);
+                    for (int r = 0; r < RCH; ++r) {
+                        const uint4 v = src[r * 32];
+                        bw[4 * r] = v.x; bw[4 * r + 1] = v.y; bw[4 * r + 2] = v.z; bw[4 * r + 3] = v.w;
+                    }
+                    // acc' = sum_k x_k (2 y_k - Aq) - tau; k-step s2 = 4h + e uses words (nt*C + h)*8 + 2e, +1
+                    int c[MT][NT][4];
 #pragma unroll
-                                    for (int m2 = 0; m2 < MT; ++m2) {
-                                        if (16 * m2 + g == ql) negtau[m2][0] = nv;
-                                        if (16 * m2 + g + 8 == ql) negtau[m2][1] = nv;
+                    for (int s2 = 0; s2 < KS; ++s2)
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                            for (int nt = 0; nt < NT; ++nt) {
+                                const uint32_t b0 = bw[(nt * C + (s2 >> 2)) * 8 + 2 * (s2 & 3)];
+                                const uint32_t b1 = bw[(nt * C + (s2 >> 2)) * 8 + 2 * (s2 & 3) + 1];
+                                if (s2 == 0) imma(c[mt][nt], a[mt][s2], b0, b1, negtau[mt][0], negtau[mt][0], negtau[mt][1], negtau[mt][1]);
+                                else imma(c[mt][nt], a[mt][s2], b0, b1, c[mt][nt][0], c[mt][nt][1], c[mt][nt][2], c[mt][nt][3]);
+                            }
+                    // any score with acc' >= 0 ?  (the AND of all results has a clear sign bit)
+                    int all = -1;
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) all &= c[mt][nt][0] & c[mt][nt][1] & c[mt][nt][2] & c[mt][nt][3];
+                    if (__any_sync(0xffffffffu, all >= 0)) {
+                        // slow path: lanes append their own hits; a row gains at most TILE keys per
+                        // iteration and is compacted as soon as fewer than TILE slots remain
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    const int v = c[mt][nt][j];
+                                    if (v >= 0) {
+                                        const int64_t doc = it * TILE + 8 * nt + 2 * t + (j & 1);
+                                        if (doc < p.n) {
+                                            const int row = 16 * mt + g + 8 * (j >> 1);
+                                            const uint32_t dist = static_cast<uint32_t>(dqrow[mt][j >> 1] + negtau[mt][j >> 1] - v);
+                                            const int pos = atomicAdd(&cnt_s[row], 1);
+                                            lists[static_cast<int64_t>(row) * p.cap + pos] =
+                                                (static_cast<uint64_t>(dist) << 32) | static_cast<uint64_t>(p.row_offset + doc);
+                                        }
                                     }
-                                } else if (lane == ql) {
-                                    st.count = cnt;
                                 }
+                        __syncwarp();
+                        unsigned need = __ballot_sync(0xffffffffu, lane < QPW && cnt_s[lane] > p.cap - TILE);
+                        while (need) {
+                            const int ql = __ffs(need) - 1;
+                            need &= need - 1;
+                            const int nv = compact_row(lists + static_cast<int64_t>(ql) * p.cap, scratch, &cnt_s[ql], p.k, ql, lane, st);
+#pragma unroll
+                            for (int mt = 0; mt < MT; ++mt) {
+                                if (16 * mt + g == ql) negtau[mt][0] = nv;
+                                if (16 * mt + g + 8 == ql) negtau[mt][1] = nv;
                             }
                         }
                     }
+                }
+            }
+            __syncthreads();
         }
-    }
 
-    // ---- emit: every query row of this warp, sorted, KEY_INF padded
-    const int64_t part = static_cast<int64_t>(blockIdx.x) * p.DW + dw;
-    for (int ql = 0; ql < QPW; ++ql) {
-        const int64_t q = q0 + ql;
-        if (q >= p.nq) break;
-        const int cnt = __shfl_sync(0xffffffffu, st.count, ql);
-        uint64_t *row = lists + static_cast<int64_t>(ql) * p.cap;
-        __syncwarp();
-        int P = 2;
-        while (P < cnt) P <<= 1;
-        for (int i = lane; i < P; i += 32) scratch[i] = i < cnt ? __ldcg(row + i) : KEY_INF;
-        __syncwarp();
-        warp_bitonic(scratch, P, lane);
-        uint64_t *dst = p.out + (part * p.nq + q) * p.k;
-        for (int i = lane; i < p.k; i += 32) dst[i] = (i < cnt && i < P) ? scratch[i] : KEY_INF;
-        __syncwarp();
+        // ---- emit: every query row of this warp, sorted, KEY_INF padded
+        if (has_q) {
+            __syncwarp();
+            for (int ql = 0; ql < QPW; ++ql) {
+                const int64_t q = q0 + ql;
+                if (q >= p.nq) break;
+                const int cnt = cnt_s[ql];
+                const uint64_t *row = lists + static_cast<int64_t>(ql) * p.cap;
+                int P = 2;
+                while (P < cnt) P <<= 1;
+                for (int i = lane; i < P; i += 32) scratch[i] = i < cnt ? __ldcg(row + i) : KEY_INF;
+                __syncwarp();
+                warp_bitonic(scratch, P, lane);
+                uint64_t *dst = p.out + (part * p.nq + q) * p.k;
+                for (int i = lane; i < p.k; i += 32) dst[i] = i < cnt ? scratch[i] : KEY_INF;
+                __syncwarp();
+            }
+        }
+        __syncthreads();
     }
+}
+
+// tau_init[q] = Dq - distance(k-th key of a sample scan), or TAU_OPEN when the sample had < k rows.
+__global__ void tau_from_keys_kernel(const uint64_t *__restrict__ keys, const int32_t *__restrict__ qconst,
+                                     int64_t nq, int k, int32_t *__restrict__ tau) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= nq) return;
+    const uint64_t kth = keys[q * k + (k - 1)];
+    tau[q] = kth == KEY_INF ? TAU_OPEN : qconst[q] - static_cast<int32_t>(kth >> 32);
 }
 
 }  // namespace mma

@@ -132,7 +132,8 @@ def test_synthetic_configs_match_reference(name):
         assert res.threshold_distance == int(z["thr"][qi]) and res.candidate_count == int(z["cand"][qi])
 
 
-@pytest.mark.parametrize("env", [{"XFBQ_FORCE_GENERIC": "1"}, {"XFBQ_SPLITS": "1"}, {"XFBQ_SPLITS": "7"},
+@pytest.mark.parametrize("env", [{"XFBQ_FORCE_GENERIC": "1"}, {"XFBQ_GRID": "1"}, {"XFBQ_GRID": "7"},
+                                 {"XFBQ_SAMPLE": "0"}, {"XFBQ_SAMPLE": "2048"}, {"XFBQ_SAMPLE": "2048", "XFBQ_GRID": "3"},
                                  {"XFBQ_ENGINE": "popc"}, {"XFBQ_ENGINE": "popc", "XFBQ_TQ": "1"},
                                  {"XFBQ_ENGINE": "popc", "XFBQ_TQ": "5", "XFBQ_SPLITS": "3"}])
 def test_scan_plans_agree(env, monkeypatch):

@@ -8,6 +8,9 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,memory.total --fo
 for s in $STAGES; do
   case $s in
     smoke) timeout 600 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" ;;
+    micro2) timeout 120 tools/bin/microbench2 > gpurun_out/microbench2.jsonl 2>&1; echo "micro2 rc=$?" ;;
+    ncumma) timeout 900 ncu --set full --clock-control none --import-source on -k regex:scan_kernel -c 2 -f -o gpurun_out/prof_mma \
+           python bench.py --steps 1 --warmup 1 --nq 2048 --no-cpu-baseline --no-extras > gpurun_out/ncumma.log 2>&1; echo "ncumma rc=$?" ;;
     micro) timeout 120 tools/bin/microbench > gpurun_out/microbench.jsonl 2>&1; echo "micro rc=$?" ;;
     tests) timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "tests rc=$?"; tail -5 gpurun_out/pytest_gpu.log ;;
     bench) timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json ;;
