@@ -451,32 +451,34 @@ merge_topk_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k,
 // rows A, B of length K2 reduce to the K2 smallest of their union by c_i = min(A_i, B_{K2-1-i})
 // (a bitonic sequence) followed by log2(K2) bitonic-merge stages; log2(G) rounds leave the answer
 // in row 0.  Far fewer barrier stages than re-sorting, so single-query latency stays small.
+template <int K2>
 __global__ void __launch_bounds__(512)
-merge_tree_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k, int K2, int G,
+merge_tree_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k, int G,
                   uint64_t *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t *buf = reinterpret_cast<uint64_t *>(smem_raw);
     const int64_t q = blockIdx.y;
     const int p0 = blockIdx.x * G;
-    int rows = min(G, parts - p0);
+    const int rows = min(G, parts - p0);
     int active = 1;
     while (active < rows) active <<= 1;
     for (int idx = threadIdx.x; idx < active * K2; idx += blockDim.x) {
-        const int r = idx / K2, i = idx - r * K2;
+        const int r = idx / K2, i = idx % K2;
         buf[idx] = (r < rows && i < k) ? in[((static_cast<int64_t>(p0) + r) * nq + q) * k + i] : KEY_INF;
     }
     __syncthreads();
     while (active > 1) {
         const int half = active >> 1;
         for (int idx = threadIdx.x; idx < half * K2; idx += blockDim.x) {
-            const int r = idx / K2, i = idx - r * K2;
+            const int r = idx / K2, i = idx % K2;
             const uint64_t a = buf[r * K2 + i], b = buf[(r + half) * K2 + (K2 - 1 - i)];
             buf[r * K2 + i] = a < b ? a : b;
         }
         __syncthreads();
+#pragma unroll 1
         for (int stride = K2 >> 1; stride > 0; stride >>= 1) {
             for (int idx = threadIdx.x; idx < half * (K2 >> 1); idx += blockDim.x) {
-                const int r = idx / (K2 >> 1), t = idx - r * (K2 >> 1);
+                const int r = idx / (K2 >> 1), t = idx % (K2 >> 1);
                 const int lo = r * K2 + 2 * t - (t & (stride - 1));
                 const int hi = lo + stride;
                 const uint64_t a = buf[lo], b = buf[hi];
@@ -578,7 +580,7 @@ int merge_k2(int k) {
 }
 
 // Parts one tree-merge CTA can hold in shared memory (power of two), 0 if K2 is too large.
-int merge_group(int k) {
+int merge_group_max(int k) {
     const int K2 = merge_k2(k);
     int G = (160 * 1024) / (K2 * 8);
     if (G < 2) return 0;
@@ -598,43 +600,81 @@ int launch_merge_stream(const uint64_t *in, int parts, int64_t nq, int k, uint64
     return check_launch("merge_topk_kernel");
 }
 
-// Number of intermediate rows-of-parts buffers a multi-level tree merge needs (elements of
-// [groups][nq][k] each); scratch must hold merge_scratch_parts(parts, k) * nq * k keys.
-int64_t merge_scratch_parts(int parts, int k) {
-    const int G = merge_group(k);
-    if (G == 0 || parts <= G) return 0;
-    const int64_t l1 = (parts + G - 1) / G;
-    const int64_t l2 = (l1 + G - 1) / G;
-    return l1 + (l1 > G ? l2 : 0);
+// Level plan of the tree merge: parts per CTA (G) and resulting groups per level.  Small query
+// counts use small groups so the first level still spreads over the whole chip.
+struct MergeLevels {
+    int levels = 0;
+    int G[8], groups[8];
+    int64_t scratch_parts = 0;  // sum of groups over the non-final levels
+};
+
+MergeLevels merge_levels(int parts, int k, int64_t nq) {
+    MergeLevels ml;
+    const int gmax = merge_group_max(k);
+    if (gmax == 0 || parts <= 1) return ml;
+    (void)nq;
+    while (parts > 1 && ml.levels < 8) {
+        // the level before the last one uses the smallest groups that still let the last level
+        // finish in one CTA per query, so that it spreads over many SMs
+        int G = gmax;
+        if (parts > gmax && parts <= gmax * gmax) {
+            G = 4;
+            while ((parts + G - 1) / G > gmax) G <<= 1;
+        }
+        const int groups = (parts + G - 1) / G;
+        ml.G[ml.levels] = G; ml.groups[ml.levels] = groups;
+        if (groups > 1) ml.scratch_parts += groups;
+        ++ml.levels;
+        parts = groups;
+    }
+    return ml;
+}
+
+int64_t merge_scratch_parts(int parts, int k, int64_t nq) { return merge_levels(parts, k, nq).scratch_parts; }
+
+typedef void (*MergeKernel)(const uint64_t *, int, int64_t, int, int, uint64_t *);
+
+MergeKernel pick_merge_kernel(int K2) {
+    switch (K2) {
+        case 32: return merge_tree_kernel<32>;
+        case 64: return merge_tree_kernel<64>;
+        case 128: return merge_tree_kernel<128>;
+        case 256: return merge_tree_kernel<256>;
+        case 512: return merge_tree_kernel<512>;
+        case 1024: return merge_tree_kernel<1024>;
+        case 2048: return merge_tree_kernel<2048>;
+        case 4096: return merge_tree_kernel<4096>;
+    }
+    return nullptr;
 }
 
 int launch_merge(const uint64_t *in, int parts, int64_t nq, int k, uint64_t *out, uint64_t *scratch,
                  cudaStream_t st) {
-    const int G = merge_group(k);
-    if (nq > 65535 || G == 0 || (parts > G && !scratch)) return launch_merge_stream(in, parts, nq, k, out, st);
+    const MergeLevels ml = merge_levels(parts, k, nq);
+    if (nq > 65535 || ml.levels == 0 || parts <= 1 || (ml.scratch_parts > 0 && !scratch) || ml.groups[ml.levels - 1] != 1)
+        return launch_merge_stream(in, parts, nq, k, out, st);
     const int K2 = merge_k2(k);
-    uint64_t *bufs[2] = {scratch, scratch ? scratch + ((parts + G - 1) / G) * nq * k : nullptr};
-    int level = 0;
-    while (true) {
-        const int groups = (parts + G - 1) / G;
+    MergeKernel kern = pick_merge_kernel(K2);
+    for (int l = 0; l < ml.levels; ++l) {
+        const int G = ml.G[l], groups = ml.groups[l];
         int rows = parts < G ? parts : G, active = 1;
         while (active < rows) active <<= 1;
         const size_t smem = static_cast<size_t>(active) * K2 * 8;
         if (smem > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(merge_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
             if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "merge smem opt-in: %s", cudaGetErrorString(e));
         }
-        uint64_t *dst = groups == 1 ? out : bufs[level & 1];
-        if (groups > 1 && level >= 2) return fail(XFBQ_E_UNSUPPORTED, "merge depth exceeded (parts=%d)", parts);
-        int threads = active * K2 / 2;
+        uint64_t *dst = groups == 1 ? out : scratch;
+        int threads = active * K2 / 4;
         threads = threads < 64 ? 64 : (threads > 512 ? 512 : threads);
-        merge_tree_kernel<<<dim3(static_cast<unsigned>(groups), static_cast<unsigned>(nq)), threads, smem, st>>>(in, parts, nq, k, K2, G, dst);
+        kern<<<dim3(static_cast<unsigned>(groups), static_cast<unsigned>(nq)), threads, smem, st>>>(in, parts, nq, k, G, dst);
         if (int rc = check_launch("merge_tree_kernel")) return rc;
         if (groups == 1) return XFBQ_OK;
         in = dst;
+        scratch += static_cast<int64_t>(groups) * nq * k;
         parts = groups;
-        ++level;
     }
+    return XFBQ_OK;
 }
 
 // ----------------------------------------------------------------------------------------------
@@ -642,6 +682,8 @@ int launch_merge(const uint64_t *in, int parts, int64_t nq, int k, uint64_t *out
 // ----------------------------------------------------------------------------------------------
 struct MmaShape {  // launch geometry of one mma::scan_kernel launch over n documents
     int MT = 2, NT = 2, QPW = 32, QW = 8, DW = 1, groups = 1, grid = 1, slots = 1, parts = 1, cap = 0;
+    int RR = 0, BR = 0;  // ring depths (RR = 0: does not fit in shared memory)
+    bool fused = false;  // one query warp: tiles go raw ring -> registers -> IMMA, no byte ring
     int64_t stages = 0, nq_pad = 0, n_pad = 0;
     size_t smem = 0, lists_bytes = 0, parts_bytes = 0, mscratch_bytes = 0;
 };
@@ -656,8 +698,9 @@ struct MmaPlan {
 
 typedef void (*MmaKernel)(const mma::Params);
 
-MmaKernel pick_mma_kernel(int wd, int C) {
-#define XFBQ_MMA_CASE(WD_, C_, MT_, NT_) if (wd == WD_ && C == C_) return mma::scan_kernel<WD_, C_, MT_, NT_>;
+MmaKernel pick_mma_kernel(int wd, int C, bool fused) {
+#define XFBQ_MMA_CASE(WD_, C_, MT_, NT_) \
+    if (wd == WD_ && C == C_) return fused ? mma::scan_kernel<WD_, C_, MT_, NT_, true> : mma::scan_kernel<WD_, C_, MT_, NT_, false>;
     XFBQ_MMA_CASE(1, 1, 2, 2) XFBQ_MMA_CASE(2, 1, 2, 2) XFBQ_MMA_CASE(3, 1, 2, 2) XFBQ_MMA_CASE(4, 1, 2, 2)
     XFBQ_MMA_CASE(1, 2, 2, 2) XFBQ_MMA_CASE(2, 2, 2, 2) XFBQ_MMA_CASE(3, 2, 2, 2) XFBQ_MMA_CASE(4, 2, 2, 2)
     XFBQ_MMA_CASE(1, 4, 1, 1) XFBQ_MMA_CASE(2, 4, 1, 1) XFBQ_MMA_CASE(3, 4, 1, 1) XFBQ_MMA_CASE(4, 4, 1, 1)
@@ -667,7 +710,8 @@ MmaKernel pick_mma_kernel(int wd, int C) {
 
 inline size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
 
-void mma_shape(int64_t n, int C, int64_t nq, int k, int sms, MmaShape *out) {
+void mma_shape(int64_t n, int wd, int C, int64_t nq, int k, const DeviceInfo &info, MmaShape *out) {
+    const int sms = info.sms;
     MmaShape sh;
     sh.MT = C == 4 ? 1 : 2;
     sh.NT = C == 4 ? 1 : 2;
@@ -706,11 +750,23 @@ void mma_shape(int64_t n, int C, int64_t nq, int k, int sms, MmaShape *out) {
     }
     sh.slots = slots;
     sh.parts = slots * sh.DW;
-    const int WPL = sh.NT * C * 8;
-    sh.smem = static_cast<size_t>(2) * mma::STAGE_ITERS * WPL * 32 * 4 + static_cast<size_t>(mma::WARPS) * cap * 8 + mma::WARPS * 32 * 4;
+    const int raw_stage = (mma::STAGE_ITERS * 8 * sh.NT / 32) * wd * C * 512;
+    const int byte_stage = mma::STAGE_ITERS * (sh.NT * C * 8) * 32 * 4;
+    sh.fused = sh.QW == 1 && sh.groups == 1 && env_int("XFBQ_NO_FUSED", 0) == 0;
+    int RR = env_int("XFBQ_RAW_STAGES", sh.fused ? 8 : 6), BR = sh.fused ? 0 : env_int("XFBQ_BYTE_STAGES", 4);
+    const int br_min = sh.fused ? 0 : mma::AHEAD + 1;
+    if (BR < br_min) BR = br_min;
+    if (RR < 1) RR = 1;
+    const size_t budget = static_cast<size_t>(info.smem_optin) - 1024;
+    while (mma::smem_layout(raw_stage, byte_stage, RR, BR, cap).total > budget && RR > 2) --RR;
+    while (mma::smem_layout(raw_stage, byte_stage, RR, BR, cap).total > budget && BR > br_min) --BR;
+    while (mma::smem_layout(raw_stage, byte_stage, RR, BR, cap).total > budget && RR > 1) --RR;
+    if (mma::smem_layout(raw_stage, byte_stage, RR, BR, cap).total > budget) RR = BR = 0;
+    sh.RR = RR; sh.BR = BR;
+    sh.smem = RR ? mma::smem_layout(raw_stage, byte_stage, RR, BR, cap).total : 0;
     sh.lists_bytes = static_cast<size_t>(sh.grid) * mma::WARPS * sh.QPW * cap * 8;
     sh.parts_bytes = sh.parts > 1 ? static_cast<size_t>(sh.parts) * nq * k * 8 : 0;
-    sh.mscratch_bytes = static_cast<size_t>(merge_scratch_parts(sh.parts, k)) * nq * k * 8;
+    sh.mscratch_bytes = static_cast<size_t>(merge_scratch_parts(sh.parts, k, nq)) * nq * k * 8;
     *out = sh;
 }
 
@@ -727,15 +783,20 @@ int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, Mma
     DeviceInfo info;
     if (int rc = device_info(&info)) return rc;
     pl.ok = true;
-    mma_shape(n, C, nq, k, info.sms, &pl.main);
+    mma_shape(n, wd, C, nq, k, info, &pl.main);
+    if (pl.main.RR == 0) {  // rings + sort scratch do not fit: leave it to the POPC engine
+        pl.ok = false;
+        *plan = pl;
+        return XFBQ_OK;
+    }
     // Small batches split the documents over every warp of the chip, so each candidate list sees
     // few documents and its own threshold tightens slowly; a sample scan of the first S documents
     // gives all of them a threshold of selectivity ~k/S up front.
     int64_t sample = env_int("XFBQ_SAMPLE", -1);
-    if (sample < 0) sample = (pl.main.groups == 1 && pl.main.DW > 1) ? 32768 : 0;
+    if (sample < 0) sample = (pl.main.groups == 1 && pl.main.DW > 1 && nq > 4) ? 32768 : 0;
     if (sample > 0 && (n < 16 * sample || sample < 4 * k)) sample = 0;
     pl.sample = sample;
-    if (sample) mma_shape(sample, C, nq, k, info.sms, &pl.pre);
+    if (sample) mma_shape(sample, wd, C, nq, k, info, &pl.pre);
     size_t off = 0;
     pl.off_qop = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 32 * C * 4);
     pl.off_qconst = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 4);
@@ -752,7 +813,7 @@ int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, Mma
 // One scan launch (+ merge of its part slots) over the first n documents of db.
 int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const void *db, int64_t n, int wd, int C,
                  int64_t nq, int k, int64_t row_offset, const int32_t *tau_init, uint64_t *keys_out, cudaStream_t st) {
-    MmaKernel kern = pick_mma_kernel(wd, C);
+    MmaKernel kern = pick_mma_kernel(wd, C, sh.fused);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh.smem));
     if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "mma scan smem opt-in (%zu bytes): %s", sh.smem, cudaGetErrorString(e));
     mma::Params p;
@@ -765,11 +826,12 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
     p.out = sh.parts > 1 ? reinterpret_cast<uint64_t *>(ws + pl.off_parts) : keys_out;
     p.nq = nq; p.stages = sh.stages; p.groups = sh.groups;
     p.k = k; p.cap = sh.cap; p.QW = sh.QW; p.DW = sh.DW;
+    p.RR = sh.RR; p.BR = sh.BR;
     if (sh.parts > 1) {  // slots a group does not use stay KEY_INF
         e = cudaMemsetAsync(p.out, 0xFF, sh.parts_bytes, st);
         if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
     }
-    kern<<<static_cast<unsigned>(sh.grid), mma::THREADS, sh.smem, st>>>(p);
+    kern<<<static_cast<unsigned>(sh.grid), mma::THREADS + 32, sh.smem, st>>>(p);
     if (int rc = check_launch("mma::scan_kernel")) return rc;
     if (sh.parts > 1)
         return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st);
@@ -910,7 +972,7 @@ XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64
     ScanPlan pl;
     if (make_plan(n, dim, wd, nq, wq, k, &pl)) return -1;
     if (pl.splits <= 1) return 0;
-    return static_cast<int64_t>(pl.splits + merge_scratch_parts(pl.splits, k)) * nq * k * 8;
+    return static_cast<int64_t>(pl.splits + merge_scratch_parts(pl.splits, k, nq)) * nq * k * 8;
 }
 
 XFBQ_API int xfbq_scan_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, int32_t out[6]) {
@@ -973,7 +1035,7 @@ XFBQ_API int xfbq_scan_topk(const void *db, int64_t n, int64_t dim, int wd, cons
     }
     ScanPlan pl;
     if (int rc = make_plan(n, dim, wd, nq, wq, k, &pl)) return rc;
-    const int64_t need = pl.splits <= 1 ? 0 : static_cast<int64_t>(pl.splits + merge_scratch_parts(pl.splits, k)) * nq * k * 8;
+    const int64_t need = pl.splits <= 1 ? 0 : static_cast<int64_t>(pl.splits + merge_scratch_parts(pl.splits, k, nq)) * nq * k * 8;
     if (need > 0 && (!workspace || workspace_bytes < need))
         return fail(XFBQ_E_INVALID, "workspace too small: need %lld bytes, got %lld", (long long)need, (long long)workspace_bytes);
     const int C = static_cast<int>(chunks128(dim));

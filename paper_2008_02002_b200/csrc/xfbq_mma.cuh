@@ -9,14 +9,14 @@
 // ~60x faster than the POPC pipe can popcount the 16 plane pairs (profiles/microbench_r1.jsonl:
 // XU/POPC 4.5 T lane-ops/s vs IMMA 568 T MAC/s).  Results are bit-identical to the POPC form.
 //
-// Data flow of one CTA (8 warps), per stage of 8 iterations x TILE = 8*NT documents:
+// Data flow of one CTA (8 worker warps + 1 TMA issuer warp), per stage of 8 iterations x TILE =
+// 8*NT documents (whole bundles, contiguous in HBM, fetched by one cp.async.bulk per stage):
 //   * queries: 16*MT query rows per warp live in registers as A fragments (s8 weights 2y-Aq,
 //     laid out by prep_queries_kernel in exactly the K-order the document side produces);
-//   * documents: warp w reads iteration w of the stage straight from the bit-plane bundle layout
-//     (one 128-byte line per plane chunk per 8-doc tile), transposes it in registers from bit
-//     planes to one byte per dimension (4x4 bit-block transpose by delta swaps + nibble split)
-//     and stores the B fragments to a double-buffered shared-memory stage, so a tile is
-//     transposed once per CTA however many query warps consume it;
+//   * documents: warp w reads iteration w of the raw stage (bit-plane bundle layout) from shared
+//     memory, transposes it in registers from bit planes to one byte per dimension (4x4 bit-block
+//     transpose by delta swaps + nibble split) and stores the B fragments to a ring of byte
+//     stages, so a tile is transposed once per CTA however many query warps consume it;
 //   * every (query-warp, doc-warp) consumes its iterations of the stage: 8 LDS.128 + MT*NT*4C
 //     IMMAs; the accumulator is initialised to -tau_q, so "distance <= threshold" is the sign
 //     bit of the result and one AND-reduction + vote per TILE x 16*MT scores decides whether the
@@ -49,6 +49,7 @@ struct Params {
     int64_t stages;           // ceil(n_pad / (STAGE_ITERS * TILE))
     int groups;               // query groups of QW * 16*MT queries
     int k, cap, QW, DW;
+    int RR, BR;               // ring depths: raw (TMA) stages, byte (B fragment) stages
 };
 
 // ------------------------------------------------------------------------------ query operand
@@ -187,24 +188,93 @@ __device__ __forceinline__ int compact_row(uint64_t *list_row, uint64_t *scratch
     return -__shfl_sync(0xffffffffu, st.tau, ql);
 }
 
-template <int WD, int C, int MT, int NT>
-__global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+// ------------------------------------------------------------------------------ mbarrier / TMA
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+// TMA bulk copy global -> shared (1-D, contiguous), completion signalled on `bar` as tx bytes.
+__device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+constexpr int AHEAD = 2;  // stages a worker transposes ahead of the stage it consumes
+
+// Shared-memory carve-up shared by host (size) and device (pointers).
+struct SmemLayout {
+    uint32_t raw_off, byte_off, scratch_off, cnt_off, bar_off, total;
+};
+__host__ __device__ inline SmemLayout smem_layout(int raw_stage_bytes, int byte_stage_bytes, int RR, int BR, int cap) {
+    SmemLayout L;
+    uint32_t off = 0;
+    L.raw_off = off; off += static_cast<uint32_t>(RR) * raw_stage_bytes;
+    off = (off + 127u) & ~127u;
+    L.byte_off = off; off += static_cast<uint32_t>(BR) * byte_stage_bytes;
+    L.scratch_off = off; off += static_cast<uint32_t>(WARPS) * cap * 8;
+    L.cnt_off = off; off += WARPS * 32 * 4;
+    L.bar_off = off; off += static_cast<uint32_t>(2 * RR + 2 * BR) * 8;
+    L.total = off;
+    return L;
+}
+
+// Ring cursor: slot index and the mbarrier phase parity to wait on; no divisions in the hot loop.
+struct Ring {
+    int idx;
+    uint32_t phase;
+    __device__ __forceinline__ void advance(int n) {
+        if (++idx == n) { idx = 0; phase ^= 1u; }
+    }
+};
+
+// One CTA = 8 worker warps + 1 issuer warp.
+//   issuer : streams this CTA's document stages HBM -> raw ring with TMA bulk copies (RR deep)
+//   ring mode (FUSED = false; several query warps share each document tile):
+//     worker w: [transpose] its iteration slot of stage i+AHEAD: raw ring -> byte ring (B fragments)
+//               [consume]   its iterations of stage i: byte ring -> IMMA -> threshold filter -> lists
+//   fused mode (FUSED = true; QW == 1, every tile is consumed by exactly one warp):
+//     worker w: raw ring -> registers (transpose) -> IMMA -> filter, no byte ring
+// Hand-offs are mbarriers (raw_full/raw_empty, byte_full/byte_empty), so a warp that runs a list
+// compaction only stalls the others once the rings' slack is used up (no per-stage block barrier).
+template <int WD, int C, int MT, int NT, bool FUSED>
+__global__ void __launch_bounds__(THREADS + 32, 1) scan_kernel(const Params p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int QPW = 16 * MT;        // query rows per warp
     constexpr int KS = 4 * C;           // k-steps of 32 dims
     constexpr int TILE = 8 * NT;        // documents per iteration
     constexpr int WPL = NT * C * 8;     // B-fragment words per lane per iteration
     constexpr int RCH = WPL / 4;        // 16-byte chunks per lane per iteration
-    constexpr int STAGE_WORDS = STAGE_ITERS * WPL * 32;
+    constexpr int STAGE_DOCS = STAGE_ITERS * TILE;
+    constexpr int RAW_STAGE_BYTES = (STAGE_DOCS / 32) * WD * C * 512;  // whole bundles, contiguous in HBM
+    constexpr int BYTE_STAGE_BYTES = STAGE_ITERS * WPL * 32 * 4;
+    static_assert(STAGE_DOCS % 32 == 0, "a stage must be whole bundles");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane >> 2, t = lane & 3;
-    const int qw = warp % p.QW, dw = warp / p.QW;
-
-    // shared memory: [2 stages of B fragments][per-warp sort scratch][per-warp row counters]
-    uint4 *stage_mem = reinterpret_cast<uint4 *>(smem_raw);
-    uint64_t *scratch = reinterpret_cast<uint64_t *>(smem_raw + 2 * STAGE_WORDS * 4) + static_cast<size_t>(warp) * p.cap;
-    int *cnt_s = reinterpret_cast<int *>(smem_raw + 2 * STAGE_WORDS * 4 + static_cast<size_t>(WARPS) * p.cap * 8) + warp * 32;
-    uint64_t *lists = p.lists + (static_cast<int64_t>(blockIdx.x) * WARPS + warp) * QPW * static_cast<int64_t>(p.cap);
+    const int RR = p.RR, BR = p.BR;
+    const SmemLayout L = smem_layout(RAW_STAGE_BYTES, BYTE_STAGE_BYTES, RR, BR, p.cap);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + L.bar_off);
+    uint64_t *raw_full = bars, *raw_empty = bars + RR, *byte_full = bars + 2 * RR, *byte_empty = bars + 2 * RR + BR;
 
     // ---- this CTA's share of the linearised (group, stage) work
     const int64_t T = p.stages;
@@ -212,62 +282,112 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     const int64_t G = gridDim.x;
     const int64_t lin_begin = static_cast<int64_t>(blockIdx.x) * W / G;
     const int64_t lin_end = (static_cast<int64_t>(blockIdx.x) + 1) * W / G;
+    const int S = static_cast<int>(lin_end - lin_begin);  // stages this CTA streams
+    const int gr_begin = static_cast<int>(lin_begin / T);
+    const int sd_begin = static_cast<int>(lin_begin - static_cast<int64_t>(gr_begin) * T);
+    const int Ti = static_cast<int>(T);
 
-    // lane (g, t) of tile nt reads, for every plane, the C words [C*t, C*t+C) of document 8*nt+g
-    auto tile_ptr = [&](int64_t it, int nt, int i) -> const uint32_t * {
-        const int64_t doc = it * TILE + 8 * nt + g;
-        const int64_t b = doc >> 5;
-        const int dl = static_cast<int>(doc & 31);
-        const int word = C * t;
-        return p.db + ((((b * WD + i) * C + (word >> 2)) * 32 + dl) << 2) + (word & 3);
-    };
-    uint32_t pw[NT][WD][C];
-    auto load_raw = [&](int64_t stage) {  // this warp's iteration of `stage` -> pw
-        const int64_t it = stage * STAGE_ITERS + warp;
-        const bool ok = (it + 1) * TILE <= p.n_pad;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < RR; ++i) { mbar_init(&raw_full[i], 1); mbar_init(&raw_empty[i], WARPS); }
+        for (int i = 0; i < BR; ++i) { mbar_init(&byte_full[i], WARPS); mbar_init(&byte_empty[i], WARPS); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == WARPS) {
+        // ================================ issuer warp ================================
+        if (lane == 0) {
+            const int64_t db_bytes = (p.n_pad / 32) * static_cast<int64_t>(WD * C * 512);
+            Ring rr{0, 1u};  // "empty" waits start on the phase that counts as already completed
+            int sd = sd_begin;
+            for (int idx = 0; idx < S; ++idx) {
+                mbar_wait(&raw_empty[rr.idx], rr.phase);
+                const int64_t off = static_cast<int64_t>(sd) * RAW_STAGE_BYTES;
+                int64_t bytes = db_bytes - off;
+                if (bytes > RAW_STAGE_BYTES) bytes = RAW_STAGE_BYTES;
+                mbar_arrive_expect_tx(&raw_full[rr.idx], static_cast<uint32_t>(bytes));
+                tma_bulk_g2s(smem_raw + L.raw_off + static_cast<size_t>(rr.idx) * RAW_STAGE_BYTES,
+                             reinterpret_cast<const unsigned char *>(p.db) + off, static_cast<uint32_t>(bytes), &raw_full[rr.idx]);
+                rr.advance(RR);
+                if (++sd == Ti) sd = 0;
+            }
+        }
+        return;
+    }
+
+    // ================================ worker warps ================================
+    const int g = lane >> 2, t = lane & 3;
+    const int qw = FUSED ? 0 : warp % p.QW, dw = FUSED ? warp : warp / p.QW;
+    const int DW = FUSED ? WARPS : p.DW;
+    uint64_t *scratch = reinterpret_cast<uint64_t *>(smem_raw + L.scratch_off) + static_cast<size_t>(warp) * p.cap;
+    int *cnt_s = reinterpret_cast<int *>(smem_raw + L.cnt_off) + warp * 32;
+    uint64_t *lists = p.lists + (static_cast<int64_t>(blockIdx.x) * WARPS + warp) * QPW * static_cast<int64_t>(p.cap);
+
+    // raw stage -> plane words of this warp's iteration slot: lane (g, t) owns, for every plane,
+    // the C words [C*t, C*t+C) of document warp*TILE + 8*nt + g
+    auto load_planes = [&](int r, uint32_t (&pw)[NT][WD][C]) {
+        const uint32_t *raw = reinterpret_cast<const uint32_t *>(smem_raw + L.raw_off + static_cast<size_t>(r) * RAW_STAGE_BYTES);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
+        for (int nt = 0; nt < NT; ++nt) {
+            const int doc = warp * TILE + 8 * nt + g;
+            const int word = C * t;
 #pragma unroll
             for (int i = 0; i < WD; ++i) {
-                if (ok) load_quarter<C>(tile_ptr(it, nt, i), pw[nt][i]);
-                else {
-#pragma unroll
-                    for (int h = 0; h < C; ++h) pw[nt][i][h] = 0u;
-                }
+                const uint32_t *src = raw + (((((doc >> 5) * WD + i) * C + (word >> 2)) * 32 + (doc & 31)) << 2) + (word & 3);
+                if (C == 1) pw[nt][i][0] = src[0];
+                else if (C == 2) { const uint2 v = *reinterpret_cast<const uint2 *>(src); pw[nt][i][0] = v.x; pw[nt][i][C > 1 ? 1 : 0] = v.y; }
+                else { const uint4 v = *reinterpret_cast<const uint4 *>(src); pw[nt][i][0] = v.x; pw[nt][i][C > 1 ? 1 : 0] = v.y; pw[nt][i][C > 2 ? 2 : 0] = v.z; pw[nt][i][C > 3 ? 3 : 0] = v.w; }
             }
+        }
     };
-    auto produce = [&](int buf) {  // pw -> byte operands -> stage buffer, slot = this warp's iteration
-        uint4 *dst = stage_mem + (static_cast<size_t>(buf) * STAGE_ITERS + warp) * (RCH * 32) + lane;
+    auto planes_to_fragments = [&](const uint32_t (&pw)[NT][WD][C], uint32_t (&bw)[WPL]) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int h = 0; h < C; ++h) {
-                uint32_t pin[4], bw[8];
+                uint32_t pin[4], o[8];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) pin[i] = i < WD ? pw[nt][i < WD ? i : 0][h] : 0u;
-                planes_to_bytes<WD>(pin, bw);
-                const int r = (nt * C + h) * 2;
-                dst[r * 32] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
-                dst[(r + 1) * 32] = make_uint4(bw[4], bw[5], bw[6], bw[7]);
+                planes_to_bytes<WD>(pin, o);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) bw[(nt * C + h) * 8 + e] = o[e];
             }
     };
 
-    for (int64_t lin = lin_begin; lin < lin_end;) {
-        const int gr = static_cast<int>(lin / T);
-        const int64_t s_begin = lin - static_cast<int64_t>(gr) * T;
-        const int64_t s_end = min(T, s_begin + (lin_end - lin));
-        lin += s_end - s_begin;
-        // part slot of this segment: CTAs overlapping group gr are numbered from the first one
+    // per-segment state
+    int64_t q0 = 0, part = 0;
+    bool has_q = false;
+    uint32_t a[MT][KS][4];
+    LaneState st;
+    st.dq = 0; st.tau = 1;
+    int negtau[MT][2], dqrow[MT][2];
+
+    auto emit_segment = [&]() {  // every query row of this warp, sorted, KEY_INF padded
+        if (!has_q) return;
+        __syncwarp();
+        for (int ql = 0; ql < QPW; ++ql) {
+            const int64_t q = q0 + ql;
+            if (q >= p.nq) break;
+            const int cnt = cnt_s[ql];
+            const uint64_t *row = lists + static_cast<int64_t>(ql) * p.cap;
+            int P = 2;
+            while (P < cnt) P <<= 1;
+            for (int i = lane; i < P; i += 32) scratch[i] = i < cnt ? __ldcg(row + i) : KEY_INF;
+            __syncwarp();
+            warp_bitonic(scratch, P, lane);
+            uint64_t *dst = p.out + (part * p.nq + q) * p.k;
+            for (int i = lane; i < p.k; i += 32) dst[i] = i < cnt ? scratch[i] : KEY_INF;
+            __syncwarp();
+        }
+    };
+    auto begin_segment = [&](int gr) {
+        // part slot: CTAs overlapping group gr are numbered from the first one
         int64_t c_first = (static_cast<int64_t>(gr) * T * G) / W;
         while (c_first > 0 && c_first * W / G > static_cast<int64_t>(gr) * T) --c_first;
         while ((c_first + 1) * W / G <= static_cast<int64_t>(gr) * T) ++c_first;
-        const int64_t part = (static_cast<int64_t>(blockIdx.x) - c_first) * p.DW + dw;
-
-        const int64_t q0 = (static_cast<int64_t>(gr) * p.QW + qw) * QPW;
-        const bool has_q = q0 < p.nq;  // warp-uniform; warps without queries still produce stages
-
-        // ---- A fragments: this warp's query rows, resident for the whole segment
-        uint32_t a[MT][KS][4];
+        part = (static_cast<int64_t>(blockIdx.x) - c_first) * DW + dw;
+        q0 = (static_cast<int64_t>(gr) * (FUSED ? 1 : p.QW) + qw) * QPW;
+        has_q = q0 < p.nq;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -276,16 +396,13 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                 if (has_q) v = __ldg(reinterpret_cast<const uint4 *>(p.qop) + (((q0 >> 4) + mt) * KS + s) * 32 + lane);
                 a[mt][s][0] = v.x; a[mt][s][1] = v.y; a[mt][s][2] = v.z; a[mt][s][3] = v.w;
             }
-        // ---- selection state: lane l <-> query row l
-        LaneState st;
-        {
-            const int64_t myq = q0 + lane;
-            const bool valid = has_q && lane < QPW && myq < p.nq;
-            st.dq = valid ? p.qconst[myq] : 0;
-            st.tau = valid ? (p.tau_init ? max(TAU_OPEN, p.tau_init[myq]) : TAU_OPEN) : 1;  // no query: acc = 0 < 1
-            cnt_s[lane] = 0;
-        }
-        int negtau[MT][2], dqrow[MT][2];
+        const int64_t myq = q0 + lane;
+        const bool valid = has_q && lane < QPW && myq < p.nq;
+        st.dq = valid ? p.qconst[myq] : 0;
+        st.tau = valid ? (p.tau_init ? max(TAU_OPEN, p.tau_init[myq]) : TAU_OPEN) : 1;  // no query: acc = 0 < 1
+        __syncwarp();
+        cnt_s[lane] = 0;
+        __syncwarp();
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -293,108 +410,133 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                 negtau[mt][hf] = -__shfl_sync(0xffffffffu, st.tau, 16 * mt + g + 8 * hf);
                 dqrow[mt][hf] = __shfl_sync(0xffffffffu, st.dq, 16 * mt + g + 8 * hf);
             }
+    };
 
-        // ---- prologue: stage s_begin into buffer 0, raw words of stage s_begin+1 in flight
-        load_raw(s_begin);
-        produce(0);
-        if (s_begin + 1 < s_end) load_raw(s_begin + 1);
-        __syncthreads();
-
-        for (int64_t s = s_begin; s < s_end; ++s) {
-            const int buf = static_cast<int>((s - s_begin) & 1);
-            if (s + 1 < s_end) {
-                produce(buf ^ 1);
-                if (s + 2 < s_end) load_raw(s + 2);
+    // IMMA + threshold filter + (rare) candidate pushes for one iteration (TILE documents from `it`)
+    auto process = [&](const uint32_t (&bw)[WPL], int64_t doc0) {
+        // acc' = sum_k x_k (2 y_k - Aq) - tau; k-step s2 = 4h + e uses words (nt*C + h)*8 + 2e, +1
+        int c[MT][NT][4];
+#pragma unroll
+        for (int s2 = 0; s2 < KS; ++s2)
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const uint32_t b0 = bw[(nt * C + (s2 >> 2)) * 8 + 2 * (s2 & 3)];
+                    const uint32_t b1 = bw[(nt * C + (s2 >> 2)) * 8 + 2 * (s2 & 3) + 1];
+                    if (s2 == 0) imma(c[mt][nt], a[mt][s2], b0, b1, negtau[mt][0], negtau[mt][0], negtau[mt][1], negtau[mt][1]);
+                    else imma(c[mt][nt], a[mt][s2], b0, b1, c[mt][nt][0], c[mt][nt][1], c[mt][nt][2], c[mt][nt][3]);
+                }
+        // any score with acc' >= 0 ?  (the AND of all results has a clear sign bit)
+        int all = -1;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) all &= c[mt][nt][0] & c[mt][nt][1] & c[mt][nt][2] & c[mt][nt][3];
+        if (__any_sync(0xffffffffu, all >= 0)) {
+            // slow path: lanes append their own hits; a row gains at most TILE keys per iteration
+            // and is compacted as soon as fewer than TILE slots remain
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int v = c[mt][nt][j];
+                        if (v >= 0) {
+                            const int64_t doc = doc0 + 8 * nt + 2 * t + (j & 1);
+                            if (doc < p.n) {
+                                const int row = 16 * mt + g + 8 * (j >> 1);
+                                const uint32_t dist = static_cast<uint32_t>(dqrow[mt][j >> 1] + negtau[mt][j >> 1] - v);
+                                const int pos = atomicAdd(&cnt_s[row], 1);
+                                lists[static_cast<int64_t>(row) * p.cap + pos] =
+                                    (static_cast<uint64_t>(dist) << 32) | static_cast<uint64_t>(p.row_offset + doc);
+                            }
+                        }
+                    }
+            __syncwarp();
+            unsigned need = __ballot_sync(0xffffffffu, lane < QPW && cnt_s[lane] > p.cap - TILE);
+            while (need) {
+                const int ql = __ffs(need) - 1;
+                need &= need - 1;
+                const int nv = compact_row(lists + static_cast<int64_t>(ql) * p.cap, scratch, &cnt_s[ql], p.k, ql, lane, st);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    if (16 * mt + g == ql) negtau[mt][0] = nv;
+                    if (16 * mt + g + 8 == ql) negtau[mt][1] = nv;
+                }
             }
+        }
+    };
+
+    int gr = gr_begin, sd = sd_begin;  // consume cursor: group and document stage
+    begin_segment(gr);
+
+    if (FUSED) {
+        Ring rf{0, 0u};
+        for (int ci = 0; ci < S; ++ci) {
+            uint32_t pw[NT][WD][C], bw[WPL];
+            mbar_wait(&raw_full[rf.idx], rf.phase);
+            load_planes(rf.idx, pw);
+            __syncwarp();  // all lanes have their words in registers before the slot is handed back
+            if (lane == 0) mbar_arrive(&raw_empty[rf.idx]);
+            rf.advance(RR);
+            const int64_t doc0 = (static_cast<int64_t>(sd) * STAGE_ITERS + warp) * TILE;
+            if (has_q && doc0 + TILE <= p.n_pad) {
+                planes_to_fragments(pw, bw);
+                process(bw, doc0);
+            }
+            if (++sd == Ti) {
+                sd = 0;
+                if (ci + 1 < S) { emit_segment(); begin_segment(++gr); }
+            }
+        }
+    } else {
+        Ring tr_raw{0, 0u}, tr_byte{0, 1u}, cs{0, 0u};
+        auto transpose_stage = [&]() {  // this warp's iteration slot: raw ring -> byte ring
+            uint32_t pw[NT][WD][C], bw[WPL];
+            mbar_wait(&byte_empty[tr_byte.idx], tr_byte.phase);
+            mbar_wait(&raw_full[tr_raw.idx], tr_raw.phase);
+            load_planes(tr_raw.idx, pw);
+            planes_to_fragments(pw, bw);
+            uint4 *dst = reinterpret_cast<uint4 *>(smem_raw + L.byte_off + static_cast<size_t>(tr_byte.idx) * BYTE_STAGE_BYTES) +
+                         static_cast<size_t>(warp) * (RCH * 32) + lane;
+#pragma unroll
+            for (int r = 0; r < RCH; ++r) dst[r * 32] = make_uint4(bw[4 * r], bw[4 * r + 1], bw[4 * r + 2], bw[4 * r + 3]);
+            __syncwarp();  // orders every lane's reads / writes before the elected lane's release-arrive
+            if (lane == 0) { mbar_arrive(&raw_empty[tr_raw.idx]); mbar_arrive(&byte_full[tr_byte.idx]); }
+            tr_raw.advance(RR);
+            tr_byte.advance(BR);
+        };
+        for (int pi = 0; pi < AHEAD && pi < S; ++pi) transpose_stage();
+        for (int ci = 0; ci < S; ++ci) {
+            if (ci + AHEAD < S) transpose_stage();
+            mbar_wait(&byte_full[cs.idx], cs.phase);
             if (has_q) {
-                for (int i = dw; i < STAGE_ITERS; i += p.DW) {
-                    const int64_t it = s * STAGE_ITERS + i;
-                    if ((it + 1) * TILE > p.n_pad) break;
-                    const uint4 *src = stage_mem + (static_cast<size_t>(buf) * STAGE_ITERS + i) * (RCH * 32) + lane;
+                for (int i = dw; i < STAGE_ITERS; i += DW) {
+                    const int64_t doc0 = (static_cast<int64_t>(sd) * STAGE_ITERS + i) * TILE;
+                    if (doc0 + TILE > p.n_pad) break;
+                    const uint4 *src = reinterpret_cast<const uint4 *>(smem_raw + L.byte_off + static_cast<size_t>(cs.idx) * BYTE_STAGE_BYTES) +
+                                       static_cast<size_t>(i) * (RCH * 32) + lane;
                     uint32_t bw[WPL];
 #pragma unroll
                     for (int r = 0; r < RCH; ++r) {
                         const uint4 v = src[r * 32];
                         bw[4 * r] = v.x; bw[4 * r + 1] = v.y; bw[4 * r + 2] = v.z; bw[4 * r + 3] = v.w;
                     }
-                    // acc' = sum_k x_k (2 y_k - Aq) - tau; k-step s2 = 4h + e uses words (nt*C + h)*8 + 2e, +1
-                    int c[MT][NT][4];
-#pragma unroll
-                    for (int s2 = 0; s2 < KS; ++s2)
-#pragma unroll
-                        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-                            for (int nt = 0; nt < NT; ++nt) {
-                                const uint32_t b0 = bw[(nt * C + (s2 >> 2)) * 8 + 2 * (s2 & 3)];
-                                const uint32_t b1 = bw[(nt * C + (s2 >> 2)) * 8 + 2 * (s2 & 3) + 1];
-                                if (s2 == 0) imma(c[mt][nt], a[mt][s2], b0, b1, negtau[mt][0], negtau[mt][0], negtau[mt][1], negtau[mt][1]);
-                                else imma(c[mt][nt], a[mt][s2], b0, b1, c[mt][nt][0], c[mt][nt][1], c[mt][nt][2], c[mt][nt][3]);
-                            }
-                    // any score with acc' >= 0 ?  (the AND of all results has a clear sign bit)
-                    int all = -1;
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-                        for (int nt = 0; nt < NT; ++nt) all &= c[mt][nt][0] & c[mt][nt][1] & c[mt][nt][2] & c[mt][nt][3];
-                    if (__any_sync(0xffffffffu, all >= 0)) {
-                        // slow path: lanes append their own hits; a row gains at most TILE keys per
-                        // iteration and is compacted as soon as fewer than TILE slots remain
-#pragma unroll
-                        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-                            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                                for (int j = 0; j < 4; ++j) {
-                                    const int v = c[mt][nt][j];
-                                    if (v >= 0) {
-                                        const int64_t doc = it * TILE + 8 * nt + 2 * t + (j & 1);
-                                        if (doc < p.n) {
-                                            const int row = 16 * mt + g + 8 * (j >> 1);
-                                            const uint32_t dist = static_cast<uint32_t>(dqrow[mt][j >> 1] + negtau[mt][j >> 1] - v);
-                                            const int pos = atomicAdd(&cnt_s[row], 1);
-                                            lists[static_cast<int64_t>(row) * p.cap + pos] =
-                                                (static_cast<uint64_t>(dist) << 32) | static_cast<uint64_t>(p.row_offset + doc);
-                                        }
-                                    }
-                                }
-                        __syncwarp();
-                        unsigned need = __ballot_sync(0xffffffffu, lane < QPW && cnt_s[lane] > p.cap - TILE);
-                        while (need) {
-                            const int ql = __ffs(need) - 1;
-                            need &= need - 1;
-                            const int nv = compact_row(lists + static_cast<int64_t>(ql) * p.cap, scratch, &cnt_s[ql], p.k, ql, lane, st);
-#pragma unroll
-                            for (int mt = 0; mt < MT; ++mt) {
-                                if (16 * mt + g == ql) negtau[mt][0] = nv;
-                                if (16 * mt + g + 8 == ql) negtau[mt][1] = nv;
-                            }
-                        }
-                    }
+                    process(bw, doc0);
                 }
             }
-            __syncthreads();
-        }
-
-        // ---- emit: every query row of this warp, sorted, KEY_INF padded
-        if (has_q) {
             __syncwarp();
-            for (int ql = 0; ql < QPW; ++ql) {
-                const int64_t q = q0 + ql;
-                if (q >= p.nq) break;
-                const int cnt = cnt_s[ql];
-                const uint64_t *row = lists + static_cast<int64_t>(ql) * p.cap;
-                int P = 2;
-                while (P < cnt) P <<= 1;
-                for (int i = lane; i < P; i += 32) scratch[i] = i < cnt ? __ldcg(row + i) : KEY_INF;
-                __syncwarp();
-                warp_bitonic(scratch, P, lane);
-                uint64_t *dst = p.out + (part * p.nq + q) * p.k;
-                for (int i = lane; i < p.k; i += 32) dst[i] = i < cnt ? scratch[i] : KEY_INF;
-                __syncwarp();
+            if (lane == 0) mbar_arrive(&byte_empty[cs.idx]);
+            cs.advance(BR);
+            if (++sd == Ti) {
+                sd = 0;
+                if (ci + 1 < S) { emit_segment(); begin_segment(++gr); }
             }
         }
-        __syncthreads();
     }
+    emit_segment();
 }
 
 // tau_init[q] = Dq - distance(k-th key of a sample scan), or TAU_OPEN when the sample had < k rows.
