@@ -793,7 +793,7 @@ int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, Mma
     // few documents and its own threshold tightens slowly; a sample scan of the first S documents
     // gives all of them a threshold of selectivity ~k/S up front.
     int64_t sample = env_int("XFBQ_SAMPLE", -1);
-    if (sample < 0) sample = (pl.main.groups == 1 && pl.main.DW > 1 && nq > 4) ? 32768 : 0;
+    if (sample < 0) sample = nq > 4 ? (pl.main.groups == 1 ? 32768 : 131072) : 0;
     if (sample > 0 && (n < 16 * sample || sample < 4 * k)) sample = 0;
     pl.sample = sample;
     if (sample) mma_shape(sample, wd, C, nq, k, info, &pl.pre);
@@ -831,7 +831,7 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
         e = cudaMemsetAsync(p.out, 0xFF, sh.parts_bytes, st);
         if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
     }
-    kern<<<static_cast<unsigned>(sh.grid), mma::THREADS + 32, sh.smem, st>>>(p);
+    kern<<<static_cast<unsigned>(sh.grid), mma::THREADS, sh.smem, st>>>(p);
     if (int rc = check_launch("mma::scan_kernel")) return rc;
     if (sh.parts > 1)
         return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st);

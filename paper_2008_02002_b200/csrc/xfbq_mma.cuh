@@ -9,7 +9,7 @@
 // ~60x faster than the POPC pipe can popcount the 16 plane pairs (profiles/microbench_r1.jsonl:
 // XU/POPC 4.5 T lane-ops/s vs IMMA 568 T MAC/s).  Results are bit-identical to the POPC form.
 //
-// Data flow of one CTA (8 worker warps + 1 TMA issuer warp), per stage of 8 iterations x TILE =
+// Data flow of one CTA (8 warps; lane 0 of warp 0 also issues the TMA copies), per stage of 8 iterations x TILE =
 // 8*NT documents (whole bundles, contiguous in HBM, fetched by one cp.async.bulk per stage):
 //   * queries: 16*MT query rows per warp live in registers as A fragments (s8 weights 2y-Aq,
 //     laid out by prep_queries_kernel in exactly the K-order the document side produces);
@@ -214,6 +214,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "memory");
     } while (!done);
 }
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
 // TMA bulk copy global -> shared (1-D, contiguous), completion signalled on `bar` as tx bytes.
 __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -249,8 +260,9 @@ struct Ring {
     }
 };
 
-// One CTA = 8 worker warps + 1 issuer warp.
-//   issuer : streams this CTA's document stages HBM -> raw ring with TMA bulk copies (RR deep)
+// One CTA = 8 worker warps.
+//   TMA    : this CTA's document stages stream HBM -> raw ring as bulk copies (RR deep), issued
+//            by thread 0 whenever a slot has been released by all warps
 //   ring mode (FUSED = false; several query warps share each document tile):
 //     worker w: [transpose] its iteration slot of stage i+AHEAD: raw ring -> byte ring (B fragments)
 //               [consume]   its iterations of stage i: byte ring -> IMMA -> threshold filter -> lists
@@ -259,7 +271,7 @@ struct Ring {
 // Hand-offs are mbarriers (raw_full/raw_empty, byte_full/byte_empty), so a warp that runs a list
 // compaction only stalls the others once the rings' slack is used up (no per-stage block barrier).
 template <int WD, int C, int MT, int NT, bool FUSED>
-__global__ void __launch_bounds__(THREADS + 32, 1) scan_kernel(const Params p) {
+__global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int QPW = 16 * MT;        // query rows per warp
     constexpr int KS = 4 * C;           // k-steps of 32 dims
@@ -294,26 +306,34 @@ __global__ void __launch_bounds__(THREADS + 32, 1) scan_kernel(const Params p) {
     }
     __syncthreads();
 
-    if (warp == WARPS) {
-        // ================================ issuer warp ================================
-        if (lane == 0) {
-            const int64_t db_bytes = (p.n_pad / 32) * static_cast<int64_t>(WD * C * 512);
-            Ring rr{0, 1u};  // "empty" waits start on the phase that counts as already completed
-            int sd = sd_begin;
-            for (int idx = 0; idx < S; ++idx) {
-                mbar_wait(&raw_empty[rr.idx], rr.phase);
-                const int64_t off = static_cast<int64_t>(sd) * RAW_STAGE_BYTES;
-                int64_t bytes = db_bytes - off;
-                if (bytes > RAW_STAGE_BYTES) bytes = RAW_STAGE_BYTES;
-                mbar_arrive_expect_tx(&raw_full[rr.idx], static_cast<uint32_t>(bytes));
-                tma_bulk_g2s(smem_raw + L.raw_off + static_cast<size_t>(rr.idx) * RAW_STAGE_BYTES,
-                             reinterpret_cast<const unsigned char *>(p.db) + off, static_cast<uint32_t>(bytes), &raw_full[rr.idx]);
-                rr.advance(RR);
-                if (++sd == Ti) sd = 0;
-            }
+    // ---- TMA issue, folded into warp 0 / lane 0: whenever it passes by (and while it spins on a
+    // barrier) it refills every raw-ring slot that all warps have released.  A 9th issuer warp
+    // would cap the kernel at 168 registers per thread (register file is carved per 4 warps).
+    const int64_t db_bytes = (p.n_pad / 32) * static_cast<int64_t>(WD * C * 512);
+    Ring is_ring{0, 1u};  // "empty" waits start on the phase that counts as already completed
+    int is_sd = sd_begin, issued = 0;
+    auto pump = [&]() {
+        if (threadIdx.x != 0) return;
+        while (issued < S && mbar_test(&raw_empty[is_ring.idx], is_ring.phase)) {
+            const int64_t off = static_cast<int64_t>(is_sd) * RAW_STAGE_BYTES;
+            int64_t bytes = db_bytes - off;
+            if (bytes > RAW_STAGE_BYTES) bytes = RAW_STAGE_BYTES;
+            mbar_arrive_expect_tx(&raw_full[is_ring.idx], static_cast<uint32_t>(bytes));
+            tma_bulk_g2s(smem_raw + L.raw_off + static_cast<size_t>(is_ring.idx) * RAW_STAGE_BYTES,
+                         reinterpret_cast<const unsigned char *>(p.db) + off, static_cast<uint32_t>(bytes), &raw_full[is_ring.idx]);
+            is_ring.advance(RR);
+            if (++is_sd == Ti) is_sd = 0;
+            ++issued;
         }
-        return;
-    }
+    };
+    auto wait_bar = [&](uint64_t *bar, uint32_t parity) {  // warp 0 keeps the TMA ring fed while it waits
+        if (warp == 0) {
+            while (!mbar_test(bar, parity)) pump();
+        } else {
+            mbar_wait(bar, parity);
+        }
+    };
+    pump();
 
     // ================================ worker warps ================================
     const int g = lane >> 2, t = lane & 3;
@@ -412,8 +432,9 @@ __global__ void __launch_bounds__(THREADS + 32, 1) scan_kernel(const Params p) {
             }
     };
 
-    // IMMA + threshold filter + (rare) candidate pushes for one iteration (TILE documents from `it`)
-    auto process = [&](const uint32_t (&bw)[WPL], int64_t doc0) {
+    // IMMA + threshold filter + (rare) candidate pushes for one iteration (TILE documents from doc0)
+    const uint32_t n_docs = static_cast<uint32_t>(p.n);
+    auto process = [&](const uint32_t (&bw)[WPL], uint32_t doc0) {
         // acc' = sum_k x_k (2 y_k - Aq) - tau; k-step s2 = 4h + e uses words (nt*C + h)*8 + 2e, +1
         int c[MT][NT][4];
 #pragma unroll
@@ -427,39 +448,42 @@ __global__ void __launch_bounds__(THREADS + 32, 1) scan_kernel(const Params p) {
                     if (s2 == 0) imma(c[mt][nt], a[mt][s2], b0, b1, negtau[mt][0], negtau[mt][0], negtau[mt][1], negtau[mt][1]);
                     else imma(c[mt][nt], a[mt][s2], b0, b1, c[mt][nt][0], c[mt][nt][1], c[mt][nt][2], c[mt][nt][3]);
                 }
-        // any score with acc' >= 0 ?  (the AND of all results has a clear sign bit)
+        // any score with acc' >= 0 ?  (the AND of the results has a clear sign bit); pm = per-tile ANDs
+        int pm[MT][NT];
         int all = -1;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) all &= c[mt][nt][0] & c[mt][nt][1] & c[mt][nt][2] & c[mt][nt][3];
+            for (int nt = 0; nt < NT; ++nt) {
+                pm[mt][nt] = (c[mt][nt][0] & c[mt][nt][1]) & (c[mt][nt][2] & c[mt][nt][3]);
+                all &= pm[mt][nt];
+            }
         if (__any_sync(0xffffffffu, all >= 0)) {
             // slow path: lanes append their own hits; a row gains at most TILE keys per iteration
             // and is compacted as soon as fewer than TILE slots remain
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt)
+                for (int nt = 0; nt < NT; ++nt) {
+                    if (pm[mt][nt] < 0) continue;  // per-lane: none of this lane's 4 scores of the tile passed
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         const int v = c[mt][nt][j];
-                        if (v >= 0) {
-                            const int64_t doc = doc0 + 8 * nt + 2 * t + (j & 1);
-                            if (doc < p.n) {
-                                const int row = 16 * mt + g + 8 * (j >> 1);
-                                const uint32_t dist = static_cast<uint32_t>(dqrow[mt][j >> 1] + negtau[mt][j >> 1] - v);
-                                const int pos = atomicAdd(&cnt_s[row], 1);
-                                lists[static_cast<int64_t>(row) * p.cap + pos] =
-                                    (static_cast<uint64_t>(dist) << 32) | static_cast<uint64_t>(p.row_offset + doc);
-                            }
+                        const uint32_t doc = doc0 + 8 * nt + 2 * t + (j & 1);
+                        if (v >= 0 && doc < n_docs) {
+                            const int row = 16 * mt + g + 8 * (j >> 1);
+                            const uint32_t dist = static_cast<uint32_t>(dqrow[mt][j >> 1] + negtau[mt][j >> 1] - v);
+                            const int pos = atomicAdd(&cnt_s[row], 1);
+                            lists[row * p.cap + pos] = (static_cast<uint64_t>(dist) << 32) | (static_cast<uint64_t>(p.row_offset) + doc);
                         }
                     }
+                }
             __syncwarp();
             unsigned need = __ballot_sync(0xffffffffu, lane < QPW && cnt_s[lane] > p.cap - TILE);
             while (need) {
                 const int ql = __ffs(need) - 1;
                 need &= need - 1;
-                const int nv = compact_row(lists + static_cast<int64_t>(ql) * p.cap, scratch, &cnt_s[ql], p.k, ql, lane, st);
+                const int nv = compact_row(lists + ql * p.cap, scratch, &cnt_s[ql], p.k, ql, lane, st);
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
                     if (16 * mt + g == ql) negtau[mt][0] = nv;
@@ -469,6 +493,7 @@ __global__ void __launch_bounds__(THREADS + 32, 1) scan_kernel(const Params p) {
         }
     };
 
+    const uint32_t n_pad32 = static_cast<uint32_t>(p.n_pad);
     int gr = gr_begin, sd = sd_begin;  // consume cursor: group and document stage
     begin_segment(gr);
 
@@ -476,13 +501,14 @@ __global__ void __launch_bounds__(THREADS + 32, 1) scan_kernel(const Params p) {
         Ring rf{0, 0u};
         for (int ci = 0; ci < S; ++ci) {
             uint32_t pw[NT][WD][C], bw[WPL];
-            mbar_wait(&raw_full[rf.idx], rf.phase);
+            wait_bar(&raw_full[rf.idx], rf.phase);
             load_planes(rf.idx, pw);
             __syncwarp();  // all lanes have their words in registers before the slot is handed back
             if (lane == 0) mbar_arrive(&raw_empty[rf.idx]);
             rf.advance(RR);
-            const int64_t doc0 = (static_cast<int64_t>(sd) * STAGE_ITERS + warp) * TILE;
-            if (has_q && doc0 + TILE <= p.n_pad) {
+            pump();
+            const uint32_t doc0 = (static_cast<uint32_t>(sd) * STAGE_ITERS + warp) * TILE;
+            if (has_q && doc0 + TILE <= n_pad32) {
                 planes_to_fragments(pw, bw);
                 process(bw, doc0);
             }
@@ -495,8 +521,8 @@ __global__ void __launch_bounds__(THREADS + 32, 1) scan_kernel(const Params p) {
         Ring tr_raw{0, 0u}, tr_byte{0, 1u}, cs{0, 0u};
         auto transpose_stage = [&]() {  // this warp's iteration slot: raw ring -> byte ring
             uint32_t pw[NT][WD][C], bw[WPL];
-            mbar_wait(&byte_empty[tr_byte.idx], tr_byte.phase);
-            mbar_wait(&raw_full[tr_raw.idx], tr_raw.phase);
+            wait_bar(&byte_empty[tr_byte.idx], tr_byte.phase);
+            wait_bar(&raw_full[tr_raw.idx], tr_raw.phase);
             load_planes(tr_raw.idx, pw);
             planes_to_fragments(pw, bw);
             uint4 *dst = reinterpret_cast<uint4 *>(smem_raw + L.byte_off + static_cast<size_t>(tr_byte.idx) * BYTE_STAGE_BYTES) +
@@ -507,24 +533,39 @@ __global__ void __launch_bounds__(THREADS + 32, 1) scan_kernel(const Params p) {
             if (lane == 0) { mbar_arrive(&raw_empty[tr_raw.idx]); mbar_arrive(&byte_full[tr_byte.idx]); }
             tr_raw.advance(RR);
             tr_byte.advance(BR);
+            pump();
         };
         for (int pi = 0; pi < AHEAD && pi < S; ++pi) transpose_stage();
         for (int ci = 0; ci < S; ++ci) {
             if (ci + AHEAD < S) transpose_stage();
-            mbar_wait(&byte_full[cs.idx], cs.phase);
+            wait_bar(&byte_full[cs.idx], cs.phase);
             if (has_q) {
-                for (int i = dw; i < STAGE_ITERS; i += DW) {
-                    const int64_t doc0 = (static_cast<int64_t>(sd) * STAGE_ITERS + i) * TILE;
-                    if (doc0 + TILE > p.n_pad) break;
-                    const uint4 *src = reinterpret_cast<const uint4 *>(smem_raw + L.byte_off + static_cast<size_t>(cs.idx) * BYTE_STAGE_BYTES) +
-                                       static_cast<size_t>(i) * (RCH * 32) + lane;
-                    uint32_t bw[WPL];
+                // iterations dw, dw+DW, ... of the stage; fragments of the next one are fetched
+                // from shared memory while the IMMAs of the current one run (two register sets)
+                const uint32_t stage_doc0 = static_cast<uint32_t>(sd) * STAGE_DOCS;
+                const uint32_t left = n_pad32 - stage_doc0;
+                const int n_it = left >= static_cast<uint32_t>(STAGE_DOCS) ? STAGE_ITERS : static_cast<int>(left / TILE);
+                const uint4 *stage_src = reinterpret_cast<const uint4 *>(smem_raw + L.byte_off + static_cast<size_t>(cs.idx) * BYTE_STAGE_BYTES) + lane;
+                auto fetch = [&](uint32_t (&bw)[WPL], int i) {
+                    const uint4 *src = stage_src + i * (RCH * 32);
 #pragma unroll
                     for (int r = 0; r < RCH; ++r) {
                         const uint4 v = src[r * 32];
                         bw[4 * r] = v.x; bw[4 * r + 1] = v.y; bw[4 * r + 2] = v.z; bw[4 * r + 3] = v.w;
                     }
-                    process(bw, doc0);
+                };
+                uint32_t bwA[WPL], bwB[WPL];
+                int i = dw;
+                if (i < n_it) fetch(bwA, i);
+                while (i < n_it) {
+                    const int i2 = i + DW;
+                    if (i2 < n_it) fetch(bwB, i2);
+                    process(bwA, stage_doc0 + i * TILE);
+                    if (i2 >= n_it) break;
+                    const int i3 = i2 + DW;
+                    if (i3 < n_it) fetch(bwA, i3);
+                    process(bwB, stage_doc0 + i2 * TILE);
+                    i = i3;
                 }
             }
             __syncwarp();
