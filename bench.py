@@ -221,7 +221,7 @@ def run_ours(a):
 
     plan = (np.zeros(6, dtype=np.int32))
     _native.check(_native.lib().xfbq_scan_plan(index.n, a.dim, a.doc_bits, min(a.nq, xsearch._QUERY_BATCH),
-                                               a.query_bits, min(a.k, index.n), plan.ctypes.data))
+                                               a.query_bits, min(a.k, index.n), 1, plan.ctypes.data))
 
     def step_device():
         return shard.search_keys(q_dev, a.k)

@@ -167,6 +167,24 @@ class PackedMatrix:
             self._planes = host
         return self._planes
 
+    @property
+    def nibbles(self):
+        """Derived nibble-layout copy of the codes for the tensor-core scan (doc_bits <= 4), built
+        on the GPU on first use and cached; None for wider codes."""
+        if self._width > 4 or self._count == 0:
+            return None
+        cached = getattr(self, "_nibbles", None)
+        if cached is None:
+            torch = _native.require_cuda()
+            L = _native.lib()
+            with torch.cuda.device(self._codes.device):
+                cached = torch.empty(int(L.xfbq_nibble_bytes(self._count, self._dim)), dtype=torch.uint8,
+                                     device=self._codes.device)
+                _native.check(L.xfbq_planes_to_nibbles(self._codes.data_ptr(), self._count, self._dim, self._width,
+                                                       cached.data_ptr(), _stream_ptr(torch)))
+            self._nibbles = cached
+        return cached
+
     def row(self, k: int) -> PackedVector:
         return PackedVector(np.ascontiguousarray(self.planes[:, :, k]), self._dim)
 

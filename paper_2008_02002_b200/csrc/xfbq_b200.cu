@@ -684,6 +684,7 @@ struct MmaShape {  // launch geometry of one mma::scan_kernel launch over n docu
     int MT = 2, NT = 2, QPW = 32, QW = 8, DW = 1, groups = 1, grid = 1, slots = 1, parts = 1, cap = 0;
     int RR = 0, BR = 0;  // ring depths (RR = 0: does not fit in shared memory)
     bool fused = false;  // one query warp: tiles go raw ring -> registers -> IMMA, no byte ring
+    int warps = mma::WARPS;
     int64_t stages = 0, nq_pad = 0, n_pad = 0;
     size_t smem = 0, lists_bytes = 0, parts_bytes = 0, mscratch_bytes = 0;
 };
@@ -698,12 +699,15 @@ struct MmaPlan {
 
 typedef void (*MmaKernel)(const mma::Params);
 
-MmaKernel pick_mma_kernel(int wd, int C, bool fused) {
-#define XFBQ_MMA_CASE(WD_, C_, MT_, NT_) \
-    if (wd == WD_ && C == C_) return fused ? mma::scan_kernel<WD_, C_, MT_, NT_, true> : mma::scan_kernel<WD_, C_, MT_, NT_, false>;
-    XFBQ_MMA_CASE(1, 1, 2, 2) XFBQ_MMA_CASE(2, 1, 2, 2) XFBQ_MMA_CASE(3, 1, 2, 2) XFBQ_MMA_CASE(4, 1, 2, 2)
-    XFBQ_MMA_CASE(1, 2, 2, 2) XFBQ_MMA_CASE(2, 2, 2, 2) XFBQ_MMA_CASE(3, 2, 2, 2) XFBQ_MMA_CASE(4, 2, 2, 2)
-    XFBQ_MMA_CASE(1, 4, 1, 1) XFBQ_MMA_CASE(2, 4, 1, 1) XFBQ_MMA_CASE(3, 4, 1, 1) XFBQ_MMA_CASE(4, 4, 1, 1)
+MmaKernel pick_mma_kernel(int C, bool fused, int warps) {
+    if (warps == mma::WARPS_WIDE) {
+        if (C == 1) return mma::scan_kernel<1, 1, 2, true, mma::WARPS_WIDE>;
+        if (C == 2) return mma::scan_kernel<2, 1, 2, true, mma::WARPS_WIDE>;
+        return nullptr;
+    }
+#define XFBQ_MMA_CASE(C_, MT_, NT_) \
+    if (C == C_) return fused ? mma::scan_kernel<C_, MT_, NT_, true, mma::WARPS> : mma::scan_kernel<C_, MT_, NT_, false, mma::WARPS>;
+    XFBQ_MMA_CASE(1, 2, 2) XFBQ_MMA_CASE(2, 2, 2) XFBQ_MMA_CASE(4, 1, 1)
 #undef XFBQ_MMA_CASE
     return nullptr;
 }
@@ -715,22 +719,26 @@ void mma_shape(int64_t n, int wd, int C, int64_t nq, int k, const DeviceInfo &in
     MmaShape sh;
     sh.MT = C == 4 ? 1 : 2;
     sh.NT = C == 4 ? 1 : 2;
+    if (nq <= 16 && C <= 2 && env_int("XFBQ_NO_WIDE", 0) == 0 && env_int("XFBQ_NO_FUSED", 0) == 0) {
+        sh.MT = 1;  // <= 16 queries: one 16-row tile, 16 warps per CTA
+        sh.warps = mma::WARPS_WIDE;
+    }
     sh.QPW = 16 * sh.MT;
     int cap = 64;
     while (cap < 2 * k) cap <<= 1;
     sh.cap = cap;
     const int64_t qwt = (nq + sh.QPW - 1) / sh.QPW;
-    if (qwt >= mma::WARPS) {
-        sh.QW = mma::WARPS; sh.DW = 1;
-        sh.groups = static_cast<int>((qwt + mma::WARPS - 1) / mma::WARPS);
+    if (qwt >= sh.warps) {
+        sh.QW = sh.warps; sh.DW = 1;
+        sh.groups = static_cast<int>((qwt + sh.warps - 1) / sh.warps);
     } else {
         int qw = 1;
         while (qw < qwt) qw <<= 1;
-        sh.QW = qw; sh.DW = mma::WARPS / qw; sh.groups = 1;
+        sh.QW = qw; sh.DW = sh.warps / qw; sh.groups = 1;
     }
     sh.nq_pad = static_cast<int64_t>(sh.groups) * sh.QW * sh.QPW;
     sh.n_pad = bundles_of(n) * 32;
-    const int64_t stage_docs = static_cast<int64_t>(mma::STAGE_ITERS) * 8 * sh.NT;
+    const int64_t stage_docs = static_cast<int64_t>(sh.warps) * 8 * sh.NT;
     sh.stages = (sh.n_pad + stage_docs - 1) / stage_docs;
     const int64_t W = static_cast<int64_t>(sh.groups) * sh.stages;
     int64_t grid = env_int("XFBQ_GRID", 0) > 0 ? env_int("XFBQ_GRID", 0) : sms;
@@ -750,32 +758,33 @@ void mma_shape(int64_t n, int wd, int C, int64_t nq, int k, const DeviceInfo &in
     }
     sh.slots = slots;
     sh.parts = slots * sh.DW;
-    const int raw_stage = (mma::STAGE_ITERS * 8 * sh.NT / 32) * wd * C * 512;
-    const int byte_stage = mma::STAGE_ITERS * (sh.NT * C * 8) * 32 * 4;
+    (void)wd;
+    const int raw_stage = sh.warps * 8 * sh.NT * 64 * C;  // nibble layout: 64C bytes per document
+    const int byte_stage = sh.warps * (sh.NT * C * 8) * 32 * 4;
     sh.fused = sh.QW == 1 && sh.groups == 1 && env_int("XFBQ_NO_FUSED", 0) == 0;
-    int RR = env_int("XFBQ_RAW_STAGES", sh.fused ? 8 : 6), BR = sh.fused ? 0 : env_int("XFBQ_BYTE_STAGES", 4);
+    int RR = env_int("XFBQ_RAW_STAGES", sh.fused ? (sh.warps == mma::WARPS ? 8 : 5) : 6), BR = sh.fused ? 0 : env_int("XFBQ_BYTE_STAGES", 4);
     const int br_min = sh.fused ? 0 : mma::AHEAD + 1;
     if (BR < br_min) BR = br_min;
     if (RR < 1) RR = 1;
     const size_t budget = static_cast<size_t>(info.smem_optin) - 1024;
-    while (mma::smem_layout(raw_stage, byte_stage, RR, BR, cap).total > budget && RR > 2) --RR;
-    while (mma::smem_layout(raw_stage, byte_stage, RR, BR, cap).total > budget && BR > br_min) --BR;
-    while (mma::smem_layout(raw_stage, byte_stage, RR, BR, cap).total > budget && RR > 1) --RR;
-    if (mma::smem_layout(raw_stage, byte_stage, RR, BR, cap).total > budget) RR = BR = 0;
+    while (mma::smem_layout(raw_stage, byte_stage, RR, BR, cap, sh.warps).total > budget && RR > 2) --RR;
+    while (mma::smem_layout(raw_stage, byte_stage, RR, BR, cap, sh.warps).total > budget && BR > br_min) --BR;
+    while (mma::smem_layout(raw_stage, byte_stage, RR, BR, cap, sh.warps).total > budget && RR > 1) --RR;
+    if (mma::smem_layout(raw_stage, byte_stage, RR, BR, cap, sh.warps).total > budget) RR = BR = 0;
     sh.RR = RR; sh.BR = BR;
-    sh.smem = RR ? mma::smem_layout(raw_stage, byte_stage, RR, BR, cap).total : 0;
-    sh.lists_bytes = static_cast<size_t>(sh.grid) * mma::WARPS * sh.QPW * cap * 8;
+    sh.smem = RR ? mma::smem_layout(raw_stage, byte_stage, RR, BR, cap, sh.warps).total : 0;
+    sh.lists_bytes = static_cast<size_t>(sh.grid) * sh.warps * sh.QPW * cap * 8;
     sh.parts_bytes = sh.parts > 1 ? static_cast<size_t>(sh.parts) * nq * k * 8 : 0;
     sh.mscratch_bytes = static_cast<size_t>(merge_scratch_parts(sh.parts, k, nq)) * nq * k * 8;
     *out = sh;
 }
 
-int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, MmaPlan *plan) {
+int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bool have_nibbles, MmaPlan *plan) {
     MmaPlan pl;
     const int C = static_cast<int>(chunks128(dim));
     const char *eng = getenv("XFBQ_ENGINE");
     const bool forced_popc = eng && strcmp(eng, "popc") == 0;
-    if (forced_popc || wd > 4 || wq > 7 || !(C == 1 || C == 2 || C == 4) || k > 1024 || nq < 1 || n < 1 ||
+    if (!have_nibbles || forced_popc || wd > 4 || wq > 7 || !(C == 1 || C == 2 || C == 4) || k > 1024 || nq < 1 || n < 1 ||
         env_int("XFBQ_FORCE_GENERIC", 0)) {
         *plan = pl;
         return XFBQ_OK;
@@ -811,13 +820,13 @@ int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, Mma
 }
 
 // One scan launch (+ merge of its part slots) over the first n documents of db.
-int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const void *db, int64_t n, int wd, int C,
+int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const void *nib, int64_t n, int C,
                  int64_t nq, int k, int64_t row_offset, const int32_t *tau_init, uint64_t *keys_out, cudaStream_t st) {
-    MmaKernel kern = pick_mma_kernel(wd, C, sh.fused);
+    MmaKernel kern = pick_mma_kernel(C, sh.fused, sh.warps);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh.smem));
     if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "mma scan smem opt-in (%zu bytes): %s", sh.smem, cudaGetErrorString(e));
     mma::Params p;
-    p.db = static_cast<const uint32_t *>(db);
+    p.db = nib;
     p.n = n; p.n_pad = sh.n_pad; p.row_offset = row_offset;
     p.qop = reinterpret_cast<const uint32_t *>(ws + pl.off_qop);
     p.qconst = reinterpret_cast<const int32_t *>(ws + pl.off_qconst);
@@ -831,7 +840,7 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
         e = cudaMemsetAsync(p.out, 0xFF, sh.parts_bytes, st);
         if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
     }
-    kern<<<static_cast<unsigned>(sh.grid), mma::THREADS, sh.smem, st>>>(p);
+    kern<<<static_cast<unsigned>(sh.grid), sh.warps * 32, sh.smem, st>>>(p);
     if (int rc = check_launch("mma::scan_kernel")) return rc;
     if (sh.parts > 1)
         return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st);
@@ -941,6 +950,21 @@ XFBQ_API int xfbq_bundles_to_planes(const void *db, int64_t n, int64_t dim, int 
     return check_launch("bundles_to_planes_kernel");
 }
 
+XFBQ_API int64_t xfbq_nibble_bytes(int64_t n, int64_t dim) { return bundles_of(n) * 32 * chunks128(dim) * 64; }
+
+XFBQ_API int xfbq_planes_to_nibbles(const void *db, int64_t n, int64_t dim, int width, void *nib_out, void *stream) {
+    if (width < 1 || width > 4) return fail(XFBQ_E_UNSUPPORTED, "nibble layout holds codes of at most 4 bits, got %d", width);
+    if (n < 0 || dim < 1) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld", (long long)n, (long long)dim);
+    if (n == 0) return XFBQ_OK;
+    if (!db || !nib_out) return fail(XFBQ_E_INVALID, "null pointer");
+    const int C = static_cast<int>(chunks128(dim));
+    const int64_t n_pad = bundles_of(n) * 32;
+    const int64_t total = n_pad * 4 * C;
+    mma::planes_to_nibbles_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint32_t *>(db), n_pad, width, C, static_cast<uint4 *>(nib_out));
+    return check_launch("planes_to_nibbles_kernel");
+}
+
 XFBQ_API int xfbq_batch_distances(const void *db, int64_t n, int64_t dim, int wd, const uint32_t *q, int wq,
                                   uint64_t *out, void *stream) {
     if (!width_ok(wd) || !width_ok(wq)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d/%d", wd, wq);
@@ -960,14 +984,14 @@ XFBQ_API int xfbq_batch_distances(const void *db, int64_t n, int64_t dim, int wd
     return check_launch("batch_distances_kernel");
 }
 
-XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k) {
+XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, int have_nibbles) {
     if (!width_ok(wd) || !width_ok(wq) || n < 0 || dim < 1 || nq < 0 || k < 1 || k > XFBQ_MAX_K) {
         fail(XFBQ_E_INVALID, "bad scan shape");
         return -1;
     }
     if (n == 0 || nq == 0) return 0;
     MmaPlan mp;
-    if (make_mma_plan(n, dim, wd, nq, wq, k, &mp)) return -1;
+    if (make_mma_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &mp)) return -1;
     if (mp.ok) return static_cast<int64_t>(mp.bytes);
     ScanPlan pl;
     if (make_plan(n, dim, wd, nq, wq, k, &pl)) return -1;
@@ -975,11 +999,11 @@ XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64
     return static_cast<int64_t>(pl.splits + merge_scratch_parts(pl.splits, k, nq)) * nq * k * 8;
 }
 
-XFBQ_API int xfbq_scan_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, int32_t out[6]) {
+XFBQ_API int xfbq_scan_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, int have_nibbles, int32_t out[6]) {
     if (!width_ok(wd) || !width_ok(wq) || n < 1 || dim < 1 || nq < 1 || k < 1 || k > XFBQ_MAX_K || !out)
         return fail(XFBQ_E_INVALID, "bad scan shape");
     MmaPlan mp;
-    if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, &mp)) return rc;
+    if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &mp)) return rc;
     if (mp.ok) {  // integer-MMA engine: tile = queries per CTA
         out[0] = mp.main.QW * mp.main.QPW; out[1] = mp.main.groups; out[2] = mp.main.parts; out[3] = mp.main.cap;
         out[4] = 2; out[5] = static_cast<int32_t>(mp.main.smem);
@@ -992,7 +1016,7 @@ XFBQ_API int xfbq_scan_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, 
     return XFBQ_OK;
 }
 
-XFBQ_API int xfbq_scan_topk(const void *db, int64_t n, int64_t dim, int wd, const uint32_t *q, int64_t nq,
+XFBQ_API int xfbq_scan_topk(const void *db, const void *nib, int64_t n, int64_t dim, int wd, const uint32_t *q, int64_t nq,
                             int wq, int k, int64_t row_offset, uint64_t *keys_out, void *workspace,
                             int64_t workspace_bytes, void *stream) {
     if (!width_ok(wd) || !width_ok(wq)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d/%d", wd, wq);
@@ -1011,7 +1035,7 @@ XFBQ_API int xfbq_scan_topk(const void *db, int64_t n, int64_t dim, int wd, cons
     }
     if (!db || !q) return fail(XFBQ_E_INVALID, "null pointer");
     MmaPlan mp;
-    if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, &mp)) return rc;
+    if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, nib != nullptr, &mp)) return rc;
     if (mp.ok) {
         if (!workspace || workspace_bytes < static_cast<int64_t>(mp.bytes))
             return fail(XFBQ_E_INVALID, "workspace too small: need %zu bytes, got %lld", mp.bytes, (long long)workspace_bytes);
@@ -1026,12 +1050,12 @@ XFBQ_API int xfbq_scan_topk(const void *db, int64_t n, int64_t dim, int wd, cons
         if (mp.sample) {
             uint64_t *prekeys = reinterpret_cast<uint64_t *>(ws + mp.off_prekeys);
             int32_t *tau = reinterpret_cast<int32_t *>(ws + mp.off_tau);
-            if (int rc = run_mma_scan(mp.pre, mp, ws, db, mp.sample, wd, C, nq, k, row_offset, nullptr, prekeys, st)) return rc;
+            if (int rc = run_mma_scan(mp.pre, mp, ws, nib, mp.sample, C, nq, k, row_offset, nullptr, prekeys, st)) return rc;
             mma::tau_from_keys_kernel<<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(prekeys, qconst, nq, k, tau);
             if (int rc = check_launch("tau_from_keys_kernel")) return rc;
             tau_init = tau;
         }
-        return run_mma_scan(mp.main, mp, ws, db, n, wd, C, nq, k, row_offset, tau_init, keys_out, st);
+        return run_mma_scan(mp.main, mp, ws, nib, n, C, nq, k, row_offset, tau_init, keys_out, st);
     }
     ScanPlan pl;
     if (int rc = make_plan(n, dim, wd, nq, wq, k, &pl)) return rc;

@@ -13,10 +13,10 @@
 // 8*NT documents (whole bundles, contiguous in HBM, fetched by one cp.async.bulk per stage):
 //   * queries: 16*MT query rows per warp live in registers as A fragments (s8 weights 2y-Aq,
 //     laid out by prep_queries_kernel in exactly the K-order the document side produces);
-//   * documents: warp w reads iteration w of the raw stage (bit-plane bundle layout) from shared
-//     memory, transposes it in registers from bit planes to one byte per dimension (4x4 bit-block
-//     transpose by delta swaps + nibble split) and stores the B fragments to a ring of byte
-//     stages, so a tile is transposed once per CTA however many query warps consume it;
+//   * documents: the engine streams the nibble layout (row-major 4-bit codes derived from the
+//     bit planes by planes_to_nibbles_kernel); warp w reads iteration w of the raw stage from
+//     shared memory, splits nibbles into bytes (3 ALU ops per 8 dims) and stores the B fragments
+//     to a ring of byte stages, so a tile is unpacked once per CTA however many warps consume it;
 //   * every (query-warp, doc-warp) consumes its iterations of the stage: 8 LDS.128 + MT*NT*4C
 //     IMMAs; the accumulator is initialised to -tau_q, so "distance <= threshold" is the sign
 //     bit of the result and one AND-reduction + vote per TILE x 16*MT scores decides whether the
@@ -29,14 +29,13 @@
 
 namespace mma {
 
-constexpr int WARPS = 8;
-constexpr int THREADS = WARPS * 32;
+constexpr int WARPS = 8;        // warps per CTA in ring (batch) mode and the default fused mode
+constexpr int WARPS_WIDE = 16;  // fused mode for <= 16 queries: twice the warps hide ALU latency
 constexpr int TAU_OPEN = -(1 << 30);  // threshold that lets every score through (no list yet)
 
-constexpr int STAGE_ITERS = WARPS;    // iterations per stage: one produced by each warp
 
 struct Params {
-    const uint32_t *db;       // bundle layout viewed as 32-bit words
+    const void *db;           // nibble layout: row-major, 64C bytes per document (see planes_to_nibbles_kernel)
     int64_t n;                // real documents
     int64_t n_pad;            // documents the buffer holds (multiple of 32)
     int64_t row_offset;
@@ -93,22 +92,34 @@ prep_queries_kernel(const uint32_t *__restrict__ q, int64_t nq, int64_t nq_pad, 
     if (lane == 0) qconst[row] = (row < nq) ? Ad * sy : 0;
 }
 
-// ------------------------------------------------------------------------------ bit planes -> bytes
-// 4 plane words (32 dims) -> 8 words of 4 bytes: out[2e + hi] byte j = code of dim 8j + e + 4hi.
-template <int WD>
-__device__ __forceinline__ void planes_to_bytes(const uint32_t (&pin)[4], uint32_t (&out)[8]) {
-    uint32_t p0 = pin[0], p1 = WD > 1 ? pin[1] : 0u, p2 = WD > 2 ? pin[2] : 0u, p3 = WD > 3 ? pin[3] : 0u;
+// ------------------------------------------------------------------------------ bit planes -> nibbles
+// The tensor engine streams a derived copy of the database: row-major 4-bit codes ("nibble
+// layout"), 64C bytes per document, one uint4 per group of 32 dims; word e of a group holds, in
+// nibble m, the code of dim 4m + e.  That is the 4x4 bit-block transpose of the group's (up to) 4
+// plane words, done with delta swaps; unpacking to MMA bytes is then 3 ALU ops per 8 dims.
+__device__ __forceinline__ uint4 planes_to_nibbles(uint32_t p0, uint32_t p1, uint32_t p2, uint32_t p3) {
     uint32_t t;
-    // 2x2 bit-block transposes inside each 4x4 block (rows = planes, columns = dims mod 4)
     t = ((p0 >> 1) ^ p1) & 0x55555555u; p1 ^= t; p0 ^= t << 1;
-    if (WD > 2) { t = ((p2 >> 1) ^ p3) & 0x55555555u; p3 ^= t; p2 ^= t << 1; }
+    t = ((p2 >> 1) ^ p3) & 0x55555555u; p3 ^= t; p2 ^= t << 1;
     t = ((p0 >> 2) ^ p2) & 0x33333333u; p2 ^= t; p0 ^= t << 2;
     t = ((p1 >> 2) ^ p3) & 0x33333333u; p3 ^= t; p1 ^= t << 2;
-    // now word p_e, nibble m = code of dim 4m + e; split even/odd nibbles into bytes
-    out[0] = p0 & 0x0F0F0F0Fu; out[1] = (p0 >> 4) & 0x0F0F0F0Fu;
-    out[2] = p1 & 0x0F0F0F0Fu; out[3] = (p1 >> 4) & 0x0F0F0F0Fu;
-    out[4] = p2 & 0x0F0F0F0Fu; out[5] = (p2 >> 4) & 0x0F0F0F0Fu;
-    out[6] = p3 & 0x0F0F0F0Fu; out[7] = (p3 >> 4) & 0x0F0F0F0Fu;
+    return make_uint4(p0, p1, p2, p3);
+}
+
+// bundle layout (bit planes) -> nibble layout; one thread per (document, 32-dim group).
+__global__ void __launch_bounds__(256)
+planes_to_nibbles_kernel(const uint32_t *__restrict__ db, int64_t n_pad, int wd, int C, uint4 *__restrict__ out) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int G = 4 * C;  // 32-dim groups per document
+    if (e >= n_pad * G) return;
+    // consecutive threads take consecutive documents of one group: coalesced reads of the bundle layout
+    const int64_t tile = e / (32 * G);
+    const int rem = static_cast<int>(e - tile * (32 * G));
+    const int grp = rem >> 5, dl = rem & 31;
+    const int64_t b = tile;  // bundle
+    uint32_t p[4] = {0u, 0u, 0u, 0u};
+    for (int i = 0; i < wd; ++i) p[i] = db[((((b * wd + i) * C + (grp >> 2)) * 32 + dl) << 2) + (grp & 3)];
+    out[(b * 32 + dl) * G + grp] = planes_to_nibbles(p[0], p[1], p[2], p[3]);
 }
 
 // D = A(s8, 16x32 row) * B(u8, 32x8 col) + C
@@ -118,24 +129,6 @@ __device__ __forceinline__ void imma(int (&d)[4], const uint32_t (&a)[4], uint32
         "mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%11,%12,%13};\n"
         : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(c0), "r"(c1), "r"(c2), "r"(c3));
-}
-
-// Quarter-row load: the C plane words (32C dims) lane t of a tile owns.
-template <int C>
-__device__ __forceinline__ void load_quarter(const uint32_t *base, uint32_t (&w)[C]);
-template <>
-__device__ __forceinline__ void load_quarter<1>(const uint32_t *base, uint32_t (&w)[1]) {
-    w[0] = __ldg(base);
-}
-template <>
-__device__ __forceinline__ void load_quarter<2>(const uint32_t *base, uint32_t (&w)[2]) {
-    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(base));
-    w[0] = v.x; w[1] = v.y;
-}
-template <>
-__device__ __forceinline__ void load_quarter<4>(const uint32_t *base, uint32_t (&w)[4]) {
-    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(base));
-    w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
 }
 
 __device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
@@ -238,14 +231,14 @@ constexpr int AHEAD = 2;  // stages a worker transposes ahead of the stage it co
 struct SmemLayout {
     uint32_t raw_off, byte_off, scratch_off, cnt_off, bar_off, total;
 };
-__host__ __device__ inline SmemLayout smem_layout(int raw_stage_bytes, int byte_stage_bytes, int RR, int BR, int cap) {
+__host__ __device__ inline SmemLayout smem_layout(int raw_stage_bytes, int byte_stage_bytes, int RR, int BR, int cap, int warps) {
     SmemLayout L;
     uint32_t off = 0;
     L.raw_off = off; off += static_cast<uint32_t>(RR) * raw_stage_bytes;
     off = (off + 127u) & ~127u;
     L.byte_off = off; off += static_cast<uint32_t>(BR) * byte_stage_bytes;
-    L.scratch_off = off; off += static_cast<uint32_t>(WARPS) * cap * 8;
-    L.cnt_off = off; off += WARPS * 32 * 4;
+    L.scratch_off = off; off += static_cast<uint32_t>(warps) * cap * 8;
+    L.cnt_off = off; off += warps * 32 * 4;
     L.bar_off = off; off += static_cast<uint32_t>(2 * RR + 2 * BR) * 8;
     L.total = off;
     return L;
@@ -270,8 +263,10 @@ struct Ring {
 //     worker w: raw ring -> registers (transpose) -> IMMA -> filter, no byte ring
 // Hand-offs are mbarriers (raw_full/raw_empty, byte_full/byte_empty), so a warp that runs a list
 // compaction only stalls the others once the rings' slack is used up (no per-stage block barrier).
-template <int WD, int C, int MT, int NT, bool FUSED>
-__global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
+template <int C, int MT, int NT, bool FUSED, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) scan_kernel(const Params p) {
+    constexpr int WARPS = NW;           // shadows the namespace default
+    constexpr int STAGE_ITERS = NW;     // iterations per stage: one produced by each warp
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int QPW = 16 * MT;        // query rows per warp
     constexpr int KS = 4 * C;           // k-steps of 32 dims
@@ -279,12 +274,13 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     constexpr int WPL = NT * C * 8;     // B-fragment words per lane per iteration
     constexpr int RCH = WPL / 4;        // 16-byte chunks per lane per iteration
     constexpr int STAGE_DOCS = STAGE_ITERS * TILE;
-    constexpr int RAW_STAGE_BYTES = (STAGE_DOCS / 32) * WD * C * 512;  // whole bundles, contiguous in HBM
+    constexpr int ROW_BYTES = 64 * C;                        // one document: 128C nibbles
+    constexpr int RAW_STAGE_BYTES = STAGE_DOCS * ROW_BYTES;  // contiguous in HBM (nibble layout is row-major)
     constexpr int BYTE_STAGE_BYTES = STAGE_ITERS * WPL * 32 * 4;
     static_assert(STAGE_DOCS % 32 == 0, "a stage must be whole bundles");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int RR = p.RR, BR = p.BR;
-    const SmemLayout L = smem_layout(RAW_STAGE_BYTES, BYTE_STAGE_BYTES, RR, BR, p.cap);
+    const SmemLayout L = smem_layout(RAW_STAGE_BYTES, BYTE_STAGE_BYTES, RR, BR, p.cap, NW);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + L.bar_off);
     uint64_t *raw_full = bars, *raw_empty = bars + RR, *byte_full = bars + 2 * RR, *byte_empty = bars + 2 * RR + BR;
 
@@ -309,7 +305,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     // ---- TMA issue, folded into warp 0 / lane 0: whenever it passes by (and while it spins on a
     // barrier) it refills every raw-ring slot that all warps have released.  A 9th issuer warp
     // would cap the kernel at 168 registers per thread (register file is carved per 4 warps).
-    const int64_t db_bytes = (p.n_pad / 32) * static_cast<int64_t>(WD * C * 512);
+    const int64_t db_bytes = p.n_pad * static_cast<int64_t>(ROW_BYTES);
     Ring is_ring{0, 1u};  // "empty" waits start on the phase that counts as already completed
     int is_sd = sd_begin, issued = 0;
     auto pump = [&]() {
@@ -343,34 +339,28 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     int *cnt_s = reinterpret_cast<int *>(smem_raw + L.cnt_off) + warp * 32;
     uint64_t *lists = p.lists + (static_cast<int64_t>(blockIdx.x) * WARPS + warp) * QPW * static_cast<int64_t>(p.cap);
 
-    // raw stage -> plane words of this warp's iteration slot: lane (g, t) owns, for every plane,
-    // the C words [C*t, C*t+C) of document warp*TILE + 8*nt + g
-    auto load_planes = [&](int r, uint32_t (&pw)[NT][WD][C]) {
-        const uint32_t *raw = reinterpret_cast<const uint32_t *>(smem_raw + L.raw_off + static_cast<size_t>(r) * RAW_STAGE_BYTES);
+    // raw stage -> nibble words of this warp's iteration slot: lane (g, t) owns the quarter
+    // [32C*t, 32C*(t+1)) of document warp*TILE + 8*nt + g, i.e. C groups of 32 dims = C uint4
+    auto load_nibbles = [&](int r, uint4 (&nw)[NT][C]) {
+        const uint4 *raw = reinterpret_cast<const uint4 *>(smem_raw + L.raw_off + static_cast<size_t>(r) * RAW_STAGE_BYTES);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            const int doc = warp * TILE + 8 * nt + g;
-            const int word = C * t;
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-            for (int i = 0; i < WD; ++i) {
-                const uint32_t *src = raw + (((((doc >> 5) * WD + i) * C + (word >> 2)) * 32 + (doc & 31)) << 2) + (word & 3);
-                if (C == 1) pw[nt][i][0] = src[0];
-                else if (C == 2) { const uint2 v = *reinterpret_cast<const uint2 *>(src); pw[nt][i][0] = v.x; pw[nt][i][C > 1 ? 1 : 0] = v.y; }
-                else { const uint4 v = *reinterpret_cast<const uint4 *>(src); pw[nt][i][0] = v.x; pw[nt][i][C > 1 ? 1 : 0] = v.y; pw[nt][i][C > 2 ? 2 : 0] = v.z; pw[nt][i][C > 3 ? 3 : 0] = v.w; }
-            }
-        }
+            for (int h = 0; h < C; ++h) nw[nt][h] = raw[(warp * TILE + 8 * nt + g) * (4 * C) + C * t + h];
     };
-    auto planes_to_fragments = [&](const uint32_t (&pw)[NT][WD][C], uint32_t (&bw)[WPL]) {
+    // nibble word e of a group holds, in nibble m, the code of dim 4m + e; even / odd nibbles split
+    // into the two byte words of k-step 4h + e: byte j = dim 8j + e (+4)
+    auto nibbles_to_fragments = [&](const uint4 (&nw)[NT][C], uint32_t (&bw)[WPL]) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int h = 0; h < C; ++h) {
-                uint32_t pin[4], o[8];
+                const uint32_t w[4] = {nw[nt][h].x, nw[nt][h].y, nw[nt][h].z, nw[nt][h].w};
 #pragma unroll
-                for (int i = 0; i < 4; ++i) pin[i] = i < WD ? pw[nt][i < WD ? i : 0][h] : 0u;
-                planes_to_bytes<WD>(pin, o);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) bw[(nt * C + h) * 8 + e] = o[e];
+                for (int e = 0; e < 4; ++e) {
+                    bw[(nt * C + h) * 8 + 2 * e] = w[e] & 0x0F0F0F0Fu;
+                    bw[(nt * C + h) * 8 + 2 * e + 1] = (w[e] >> 4) & 0x0F0F0F0Fu;
+                }
             }
     };
 
@@ -500,16 +490,17 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     if (FUSED) {
         Ring rf{0, 0u};
         for (int ci = 0; ci < S; ++ci) {
-            uint32_t pw[NT][WD][C], bw[WPL];
+            uint4 nw[NT][C];
+            uint32_t bw[WPL];
             wait_bar(&raw_full[rf.idx], rf.phase);
-            load_planes(rf.idx, pw);
+            load_nibbles(rf.idx, nw);
             __syncwarp();  // all lanes have their words in registers before the slot is handed back
             if (lane == 0) mbar_arrive(&raw_empty[rf.idx]);
             rf.advance(RR);
             pump();
             const uint32_t doc0 = (static_cast<uint32_t>(sd) * STAGE_ITERS + warp) * TILE;
             if (has_q && doc0 + TILE <= n_pad32) {
-                planes_to_fragments(pw, bw);
+                nibbles_to_fragments(nw, bw);
                 process(bw, doc0);
             }
             if (++sd == Ti) {
@@ -520,11 +511,12 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     } else {
         Ring tr_raw{0, 0u}, tr_byte{0, 1u}, cs{0, 0u};
         auto transpose_stage = [&]() {  // this warp's iteration slot: raw ring -> byte ring
-            uint32_t pw[NT][WD][C], bw[WPL];
+            uint4 nw[NT][C];
+            uint32_t bw[WPL];
             wait_bar(&byte_empty[tr_byte.idx], tr_byte.phase);
             wait_bar(&raw_full[tr_raw.idx], tr_raw.phase);
-            load_planes(tr_raw.idx, pw);
-            planes_to_fragments(pw, bw);
+            load_nibbles(tr_raw.idx, nw);
+            nibbles_to_fragments(nw, bw);
             uint4 *dst = reinterpret_cast<uint4 *>(smem_raw + L.byte_off + static_cast<size_t>(tr_byte.idx) * BYTE_STAGE_BYTES) +
                          static_cast<size_t>(warp) * (RCH * 32) + lane;
 #pragma unroll

@@ -72,9 +72,12 @@ def scan_topk_device(packed: PackedMatrix, qwords, nq: int, query_bits: int, k: 
         C = (packed.dim + 127) // 128
         words_per_query = query_bits * 4 * C  # int32 elements
         st = _stream_ptr(torch)
+        nib = packed.nibbles if query_bits <= 7 and k <= 1024 else None
+        nib_ptr = nib.data_ptr() if nib is not None else None
         for q0 in range(0, nq, _QUERY_BATCH):
             qn = min(_QUERY_BATCH, nq - q0)
-            ws_bytes = int(L.xfbq_scan_workspace_bytes(packed.count, packed.dim, packed.width, qn, query_bits, k))
+            ws_bytes = int(L.xfbq_scan_workspace_bytes(packed.count, packed.dim, packed.width, qn, query_bits, k,
+                                                       1 if nib is not None else 0))
             if ws_bytes < 0:
                 _native.check(_native.E_UNSUPPORTED if k > MAX_K else _native.E_INVALID)
             ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
@@ -82,7 +85,7 @@ def scan_topk_device(packed: PackedMatrix, qwords, nq: int, query_bits: int, k: 
             if SCAN_EVENTS is not None:
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 ev[0].record()
-            _native.check(L.xfbq_scan_topk(packed.codes.data_ptr(), packed.count, packed.dim, packed.width,
+            _native.check(L.xfbq_scan_topk(packed.codes.data_ptr(), nib_ptr, packed.count, packed.dim, packed.width,
                                            qptr, qn, query_bits, k, int(row_offset),
                                            keys.data_ptr() + q0 * k * 8, ws.data_ptr(), ws_bytes, st))
             if SCAN_EVENTS is not None:

@@ -15,6 +15,7 @@ for s in $STAGES; do
            python tools/small_batch.py 1 4 > gpurun_out/q1.log 2>&1; echo "q1 rc=$?"; timeout 300 python tools/small_batch.py 1 50 ; timeout 300 python tools/small_batch.py 8 50 ;;
     ncuq1) timeout 900 ncu --set full --clock-control none --import-source on -k regex:scan_kernel -s 2 -c 2 -f -o gpurun_out/prof_q1 \
            python tools/small_batch.py 1 2 > gpurun_out/ncuq1.log 2>&1; echo "ncuq1 rc=$?" ;;
+    bw) timeout 600 python tools/bw_probe.py > gpurun_out/bw_probe.log 2>&1; echo "bw rc=$?"; cat gpurun_out/bw_probe.log ;;
     micro) timeout 120 tools/bin/microbench > gpurun_out/microbench.jsonl 2>&1; echo "micro rc=$?" ;;
     tests) timeout 400 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "tests rc=$?"; tail -5 gpurun_out/pytest_gpu.log ;;
     bench) timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json ;;
