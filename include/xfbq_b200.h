@@ -149,6 +149,12 @@ int xfbq_merge_topk(const uint64_t *keys_in_dev, int parts, int64_t nq, int k,
 int xfbq_unpack_keys(const uint64_t *keys_dev, int64_t count, int64_t *dist_out_dev,
                      int64_t *id_out_dev, void *stream);
 
+/* Measurement aid: when enabled, the calling host thread records CUDA events on the scan's stream
+ * around the dominant kernel of every xfbq_scan_topk call (the scan itself, not query preparation
+ * or the merge); xfbq_last_scan_ms synchronises on the last one and returns its duration. */
+int xfbq_set_timing(int enable);
+int xfbq_last_scan_ms(float *ms_out);
+
 /* Number of kernels this library has launched in the calling process (for bench accounting). */
 int64_t xfbq_launch_count(void);
 

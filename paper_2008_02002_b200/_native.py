@@ -32,7 +32,7 @@ SYMBOLS = [
     "xfbq_distance_upper_bound", "xfbq_quantize_pack_f32", "xfbq_quantize_pack_f64",
     "xfbq_quantize_queries_f32", "xfbq_quantize_queries_f64", "xfbq_planes_to_bundles",
     "xfbq_bundles_to_planes", "xfbq_nibble_bytes", "xfbq_planes_to_nibbles", "xfbq_batch_distances", "xfbq_scan_workspace_bytes",
-    "xfbq_scan_plan", "xfbq_scan_topk", "xfbq_merge_topk", "xfbq_unpack_keys", "xfbq_launch_count",
+    "xfbq_scan_plan", "xfbq_scan_topk", "xfbq_merge_topk", "xfbq_unpack_keys", "xfbq_set_timing", "xfbq_last_scan_ms", "xfbq_launch_count",
 ]
 
 
@@ -106,6 +106,8 @@ def lib():
         "xfbq_scan_topk": (i32, [vp, vp, i64, i64, i32, vp, i64, i32, i32, i64, vp, vp, i64, vp]),
         "xfbq_merge_topk": (i32, [vp, i32, i64, i32, vp, vp]),
         "xfbq_unpack_keys": (i32, [vp, i64, vp, vp, vp]),
+        "xfbq_set_timing": (i32, [i32]),
+        "xfbq_last_scan_ms": (i32, [vp]),
         "xfbq_launch_count": (i64, []),
     }
     for name in SYMBOLS:
@@ -130,6 +132,17 @@ def check(rc: int) -> None:
             raise DimensionMismatchError(msg)
         raise InvalidInputError(msg)
     raise NativeLibraryError(msg)
+
+
+def set_timing(enable: bool) -> None:
+    check(lib().xfbq_set_timing(1 if enable else 0))
+
+
+def last_scan_ms() -> float:
+    """Device time of the dominant kernel of the last scan issued by this thread (needs set_timing)."""
+    out = ctypes.c_float(0.0)
+    check(lib().xfbq_last_scan_ms(ctypes.byref(out)))
+    return float(out.value)
 
 
 def launch_count() -> int:

@@ -27,6 +27,10 @@ constexpr int SCAN_THREADS = 256;  // 8 warps = 8 bundles = 256 documents per st
 constexpr int SCAN_WARPS = SCAN_THREADS / 32;
 
 thread_local char g_err[512] = "";
+// optional device timing of the main scan kernel (xfbq_set_timing): events live per host thread
+thread_local bool g_timing = false;
+thread_local cudaEvent_t g_ev0 = nullptr, g_ev1 = nullptr;
+thread_local bool g_ev_valid = false;
 std::atomic<int64_t> g_launches{0};
 
 int fail(int code, const char *fmt, ...) {
@@ -802,7 +806,7 @@ int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, boo
     // few documents and its own threshold tightens slowly; a sample scan of the first S documents
     // gives all of them a threshold of selectivity ~k/S up front.
     int64_t sample = env_int("XFBQ_SAMPLE", -1);
-    if (sample < 0) sample = nq > 4 ? (pl.main.groups == 1 ? 32768 : 131072) : 0;
+    if (sample < 0) sample = pl.main.groups == 1 ? 32768 : 131072;
     if (sample > 0 && (n < 16 * sample || sample < 4 * k)) sample = 0;
     pl.sample = sample;
     if (sample) mma_shape(sample, wd, C, nq, k, info, &pl.pre);
@@ -840,7 +844,10 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
         e = cudaMemsetAsync(p.out, 0xFF, sh.parts_bytes, st);
         if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
     }
+    const bool timed = g_timing && &sh == &pl.main;
+    if (timed) cudaEventRecord(g_ev0, st);
     kern<<<static_cast<unsigned>(sh.grid), sh.warps * 32, sh.smem, st>>>(p);
+    if (timed) { cudaEventRecord(g_ev1, st); g_ev_valid = true; }
     if (int rc = check_launch("mma::scan_kernel")) return rc;
     if (sh.parts > 1)
         return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st);
@@ -889,6 +896,25 @@ int quantize_queries_impl(const T *x, int64_t nq, int64_t dim, int64_t ld, doubl
 // ------------------------------------------------------------------------------------- C ABI
 XFBQ_API int xfbq_abi_version(void) { return XFBQ_ABI_VERSION; }
 XFBQ_API const char *xfbq_last_error(void) { return g_err; }
+XFBQ_API int xfbq_set_timing(int enable) {
+    if (enable && !g_ev0) {
+        if (cudaEventCreate(&g_ev0) != cudaSuccess || cudaEventCreate(&g_ev1) != cudaSuccess)
+            return fail(XFBQ_E_CUDA, "cudaEventCreate failed");
+    }
+    g_timing = enable != 0;
+    g_ev_valid = false;
+    return XFBQ_OK;
+}
+
+XFBQ_API int xfbq_last_scan_ms(float *ms_out) {
+    if (!ms_out) return fail(XFBQ_E_INVALID, "null pointer");
+    if (!g_ev_valid) return fail(XFBQ_E_INVALID, "no timed scan recorded (call xfbq_set_timing(1) first)");
+    cudaError_t e = cudaEventSynchronize(g_ev1);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(ms_out, g_ev0, g_ev1);
+    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "event timing: %s", cudaGetErrorString(e));
+    return XFBQ_OK;
+}
+
 XFBQ_API int64_t xfbq_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 XFBQ_API int64_t xfbq_chunks128(int64_t dim) { return chunks128(dim); }
 
@@ -1079,7 +1105,9 @@ XFBQ_API int xfbq_scan_topk(const void *db, const void *nib, int64_t n, int64_t 
     p.k = k; p.cap = pl.cap; p.tq = pl.tq;
     dim3 grid(static_cast<unsigned>(pl.splits), static_cast<unsigned>(pl.q_tiles));
     if (pl.q_tiles > 65535) return fail(XFBQ_E_UNSUPPORTED, "too many query tiles (%d); split the batch", pl.q_tiles);
+    if (g_timing) cudaEventRecord(g_ev0, st);
     kern<<<grid, SCAN_THREADS, pl.smem, st>>>(p);
+    if (g_timing) { cudaEventRecord(g_ev1, st); g_ev_valid = true; }
     if (int rc = check_launch("scan_topk_kernel")) return rc;
     if (pl.splits > 1)
         return launch_merge(static_cast<const uint64_t *>(workspace), pl.splits, nq, k, keys_out,
