@@ -60,13 +60,15 @@ def workload_name(a):
 
 
 def peaks():
+    """(hbm GB/s, dense bf16 TFLOP/s burst, source string)."""
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         try:
-            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+            d = json.loads(p.read_text())
+            return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured (MEASURED_PEAKS.json)"
         except Exception:
             pass
-    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+    return 6650.0, 1590.0, "fallback (B200_PROFILING.md: 6.65 TB/s, 1.59 PFLOP/s)"
 
 
 # ------------------------------------------------------------------------------------ clocks
@@ -237,6 +239,7 @@ def run_ours(a):
     if rank == 0:
         sampler.start()
     xsearch.SCAN_EVENTS = []
+    _native.set_timing(True)
     launches0 = _native.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -248,7 +251,9 @@ def run_ours(a):
     scan_events, xsearch.SCAN_EVENTS = xsearch.SCAN_EVENTS, None
     ms_step = max_over_ranks(e0.elapsed_time(e1) / a.steps)
     scan_ms = [s.elapsed_time(e) for s, e in scan_events]
-    scan_ms_avg = sum(scan_ms) / len(scan_ms)
+    scan_ms_avg = sum(scan_ms) / len(scan_ms)          # whole xfbq_scan_topk call (prep + sample + scan + merge)
+    kernel_ms = _native.last_scan_ms()                  # the dominant kernel alone (last launch of the timed region)
+    _native.set_timing(False)
 
     # ---- end-to-end through the public API with host buffers
     for _ in range(max(1, a.warmup - 1)):
@@ -276,53 +281,72 @@ def run_ours(a):
             e1.record()
             barrier()
             ms = max_over_ranks(e0.elapsed_time(e1) / reps)
+            _native.set_timing(True)
+            kms = []
+            for r in range(5):
+                shard.search_keys(q_dev[r * nq1:(r + 1) * nq1], a.k)
+                kms.append(_native.last_scan_ms())
+            _native.set_timing(False)
+            kms = max_over_ranks(statistics.median(kms))
             single[f"nq{nq1}"] = {"latency_us": round(ms * 1e3, 1), "qps": round(nq1 / ms * 1e3, 1),
-                                  "db_scan_GBps": round(db_bytes_total / ms / 1e6, 1)}
+                                  "scan_kernel_us": round(kms * 1e3, 1),
+                                  "scan_kernel_GBps": round(db_bytes_local / kms / 1e6, 1)}
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
-    peak, peak_src = peaks()
-    scans_per_launch = int(plan[1]) * (min(a.nq, xsearch._QUERY_BATCH) / min(a.nq, xsearch._QUERY_BATCH))
+    hbm_peak, bf16_peak, peak_src = peaks()
     launches_per_step = -(-a.nq // xsearch._QUERY_BATCH)
     q_tiles_total = sum(-(-min(xsearch._QUERY_BATCH, a.nq - q0) // int(plan[0])) for q0 in range(0, a.nq, xsearch._QUERY_BATCH))
     algo_bytes_per_launch = db_bytes_local * q_tiles_total / launches_per_step
-    achieved = algo_bytes_per_launch / (scan_ms_avg * 1e-3) / 1e9
-    popc32 = index.n * a.nq * a.doc_bits * a.query_bits * ((a.dim + 31) // 32)
-    sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
-    popc_peak = 16 * 148 * sm_mhz * 1e6
+    engine = {2: "imma", 1: "popc-specialised", 0: "popc-generic"}[int(plan[4])]
+    # integer work of one launch: nq x n_local x dim_padded multiply-accumulates (u8 x s8 -> s32)
+    dim_pad = ((a.dim + 127) // 128) * 128
+    macs_per_launch = float(index.n) * min(a.nq, xsearch._QUERY_BATCH) * dim_pad
+    tops = 2.0 * macs_per_launch / (kernel_ms * 1e-3) / 1e12
+    int8_peak = 2.0 * bf16_peak  # dense int8 tensor rate = 2 x dense bf16 on B200 (tcgen05 path)
+    sb = (single or {}).get("nq16") or {}
     out = {
         "metric": METRIC, "value": round(a.nq / ms_step * 1e3, 2), "unit": "queries/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u32 (XOR/POPC on packed bit planes; u64 keys)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8 x s8 -> s32 (exact integer form of the XOR/POPC distance); u64 keys",
         "data": "synthetic",
         "config": {"workload": workload_name(a), "n": a.n, "dim": a.dim, "doc_bits": a.doc_bits,
                    "query_bits": a.query_bits, "nq": a.nq, "k": a.k,
                    "sharding": f"rows/{world}" if world > 1 else "none",
                    "l2": "inputs larger than L2 (packed DB %.0f MB per GPU streamed every scan)" % (db_bytes_local / 1e6),
-                   "plan": {"queries_per_tile": int(plan[0]), "query_tiles": int(plan[1]), "doc_splits": int(plan[2]),
-                            "cand_capacity": int(plan[3]), "specialised_kernel": bool(plan[4]), "smem_bytes": int(plan[5])}},
+                   "plan": {"engine": engine, "queries_per_cta": int(plan[0]), "query_groups": int(plan[1]), "partial_results": int(plan[2]),
+                            "cand_capacity": int(plan[3]), "smem_bytes": int(plan[5])}},
         "e2e": {"value": round(a.nq / e2e_ms * 1e3, 2), "unit": "queries/s", "ms_per_step": round(e2e_ms, 3),
                 "h2d_bytes_per_step": int(q_pinned.numel() * 4), "d2h_bytes_per_step": int(a.nq * min(a.k, a.n) * 8)},
         "gpu_launches": int(launches),
         "clocks": clocks,
-        "roofline": {"bound": "hbm", "kernel": "scan_topk_kernel (+ partial-result merge)", "achieved": round(achieved, 1),
-                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                     "peak_source": peak_src, "launch_ms": round(scan_ms_avg, 3),
-                     "algorithmic_bytes_per_launch": int(algo_bytes_per_launch),
-                     "note": "one launch scans the shard once per query tile; large batches are integer-pipe bound"},
-        "integer_pipe": {"popc32_per_step": int(popc32), "achieved_Gpopc_per_s": round(popc32 / (scan_ms_avg * launches_per_step * 1e-3) / 1e9, 1),
-                         "peak_Gpopc_per_s": round(popc_peak / 1e9, 1), "peak_basis": "16 POPC/clk/SM x 148 SMs x median SM clock",
-                         "frac": round(popc32 / (scan_ms_avg * launches_per_step * 1e-3) / popc_peak, 4)},
+        "roofline": {"bound": "tensor",
+                     "kernel": "mma::scan_kernel (batch plan: IMMA.16832 + fused top-K)" if engine == "imma" else "scan_topk_kernel",
+                     "achieved": round(tops, 1), "peak": round(int8_peak, 1), "unit": "TOP/s (int8, dense)",
+                     "frac": round(tops / int8_peak, 4), "traffic": None,
+                     "peak_source": peak_src + ": 2 x dense bf16 burst = int8 rate of the tcgen05 path",
+                     "launch_ms": round(kernel_ms, 3), "macs_per_launch": int(macs_per_launch),
+                     "legacy_imma_pipe_peak_TOPs": 1163.7, "frac_of_legacy_imma_pipe": round(tops / 1163.7, 4),
+                     "note": "mma.sync int8 (IMMA.16832) pipe peak is 4096 op/clk/SM (ncu) = 1164 TOP/s; "
+                             "the tcgen05 int8 path would be 4x that"},
+        "roofline_hbm": {"bound": "hbm", "kernel": "mma::scan_kernel (small-batch plan, nq=16)",
+                         "achieved": sb.get("scan_kernel_GBps"), "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(sb["scan_kernel_GBps"] / hbm_peak, 4) if sb else None,
+                         "algorithmic_bytes_per_launch": int(db_bytes_local), "launch_us": sb.get("scan_kernel_us"),
+                         "peak_source": peak_src,
+                         "note": "one launch streams the shard once (n x doc_bits x ceil(dim/64) x 8 bytes) for a tile of <= 16 queries"},
+        "batch_scan": {"engine": engine, "call_ms": round(scan_ms_avg, 3), "kernel_ms": round(kernel_ms, 3),
+                       "db_passes_per_launch": q_tiles_total / launches_per_step,
+                       "algorithmic_GBps": round(algo_bytes_per_launch / (kernel_ms * 1e-3) / 1e9, 1)},
         "small_batch": single,
         "recall_at_k_vs_float_cosine": recall,
         "build": {"rows_per_s": round((hi - lo) / build_s, 1), "seconds": round(build_s, 3),
                   "quantize_kernel_ms": round(quant_ms, 3),
                   "quantize_read_GBps": round((hi - lo) * a.dim * 4 / (quant_ms * 1e-3) / 1e9, 1)},
     }
-    del scans_per_launch
     if world == 1 and not a.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_from_index(a, index, q_host, res)
     print(json.dumps(out))
