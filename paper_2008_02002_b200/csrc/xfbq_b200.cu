@@ -709,6 +709,12 @@ MmaKernel pick_mma_kernel(int C, bool fused, int warps) {
         if (C == 2) return mma::scan_kernel<2, 1, 2, true, mma::WARPS_WIDE>;
         return nullptr;
     }
+    if (warps == mma::WARPS_BATCH) {
+        if (C == 1) return mma::scan_kernel<1, 2, 2, false, mma::WARPS_BATCH>;
+        if (C == 2) return mma::scan_kernel<2, 2, 2, false, mma::WARPS_BATCH>;
+        if (C == 4) return mma::scan_kernel<4, 1, 1, false, mma::WARPS_BATCH>;
+        return nullptr;
+    }
 #define XFBQ_MMA_CASE(C_, MT_, NT_) \
     if (C == C_) return fused ? mma::scan_kernel<C_, MT_, NT_, true, mma::WARPS> : mma::scan_kernel<C_, MT_, NT_, false, mma::WARPS>;
     XFBQ_MMA_CASE(1, 2, 2) XFBQ_MMA_CASE(2, 2, 2) XFBQ_MMA_CASE(4, 1, 1)
@@ -728,6 +734,8 @@ void mma_shape(int64_t n, int wd, int C, int64_t nq, int k, const DeviceInfo &in
         sh.warps = mma::WARPS_WIDE;
     }
     sh.QPW = 16 * sh.MT;
+    if ((nq + sh.QPW - 1) / sh.QPW >= mma::WARPS_BATCH && env_int("XFBQ_BATCH_WARPS", mma::WARPS_BATCH) == mma::WARPS_BATCH)
+        sh.warps = mma::WARPS_BATCH;  // full batch: 12 query warps per CTA
     int cap = 64;
     while (cap < 2 * k) cap <<= 1;
     sh.cap = cap;
@@ -766,7 +774,7 @@ void mma_shape(int64_t n, int wd, int C, int64_t nq, int k, const DeviceInfo &in
     const int raw_stage = sh.warps * 8 * sh.NT * 64 * C;  // nibble layout: 64C bytes per document
     const int byte_stage = sh.warps * (sh.NT * C * 8) * 32 * 4;
     sh.fused = sh.QW == 1 && sh.groups == 1 && env_int("XFBQ_NO_FUSED", 0) == 0;
-    int RR = env_int("XFBQ_RAW_STAGES", sh.fused ? (sh.warps == mma::WARPS ? 8 : 5) : 6), BR = sh.fused ? 0 : env_int("XFBQ_BYTE_STAGES", 4);
+    int RR = env_int("XFBQ_RAW_STAGES", sh.fused ? (sh.warps == mma::WARPS ? 8 : 5) : (sh.warps == mma::WARPS ? 6 : 3)), BR = sh.fused ? 0 : env_int("XFBQ_BYTE_STAGES", sh.warps == mma::WARPS ? 4 : 3);
     const int br_min = sh.fused ? 0 : mma::AHEAD + 1;
     if (BR < br_min) BR = br_min;
     if (RR < 1) RR = 1;

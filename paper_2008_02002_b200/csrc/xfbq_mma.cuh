@@ -31,6 +31,7 @@ namespace mma {
 
 constexpr int WARPS = 8;        // warps per CTA in ring (batch) mode and the default fused mode
 constexpr int WARPS_WIDE = 16;  // fused mode for <= 16 queries: twice the warps hide ALU latency
+constexpr int WARPS_BATCH = 12; // ring mode with >= 12 query warps: 3 warps per scheduler
 constexpr int TAU_OPEN = -(1 << 30);  // threshold that lets every score through (no list yet)
 
 
@@ -266,6 +267,7 @@ struct Ring {
 template <int C, int MT, int NT, bool FUSED, int NW>
 __global__ void __launch_bounds__(NW * 32, 1) scan_kernel(const Params p) {
     constexpr int WARPS = NW;           // shadows the namespace default
+    constexpr int WARPS_DEFAULT = 8;
     constexpr int STAGE_ITERS = NW;     // iterations per stage: one produced by each warp
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int QPW = 16 * MT;        // query rows per warp
@@ -546,18 +548,28 @@ __global__ void __launch_bounds__(NW * 32, 1) scan_kernel(const Params p) {
                         bw[4 * r] = v.x; bw[4 * r + 1] = v.y; bw[4 * r + 2] = v.z; bw[4 * r + 3] = v.w;
                     }
                 };
-                uint32_t bwA[WPL], bwB[WPL];
-                int i = dw;
-                if (i < n_it) fetch(bwA, i);
-                while (i < n_it) {
-                    const int i2 = i + DW;
-                    if (i2 < n_it) fetch(bwB, i2);
-                    process(bwA, stage_doc0 + i * TILE);
-                    if (i2 >= n_it) break;
-                    const int i3 = i2 + DW;
-                    if (i3 < n_it) fetch(bwA, i3);
-                    process(bwB, stage_doc0 + i2 * TILE);
-                    i = i3;
+                if (NW <= WARPS_DEFAULT) {
+                    // two fragment register sets: the LDS of iteration i+1 overlap the IMMAs of i
+                    uint32_t bwA[WPL], bwB[WPL];
+                    int i = dw;
+                    if (i < n_it) fetch(bwA, i);
+                    while (i < n_it) {
+                        const int i2 = i + DW;
+                        if (i2 < n_it) fetch(bwB, i2);
+                        process(bwA, stage_doc0 + i * TILE);
+                        if (i2 >= n_it) break;
+                        const int i3 = i2 + DW;
+                        if (i3 < n_it) fetch(bwA, i3);
+                        process(bwB, stage_doc0 + i2 * TILE);
+                        i = i3;
+                    }
+                } else {
+                    // more warps per scheduler instead (register budget 168): single fragment set
+                    for (int i = dw; i < n_it; i += DW) {
+                        uint32_t bw[WPL];
+                        fetch(bw, i);
+                        process(bw, stage_doc0 + i * TILE);
+                    }
                 }
             }
             __syncwarp();

@@ -20,7 +20,7 @@ for s in $STAGES; do
     tests) timeout 400 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "tests rc=$?"; tail -5 gpurun_out/pytest_gpu.log ;;
     bench) timeout 900 python bench.py --steps 3 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json ;;
     ncu) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
-           python bench.py --steps 1 --warmup 1 --nq 2048 --no-cpu-baseline --no-extras > gpurun_out/ncu_bench.log 2>&1; echo "ncu rc=$?" ;;
+           python bench.py --steps 1 --warmup 1 --nq 10000 --no-cpu-baseline --no-extras > gpurun_out/ncu_bench.log 2>&1; echo "ncu rc=$?" ;;
     ncufull) timeout 900 ncu --set full --clock-control none --import-source on -k regex:scan_topk -c 3 -f -o gpurun_out/prof_scan \
            python bench.py --steps 1 --warmup 1 --nq 512 --no-cpu-baseline > gpurun_out/ncufull.log 2>&1; echo "ncufull rc=$?" ;;
   esac
