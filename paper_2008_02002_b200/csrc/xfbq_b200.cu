@@ -455,7 +455,7 @@ merge_topk_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k,
 // rows A, B of length K2 reduce to the K2 smallest of their union by c_i = min(A_i, B_{K2-1-i})
 // (a bitonic sequence) followed by log2(K2) bitonic-merge stages; log2(G) rounds leave the answer
 // in row 0.  Far fewer barrier stages than re-sorting, so single-query latency stays small.
-template <int K2>
+template <int K2, bool SORT>
 __global__ void __launch_bounds__(512)
 merge_tree_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k, int G,
                   uint64_t *__restrict__ out) {
@@ -471,6 +471,20 @@ merge_tree_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k,
         buf[idx] = (r < rows && i < k) ? in[((static_cast<int64_t>(p0) + r) * nq + q) * k + i] : KEY_INF;
     }
     __syncthreads();
+    if (SORT) {  // rows arrive unsorted (tensor engine emits its lists as they are): bitonic sort of every row
+        for (int size = 2; size <= K2; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int idx = threadIdx.x; idx < active * (K2 >> 1); idx += blockDim.x) {
+                    const int r = idx / (K2 >> 1), t = idx % (K2 >> 1);
+                    const int c = 2 * t - (t & (stride - 1));
+                    const int lo = r * K2 + c, hi = lo + stride;
+                    const bool up = (c & size) == 0;
+                    const uint64_t a = buf[lo], b = buf[hi];
+                    if ((a > b) == up) { buf[lo] = b; buf[hi] = a; }
+                }
+                __syncthreads();
+            }
+    }
     while (active > 1) {
         const int half = active >> 1;
         for (int idx = threadIdx.x; idx < half * K2; idx += blockDim.x) {
@@ -638,28 +652,30 @@ int64_t merge_scratch_parts(int parts, int k, int64_t nq) { return merge_levels(
 
 typedef void (*MergeKernel)(const uint64_t *, int, int64_t, int, int, uint64_t *);
 
-MergeKernel pick_merge_kernel(int K2) {
+MergeKernel pick_merge_kernel(int K2, bool sort) {
+#define XFBQ_MERGE_CASE(K_) case K_: return sort ? merge_tree_kernel<K_, true> : merge_tree_kernel<K_, false>;
     switch (K2) {
-        case 32: return merge_tree_kernel<32>;
-        case 64: return merge_tree_kernel<64>;
-        case 128: return merge_tree_kernel<128>;
-        case 256: return merge_tree_kernel<256>;
-        case 512: return merge_tree_kernel<512>;
-        case 1024: return merge_tree_kernel<1024>;
-        case 2048: return merge_tree_kernel<2048>;
-        case 4096: return merge_tree_kernel<4096>;
+        XFBQ_MERGE_CASE(32) XFBQ_MERGE_CASE(64) XFBQ_MERGE_CASE(128) XFBQ_MERGE_CASE(256)
+        XFBQ_MERGE_CASE(512) XFBQ_MERGE_CASE(1024) XFBQ_MERGE_CASE(2048) XFBQ_MERGE_CASE(4096)
     }
+#undef XFBQ_MERGE_CASE
     return nullptr;
 }
 
 int launch_merge(const uint64_t *in, int parts, int64_t nq, int k, uint64_t *out, uint64_t *scratch,
-                 cudaStream_t st) {
-    const MergeLevels ml = merge_levels(parts, k, nq);
-    if (nq > 65535 || ml.levels == 0 || parts <= 1 || (ml.scratch_parts > 0 && !scratch) || ml.groups[ml.levels - 1] != 1)
+                 cudaStream_t st, bool sort_input = false) {
+    MergeLevels ml = merge_levels(parts, k, nq);
+    if (sort_input && parts == 1 && merge_group_max(k) > 0) {  // nothing to merge, but the row must be sorted
+        ml.levels = 1; ml.G[0] = 1; ml.groups[0] = 1; ml.scratch_parts = 0;
+    }
+    const bool tree_ok = nq <= 65535 && ml.levels > 0 && !(ml.scratch_parts > 0 && !scratch) && ml.groups[ml.levels - 1] == 1;
+    if (!tree_ok) {
+        if (sort_input) return fail(XFBQ_E_UNSUPPORTED, "unsorted partial results need the tree merge (parts=%d nq=%lld k=%d)", parts, (long long)nq, k);
         return launch_merge_stream(in, parts, nq, k, out, st);
+    }
     const int K2 = merge_k2(k);
-    MergeKernel kern = pick_merge_kernel(K2);
     for (int l = 0; l < ml.levels; ++l) {
+        MergeKernel kern = pick_merge_kernel(K2, sort_input && l == 0);
         const int G = ml.G[l], groups = ml.groups[l];
         int rows = parts < G ? parts : G, active = 1;
         while (active < rows) active <<= 1;
@@ -786,7 +802,7 @@ void mma_shape(int64_t n, int wd, int C, int64_t nq, int k, const DeviceInfo &in
     sh.RR = RR; sh.BR = BR;
     sh.smem = RR ? mma::smem_layout(raw_stage, byte_stage, RR, BR, cap, sh.warps).total : 0;
     sh.lists_bytes = static_cast<size_t>(sh.grid) * sh.warps * sh.QPW * cap * 8;
-    sh.parts_bytes = sh.parts > 1 ? static_cast<size_t>(sh.parts) * nq * k * 8 : 0;
+    sh.parts_bytes = static_cast<size_t>(sh.parts) * nq * k * 8;  // lists are emitted unsorted: always merged/sorted
     sh.mscratch_bytes = static_cast<size_t>(merge_scratch_parts(sh.parts, k, nq)) * nq * k * 8;
     *out = sh;
 }
@@ -814,7 +830,9 @@ int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, boo
     // few documents and its own threshold tightens slowly; a sample scan of the first S documents
     // gives all of them a threshold of selectivity ~k/S up front.
     int64_t sample = env_int("XFBQ_SAMPLE", -1);
-    if (sample < 0) sample = pl.main.groups == 1 ? 32768 : 131072;
+    // (Measured: for full batches the sample scan costs more than it saves -- every candidate list
+    // of the sample scan floods from an open threshold -- so only small batches use it.)
+    if (sample < 0) sample = pl.main.groups == 1 ? (nq <= 4 ? 32768 : 65536) : 131072;
     if (sample > 0 && (n < 16 * sample || sample < 4 * k)) sample = 0;
     pl.sample = sample;
     if (sample) mma_shape(sample, wd, C, nq, k, info, &pl.pre);
@@ -844,11 +862,12 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
     p.qconst = reinterpret_cast<const int32_t *>(ws + pl.off_qconst);
     p.tau_init = tau_init;
     p.lists = reinterpret_cast<uint64_t *>(ws + pl.off_lists);
-    p.out = sh.parts > 1 ? reinterpret_cast<uint64_t *>(ws + pl.off_parts) : keys_out;
+    const bool direct = sh.parts == 1 && sh.cap <= mma::SORT_CAP_MAX;  // one sorted part: it is the result
+    p.out = direct ? keys_out : reinterpret_cast<uint64_t *>(ws + pl.off_parts);
     p.nq = nq; p.stages = sh.stages; p.groups = sh.groups;
     p.k = k; p.cap = sh.cap; p.QW = sh.QW; p.DW = sh.DW;
     p.RR = sh.RR; p.BR = sh.BR;
-    if (sh.parts > 1) {  // slots a group does not use stay KEY_INF
+    if (sh.slots > 1) {  // slots a group does not use stay KEY_INF
         e = cudaMemsetAsync(p.out, 0xFF, sh.parts_bytes, st);
         if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
     }
@@ -857,9 +876,9 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
     kern<<<static_cast<unsigned>(sh.grid), sh.warps * 32, sh.smem, st>>>(p);
     if (timed) { cudaEventRecord(g_ev1, st); g_ev_valid = true; }
     if (int rc = check_launch("mma::scan_kernel")) return rc;
-    if (sh.parts > 1)
-        return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st);
-    return XFBQ_OK;
+    if (direct) return XFBQ_OK;
+    return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st,
+                        sh.cap > mma::SORT_CAP_MAX);  // large lists are emitted unsorted
 }
 
 template <typename T>

@@ -138,7 +138,99 @@ __device__ __forceinline__ uint64_t shfl_u64(uint64_t v, int src) {
     return (static_cast<uint64_t>(hi) << 32) | lo;
 }
 
-// Warp-level bitonic sort of P (power of two) keys in this warp's shared scratch.
+// Per-lane selection state: lane l owns query row l of the warp.
+struct LaneState {
+    int dq;   // Dq = Ad * sum(y) of the row's query
+    int tau;  // pass iff acc >= tau  (tau = Dq - distance of the k-th best key so far)
+};
+
+// Warp-level radix select, in place on a candidate list row in global memory (read through L2):
+// keeps exactly the k smallest of the cnt > k unique keys (order not preserved) and returns the
+// k-th smallest key.  MSB-first, one byte per pass, starting at the highest byte in which the keys
+// differ; 256-bin histogram per warp in shared memory.  Cost ~ (passes + 2) * cnt / 32 loads per
+// lane, instead of a cnt * log^2(cnt) sort.
+__device__ __noinline__ uint64_t select_row(uint64_t *row, int cnt, int k, int *hist, int lane) {
+    __syncwarp();
+    const uint64_t first = __ldcg(row);
+    uint64_t diff = 0;
+    for (int i = lane; i < cnt; i += 32) diff |= __ldcg(row + i) ^ first;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t lo = __shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(diff), o);
+        const uint32_t hi = __shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(diff >> 32), o);
+        diff |= (static_cast<uint64_t>(hi) << 32) | lo;
+    }
+    int shift = ((63 - __clzll(static_cast<long long>(diff | 1ull))) >> 3) << 3;  // byte holding the top differing bit
+    uint64_t hi_mask = shift + 8 >= 64 ? 0ull : ~((1ull << (shift + 8)) - 1ull);    // bits already common to all keys
+    uint64_t prefix = first & hi_mask;
+    int want = k;  // rank of the k-th key inside the current candidate bucket (1-based)
+    while (true) {
+        for (int b = lane; b < 256; b += 32) hist[b] = 0;
+        __syncwarp();
+        for (int i = lane; i < cnt; i += 32) {
+            const uint64_t key = __ldcg(row + i);
+            if ((key & hi_mask) == prefix) atomicAdd(&hist[static_cast<int>(key >> shift) & 255], 1);
+        }
+        __syncwarp();
+        int h[8], s = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) { h[e] = hist[8 * lane + e]; s += h[e]; }
+        int inc = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        const int exc = inc - s;
+        const bool mine = exc < want && want <= inc;  // exactly one lane
+        int bucket = 0, below = exc, bcnt = 0;
+        if (mine) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if (bcnt == 0) {
+                    if (below + h[e] >= want) { bucket = 8 * lane + e; bcnt = h[e]; }
+                    else below += h[e];
+                }
+            }
+        }
+        const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+        bucket = __shfl_sync(0xffffffffu, bucket, src);
+        below = __shfl_sync(0xffffffffu, below, src);
+        bcnt = __shfl_sync(0xffffffffu, bcnt, src);
+        prefix |= static_cast<uint64_t>(bucket) << shift;
+        hi_mask |= 0xFFull << shift;
+        want -= below;
+        __syncwarp();
+        if (bcnt == want || shift == 0) break;  // the whole bucket belongs to the k smallest
+        shift -= 8;
+    }
+    // partition in place: keep keys whose fixed bits are <= prefix (exactly k of them); k-th = their max
+    uint64_t kth = 0;
+    int out = 0;
+    for (int base = 0; base < cnt; base += 32) {
+        const int i = base + lane;
+        const uint64_t key = i < cnt ? __ldcg(row + i) : KEY_INF;
+        const bool keep = i < cnt && (key & hi_mask) <= prefix;
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            row[out + __popc(m & ((1u << lane) - 1u))] = key;  // out + rank <= i: never overwrites unread keys
+            kth = key > kth ? key : kth;
+        }
+        out += __popc(m);
+        __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t lo = __shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(kth), o);
+        const uint32_t hi = __shfl_xor_sync(0xffffffffu, static_cast<uint32_t>(kth >> 32), o);
+        const uint64_t other = (static_cast<uint64_t>(hi) << 32) | lo;
+        kth = other > kth ? other : kth;
+    }
+    __syncwarp();
+    return kth;
+}
+
+// Warp-level bitonic sort of P (power of two) keys in this warp's shared scratch (small lists).
 __device__ __forceinline__ void warp_bitonic(uint64_t *s, int P, int lane) {
     for (int size = 2; size <= P; size <<= 1)
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
@@ -153,16 +245,9 @@ __device__ __forceinline__ void warp_bitonic(uint64_t *s, int P, int lane) {
         }
 }
 
-// Per-lane selection state: lane l owns query row l of the warp.
-struct LaneState {
-    int dq;   // Dq = Ad * sum(y) of the row's query
-    int tau;  // pass iff acc >= tau  (tau = Dq - distance of the k-th best key so far)
-};
-
-// Sort list row `ql` through the warp's scratch, keep the k best, refresh the row's threshold.
-// Warp-uniform call.  Returns -tau of the row (for the per-lane accumulator bias copies).
-__device__ __forceinline__ int compact_row(uint64_t *list_row, uint64_t *scratch, int *cnt_p, int k, int ql,
-                                           int lane, LaneState &st) {
+// Small lists (cap <= 512): sort the row through the warp's shared scratch, keep the k best.
+__device__ __noinline__ int compact_row_sorted(uint64_t *list_row, uint64_t *scratch, int *cnt_p, int k, int ql,
+                                               int lane, int dq, int *tau_io) {
     __syncwarp();
     const int cnt = *cnt_p;
     int P = 2;
@@ -174,12 +259,52 @@ __device__ __forceinline__ int compact_row(uint64_t *list_row, uint64_t *scratch
     for (int i = lane; i < keep; i += 32) list_row[i] = scratch[i];
     const uint64_t kth = cnt >= k ? scratch[k - 1] : KEY_INF;
     __syncwarp();
+    int tau = *tau_io;
     if (lane == ql) {
         *cnt_p = keep;
-        if (cnt >= k) st.tau = st.dq - static_cast<int>(kth >> 32);
+        if (cnt >= k) tau = dq - static_cast<int>(kth >> 32);
     }
+    *tau_io = tau;
     __syncwarp();
-    return -__shfl_sync(0xffffffffu, st.tau, ql);
+    return -__shfl_sync(0xffffffffu, tau, ql);
+}
+
+// Cut list row `ql` to its k best keys and refresh the row's threshold.  Warp-uniform call.
+// Returns -tau of the row (for the per-lane accumulator bias copies).
+__device__ __noinline__ int compact_row(uint64_t *list_row, int *hist, int *cnt_p, int k, int ql, int lane,
+                                        int dq, int *tau_io) {
+    __syncwarp();
+    const int cnt = *cnt_p;
+    int tau = *tau_io;
+    if (cnt > k) {
+        const uint64_t kth = select_row(list_row, cnt, k, hist, lane);
+        if (lane == ql) {
+            *cnt_p = k;
+            tau = dq - static_cast<int>(kth >> 32);
+        }
+    }
+    *tau_io = tau;
+    __syncwarp();
+    return -__shfl_sync(0xffffffffu, tau, ql);
+}
+
+// Out-of-line candidate push for one 16-row x 8-doc tile (keeps the cold code out of the hot loop's
+// instruction-cache footprint): lanes whose score passed append (distance << 32 | row id).
+__device__ __noinline__ void push_tile(int v0, int v1, int v2, int v3, int dq0, int dq1, int nt0, int nt1,
+                                       uint32_t doc_a, uint32_t n_docs, int row_a, uint64_t row_offset,
+                                       uint64_t *lists, int *cnt_s, int cap) {
+    // (v0, v1): row row_a, docs doc_a, doc_a+1;  (v2, v3): row row_a+8, same docs
+    const int v[4] = {v0, v1, v2, v3};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t doc = doc_a + (j & 1);
+        if (v[j] >= 0 && doc < n_docs) {
+            const int row = row_a + 8 * (j >> 1);
+            const uint32_t dist = static_cast<uint32_t>((j >> 1 ? dq1 + nt1 : dq0 + nt0) - v[j]);
+            const int pos = atomicAdd(&cnt_s[row], 1);
+            lists[row * cap + pos] = (static_cast<uint64_t>(dist) << 32) | (row_offset + doc);
+        }
+    }
 }
 
 // ------------------------------------------------------------------------------ mbarrier / TMA
@@ -227,6 +352,7 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_
 }
 
 constexpr int AHEAD = 2;  // stages a worker transposes ahead of the stage it consumes
+constexpr int SORT_CAP_MAX = 512;  // lists up to this capacity are compacted by a shared-memory sort
 
 // Shared-memory carve-up shared by host (size) and device (pointers).
 struct SmemLayout {
@@ -238,7 +364,8 @@ __host__ __device__ inline SmemLayout smem_layout(int raw_stage_bytes, int byte_
     L.raw_off = off; off += static_cast<uint32_t>(RR) * raw_stage_bytes;
     off = (off + 127u) & ~127u;
     L.byte_off = off; off += static_cast<uint32_t>(BR) * byte_stage_bytes;
-    L.scratch_off = off; off += static_cast<uint32_t>(warps) * cap * 8;
+    // per warp: sort scratch for small lists (cap <= 512 keys), else the radix-select histogram
+    L.scratch_off = off; off += static_cast<uint32_t>(warps) * (cap <= SORT_CAP_MAX ? cap * 8 : 256 * 4);
     L.cnt_off = off; off += warps * 32 * 4;
     L.bar_off = off; off += static_cast<uint32_t>(2 * RR + 2 * BR) * 8;
     L.total = off;
@@ -337,7 +464,9 @@ __global__ void __launch_bounds__(NW * 32, 1) scan_kernel(const Params p) {
     const int g = lane >> 2, t = lane & 3;
     const int qw = FUSED ? 0 : warp % p.QW, dw = FUSED ? warp : warp / p.QW;
     const int DW = FUSED ? WARPS : p.DW;
+    const bool small_lists = p.cap <= SORT_CAP_MAX;  // sorted (bitonic) vs selected (radix) compaction / emission
     uint64_t *scratch = reinterpret_cast<uint64_t *>(smem_raw + L.scratch_off) + static_cast<size_t>(warp) * p.cap;
+    int *hist = reinterpret_cast<int *>(smem_raw + L.scratch_off) + warp * 256;
     int *cnt_s = reinterpret_cast<int *>(smem_raw + L.cnt_off) + warp * 32;
     uint64_t *lists = p.lists + (static_cast<int64_t>(blockIdx.x) * WARPS + warp) * QPW * static_cast<int64_t>(p.cap);
 
@@ -374,23 +503,33 @@ __global__ void __launch_bounds__(NW * 32, 1) scan_kernel(const Params p) {
     st.dq = 0; st.tau = 1;
     int negtau[MT][2], dqrow[MT][2];
 
-    auto emit_segment = [&]() {  // every query row of this warp, sorted, KEY_INF padded
-        if (!has_q) return;
+    auto emit_segment = [&]() {  // every query row of this warp: its <= k best keys, KEY_INF padded
+        if (!has_q) return;        // (sorted for small lists, unsorted otherwise: the merge sorts those)
         __syncwarp();
         for (int ql = 0; ql < QPW; ++ql) {
             const int64_t q = q0 + ql;
             if (q >= p.nq) break;
-            const int cnt = cnt_s[ql];
-            const uint64_t *row = lists + static_cast<int64_t>(ql) * p.cap;
-            int P = 2;
-            while (P < cnt) P <<= 1;
-            for (int i = lane; i < P; i += 32) scratch[i] = i < cnt ? __ldcg(row + i) : KEY_INF;
-            __syncwarp();
-            warp_bitonic(scratch, P, lane);
+            int cnt = cnt_s[ql];
+            uint64_t *row = lists + static_cast<int64_t>(ql) * p.cap;
             uint64_t *dst = p.out + (part * p.nq + q) * p.k;
-            for (int i = lane; i < p.k; i += 32) dst[i] = i < cnt ? scratch[i] : KEY_INF;
-            __syncwarp();
+            if (small_lists) {
+                int P = 2;
+                while (P < cnt) P <<= 1;
+                for (int i = lane; i < P; i += 32) scratch[i] = i < cnt ? __ldcg(row + i) : KEY_INF;
+                __syncwarp();
+                warp_bitonic(scratch, P, lane);
+                for (int i = lane; i < p.k; i += 32) dst[i] = i < cnt ? scratch[i] : KEY_INF;
+                __syncwarp();
+            } else {
+                if (cnt > p.k) {
+                    select_row(row, cnt, p.k, hist, lane);
+                    cnt = p.k;
+                }
+                __syncwarp();
+                for (int i = lane; i < p.k; i += 32) dst[i] = i < cnt ? __ldcg(row + i) : KEY_INF;
+            }
         }
+        __syncwarp();
     };
     auto begin_segment = [&](int gr) {
         // part slot: CTAs overlapping group gr are numbered from the first one
@@ -457,25 +596,19 @@ __global__ void __launch_bounds__(NW * 32, 1) scan_kernel(const Params p) {
             for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) {
-                    if (pm[mt][nt] < 0) continue;  // per-lane: none of this lane's 4 scores of the tile passed
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int v = c[mt][nt][j];
-                        const uint32_t doc = doc0 + 8 * nt + 2 * t + (j & 1);
-                        if (v >= 0 && doc < n_docs) {
-                            const int row = 16 * mt + g + 8 * (j >> 1);
-                            const uint32_t dist = static_cast<uint32_t>(dqrow[mt][j >> 1] + negtau[mt][j >> 1] - v);
-                            const int pos = atomicAdd(&cnt_s[row], 1);
-                            lists[row * p.cap + pos] = (static_cast<uint64_t>(dist) << 32) | (static_cast<uint64_t>(p.row_offset) + doc);
-                        }
-                    }
+                    if (pm[mt][nt] >= 0)  // per-lane: one of this lane's 4 scores of the tile passed
+                        push_tile(c[mt][nt][0], c[mt][nt][1], c[mt][nt][2], c[mt][nt][3], dqrow[mt][0], dqrow[mt][1],
+                                  negtau[mt][0], negtau[mt][1], doc0 + 8 * nt + 2 * t, n_docs, 16 * mt + g,
+                                  static_cast<uint64_t>(p.row_offset), lists, cnt_s, p.cap);
                 }
             __syncwarp();
             unsigned need = __ballot_sync(0xffffffffu, lane < QPW && cnt_s[lane] > p.cap - TILE);
             while (need) {
                 const int ql = __ffs(need) - 1;
                 need &= need - 1;
-                const int nv = compact_row(lists + ql * p.cap, scratch, &cnt_s[ql], p.k, ql, lane, st);
+                const int nv = small_lists
+                                   ? compact_row_sorted(lists + ql * p.cap, scratch, &cnt_s[ql], p.k, ql, lane, st.dq, &st.tau)
+                                   : compact_row(lists + ql * p.cap, hist, &cnt_s[ql], p.k, ql, lane, st.dq, &st.tau);
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
                     if (16 * mt + g == ql) negtau[mt][0] = nv;
