@@ -301,7 +301,7 @@ def run_ours(a):
     launches_per_step = -(-a.nq // xsearch._QUERY_BATCH)
     q_tiles_total = sum(-(-min(xsearch._QUERY_BATCH, a.nq - q0) // int(plan[0])) for q0 in range(0, a.nq, xsearch._QUERY_BATCH))
     algo_bytes_per_launch = db_bytes_local * q_tiles_total / launches_per_step
-    engine = {2: "imma", 1: "popc-specialised", 0: "popc-generic"}[int(plan[4])]
+    engine = {3: "umma", 2: "imma", 1: "popc-specialised", 0: "popc-generic"}[int(plan[4])]
     # integer work of one launch: nq x n_local x dim_padded multiply-accumulates (u8 x s8 -> s32)
     dim_pad = ((a.dim + 127) // 128) * 128
     macs_per_launch = float(index.n) * min(a.nq, xsearch._QUERY_BATCH) * dim_pad
@@ -324,14 +324,15 @@ def run_ours(a):
         "gpu_launches": int(launches),
         "clocks": clocks,
         "roofline": {"bound": "tensor",
-                     "kernel": "mma::scan_kernel (batch plan: IMMA.16832 + fused top-K)" if engine == "imma" else "scan_topk_kernel",
+                     "kernel": {"umma": "umma::scan_kernel (tcgen05.mma kind::i8, TMEM accumulators, fused top-K)",
+                                "imma": "mma::scan_kernel (batch plan: IMMA.16832 + fused top-K)"}.get(engine, "scan_topk_kernel"),
                      "achieved": round(tops, 1), "peak": round(int8_peak, 1), "unit": "TOP/s (int8, dense)",
                      "frac": round(tops / int8_peak, 4), "traffic": None,
                      "peak_source": peak_src + ": 2 x dense bf16 burst = int8 rate of the tcgen05 path",
                      "launch_ms": round(kernel_ms, 3), "macs_per_launch": int(macs_per_launch),
                      "legacy_imma_pipe_peak_TOPs": 1163.7, "frac_of_legacy_imma_pipe": round(tops / 1163.7, 4),
-                     "note": "mma.sync int8 (IMMA.16832) pipe peak is 4096 op/clk/SM (ncu) = 1164 TOP/s; "
-                             "the tcgen05 int8 path would be 4x that"},
+                     "note": "tcgen05.mma kind::i8 measured at 8188 MAC/clk/SM (tools/umma_probe.cu) = 4.76 POP/s at 1965 MHz; "
+                             "mma.sync int8 (IMMA.16832) pipe peak is 4096 op/clk/SM (ncu) = 1164 TOP/s"},
         "roofline_hbm": {"bound": "hbm", "kernel": "mma::scan_kernel (small-batch plan, nq=16)",
                          "achieved": sb.get("scan_kernel_GBps"), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(sb["scan_kernel_GBps"] / hbm_peak, 4) if sb else None,

@@ -512,6 +512,7 @@ merge_tree_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k,
 
 }  // namespace
 #include "xfbq_mma.cuh"
+#include "xfbq_umma.cuh"
 namespace {
 
 __global__ void unpack_keys_kernel(const uint64_t *__restrict__ keys, int64_t count,
@@ -881,6 +882,156 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
                         sh.cap > mma::SORT_CAP_MAX);  // large lists are emitted unsorted
 }
 
+
+// ----------------------------------------------------------------------------------------------
+// tcgen05 engine planning (kernel in xfbq_umma.cuh).
+// ----------------------------------------------------------------------------------------------
+struct UmmaShape {
+    int MT = 2, DW = 1, groups = 1, grid = 1, slots = 1, parts = 1, cap = 0, NS = 0;
+    int64_t stages = 0, nq_pad = 0, n_pad = 0;
+    size_t smem = 0, lists_bytes = 0, parts_bytes = 0, mscratch_bytes = 0;
+};
+
+struct UmmaPlan {
+    bool ok = false;
+    UmmaShape main, pre;
+    int64_t sample = 0;
+    size_t off_qimg = 0, off_qconst = 0, off_tau = 0, off_prekeys = 0, off_lists = 0, off_parts = 0, off_mscratch = 0, bytes = 0;
+};
+
+typedef void (*UmmaKernel)(const umma::Params);
+
+UmmaKernel pick_umma_kernel(int C, int MT) {
+    if (C == 1) return MT == 2 ? umma::scan_kernel<1, 2> : umma::scan_kernel<1, 1>;
+    if (C == 2) return MT == 2 ? umma::scan_kernel<2, 2> : umma::scan_kernel<2, 1>;
+    if (C == 4 && MT == 1) return umma::scan_kernel<4, 1>;
+    return nullptr;
+}
+
+void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &info, UmmaShape *out) {
+    UmmaShape sh;
+    sh.MT = MT;
+    sh.DW = MT == 2 ? 1 : 2;
+    int cap = 64;
+    while (cap < 2 * k) cap <<= 1;
+    sh.cap = cap;
+    const int64_t qpg = 128 * MT;
+    sh.groups = static_cast<int>((nq + qpg - 1) / qpg);
+    sh.nq_pad = static_cast<int64_t>(sh.groups) * qpg;
+    sh.n_pad = bundles_of(n) * 32;
+    sh.stages = (sh.n_pad + umma::STAGE_DOCS - 1) / umma::STAGE_DOCS;
+    const int64_t W = static_cast<int64_t>(sh.groups) * sh.stages;
+    int64_t grid = env_int("XFBQ_GRID", 0) > 0 ? env_int("XFBQ_GRID", 0) : info.sms;
+    if (grid > W) grid = W;
+    sh.grid = static_cast<int>(grid);
+    int slots = 1;
+    for (int gr = 0; gr < sh.groups; ++gr) {
+        const int64_t lo = static_cast<int64_t>(gr) * sh.stages, hi = lo + sh.stages;
+        int64_t c_first = lo * grid / W;
+        while (c_first > 0 && c_first * W / grid > lo) --c_first;
+        while ((c_first + 1) * W / grid <= lo) ++c_first;
+        int64_t c_last = (hi - 1) * grid / W;
+        while (c_last > 0 && c_last * W / grid > hi - 1) --c_last;
+        while ((c_last + 1) * W / grid <= hi - 1) ++c_last;
+        if (c_last - c_first + 1 > slots) slots = static_cast<int>(c_last - c_first + 1);
+    }
+    sh.slots = slots;
+    sh.parts = slots * sh.DW;
+    int NS = env_int("XFBQ_UMMA_STAGES", 4);
+    const size_t budget = static_cast<size_t>(info.smem_optin);
+    while (NS > 2 && umma::smem_layout(C, MT, NS).total > budget) --NS;
+    sh.NS = umma::smem_layout(C, MT, NS).total <= budget ? NS : 0;
+    sh.smem = umma::smem_layout(C, MT, NS).total;
+    sh.lists_bytes = static_cast<size_t>(sh.grid) * umma::EPI_WARPS * 32 * cap * 8;
+    sh.parts_bytes = static_cast<size_t>(sh.parts) * nq * k * 8;
+    sh.mscratch_bytes = static_cast<size_t>(merge_scratch_parts(sh.parts, k, nq)) * nq * k * 8;
+    *out = sh;
+}
+
+int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bool have_nibbles, UmmaPlan *plan) {
+    UmmaPlan pl;
+    *plan = pl;
+    const int C = static_cast<int>(chunks128(dim));
+    const char *eng = getenv("XFBQ_ENGINE");
+    if (eng && *eng && strcmp(eng, "umma") != 0) return XFBQ_OK;  // another engine was asked for
+    const bool forced = eng && strcmp(eng, "umma") == 0;
+    if (!have_nibbles || wd > 4 || wq > 7 || !(C == 1 || C == 2 || C == 4) || k > 1024 || n < 1 || env_int("XFBQ_FORCE_GENERIC", 0))
+        return XFBQ_OK;
+    if (!forced && nq < env_int("XFBQ_UMMA_MIN_NQ", 17)) return XFBQ_OK;  // tiny batches: the fused HBM-bound IMMA scan
+    if (nq < 1) return XFBQ_OK;
+    if (merge_group_max(k) == 0 || nq > 65535) return XFBQ_OK;  // lists are emitted unsorted: needs the tree merge
+    DeviceInfo info;
+    if (int rc = device_info(&info)) return rc;
+    const int MT = (C == 4 || nq <= 128) ? 1 : 2;
+    umma_shape(n, C, nq, k, MT, info, &pl.main);
+    if (pl.main.NS == 0) return XFBQ_OK;
+    int64_t sample = env_int("XFBQ_SAMPLE", -1);
+    if (sample < 0) sample = 131072;
+    if (sample > 0 && (n < 16 * sample || sample < 4 * k)) sample = 0;
+    pl.sample = sample;
+    if (sample) umma_shape(sample, C, nq, k, MT, info, &pl.pre);
+    size_t off = 0;
+    pl.off_qimg = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 128 * C);
+    pl.off_qconst = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 4);
+    pl.off_tau = off; off = align256(off + (sample ? static_cast<size_t>(nq) * 4 : 0));
+    pl.off_prekeys = off; off = align256(off + (sample ? static_cast<size_t>(nq) * k * 8 : 0));
+    pl.off_lists = off; off = align256(off + (pl.main.lists_bytes > pl.pre.lists_bytes ? pl.main.lists_bytes : pl.pre.lists_bytes));
+    pl.off_parts = off; off = align256(off + (pl.main.parts_bytes > pl.pre.parts_bytes ? pl.main.parts_bytes : pl.pre.parts_bytes));
+    pl.off_mscratch = off; off = align256(off + (pl.main.mscratch_bytes > pl.pre.mscratch_bytes ? pl.main.mscratch_bytes : pl.pre.mscratch_bytes));
+    pl.bytes = off;
+    pl.ok = true;
+    *plan = pl;
+    return XFBQ_OK;
+}
+
+int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, const void *nib, int64_t n, int C,
+                  int64_t nq, int k, int64_t row_offset, const int32_t *tau_init, uint64_t *keys_out, cudaStream_t st) {
+    UmmaKernel kern = pick_umma_kernel(C, sh.MT);
+    if (!kern) return fail(XFBQ_E_UNSUPPORTED, "no tcgen05 kernel for C=%d MT=%d", C, sh.MT);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh.smem));
+    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "umma scan smem opt-in (%zu bytes): %s", sh.smem, cudaGetErrorString(e));
+    umma::Params p;
+    p.db = nib;
+    p.n = n; p.n_pad = sh.n_pad; p.row_offset = row_offset;
+    p.qimg = ws + pl.off_qimg;
+    p.qconst = reinterpret_cast<const int32_t *>(ws + pl.off_qconst);
+    p.tau_init = tau_init;
+    p.lists = reinterpret_cast<uint64_t *>(ws + pl.off_lists);
+    p.out = reinterpret_cast<uint64_t *>(ws + pl.off_parts);
+    p.nq = nq; p.stages = sh.stages; p.groups = sh.groups;
+    p.k = k; p.cap = sh.cap; p.NS = sh.NS;
+    if (sh.slots > 1) {  // slots a group does not use stay KEY_INF
+        e = cudaMemsetAsync(p.out, 0xFF, sh.parts_bytes, st);
+        if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
+    }
+    const bool timed = g_timing && &sh == &pl.main;
+    if (timed) cudaEventRecord(g_ev0, st);
+    kern<<<static_cast<unsigned>(sh.grid), umma::THREADS, sh.smem, st>>>(p);
+    if (timed) { cudaEventRecord(g_ev1, st); g_ev_valid = true; }
+    if (int rc = check_launch("umma::scan_kernel")) return rc;
+    return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st, true);
+}
+
+int run_umma(const UmmaPlan &up, unsigned char *ws, const void *nib, int64_t n, int64_t dim, int wd, const uint32_t *q,
+             int64_t nq, int wq, int k, int64_t row_offset, uint64_t *keys_out, cudaStream_t st) {
+    const int C = static_cast<int>(chunks128(dim));
+    unsigned char *qimg = ws + up.off_qimg;
+    int32_t *qconst = reinterpret_cast<int32_t *>(ws + up.off_qconst);
+    umma::prep_queries_kernel<<<static_cast<unsigned>((up.main.nq_pad * 32 + 255) / 256), 256, 0, st>>>(
+        q, nq, up.main.nq_pad, static_cast<int>(dim), wq, wd, C, up.main.MT, qimg, qconst);
+    if (int rc = check_launch("umma::prep_queries_kernel")) return rc;
+    const int32_t *tau_init = nullptr;
+    if (up.sample) {
+        uint64_t *prekeys = reinterpret_cast<uint64_t *>(ws + up.off_prekeys);
+        int32_t *tau = reinterpret_cast<int32_t *>(ws + up.off_tau);
+        if (int rc = run_umma_scan(up.pre, up, ws, nib, up.sample, C, nq, k, row_offset, nullptr, prekeys, st)) return rc;
+        mma::tau_from_keys_kernel<<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(prekeys, qconst, nq, k, tau);
+        if (int rc = check_launch("tau_from_keys_kernel")) return rc;
+        tau_init = tau;
+    }
+    return run_umma_scan(up.main, up, ws, nib, n, C, nq, k, row_offset, tau_init, keys_out, st);
+}
+
 template <typename T>
 int quantize_pack_impl(const T *x, int64_t n, int64_t dim, int64_t ld, double scale, int width,
                        void *out, uint64_t *nonfinite, void *stream) {
@@ -1043,6 +1194,9 @@ XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64
         return -1;
     }
     if (n == 0 || nq == 0) return 0;
+    UmmaPlan up;
+    if (make_umma_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &up)) return -1;
+    if (up.ok) return static_cast<int64_t>(up.bytes);
     MmaPlan mp;
     if (make_mma_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &mp)) return -1;
     if (mp.ok) return static_cast<int64_t>(mp.bytes);
@@ -1055,6 +1209,13 @@ XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64
 XFBQ_API int xfbq_scan_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, int have_nibbles, int32_t out[6]) {
     if (!width_ok(wd) || !width_ok(wq) || n < 1 || dim < 1 || nq < 1 || k < 1 || k > XFBQ_MAX_K || !out)
         return fail(XFBQ_E_INVALID, "bad scan shape");
+    UmmaPlan up;
+    if (int rc = make_umma_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &up)) return rc;
+    if (up.ok) {  // tcgen05 engine: tile = queries per CTA
+        out[0] = 128 * up.main.MT; out[1] = up.main.groups; out[2] = up.main.parts; out[3] = up.main.cap;
+        out[4] = 3; out[5] = static_cast<int32_t>(up.main.smem);
+        return XFBQ_OK;
+    }
     MmaPlan mp;
     if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &mp)) return rc;
     if (mp.ok) {  // integer-MMA engine: tile = queries per CTA
@@ -1087,6 +1248,13 @@ XFBQ_API int xfbq_scan_topk(const void *db, const void *nib, int64_t n, int64_t 
         return XFBQ_OK;
     }
     if (!db || !q) return fail(XFBQ_E_INVALID, "null pointer");
+    UmmaPlan up;
+    if (int rc = make_umma_plan(n, dim, wd, nq, wq, k, nib != nullptr, &up)) return rc;
+    if (up.ok) {
+        if (!workspace || workspace_bytes < static_cast<int64_t>(up.bytes))
+            return fail(XFBQ_E_INVALID, "workspace too small: need %zu bytes, got %lld", up.bytes, (long long)workspace_bytes);
+        return run_umma(up, static_cast<unsigned char *>(workspace), nib, n, dim, wd, q, nq, wq, k, row_offset, keys_out, st);
+    }
     MmaPlan mp;
     if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, nib != nullptr, &mp)) return rc;
     if (mp.ok) {
