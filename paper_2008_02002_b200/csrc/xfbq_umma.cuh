@@ -5,7 +5,7 @@
 // run on tcgen05.mma.kind::i8 (measured 8 188 MAC/clk/SM, 4x the mma.sync IMMA pipe) with the
 // accumulators in tensor memory.
 //
-// One persistent CTA per SM, 13 warps in three roles that only meet at mbarriers:
+// One persistent CTA per SM, 16 warps (13 working) in three roles that only meet at mbarriers:
 //   producers (4 warps)  nibble layout (row-major 4-bit codes, 64C bytes per document) -> registers
 //                        (two stages of LDG.128 in flight) -> split nibbles to bytes -> the B operand
 //                        stage in shared memory: 128 documents x 128C bytes, K-major, 128-byte swizzle
@@ -25,13 +25,15 @@
 
 namespace umma {
 
-constexpr int EPI_WARPS = 8;
-constexpr int PROD_WARPS = 4;
-constexpr int THREADS = (EPI_WARPS + 1 + PROD_WARPS) * 32;
+constexpr int EPI_WARPS = 8;    // warpgroups 0-1
+constexpr int PROD_WARPS = 4;   // warpgroup 2
+constexpr int MMA_WARP = 12;    // first warp of warpgroup 3 (its other three warps only take part in block barriers)
+constexpr int THREADS = 512;    // whole warpgroups, so that setmaxnreg can move registers between the roles
+constexpr int EPI_REGS = 168, PROD_REGS = 104, MMA_REGS = 40;  // 8*168 + 4*104 + 4*40 = 1920 <= 2048 per lane slot
 constexpr int STAGE_DOCS = 128;  // N of one MMA
 constexpr int ACC_BUFS = 4;      // 4 x 128 columns = the whole tensor memory
 constexpr int TAU_OPEN = -(1 << 30);
-constexpr int TAU_NEVER = 0x7FFFFFFF;
+constexpr int TAU_NEVER = 1 << 30;     // |acc| <= 512 * 15 * 127 < 2^20, so acc - tau never overflows
 
 struct Params {
     const void *db;            // nibble layout
@@ -88,6 +90,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
         : "r"(taddr) : "memory");
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+template <int R> __device__ __forceinline__ void reg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R)); }
+template <int R> __device__ __forceinline__ void reg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R)); }
+
+__device__ __forceinline__ int tmem_ld1(uint32_t taddr) {
+    int v;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void cta_sync() { asm volatile("bar.sync 0;" ::: "memory"); }
+__device__ __forceinline__ int max8(const int *v) {
+    return max(max(max(v[0], v[1]), v[2]), max(max(max(v[3], v[4]), v[5]), max(v[6], v[7])));
+}
 
 // byte offset of (row r, K position kpos) inside a K-major SWIZZLE_128B operand of R rows
 __host__ __device__ __forceinline__ uint32_t sw128_offset(int r, int kpos, int R) {
@@ -148,6 +162,22 @@ __host__ __device__ inline SmemLayout smem_layout(int C, int MT, int NS) {
     return L;
 }
 
+// A CTA's share of the linearised (group, stage) work, cut into segments of one query group each.
+struct Segments {
+    int64_t lin, lin_end, T;
+    int gr, sd0, cnt;
+    __device__ __forceinline__ bool next() {
+        if (lin >= lin_end) return false;
+        gr = static_cast<int>(lin / T);
+        sd0 = static_cast<int>(lin - static_cast<int64_t>(gr) * T);
+        int64_t left = lin_end - lin;
+        if (left > T - sd0) left = T - sd0;
+        cnt = static_cast<int>(left);
+        lin += left;
+        return true;
+    }
+};
+
 template <int C, int MT>
 __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     constexpr int ROW_BYTES = 64 * C;                 // one document in the nibble layout
@@ -169,12 +199,10 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 2 * ACC_BUFS);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    // ---- this CTA's share of the linearised (group, stage) work
     const int64_t T = p.stages;
     const int64_t W = static_cast<int64_t>(p.groups) * T;
     const int64_t G = gridDim.x;
-    const int64_t lin_begin = static_cast<int64_t>(blockIdx.x) * W / G;
-    const int64_t lin_end = (static_cast<int64_t>(blockIdx.x) + 1) * W / G;
+    Segments sg{static_cast<int64_t>(blockIdx.x) * W / G, (static_cast<int64_t>(blockIdx.x) + 1) * W / G, T, 0, 0, 0};
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NS; ++i) { mbar_init(&b_full[i], PROD_WARPS); mbar_init(&b_empty[i], 1); }
@@ -183,98 +211,111 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     }
     if (warp == 0) tmem_alloc(tmem_slot, 512);
     fence_before();
-    __syncthreads();
+    cta_sync();
     fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    // Every role runs the same segment loop:  stage the group's query operand (all threads, generic
+    // proxy + proxy fence) | barrier | role work | barrier (every MMA that read the operand is done:
+    // the epilogue has consumed its result).
+    auto stage_queries = [&](int gr) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(p.qimg + static_cast<int64_t>(gr) * MT * A_TILE);
+        uint4 *dst = reinterpret_cast<uint4 *>(sA);
+        for (int i = threadIdx.x; i < MT * A_TILE / 16; i += THREADS) dst[i] = __ldg(src + i);
+        fence_async_smem();
+    };
     uint32_t s_run = 0;  // stages this CTA has processed so far (drives every ring cursor)
-    int64_t lin = lin_begin;
-    while (lin < lin_end) {
-        const int gr = static_cast<int>(lin / T);
-        const int sd0 = static_cast<int>(lin - static_cast<int64_t>(gr) * T);
-        int64_t left = lin_end - lin;
-        if (left > T - sd0) left = T - sd0;
-        const int cnt_st = static_cast<int>(left);
 
-        // ---- stage the query operand of this group (generic-proxy writes, then a proxy fence)
-        {
-            const uint4 *src = reinterpret_cast<const uint4 *>(p.qimg + static_cast<int64_t>(gr) * MT * A_TILE);
-            uint4 *dst = reinterpret_cast<uint4 *>(sA);
-            for (int i = threadIdx.x; i < MT * A_TILE / 16; i += THREADS) dst[i] = __ldg(src + i);
-            fence_async_smem();
-        }
-        __syncthreads();
-
-        if (warp < EPI_WARPS) {
-            // ================================ epilogue ================================
-            const int q4 = warp & 3, idx = warp >> 2;
-            const int mt = MT == 2 ? idx : 0;
-            const int col0 = MT == 2 ? 0 : idx * COLS;
-            const int64_t q0 = (static_cast<int64_t>(gr) * MT + mt) * 128 + q4 * 32;  // first query row of this warp
+    if (warp < EPI_WARPS) {
+        // ================================ epilogue ================================
+        reg_inc<EPI_REGS>();
+        const int q4 = warp & 3, idx = warp >> 2;
+        const int mt = MT == 2 ? idx : 0;
+        const int col0 = MT == 2 ? 0 : idx * COLS;
+        uint64_t *warp_lists = p.lists + (static_cast<int64_t>(blockIdx.x) * EPI_WARPS + warp) * 32 * static_cast<int64_t>(p.cap);
+        uint64_t *my_list = warp_lists + static_cast<int64_t>(lane) * p.cap;
+        int *hist = reinterpret_cast<int *>(smem + L.hist_off) + warp * 256;
+        const uint32_t n_docs = static_cast<uint32_t>(p.n);
+        const uint32_t id_off = static_cast<uint32_t>(p.row_offset);  // row ids fit 32 bits (checked on the host)
+        const int cap = p.cap, k = p.k;
+        while (sg.next()) {
+            stage_queries(sg.gr);
+            cta_sync();
+            const int64_t q0 = (static_cast<int64_t>(sg.gr) * MT + mt) * 128 + q4 * 32;  // first query row of this warp
             const int64_t myq = q0 + lane;
             const bool valid = myq < p.nq;
             const int dq = valid ? p.qconst[myq] : 0;
             int theta = valid ? (p.tau_init ? max(TAU_OPEN, p.tau_init[myq]) : TAU_OPEN) : TAU_NEVER;
             int cnt = 0;
-            uint64_t *warp_lists = p.lists + (static_cast<int64_t>(blockIdx.x) * EPI_WARPS + warp) * 32 * static_cast<int64_t>(p.cap);
-            uint64_t *my_list = warp_lists + static_cast<int64_t>(lane) * p.cap;
-            int *hist = reinterpret_cast<int *>(smem + L.hist_off) + warp * 256;
-            const uint32_t n_docs = static_cast<uint32_t>(p.n);
-            const uint64_t row_off = static_cast<uint64_t>(p.row_offset);
-            const int cap = p.cap, k = p.k;
 
-            auto filter = [&](const int (&v)[32], uint32_t doc0) {
-                int m = v[0];
+            // 32 scores of this thread's query row: 3-input max tree, one compare, one vote.  On a hit
+            // (rare once thresholds have tightened) the warp builds per-lane hit masks from sign bits
+            // and re-reads just the hit columns from tensor memory, so no score is indexed dynamically.
+            auto filter = [&](const int (&v)[32], uint32_t taddr_c, uint32_t doc0) {
+                const int g0 = max8(v), g1 = max8(v + 8), g2 = max8(v + 16), g3 = max8(v + 24);
+                const int m = max(max(g0, g1), max(g2, g3));
+                if (__any_sync(0xffffffffu, m >= theta)) {
+                    const int gm[4] = {g0, g1, g2, g3};
+                    uint32_t hits = 0;
 #pragma unroll
-                for (int j = 1; j < 32; ++j) m = max(m, v[j]);
-                if (m >= theta) {  // rare once the threshold has tightened: this lane appends its hits
+                    for (int qg = 0; qg < 4; ++qg)
+                        if (__any_sync(0xffffffffu, gm[qg] >= theta)) {
+                            uint32_t below = 0;  // bit j: v[8 qg + j] < theta
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (v[j] >= theta && doc0 + j < n_docs)
-                            my_list[cnt++] = (static_cast<uint64_t>(static_cast<uint32_t>(dq - v[j])) << 32) | (row_off + doc0 + j);
-                }
-                __syncwarp();
-                unsigned need = __ballot_sync(0xffffffffu, cnt > cap - 32);
-                while (need) {  // a list that the next 32 documents could overflow: keep its k best
-                    const int ql = __ffs(need) - 1;
-                    need &= need - 1;
-                    const int c = __shfl_sync(0xffffffffu, cnt, ql);
-                    const uint64_t kth = mma::select_row(warp_lists + static_cast<int64_t>(ql) * cap, c, k, hist, lane);
-                    if (lane == ql) { cnt = k; theta = dq - static_cast<int>(kth >> 32); }
+                            for (int j = 7; j >= 0; --j) below = __funnelshift_l(static_cast<uint32_t>(v[8 * qg + j] - theta), below, 1);
+                            hits |= (~below & 0xFFu) << (8 * qg);
+                        }
+                    uint32_t cols = __reduce_or_sync(0xffffffffu, hits);
+                    while (cols) {
+                        const int j = __ffs(cols) - 1;
+                        cols &= cols - 1;
+                        const int val = tmem_ld1(taddr_c + j);
+                        tmem_ld_wait();
+                        if (((hits >> j) & 1u) && doc0 + j < n_docs) {
+                            my_list[cnt] = (static_cast<uint64_t>(static_cast<uint32_t>(dq - val)) << 32) | (id_off + doc0 + j);
+                            ++cnt;
+                        }
+                    }
+                    __syncwarp();
+                    unsigned need = __ballot_sync(0xffffffffu, cnt > cap - 32);
+                    while (need) {  // a list that the next 32 documents could overflow: keep its k best
+                        const int ql = __ffs(need) - 1;
+                        need &= need - 1;
+                        const int c = __shfl_sync(0xffffffffu, cnt, ql);
+                        const uint64_t kth = mma::select_row(warp_lists + static_cast<int64_t>(ql) * cap, c, k, hist, lane);
+                        if (lane == ql) { cnt = k; theta = dq - static_cast<int>(kth >> 32); }
+                    }
                 }
             };
 
-            for (int i = 0; i < cnt_st; ++i) {
+            for (int i = 0; i < sg.cnt; ++i) {
                 const uint32_t u = (s_run + i) * MT + mt;
                 const uint32_t buf = u & (ACC_BUFS - 1), use = u / ACC_BUFS;
                 mbar_wait(&acc_full[buf], use & 1u);
                 fence_after();
                 const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + buf * STAGE_DOCS + col0;
-                const uint32_t doc0 = static_cast<uint32_t>(sd0 + i) * STAGE_DOCS + col0;
+                const uint32_t doc0 = static_cast<uint32_t>(sg.sd0 + i) * STAGE_DOCS + col0;
                 int va[32], vb[32];
                 tmem_ld32(taddr, va);
                 tmem_ld_wait();
-#pragma unroll
+#pragma unroll 1
                 for (int c = 0; c < COLS / 32; c += 2) {
                     tmem_ld32(taddr + (c + 1) * 32, vb);
-                    filter(va, doc0 + c * 32);
+                    filter(va, taddr + c * 32, doc0 + c * 32);
                     tmem_ld_wait();
-                    if (c + 2 < COLS / 32) {
-                        tmem_ld32(taddr + (c + 2) * 32, va);
-                    } else {  // every column of the accumulator is in registers: hand it back
-                        fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&acc_empty[buf]);
-                    }
-                    filter(vb, doc0 + (c + 1) * 32);
-                    if (c + 2 < COLS / 32) tmem_ld_wait();
+                    if (c + 2 < COLS / 32) tmem_ld32(taddr + (c + 2) * 32, va);
+                    filter(vb, taddr + (c + 1) * 32, doc0 + (c + 1) * 32);
+                    tmem_ld_wait();
                 }
+                fence_before();  // the accumulator has been read: hand it back to the issuer
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[buf]);
             }
             // ---- emit: every query row of this warp, its <= k best keys (unsorted), KEY_INF padded
             {
-                int64_t c_first = (static_cast<int64_t>(gr) * T * G) / W;
-                while (c_first > 0 && c_first * W / G > static_cast<int64_t>(gr) * T) --c_first;
-                while ((c_first + 1) * W / G <= static_cast<int64_t>(gr) * T) ++c_first;
+                int64_t c_first = (static_cast<int64_t>(sg.gr) * T * G) / W;
+                while (c_first > 0 && c_first * W / G > static_cast<int64_t>(sg.gr) * T) --c_first;
+                while ((c_first + 1) * W / G <= static_cast<int64_t>(sg.gr) * T) ++c_first;
                 const int64_t part = (static_cast<int64_t>(blockIdx.x) - c_first) * (MT == 2 ? 1 : 2) + (MT == 2 ? 0 : idx);
                 __syncwarp();
                 for (int ql = 0; ql < 32; ++ql) {
@@ -289,12 +330,74 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                 }
                 __syncwarp();
             }
-        } else if (warp == EPI_WARPS) {
-            // ================================ MMA issuer ================================
-            if (lane == 0) {
+            s_run += static_cast<uint32_t>(sg.cnt);
+            cta_sync();
+        }
+    } else if (warp < EPI_WARPS + PROD_WARPS) {
+        // ================================ producers ================================
+        reg_dec<PROD_REGS>();
+        const int pw = warp - EPI_WARPS;
+        const int qd = lane >> 3, d = (lane >> 2) & 1, gg = lane & 3;
+        const int kb = qd % C, doc_in_it = 2 * (qd / C) + d, g = 4 * kb + gg;
+        const unsigned char *db = reinterpret_cast<const unsigned char *>(p.db);
+        const uint32_t n_pad32 = static_cast<uint32_t>(p.n_pad);
+        auto load_stage = [&](uint4 (&r)[ITW], int sd) {
+#pragma unroll
+            for (int it = 0; it < ITW; ++it) {
+                const uint32_t row = static_cast<uint32_t>(sd) * STAGE_DOCS + (it * PROD_WARPS + pw) * DPI + doc_in_it;
+                r[it] = row < n_pad32 ? __ldg(reinterpret_cast<const uint4 *>(db + static_cast<int64_t>(row) * ROW_BYTES + g * 16))
+                                      : make_uint4(0u, 0u, 0u, 0u);
+            }
+        };
+        auto store_stage = [&](const uint4 (&r)[ITW], int slot) {
+            unsigned char *stage = sB + static_cast<size_t>(slot) * B_STAGE + kb * (STAGE_DOCS * 128);
+#pragma unroll
+            for (int it = 0; it < ITW; ++it) {
+                const int row = (it * PROD_WARPS + pw) * DPI + doc_in_it;
+                unsigned char *rowp = stage + (row >> 3) * 1024 + (row & 7) * 128;
+                const uint4 w = r[it];
+                *reinterpret_cast<uint4 *>(rowp + (((2 * gg) ^ (row & 7)) << 4)) =
+                    make_uint4(w.x & 0x0F0F0F0Fu, (w.x >> 4) & 0x0F0F0F0Fu, w.y & 0x0F0F0F0Fu, (w.y >> 4) & 0x0F0F0F0Fu);
+                *reinterpret_cast<uint4 *>(rowp + (((2 * gg + 1) ^ (row & 7)) << 4)) =
+                    make_uint4(w.z & 0x0F0F0F0Fu, (w.z >> 4) & 0x0F0F0F0Fu, w.w & 0x0F0F0F0Fu, (w.w >> 4) & 0x0F0F0F0Fu);
+            }
+        };
+        while (sg.next()) {
+            stage_queries(sg.gr);
+            cta_sync();
+            Ring rb{static_cast<int>(s_run % NS), ((s_run / NS) & 1u) ^ 1u};  // "empty" waits start on the completed phase
+            auto publish = [&](const uint4 (&r)[ITW]) {
+                mbar_wait(&b_empty[rb.idx], rb.phase);
+                store_stage(r, rb.idx);
+                fence_async_smem();  // generic-proxy stores -> visible to the tensor core's async proxy
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&b_full[rb.idx]);
+                rb.advance(NS);
+            };
+            uint4 ra[ITW], rbuf[ITW];
+            load_stage(ra, sg.sd0);
+            if (sg.cnt > 1) load_stage(rbuf, sg.sd0 + 1);
+            for (int i = 0; i < sg.cnt; i += 2) {
+                publish(ra);
+                if (i + 2 < sg.cnt) load_stage(ra, sg.sd0 + i + 2);
+                if (i + 1 < sg.cnt) {
+                    publish(rbuf);
+                    if (i + 3 < sg.cnt) load_stage(rbuf, sg.sd0 + i + 3);
+                }
+            }
+            s_run += static_cast<uint32_t>(sg.cnt);
+            cta_sync();
+        }
+    } else {
+        // ================================ MMA issuer (+ three idle warps) ================================
+        reg_dec<MMA_REGS>();
+        const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+        while (sg.next()) {
+            stage_queries(sg.gr);
+            cta_sync();
+            if (warp == MMA_WARP && lane == 0) {
                 Ring rb{static_cast<int>(s_run % NS), (s_run / NS) & 1u};
-                const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-                for (int i = 0; i < cnt_st; ++i) {
+                for (int i = 0; i < sg.cnt; ++i) {
                     mbar_wait(&b_full[rb.idx], rb.phase);
                     fence_after();
 #pragma unroll
@@ -316,61 +419,12 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                 }
             }
             __syncwarp();
-        } else {
-            // ================================ producers ================================
-            const int pw = warp - EPI_WARPS - 1;
-            const int qd = lane >> 3, d = (lane >> 2) & 1, gg = lane & 3;
-            const int kb = qd % C, doc_in_it = 2 * (qd / C) + d, g = 4 * kb + gg;
-            const unsigned char *db = reinterpret_cast<const unsigned char *>(p.db);
-            const uint32_t n_pad32 = static_cast<uint32_t>(p.n_pad);
-            auto load_stage = [&](uint4 (&r)[ITW], int sd) {
-#pragma unroll
-                for (int it = 0; it < ITW; ++it) {
-                    const uint32_t row = static_cast<uint32_t>(sd) * STAGE_DOCS + (it * PROD_WARPS + pw) * DPI + doc_in_it;
-                    r[it] = row < n_pad32 ? __ldg(reinterpret_cast<const uint4 *>(db + static_cast<int64_t>(row) * ROW_BYTES + g * 16))
-                                          : make_uint4(0u, 0u, 0u, 0u);
-                }
-            };
-            auto store_stage = [&](const uint4 (&r)[ITW], int slot) {
-                unsigned char *stage = sB + static_cast<size_t>(slot) * B_STAGE + kb * (STAGE_DOCS * 128);
-#pragma unroll
-                for (int it = 0; it < ITW; ++it) {
-                    const int row = (it * PROD_WARPS + pw) * DPI + doc_in_it;
-                    unsigned char *rowp = stage + (row >> 3) * 1024 + (row & 7) * 128;
-                    const uint4 w = r[it];
-                    *reinterpret_cast<uint4 *>(rowp + (((2 * gg) ^ (row & 7)) << 4)) =
-                        make_uint4(w.x & 0x0F0F0F0Fu, (w.x >> 4) & 0x0F0F0F0Fu, w.y & 0x0F0F0F0Fu, (w.y >> 4) & 0x0F0F0F0Fu);
-                    *reinterpret_cast<uint4 *>(rowp + (((2 * gg + 1) ^ (row & 7)) << 4)) =
-                        make_uint4(w.z & 0x0F0F0F0Fu, (w.z >> 4) & 0x0F0F0F0Fu, w.w & 0x0F0F0F0Fu, (w.w >> 4) & 0x0F0F0F0Fu);
-                }
-            };
-            Ring rb{static_cast<int>(s_run % NS), ((s_run / NS) & 1u) ^ 1u};  // "empty" waits start on the completed phase
-            auto publish = [&](const uint4 (&r)[ITW]) {
-                mbar_wait(&b_empty[rb.idx], rb.phase);
-                store_stage(r, rb.idx);
-                fence_async_smem();  // generic-proxy stores -> visible to the tensor core's async proxy
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&b_full[rb.idx]);
-                rb.advance(NS);
-            };
-            uint4 ra[ITW], rbuf[ITW];
-            load_stage(ra, sd0);
-            if (cnt_st > 1) load_stage(rbuf, sd0 + 1);
-            for (int i = 0; i < cnt_st; i += 2) {
-                publish(ra);
-                if (i + 2 < cnt_st) load_stage(ra, sd0 + i + 2);
-                if (i + 1 < cnt_st) {
-                    publish(rbuf);
-                    if (i + 3 < cnt_st) load_stage(rbuf, sd0 + i + 3);
-                }
-            }
+            s_run += static_cast<uint32_t>(sg.cnt);
+            cta_sync();
         }
-        s_run += static_cast<uint32_t>(cnt_st);
-        lin += cnt_st;
-        __syncthreads();  // every MMA that read the query operand has completed (the epilogue consumed its result)
     }
     fence_before();
-    __syncthreads();
+    cta_sync();
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
