@@ -154,6 +154,10 @@ int xfbq_unpack_keys(const uint64_t *keys_dev, int64_t count, int64_t *dist_out_
  * or the merge); xfbq_last_scan_ms synchronises on the last one and returns its duration. */
 int xfbq_set_timing(int enable);
 int xfbq_last_scan_ms(float *ms_out);
+/* Debug hook (per host thread): device buffer of gridDim.x * 12 uint64 counters that the tcgen05 scan
+ * kernel of the following xfbq_scan_topk calls fills with cycles spent waiting per role
+ * (tools/umma_profile.py); NULL switches it off. */
+int xfbq_debug_profile(void *device_counters);
 
 /* Number of kernels this library has launched in the calling process (for bench accounting). */
 int64_t xfbq_launch_count(void);

@@ -32,7 +32,7 @@ SYMBOLS = [
     "xfbq_distance_upper_bound", "xfbq_quantize_pack_f32", "xfbq_quantize_pack_f64",
     "xfbq_quantize_queries_f32", "xfbq_quantize_queries_f64", "xfbq_planes_to_bundles",
     "xfbq_bundles_to_planes", "xfbq_nibble_bytes", "xfbq_planes_to_nibbles", "xfbq_batch_distances", "xfbq_scan_workspace_bytes",
-    "xfbq_scan_plan", "xfbq_scan_topk", "xfbq_merge_topk", "xfbq_unpack_keys", "xfbq_set_timing", "xfbq_last_scan_ms", "xfbq_launch_count",
+    "xfbq_scan_plan", "xfbq_scan_topk", "xfbq_merge_topk", "xfbq_unpack_keys", "xfbq_set_timing", "xfbq_last_scan_ms", "xfbq_launch_count", "xfbq_debug_profile",
 ]
 
 
@@ -108,6 +108,7 @@ def lib():
         "xfbq_unpack_keys": (i32, [vp, i64, vp, vp, vp]),
         "xfbq_set_timing": (i32, [i32]),
         "xfbq_last_scan_ms": (i32, [vp]),
+        "xfbq_debug_profile": (i32, [vp]),
         "xfbq_launch_count": (i64, []),
     }
     for name in SYMBOLS:

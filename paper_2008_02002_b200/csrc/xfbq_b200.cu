@@ -32,6 +32,7 @@ thread_local bool g_timing = false;
 thread_local cudaEvent_t g_ev0 = nullptr, g_ev1 = nullptr;
 thread_local bool g_ev_valid = false;
 std::atomic<int64_t> g_launches{0};
+thread_local unsigned long long *g_prof = nullptr;  // debug: device buffer for the tcgen05 engine's wait counters
 
 int fail(int code, const char *fmt, ...) {
     va_list ap;
@@ -937,7 +938,7 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
     }
     sh.slots = slots;
     sh.parts = slots * sh.DW;
-    int NS = env_int("XFBQ_UMMA_STAGES", 4);
+    int NS = env_int("XFBQ_UMMA_STAGES", 6);
     const size_t budget = static_cast<size_t>(info.smem_optin);
     while (NS > 2 && umma::smem_layout(C, MT, NS).total > budget) --NS;
     sh.NS = umma::smem_layout(C, MT, NS).total <= budget ? NS : 0;
@@ -991,15 +992,18 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh.smem));
     if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "umma scan smem opt-in (%zu bytes): %s", sh.smem, cudaGetErrorString(e));
     umma::Params p;
-    p.db = nib;
+    p.db = nib;  // byte tiles (the caller passes the tile region of the derived buffer)
     p.n = n; p.n_pad = sh.n_pad; p.row_offset = row_offset;
     p.qimg = ws + pl.off_qimg;
     p.qconst = reinterpret_cast<const int32_t *>(ws + pl.off_qconst);
     p.tau_init = tau_init;
+    p.theta_g = (tau_init && env_int("XFBQ_UMMA_SHARE", 1)) ? const_cast<int32_t *>(tau_init) : nullptr;  // the seeded thresholds double as the shared ones
     p.lists = reinterpret_cast<uint64_t *>(ws + pl.off_lists);
     p.out = reinterpret_cast<uint64_t *>(ws + pl.off_parts);
     p.nq = nq; p.stages = sh.stages; p.groups = sh.groups;
     p.k = k; p.cap = sh.cap; p.NS = sh.NS;
+    p.prof = (&sh == &pl.main) ? g_prof : nullptr;
+    p.debug = env_int("XFBQ_UMMA_DEBUG", 0);
     if (sh.slots > 1) {  // slots a group does not use stay KEY_INF
         e = cudaMemsetAsync(p.out, 0xFF, sh.parts_bytes, st);
         if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
@@ -1028,6 +1032,7 @@ int run_umma(const UmmaPlan &up, unsigned char *ws, const void *nib, int64_t n, 
         mma::tau_from_keys_kernel<<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(prekeys, qconst, nq, k, tau);
         if (int rc = check_launch("tau_from_keys_kernel")) return rc;
         tau_init = tau;
+        if (env_int("XFBQ_DEBUG_TAU_NEVER", 0)) cudaMemsetAsync(tau, 0x40, static_cast<size_t>(nq) * 4, st);  // timing experiments only: nothing passes
     }
     return run_umma_scan(up.main, up, ws, nib, n, C, nq, k, row_offset, tau_init, keys_out, st);
 }
@@ -1081,6 +1086,11 @@ XFBQ_API int xfbq_set_timing(int enable) {
     }
     g_timing = enable != 0;
     g_ev_valid = false;
+    return XFBQ_OK;
+}
+
+XFBQ_API int xfbq_debug_profile(void *device_counters) {
+    g_prof = static_cast<unsigned long long *>(device_counters);
     return XFBQ_OK;
 }
 
@@ -1154,7 +1164,16 @@ XFBQ_API int xfbq_bundles_to_planes(const void *db, int64_t n, int64_t dim, int 
     return check_launch("bundles_to_planes_kernel");
 }
 
-XFBQ_API int64_t xfbq_nibble_bytes(int64_t n, int64_t dim) { return bundles_of(n) * 32 * chunks128(dim) * 64; }
+// Derived layouts of one index, in one buffer: [nibble layout][byte tiles].
+inline int64_t nibble_region_bytes(int64_t n, int64_t dim) {
+    return ((bundles_of(n) * 32 * chunks128(dim) * 64 + 1023) / 1024) * 1024;
+}
+inline int64_t tile_count(int64_t n) { return (n + umma::STAGE_DOCS - 1) / umma::STAGE_DOCS; }
+inline bool tiles_supported(int64_t dim) { const int64_t C = chunks128(dim); return C == 1 || C == 2 || C == 4; }
+
+XFBQ_API int64_t xfbq_nibble_bytes(int64_t n, int64_t dim) {
+    return nibble_region_bytes(n, dim) + (tiles_supported(dim) ? tile_count(n) * umma::STAGE_DOCS * chunks128(dim) * 128 : 0);
+}
 
 XFBQ_API int xfbq_planes_to_nibbles(const void *db, int64_t n, int64_t dim, int width, void *nib_out, void *stream) {
     if (width < 1 || width > 4) return fail(XFBQ_E_UNSUPPORTED, "nibble layout holds codes of at most 4 bits, got %d", width);
@@ -1166,7 +1185,12 @@ XFBQ_API int xfbq_planes_to_nibbles(const void *db, int64_t n, int64_t dim, int 
     const int64_t total = n_pad * 4 * C;
     mma::planes_to_nibbles_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const uint32_t *>(db), n_pad, width, C, static_cast<uint4 *>(nib_out));
-    return check_launch("planes_to_nibbles_kernel");
+    if (int rc = check_launch("planes_to_nibbles_kernel")) return rc;
+    if (!tiles_supported(dim)) return XFBQ_OK;
+    const int64_t tiles = tile_count(n), groups = tiles * umma::STAGE_DOCS * 4 * C;
+    umma::nibbles_to_tiles_kernel<<<static_cast<unsigned>((groups + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4 *>(nib_out), n_pad, tiles, C, static_cast<unsigned char *>(nib_out) + nibble_region_bytes(n, dim));
+    return check_launch("nibbles_to_tiles_kernel");
 }
 
 XFBQ_API int xfbq_batch_distances(const void *db, int64_t n, int64_t dim, int wd, const uint32_t *q, int wq,
@@ -1253,7 +1277,8 @@ XFBQ_API int xfbq_scan_topk(const void *db, const void *nib, int64_t n, int64_t 
     if (up.ok) {
         if (!workspace || workspace_bytes < static_cast<int64_t>(up.bytes))
             return fail(XFBQ_E_INVALID, "workspace too small: need %zu bytes, got %lld", up.bytes, (long long)workspace_bytes);
-        return run_umma(up, static_cast<unsigned char *>(workspace), nib, n, dim, wd, q, nq, wq, k, row_offset, keys_out, st);
+        return run_umma(up, static_cast<unsigned char *>(workspace), static_cast<const unsigned char *>(nib) + nibble_region_bytes(n, dim),
+                        n, dim, wd, q, nq, wq, k, row_offset, keys_out, st);
     }
     MmaPlan mp;
     if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, nib != nullptr, &mp)) return rc;

@@ -5,46 +5,51 @@
 // run on tcgen05.mma.kind::i8 (measured 8 188 MAC/clk/SM, 4x the mma.sync IMMA pipe) with the
 // accumulators in tensor memory.
 //
-// One persistent CTA per SM, 16 warps (13 working) in three roles that only meet at mbarriers:
-//   producers (4 warps)  nibble layout (row-major 4-bit codes, 64C bytes per document) -> registers
-//                        (two stages of LDG.128 in flight) -> split nibbles to bytes -> the B operand
-//                        stage in shared memory: 128 documents x 128C bytes, K-major, 128-byte swizzle
-//                        (the canonical UMMA layout, written with conflict-free STS.128)
+// One persistent CTA per SM, 10 warps in three roles that only meet at mbarriers:
+//   loader (1 thread)    one cp.async.bulk per stage: the engine streams a derived "byte tile" copy of the
+//                        codes -- 128 documents x 128C bytes, K-major with the 128-byte swizzle, i.e. the
+//                        exact shared-memory image of a tcgen05 B operand -- so nothing touches the data
+//                        between HBM/L2 and the tensor core (a CUDA-core unpack stage cost more than the MMAs)
 //   issuer (1 thread)    per stage and per 128-query tile: 4C x tcgen05.mma (M = 128 queries, N = 128
-//                        documents, K = 32) into one of four 128-column TMEM accumulators;
+//                        documents, K = 32) into one of three 128-column TMEM accumulators;
 //                        tcgen05.commit releases the operand stage / publishes the accumulator
-//   epilogue (8 warps)   tcgen05.ld 32 lanes x 32 columns: a thread owns ONE query row, so its threshold
-//                        is a register and its candidate list is private: 3-input max over the 32
-//                        scores, compare once, and only on a hit append (distance << 32 | row id) keys;
-//                        a list that could overflow is cut to its k best by a warp-level radix select
-//                        (search.py:129-131 order on the full key), which also tightens the threshold.
-// The query operand (s8 weights 2y - Aq in the same K permutation the producers emit) is staged once
-// per query group as a ready-made swizzled image (prep_queries_kernel).  Work = groups x stages is
-// linearised and cut into gridDim.x equal ranges, as in the IMMA engine.
+//   epilogue (8 warps)   tcgen05.ld of the warp's 32 lanes x 128 columns into registers, accumulator handed
+//                        back at once (it is on the MMA critical path), then per 32 scores of the thread's
+//                        OWN query row: 3-input max tree, compare with the row's threshold register, vote;
+//                        only on a hit are (distance << 32 | row id) keys appended to the thread-private
+//                        candidate list; a list that could overflow is cut to its k best by a warp-level
+//                        radix select (search.py:129-131 order on the full key), which tightens the threshold.
+// The query operand (s8 weights 2y - Aq, same K permutation as the byte tiles) lives in tensor memory too
+// (A-from-TMEM form of tcgen05.mma: lane = query row, 4 K-elements per 32-bit column), stored once per query
+// group with tcgen05.st, so shared-memory bandwidth only carries the document operand.  Work = groups x
+// stages is linearised and cut into gridDim.x equal ranges, as in the IMMA engine.
 #pragma once
 
 namespace umma {
 
-constexpr int EPI_WARPS = 8;    // warpgroups 0-1
-constexpr int PROD_WARPS = 4;   // warpgroup 2
-constexpr int MMA_WARP = 12;    // first warp of warpgroup 3 (its other three warps only take part in block barriers)
-constexpr int THREADS = 512;    // whole warpgroups, so that setmaxnreg can move registers between the roles
-constexpr int EPI_REGS = 168, PROD_REGS = 104, MMA_REGS = 40;  // 8*168 + 4*104 + 4*40 = 1920 <= 2048 per lane slot
+constexpr int EPI_WARPS = 8;
+constexpr int MMA_WARP = 8;
+constexpr int TMA_WARP = 9;
+constexpr int THREADS = 320;    // 10 warps: registers are carved per 4 warps, so 12 warps' worth -> 168 per thread
 constexpr int STAGE_DOCS = 128;  // N of one MMA
-constexpr int ACC_BUFS = 4;      // 4 x 128 columns = the whole tensor memory
+constexpr int ACC_BUFS = 3;      // 3 x 128 accumulator columns; columns 384..511 hold the query operand
+constexpr int A_COL0 = ACC_BUFS * STAGE_DOCS;
 constexpr int TAU_OPEN = -(1 << 30);
 constexpr int TAU_NEVER = 1 << 30;     // |acc| <= 512 * 15 * 127 < 2^20, so acc - tau never overflows
 
 struct Params {
-    const void *db;            // nibble layout
+    const void *db;            // byte tiles: [ceil(n/128)][C][128 rows x 128 B swizzled] u8 codes
     int64_t n, n_pad, row_offset;
-    const unsigned char *qimg; // [groups][MT][C][128 rows x 128 B, swizzled] s8 weights
+    const unsigned char *qimg; // [nq_pad][128C] s8 weights, K-permuted rows
     const int32_t *qconst;     // [nq_pad] Dq
     const int32_t *tau_init;   // [nq] or nullptr
+    int *theta_g;              // [nq] thresholds shared by all CTAs (acc domain, atomicMax), or nullptr
     uint64_t *lists;           // [grid][EPI_WARPS][32][cap]
     uint64_t *out;             // [slots * DW][nq][k], KEY_INF pre-filled when slots > 1
     int64_t nq, stages;
     int groups, k, cap, NS;    // NS = operand stages in shared memory
+    int debug;                 // timing experiments (XFBQ_UMMA_DEBUG): 1 skip operand stores, 2 skip document loads, 4 skip the filter
+    unsigned long long *prof;  // optional [grid][8] wait-cycle counters (xfbq_debug_profile), else nullptr
 };
 
 using mma::smem_u32;
@@ -66,20 +71,28 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// Shared-memory operand descriptor, K-major, SWIZZLE_128B: rows of 128 bytes, 8-row groups 1024 B apart
-// (start address >> 4 | LBO (unused) | SBO = 1024 >> 4 | version 1 | layout type 2).
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
-    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (1ull << 16) | (static_cast<uint64_t>(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
-}
+// Shared-memory operand descriptor, K-major, SWIZZLE_128B: rows of 128 bytes, 8-row groups 1024 B apart:
+// bits 0-13 start address >> 4 | 16-29 LBO (unused) | 32-45 SBO = 1024 >> 4 | 46-47 version 1 | 61-63 layout 2.
+// low word of the descriptor; advancing the start address by `bytes` adds bytes >> 4 (the 14-bit field cannot
+// overflow: shared memory ends below 256 KB)
+__device__ __forceinline__ uint32_t desc_lo(uint32_t saddr) { return ((saddr >> 4) & 0x3FFFu) | (1u << 16); }
+constexpr uint32_t DESC_HI = (1024u >> 4) | (1u << 14) | (2u << 29);
 // Instruction descriptor: D = s32, A = B = signed 8-bit, both K-major, N >> 3 at bit 17, M >> 4 at bit 24.
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(STAGE_DOCS >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
 
-__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+template <bool ACC>
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
-        ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate) : "memory");
+        "{\n\t.reg .pred p;\n\t.reg .b64 db;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "mov.b64 db, {%2, %5};\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], db, %3, p;\n\t}"
+        ::"r"(d_tmem), "r"(a_tmem), "r"(b_lo), "r"(IDESC), "n"(ACC ? 1 : 0), "r"(DESC_HI) : "memory");
 }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint4 &a, const uint4 &b) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 ::"r"(taddr), "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w) : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -90,13 +103,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
         : "r"(taddr) : "memory");
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-template <int R> __device__ __forceinline__ void reg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R)); }
-template <int R> __device__ __forceinline__ void reg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R)); }
 
 __device__ __forceinline__ int tmem_ld1(uint32_t taddr) {
     int v;
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr) : "memory");
     return v;
+}
+__device__ __forceinline__ bool elect_one() {  // one lane of a converged warp
+    uint32_t pred;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+    return pred != 0;
 }
 __device__ __forceinline__ void cta_sync() { asm volatile("bar.sync 0;" ::: "memory"); }
 __device__ __forceinline__ int max8(const int *v) {
@@ -112,7 +128,7 @@ __host__ __device__ __forceinline__ uint32_t sw128_offset(int r, int kpos, int R
 // ------------------------------------------------------------------------------ query operand
 // One warp per padded query row.  K position of a dimension = the order in which the producers'
 // nibble split emits it: inside a group of 32 dims, word wi = 2e + hi holds bytes j = 0..3 for
-// dim = 32g + e + 4hi + 8j.  The image is exactly what the MMA reads from shared memory.
+// dim = 32g + e + 4hi + 8j.  Rows are plain: the epilogue threads copy theirs into tensor memory.
 __global__ void __launch_bounds__(256)
 prep_queries_kernel(const uint32_t *__restrict__ q, int64_t nq, int64_t nq_pad, int dim, int wq, int wd, int C, int MT,
                     unsigned char *__restrict__ qimg, int32_t *__restrict__ qconst) {
@@ -121,9 +137,7 @@ prep_queries_kernel(const uint32_t *__restrict__ q, int64_t nq, int64_t nq_pad, 
     if (row >= nq_pad) return;
     const int W = 4 * C;
     const int Aq = (1 << wq) - 1, Ad = (1 << wd) - 1;
-    const int64_t tile = row >> 7;  // = group * MT + mt
-    const int r = static_cast<int>(row & 127);
-    unsigned char *img = qimg + tile * (static_cast<int64_t>(C) * 128 * 128);
+    unsigned char *img = qimg + row * (static_cast<int64_t>(C) * 128);
     (void)MT;
     int sy = 0;
     for (int ow = lane; ow < 32 * C; ow += 32) {
@@ -141,7 +155,7 @@ prep_queries_kernel(const uint32_t *__restrict__ q, int64_t nq, int64_t nq_pad, 
                 packed |= (static_cast<uint32_t>(w) & 0xFFu) << (8 * j);
             }
         }
-        *reinterpret_cast<uint32_t *>(img + sw128_offset(r, 4 * ow, 128)) = packed;
+        *reinterpret_cast<uint32_t *>(img + 4 * ow) = packed;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sy += __shfl_xor_sync(0xffffffffu, sy, o);
@@ -154,12 +168,146 @@ struct SmemLayout {
 __host__ __device__ inline SmemLayout smem_layout(int C, int MT, int NS) {
     SmemLayout L;
     uint32_t off = 0;
-    L.a_off = off; off += static_cast<uint32_t>(MT) * 128 * 128 * C;
+    L.a_off = off; (void)MT;
     L.b_off = off; off += static_cast<uint32_t>(NS) * STAGE_DOCS * 128 * C;
     L.hist_off = off; off += EPI_WARPS * 256 * 4;
     L.bar_off = off; off += (2 * NS + 2 * ACC_BUFS) * 8 + 16;
     L.total = off + 1024;  // slack for the manual 1024-byte alignment of the operand area
     return L;
+}
+
+// nibble layout -> byte tiles; one thread per (document, group of 32 dims).  A group's nibble word e holds in
+// nibble m the code of dim 4m + e: even / odd nibbles split into words (e, lo), (e, hi) -> K positions
+// 32g + 8e + 4hi + j for dim 32g + e + 4hi + 8j (prep_queries_kernel applies the same permutation).
+__global__ void __launch_bounds__(256)
+nibbles_to_tiles_kernel(const uint4 *__restrict__ nib, int64_t n_pad, int64_t n_tiles, int C, unsigned char *__restrict__ tiles) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int G = 4 * C;
+    if (e >= n_tiles * STAGE_DOCS * G) return;
+    const int64_t doc = e / G;
+    const int g = static_cast<int>(e - doc * G);
+    uint4 w = make_uint4(0u, 0u, 0u, 0u);
+    if (doc < n_pad) w = nib[doc * G + g];
+    const int64_t tile = doc / STAGE_DOCS;
+    const int r = static_cast<int>(doc - tile * STAGE_DOCS);
+    const int kb = g >> 2, gg = g & 3;
+    unsigned char *rowp = tiles + tile * (static_cast<int64_t>(STAGE_DOCS) * 128 * C) + kb * (STAGE_DOCS * 128) + (r >> 3) * 1024 + (r & 7) * 128;
+    *reinterpret_cast<uint4 *>(rowp + (((2 * gg) ^ (r & 7)) << 4)) =
+        make_uint4(w.x & 0x0F0F0F0Fu, (w.x >> 4) & 0x0F0F0F0Fu, w.y & 0x0F0F0F0Fu, (w.y >> 4) & 0x0F0F0F0Fu);
+    *reinterpret_cast<uint4 *>(rowp + (((2 * gg + 1) ^ (r & 7)) << 4)) =
+        make_uint4(w.z & 0x0F0F0F0Fu, (w.z >> 4) & 0x0F0F0F0Fu, w.w & 0x0F0F0F0Fu, (w.w >> 4) & 0x0F0F0F0Fu);
+}
+
+// mbarrier wait (every lane polls: measured far faster than one polling lane + warp barrier) that adds the
+// cycles spent waiting to `acc` when profiling is on
+__device__ __forceinline__ void mbar_wait_prof(uint64_t *bar, uint32_t parity, bool prof, long long &acc) {
+    if (!prof) { mbar_wait(bar, parity); return; }
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    acc += clock64() - t0;
+}
+
+// v[j] for a warp-uniform j without dynamic register indexing (a jump table of 32 moves)
+__device__ __forceinline__ int pick32(const int (&v)[32], int j) {
+    int r = v[0];
+    switch (j) {
+#define XFBQ_PICK(J) case J: r = v[J]; break;
+        XFBQ_PICK(1) XFBQ_PICK(2) XFBQ_PICK(3) XFBQ_PICK(4) XFBQ_PICK(5) XFBQ_PICK(6) XFBQ_PICK(7) XFBQ_PICK(8)
+        XFBQ_PICK(9) XFBQ_PICK(10) XFBQ_PICK(11) XFBQ_PICK(12) XFBQ_PICK(13) XFBQ_PICK(14) XFBQ_PICK(15) XFBQ_PICK(16)
+        XFBQ_PICK(17) XFBQ_PICK(18) XFBQ_PICK(19) XFBQ_PICK(20) XFBQ_PICK(21) XFBQ_PICK(22) XFBQ_PICK(23) XFBQ_PICK(24)
+        XFBQ_PICK(25) XFBQ_PICK(26) XFBQ_PICK(27) XFBQ_PICK(28) XFBQ_PICK(29) XFBQ_PICK(30) XFBQ_PICK(31)
+#undef XFBQ_PICK
+        default: break;
+    }
+    return r;
+}
+
+// Warp-level radix select for short lists (cnt <= 32 * KPL): same contract as mma::select_row (keeps exactly
+// the k smallest of the cnt > k unique keys at the front of the row, returns the k-th), but the keys are
+// read from L2 once and every pass works on registers, so a compaction costs one L2 round trip instead of
+// one per pass.
+template <int KPL>
+__device__ __noinline__ uint64_t select_small(uint64_t *row, int cnt, int k, int *hist, int lane) {
+    __syncwarp();
+    uint64_t key[KPL];
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) key[i] = (i * 32 + lane < cnt) ? __ldcg(row + i * 32 + lane) : KEY_INF;
+    const uint64_t first = mma::shfl_u64(key[0], 0);
+    uint64_t diff = 0;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) if (i * 32 + lane < cnt) diff |= key[i] ^ first;
+    {
+        const uint32_t lo = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(diff));
+        const uint32_t hi = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(diff >> 32));
+        diff = (static_cast<uint64_t>(hi) << 32) | lo;
+    }
+    int shift = ((63 - __clzll(static_cast<long long>(diff | 1ull))) >> 3) << 3;  // byte holding the top differing bit
+    uint64_t hi_mask = shift + 8 >= 64 ? 0ull : ~((1ull << (shift + 8)) - 1ull);    // bits common to all keys
+    uint64_t prefix = first & hi_mask;
+    int want = k;
+    while (true) {
+#pragma unroll
+        for (int b = 0; b < 8; ++b) hist[8 * lane + b] = 0;
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < KPL; ++i)
+            if (i * 32 + lane < cnt && (key[i] & hi_mask) == prefix) atomicAdd(&hist[static_cast<int>(key[i] >> shift) & 255], 1);
+        __syncwarp();
+        int h[8], sum = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) { h[e] = hist[8 * lane + e]; sum += h[e]; }
+        int inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        const int exc = inc - sum;
+        const bool mine = exc < want && want <= inc;  // exactly one lane
+        int bucket = 0, below = exc, bcnt = 0;
+        if (mine) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if (bcnt == 0) {
+                    if (below + h[e] >= want) { bucket = 8 * lane + e; bcnt = h[e]; }
+                    else below += h[e];
+                }
+            }
+        }
+        const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+        bucket = __shfl_sync(0xffffffffu, bucket, src);
+        below = __shfl_sync(0xffffffffu, below, src);
+        bcnt = __shfl_sync(0xffffffffu, bcnt, src);
+        prefix |= static_cast<uint64_t>(bucket) << shift;
+        hi_mask |= 0xFFull << shift;
+        want -= below;
+        __syncwarp();
+        if (bcnt == want || shift == 0) break;  // the whole bucket belongs to the k smallest
+        shift -= 8;
+    }
+    uint64_t kth = 0;
+    int out = 0;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+        const bool keep = i * 32 + lane < cnt && (key[i] & hi_mask) <= prefix;
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            row[out + __popc(m & ((1u << lane) - 1u))] = key[i];
+            kth = key[i] > kth ? key[i] : kth;
+        }
+        out += __popc(m);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t other = mma::shfl_u64(kth, lane ^ o);
+        kth = other > kth ? other : kth;
+    }
+    __syncwarp();
+    return kth;
+}
+__device__ __forceinline__ uint64_t select_any(uint64_t *row, int cnt, int k, int *hist, int lane) {
+    if (cnt <= 256) return select_small<8>(row, cnt, k, hist, lane);
+    return mma::select_row(row, cnt, k, hist, lane);
 }
 
 // A CTA's share of the linearised (group, stage) work, cut into segments of one query group each.
@@ -180,20 +328,17 @@ struct Segments {
 
 template <int C, int MT>
 __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
-    constexpr int ROW_BYTES = 64 * C;                 // one document in the nibble layout
-    constexpr int A_TILE = 128 * 128 * C;             // one 128-query operand tile
-    constexpr int B_STAGE = STAGE_DOCS * 128 * C;     // one document stage, bytes
+    constexpr int B_STAGE = STAGE_DOCS * 128 * C;     // one document stage = one byte tile
     constexpr int KSTEPS = 4 * C;                     // K = 32 per MMA
-    constexpr int DPI = 8 / C;                        // documents per producer warp-iteration (32 x 16 B)
-    constexpr int ITW = (STAGE_DOCS / DPI) / PROD_WARPS;  // warp-iterations per producer warp per stage
     constexpr int COLS = MT == 2 ? 128 : 64;          // accumulator columns an epilogue warp drains
     constexpr int EPI_PER_BUF = MT == 2 ? 4 : 8;      // epilogue warps reading one accumulator
+    constexpr int A_COLS = 32 * C;                    // tensor-memory columns of one 128-query operand tile
     extern __shared__ unsigned char smem_unaligned[];
     const uint32_t pad = (1024u - (smem_u32(smem_unaligned) & 1023u)) & 1023u;
     unsigned char *smem = smem_unaligned + pad;
     const int NS = p.NS;
     const SmemLayout L = smem_layout(C, MT, NS);
-    unsigned char *sA = smem + L.a_off, *sB = smem + L.b_off;
+    unsigned char *sB = smem + L.b_off;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L.bar_off);
     uint64_t *b_full = bars, *b_empty = bars + NS, *acc_full = bars + 2 * NS, *acc_empty = bars + 2 * NS + ACC_BUFS;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 2 * ACC_BUFS);
@@ -205,7 +350,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     Segments sg{static_cast<int64_t>(blockIdx.x) * W / G, (static_cast<int64_t>(blockIdx.x) + 1) * W / G, T, 0, 0, 0};
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < NS; ++i) { mbar_init(&b_full[i], PROD_WARPS); mbar_init(&b_empty[i], 1); }
+        for (int i = 0; i < NS; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
         for (int i = 0; i < ACC_BUFS; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], EPI_PER_BUF); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -215,20 +360,17 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    // Every role runs the same segment loop:  stage the group's query operand (all threads, generic
-    // proxy + proxy fence) | barrier | role work | barrier (every MMA that read the operand is done:
-    // the epilogue has consumed its result).
-    auto stage_queries = [&](int gr) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(p.qimg + static_cast<int64_t>(gr) * MT * A_TILE);
-        uint4 *dst = reinterpret_cast<uint4 *>(sA);
-        for (int i = threadIdx.x; i < MT * A_TILE / 16; i += THREADS) dst[i] = __ldg(src + i);
-        fence_async_smem();
-    };
+    // Every role runs the same segment loop:  [epilogue: store the group's query operand to tensor memory]
+    // | barrier | role work | barrier (every MMA that read the operand is done: the epilogue has consumed
+    // its result).
     uint32_t s_run = 0;  // stages this CTA has processed so far (drives every ring cursor)
+    const bool prof = p.prof != nullptr;
+    long long w0 = 0, w1 = 0;
+    int w2 = 0;
+    const long long t_begin = prof ? clock64() : 0;
 
     if (warp < EPI_WARPS) {
         // ================================ epilogue ================================
-        reg_inc<EPI_REGS>();
         const int q4 = warp & 3, idx = warp >> 2;
         const int mt = MT == 2 ? idx : 0;
         const int col0 = MT == 2 ? 0 : idx * COLS;
@@ -239,22 +381,31 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
         const uint32_t id_off = static_cast<uint32_t>(p.row_offset);  // row ids fit 32 bits (checked on the host)
         const int cap = p.cap, k = p.k;
         while (sg.next()) {
-            stage_queries(sg.gr);
-            cta_sync();
             const int64_t q0 = (static_cast<int64_t>(sg.gr) * MT + mt) * 128 + q4 * 32;  // first query row of this warp
             const int64_t myq = q0 + lane;
+            if (MT == 2 || idx == 0) {  // this thread's query row -> lane (32 q4 + lane), columns of tile mt
+                const uint4 *src = reinterpret_cast<const uint4 *>(p.qimg + myq * (128 * C));
+                const uint32_t ta = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + A_COL0 + mt * A_COLS;
+#pragma unroll
+                for (int c = 0; c < A_COLS / 8; ++c) tmem_st8(ta + c * 8, __ldg(src + 2 * c), __ldg(src + 2 * c + 1));
+                tmem_st_wait();
+            }
+            fence_before();
+            cta_sync();
             const bool valid = myq < p.nq;
             const int dq = valid ? p.qconst[myq] : 0;
             int theta = valid ? (p.tau_init ? max(TAU_OPEN, p.tau_init[myq]) : TAU_OPEN) : TAU_NEVER;
             int cnt = 0;
 
-            // 32 scores of this thread's query row: 3-input max tree, one compare, one vote.  On a hit
-            // (rare once thresholds have tightened) the warp builds per-lane hit masks from sign bits
-            // and re-reads just the hit columns from tensor memory, so no score is indexed dynamically.
-            auto filter = [&](const int (&v)[32], uint32_t taddr_c, uint32_t doc0) {
+            // 32 scores of this thread's query row: 3-input max tree, one compare, one vote.  On a hit (rare
+            // once thresholds have tightened) the warp builds per-lane hit masks from sign bits.  A lane with
+            // exactly one hit -- the common case -- knows the score already (it is the row maximum) and the
+            // column from the mask; only lanes with several hits walk their columns (jump-table pick).
+            auto filter = [&](const int (&v)[32], uint32_t doc0) {
                 const int g0 = max8(v), g1 = max8(v + 8), g2 = max8(v + 16), g3 = max8(v + 24);
                 const int m = max(max(g0, g1), max(g2, g3));
                 if (__any_sync(0xffffffffu, m >= theta)) {
+                    ++w1;
                     const int gm[4] = {g0, g1, g2, g3};
                     uint32_t hits = 0;
 #pragma unroll
@@ -265,51 +416,70 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                             for (int j = 7; j >= 0; --j) below = __funnelshift_l(static_cast<uint32_t>(v[8 * qg + j] - theta), below, 1);
                             hits |= (~below & 0xFFu) << (8 * qg);
                         }
-                    uint32_t cols = __reduce_or_sync(0xffffffffu, hits);
+                    const bool single = (hits & (hits - 1)) == 0;
+                    if (hits && single) {
+                        const uint32_t doc = doc0 + (__ffs(hits) - 1);
+                        if (doc < n_docs) {
+                            my_list[cnt] = (static_cast<uint64_t>(static_cast<uint32_t>(dq - m)) << 32) | (id_off + doc);
+                            ++cnt;
+                        }
+                    }
+                    uint32_t cols = __reduce_or_sync(0xffffffffu, single ? 0u : hits);
                     while (cols) {
                         const int j = __ffs(cols) - 1;
                         cols &= cols - 1;
-                        const int val = tmem_ld1(taddr_c + j);
-                        tmem_ld_wait();
-                        if (((hits >> j) & 1u) && doc0 + j < n_docs) {
+                        const int val = pick32(v, j);
+                        if (!single && ((hits >> j) & 1u) && doc0 + j < n_docs) {
                             my_list[cnt] = (static_cast<uint64_t>(static_cast<uint32_t>(dq - val)) << 32) | (id_off + doc0 + j);
                             ++cnt;
                         }
                     }
                     __syncwarp();
                     unsigned need = __ballot_sync(0xffffffffu, cnt > cap - 32);
-                    while (need) {  // a list that the next 32 documents could overflow: keep its k best
-                        const int ql = __ffs(need) - 1;
-                        need &= need - 1;
-                        const int c = __shfl_sync(0xffffffffu, cnt, ql);
-                        const uint64_t kth = mma::select_row(warp_lists + static_cast<int64_t>(ql) * cap, c, k, hist, lane);
-                        if (lane == ql) { cnt = k; theta = dq - static_cast<int>(kth >> 32); }
+                    if (need) {
+                        w2 += __popc(need);
+                        do {  // a list that the next 32 documents could overflow: keep its k best
+                            const int ql = __ffs(need) - 1;
+                            need &= need - 1;
+                            const int c = __shfl_sync(0xffffffffu, cnt, ql);
+                            const uint64_t kth = select_any(warp_lists + static_cast<int64_t>(ql) * cap, c, k, hist, lane);
+                            if (lane == ql) {
+                                cnt = k;
+                                theta = dq - static_cast<int>(kth >> 32);
+                                if (p.theta_g) atomicMax(p.theta_g + myq, theta);  // every CTA scanning this query tightens with us
+                            }
+                        } while (need);
                     }
                 }
             };
 
+            const uint32_t u0 = s_run * MT + mt;
+            Ring ac{static_cast<int>(u0 % ACC_BUFS), (u0 / ACC_BUFS) & 1u};
             for (int i = 0; i < sg.cnt; ++i) {
-                const uint32_t u = (s_run + i) * MT + mt;
-                const uint32_t buf = u & (ACC_BUFS - 1), use = u / ACC_BUFS;
-                mbar_wait(&acc_full[buf], use & 1u);
+                const uint32_t buf = ac.idx;
+                const int shared_theta = (p.theta_g && valid) ? __ldcg(p.theta_g + myq) : TAU_OPEN;  // in flight during the wait
+                mbar_wait_prof(&acc_full[buf], ac.phase, prof, w0);
                 fence_after();
                 const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + buf * STAGE_DOCS + col0;
                 const uint32_t doc0 = static_cast<uint32_t>(sg.sd0 + i) * STAGE_DOCS + col0;
-                int va[32], vb[32];
-                tmem_ld32(taddr, va);
-                tmem_ld_wait();
-#pragma unroll 1
-                for (int c = 0; c < COLS / 32; c += 2) {
-                    tmem_ld32(taddr + (c + 1) * 32, vb);
-                    filter(va, taddr + c * 32, doc0 + c * 32);
-                    tmem_ld_wait();
-                    if (c + 2 < COLS / 32) tmem_ld32(taddr + (c + 2) * 32, va);
-                    filter(vb, taddr + (c + 1) * 32, doc0 + (c + 1) * 32);
+                // the whole accumulator slice goes to registers first, so the buffer returns to the issuer after
+                // one tensor-memory read time instead of after the filter: it is on the MMA pipe's critical path
+                int v[COLS / 32][32];
+                if (!(p.debug & 4)) {
+#pragma unroll
+                    for (int c = 0; c < COLS / 32; ++c) tmem_ld32(taddr + c * 32, v[c]);
                     tmem_ld_wait();
                 }
-                fence_before();  // the accumulator has been read: hand it back to the issuer
+                fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&acc_empty[buf]);
+                theta = max(theta, shared_theta);
+                if (!(p.debug & 4)) {
+#pragma unroll
+                    for (int c = 0; c < COLS / 32; ++c) filter(v[c], doc0 + c * 32);
+                }
+#pragma unroll
+                for (int a = 0; a < MT; ++a) ac.advance(ACC_BUFS);
             }
             // ---- emit: every query row of this warp, its <= k best keys (unsorted), KEY_INF padded
             {
@@ -323,7 +493,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                     if (qq >= p.nq) break;
                     int c = __shfl_sync(0xffffffffu, cnt, ql);
                     uint64_t *row = warp_lists + static_cast<int64_t>(ql) * cap;
-                    if (c > k) { mma::select_row(row, c, k, hist, lane); c = k; }
+                    if (c > k) { select_any(row, c, k, hist, lane); c = k; }
                     __syncwarp();
                     uint64_t *dst = p.out + (part * p.nq + qq) * k;
                     for (int e = lane; e < k; e += 32) dst[e] = e < c ? __ldcg(row + e) : KEY_INF;
@@ -333,88 +503,63 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
             s_run += static_cast<uint32_t>(sg.cnt);
             cta_sync();
         }
-    } else if (warp < EPI_WARPS + PROD_WARPS) {
-        // ================================ producers ================================
-        reg_dec<PROD_REGS>();
-        const int pw = warp - EPI_WARPS;
-        const int qd = lane >> 3, d = (lane >> 2) & 1, gg = lane & 3;
-        const int kb = qd % C, doc_in_it = 2 * (qd / C) + d, g = 4 * kb + gg;
-        const unsigned char *db = reinterpret_cast<const unsigned char *>(p.db);
-        const uint32_t n_pad32 = static_cast<uint32_t>(p.n_pad);
-        auto load_stage = [&](uint4 (&r)[ITW], int sd) {
-#pragma unroll
-            for (int it = 0; it < ITW; ++it) {
-                const uint32_t row = static_cast<uint32_t>(sd) * STAGE_DOCS + (it * PROD_WARPS + pw) * DPI + doc_in_it;
-                r[it] = row < n_pad32 ? __ldg(reinterpret_cast<const uint4 *>(db + static_cast<int64_t>(row) * ROW_BYTES + g * 16))
-                                      : make_uint4(0u, 0u, 0u, 0u);
-            }
-        };
-        auto store_stage = [&](const uint4 (&r)[ITW], int slot) {
-            unsigned char *stage = sB + static_cast<size_t>(slot) * B_STAGE + kb * (STAGE_DOCS * 128);
-#pragma unroll
-            for (int it = 0; it < ITW; ++it) {
-                const int row = (it * PROD_WARPS + pw) * DPI + doc_in_it;
-                unsigned char *rowp = stage + (row >> 3) * 1024 + (row & 7) * 128;
-                const uint4 w = r[it];
-                *reinterpret_cast<uint4 *>(rowp + (((2 * gg) ^ (row & 7)) << 4)) =
-                    make_uint4(w.x & 0x0F0F0F0Fu, (w.x >> 4) & 0x0F0F0F0Fu, w.y & 0x0F0F0F0Fu, (w.y >> 4) & 0x0F0F0F0Fu);
-                *reinterpret_cast<uint4 *>(rowp + (((2 * gg + 1) ^ (row & 7)) << 4)) =
-                    make_uint4(w.z & 0x0F0F0F0Fu, (w.z >> 4) & 0x0F0F0F0Fu, w.w & 0x0F0F0F0Fu, (w.w >> 4) & 0x0F0F0F0Fu);
-            }
-        };
+        if (prof && threadIdx.x == 0) {
+            unsigned long long *o = p.prof + blockIdx.x * 8, *x = p.prof + gridDim.x * 8 + blockIdx.x * 4;
+            o[0] = w0; o[1] = w1; o[6] = clock64() - t_begin; o[7] = s_run;
+            x[0] = 0; x[1] = 0; x[2] = w2;
+        }
+    } else if (warp == MMA_WARP) {
+        // ================================ MMA issuer ================================
+        const uint32_t b_lo0 = desc_lo(smem_u32(sB));
+        const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // warp-uniform by construction
         while (sg.next()) {
-            stage_queries(sg.gr);
             cta_sync();
-            Ring rb{static_cast<int>(s_run % NS), ((s_run / NS) & 1u) ^ 1u};  // "empty" waits start on the completed phase
-            auto publish = [&](const uint4 (&r)[ITW]) {
-                mbar_wait(&b_empty[rb.idx], rb.phase);
-                store_stage(r, rb.idx);
-                fence_async_smem();  // generic-proxy stores -> visible to the tensor core's async proxy
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&b_full[rb.idx]);
-                rb.advance(NS);
-            };
-            uint4 ra[ITW], rbuf[ITW];
-            load_stage(ra, sg.sd0);
-            if (sg.cnt > 1) load_stage(rbuf, sg.sd0 + 1);
-            for (int i = 0; i < sg.cnt; i += 2) {
-                publish(ra);
-                if (i + 2 < sg.cnt) load_stage(ra, sg.sd0 + i + 2);
-                if (i + 1 < sg.cnt) {
-                    publish(rbuf);
-                    if (i + 3 < sg.cnt) load_stage(rbuf, sg.sd0 + i + 3);
+            fence_after();  // the query operand stored by the epilogue warps is in tensor memory
+            Ring rb{static_cast<int>(s_run % NS), (s_run / NS) & 1u};
+            const uint32_t u0 = s_run * MT;
+            Ring ac{static_cast<int>(u0 % ACC_BUFS), ((u0 / ACC_BUFS) & 1u) ^ 1u};  // "empty" waits: completed phase first
+            for (int i = 0; i < sg.cnt; ++i) {  // the whole warp walks the pipeline, one elected lane issues
+                mbar_wait_prof(&b_full[rb.idx], rb.phase, prof, w0);
+                fence_after();
+                const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const uint32_t buf = ac.idx;
+                    mbar_wait_prof(&acc_empty[buf], ac.phase, prof, w1);
+                    fence_after();
+                    if (elect_one()) {
+                        const uint32_t d = tm + buf * STAGE_DOCS;
+#pragma unroll
+                        for (int ks = 0; ks < KSTEPS; ++ks) {
+                            const uint32_t ta = tm + A_COL0 + mt * A_COLS + ks * 8;  // K = 32 signed bytes = 8 columns
+                            const uint32_t bo = ((ks >> 2) * (STAGE_DOCS * 128) + (ks & 3) * 32) >> 4;
+                            if (ks == 0) umma_i8<false>(d, ta, b_lo + bo);
+                            else umma_i8<true>(d, ta, b_lo + bo);
+                        }
+                        umma_commit(&acc_full[buf]);
+                    }
+                    __syncwarp();
+                    ac.advance(ACC_BUFS);
                 }
+                if (elect_one()) umma_commit(&b_empty[rb.idx]);
+                __syncwarp();
+                rb.advance(NS);
             }
             s_run += static_cast<uint32_t>(sg.cnt);
             cta_sync();
         }
+        if (prof && lane == 0) { p.prof[blockIdx.x * 8 + 2] = w0; p.prof[blockIdx.x * 8 + 3] = w1; }
     } else {
-        // ================================ MMA issuer (+ three idle warps) ================================
-        reg_dec<MMA_REGS>();
-        const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+        // ================================ loader ================================
+        const unsigned char *db = reinterpret_cast<const unsigned char *>(p.db);
         while (sg.next()) {
-            stage_queries(sg.gr);
             cta_sync();
-            if (warp == MMA_WARP && lane == 0) {
-                Ring rb{static_cast<int>(s_run % NS), (s_run / NS) & 1u};
+            if (lane == 0) {
+                Ring rb{static_cast<int>(s_run % NS), ((s_run / NS) & 1u) ^ 1u};  // "empty" waits start on the completed phase
                 for (int i = 0; i < sg.cnt; ++i) {
-                    mbar_wait(&b_full[rb.idx], rb.phase);
-                    fence_after();
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) {
-                        const uint32_t u = (s_run + i) * MT + mt;
-                        const uint32_t buf = u & (ACC_BUFS - 1), use = u / ACC_BUFS;
-                        mbar_wait(&acc_empty[buf], (use & 1u) ^ 1u);
-                        fence_after();
-#pragma unroll
-                        for (int ks = 0; ks < KSTEPS; ++ks) {
-                            const uint64_t ad = make_desc(a_base + mt * A_TILE + (ks >> 2) * (128 * 128) + (ks & 3) * 32);
-                            const uint64_t bd = make_desc(b_base + rb.idx * B_STAGE + (ks >> 2) * (STAGE_DOCS * 128) + (ks & 3) * 32);
-                            umma_i8(tmem + buf * STAGE_DOCS, ad, bd, ks > 0 ? 1u : 0u);
-                        }
-                        umma_commit(&acc_full[buf]);
-                    }
-                    umma_commit(&b_empty[rb.idx]);
+                    mbar_wait_prof(&b_empty[rb.idx], rb.phase, prof, w0);
+                    mma::mbar_arrive_expect_tx(&b_full[rb.idx], B_STAGE);
+                    mma::tma_bulk_g2s(sB + static_cast<size_t>(rb.idx) * B_STAGE, db + static_cast<int64_t>(sg.sd0 + i) * B_STAGE, B_STAGE, &b_full[rb.idx]);
                     rb.advance(NS);
                 }
             }
@@ -422,6 +567,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
             s_run += static_cast<uint32_t>(sg.cnt);
             cta_sync();
         }
+        if (prof && lane == 0) { p.prof[blockIdx.x * 8 + 4] = w0; p.prof[blockIdx.x * 8 + 5] = 0; }
     }
     fence_before();
     cta_sync();

@@ -82,6 +82,74 @@ __host__ __device__ inline uint32_t sw128_offset(int r, int kbyte, int R) {
 
 constexpr int M_ = 128, N_ = 256, K_ = 256;
 
+__device__ __forceinline__ void umma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]) : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// ---------------------------------------------------------------- test 5: A operand in tensor memory
+// Assumed layout: row m of A in lane m, column c holds K elements 4c..4c+3 (little endian), 8 columns per K = 32 step.
+__global__ void __launch_bounds__(128, 1) tile_ts_kernel(const int8_t *A, const int8_t *B, int32_t *D, int *err) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char *sB = smem;       // 256 x 256 = 64 KB
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base_s;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < N_ * K_; i += blockDim.x) sB[sw128_offset(i / K_, i % K_, N_)] = static_cast<unsigned char>(B[i]);
+    fence_async_smem();
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+    if (warp == 0) tmem_alloc(&tmem_base_s, 512);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const uint32_t a_tmem = tmem + 256;  // columns 256..319
+    {
+        const int m = warp * 32 + lane;
+        const uint32_t *arow = reinterpret_cast<const uint32_t *>(A + m * K_);
+        for (int c0 = 0; c0 < K_ / 4; c0 += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = arow[c0 + j];
+            tmem_st8(a_tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+        }
+        tmem_st_wait();
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    if (threadIdx.x == 0) {
+        const uint32_t idesc = make_idesc(M_, N_, true, true);
+        for (int ks = 0; ks < K_ / 32; ++ks) {
+            const uint64_t bd = make_desc(smem_u32(sB) + (ks >> 2) * (N_ * 128) + (ks & 3) * 32);
+            umma_i8_ts(tmem, a_tmem + ks * 8, bd, idesc, ks > 0 ? 1u : 0u);
+        }
+        umma_commit(&bar);
+    }
+    __syncwarp();
+    if (!mbar_wait_bounded(&bar, 0)) { if (lane == 0) atomicExch(err, 1); }
+    else {
+        fence_after();
+        for (int c0 = 0; c0 < N_; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) D[(warp * 32 + lane) * N_ + c0 + j] = static_cast<int32_t>(v[j]);
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 // ---------------------------------------------------------------- test 1
 __global__ void __launch_bounds__(128, 1) tile_kernel(const int8_t *A, const int8_t *B, int32_t *D, int *err, int b_signed) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -129,7 +197,7 @@ __global__ void __launch_bounds__(128, 1) tile_kernel(const int8_t *A, const int
 
 // ---------------------------------------------------------------- tests 2-4
 // warps 0..LW-1: tcgen05.ld loops (if do_ld); warp LW: MMA issuer (if do_mma).
-template <int N>
+template <int N, bool TS = false>
 __global__ void __launch_bounds__(288, 1) rate_kernel(int iters_mma, int iters_ld, int do_mma, int do_ld, int ld_warps,
                                                       long long *mma_clk, long long *ld_clk, int *err, uint32_t *sink) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -154,7 +222,8 @@ __global__ void __launch_bounds__(288, 1) rate_kernel(int iters_mma, int iters_l
                 const int ks = it & 3;
                 const uint64_t ad = make_desc(smem_u32(sA) + ks * 32);
                 const uint64_t bd = make_desc(smem_u32(sB) + ks * 32);
-                umma_i8(tmem + ((it >> 2) & 1) * 256, ad, bd, idesc, 1u);
+                if (TS) umma_i8_ts(tmem + ((it >> 2) & 1) * 128, tmem + 384 + ks * 8, bd, idesc, 1u);
+                else umma_i8(tmem + ((it >> 2) & 1) * 256, ad, bd, idesc, 1u);
             }
             umma_commit(&bar);
             if (!mbar_wait_bounded(&bar, 0)) atomicExch(err, 2);
@@ -221,15 +290,47 @@ int main(int argc, char **argv) {
             CK(cudaMemset(err, 0, 4));
         }
     }
+    if (which == 0 || which == 5) {
+        std::vector<int8_t> A(M_ * K_), B(N_ * K_);
+        srand(4321);
+        for (auto &a : A) a = static_cast<int8_t>(2 * (rand() % 16) - 15);
+        for (auto &b : B) b = static_cast<int8_t>(rand() % 16);
+        int8_t *dA, *dB; int32_t *dD;
+        CK(cudaMalloc(&dA, A.size())); CK(cudaMalloc(&dB, B.size())); CK(cudaMalloc(&dD, M_ * N_ * 4));
+        CK(cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemset(dD, 0xCC, M_ * N_ * 4));
+        const int smem = N_ * K_;
+        CK(cudaFuncSetAttribute(tile_ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        tile_ts_kernel<<<1, 128, smem>>>(dA, dB, dD, err);
+        CK(cudaDeviceSynchronize());
+        int herr = 0;
+        CK(cudaMemcpy(&herr, err, 4, cudaMemcpyDeviceToHost));
+        std::vector<int32_t> D(M_ * N_);
+        CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
+        long long bad = 0; int first = -1;
+        for (int m = 0; m < M_; ++m)
+            for (int n = 0; n < N_; ++n) {
+                int32_t s = 0;
+                for (int k = 0; k < K_; ++k) s += static_cast<int32_t>(A[m * K_ + k]) * static_cast<int32_t>(B[n * K_ + k]);
+                if (s != D[m * N_ + n]) { if (first < 0) first = m * N_ + n; ++bad; }
+            }
+        printf("{\"test\": \"tile_ts_128x256x256_i8 (A in TMEM)\", \"timeout\": %d, \"mismatches\": %lld, \"first_bad\": %d, \"d0\": %d}\n", herr, bad, first, D[0]);
+        fflush(stdout);
+        CK(cudaMemset(err, 0, 4));
+    }
     long long *mma_clk, *ld_clk; uint32_t *sink;
     CK(cudaMalloc(&mma_clk, sms * 8)); CK(cudaMalloc(&ld_clk, sms * 64)); CK(cudaMalloc(&sink, 4));
-    auto run_rate = [&](int N, int do_mma, int do_ld, int ld_warps) -> int {
+    auto run_rate = [&](int N, int do_mma, int do_ld, int ld_warps, bool ts = false) -> int {
         const int iters_mma = 8192, iters_ld = 4096;
         const int smem = (128 + N) * 128;
         CK(cudaMemset(mma_clk, 0, sms * 8)); CK(cudaMemset(ld_clk, 0, sms * 64));
         if (N == 256) {
             CK(cudaFuncSetAttribute(rate_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             rate_kernel<256><<<sms, 288, smem>>>(iters_mma, iters_ld, do_mma, do_ld, ld_warps, mma_clk, ld_clk, err, sink);
+        } else if (ts) {
+            CK(cudaFuncSetAttribute(rate_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            rate_kernel<128, true><<<sms, 288, smem>>>(iters_mma, iters_ld, do_mma, do_ld, ld_warps, mma_clk, ld_clk, err, sink);
         } else {
             CK(cudaFuncSetAttribute(rate_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             rate_kernel<128><<<sms, 288, smem>>>(iters_mma, iters_ld, do_mma, do_ld, ld_warps, mma_clk, ld_clk, err, sink);
@@ -245,9 +346,9 @@ int main(int argc, char **argv) {
         for (auto v : lc) if (v > lmax) lmax = v;
         const double mac_per_clk = do_mma && mmax ? 128.0 * N * 32 * iters_mma / mmax : 0.0;
         const double ld_bytes_per_clk = do_ld && lmax ? 4096.0 * iters_ld * ld_warps / lmax : 0.0;
-        printf("{\"test\": \"rate\", \"N\": %d, \"mma\": %d, \"ld\": %d, \"ld_warps\": %d, \"timeout\": %d, \"mma_clk_per_inst\": %.1f, "
+        printf("{\"test\": \"rate%s\", \"N\": %d, \"mma\": %d, \"ld\": %d, \"ld_warps\": %d, \"timeout\": %d, \"mma_clk_per_inst\": %.1f, "
                "\"mac_per_clk_per_sm\": %.0f, \"ld_clk_per_inst\": %.1f, \"ld_bytes_per_clk_per_sm\": %.1f}\n",
-               N, do_mma, do_ld, ld_warps, herr, do_mma ? double(mmax) / iters_mma : 0.0, mac_per_clk,
+               ts ? "_ts" : "", N, do_mma, do_ld, ld_warps, herr, do_mma ? double(mmax) / iters_mma : 0.0, mac_per_clk,
                do_ld ? double(lmax) / iters_ld : 0.0, ld_bytes_per_clk);
         fflush(stdout);
         CK(cudaMemset(err, 0, 4));
@@ -256,5 +357,6 @@ int main(int argc, char **argv) {
     if (which == 0 || which == 2) { if (run_rate(256, 1, 0, 0)) return 1; if (run_rate(128, 1, 0, 0)) return 1; }
     if (which == 0 || which == 3) { if (run_rate(256, 0, 1, 4)) return 1; if (run_rate(256, 0, 1, 8)) return 1; }
     if (which == 0 || which == 4) { if (run_rate(256, 1, 1, 4)) return 1; if (run_rate(256, 1, 1, 8)) return 1; if (run_rate(128, 1, 1, 8)) return 1; }
+    if (which == 0 || which == 6) { if (run_rate(128, 1, 0, 0, true)) return 1; if (run_rate(128, 1, 1, 8, true)) return 1; }
     return 0;
 }

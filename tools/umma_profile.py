@@ -1,0 +1,47 @@
+"""Per-role wait-cycle breakdown of the tcgen05 scan kernel (xfbq_debug_profile counters).
+Usage (under gpurun): python tools/umma_profile.py [nq] [n] [dim]"""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_2008_02002_b200 as xb  # noqa: E402
+from paper_2008_02002_b200 import _native  # noqa: E402
+
+nq = int(sys.argv[1]) if len(sys.argv) > 1 else 10000
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 10_000_000
+dim = int(sys.argv[3]) if len(sys.argv) > 3 else 256
+k = 100
+g = torch.Generator(device="cuda").manual_seed(1)
+docs = torch.randn((n, dim), generator=g, device="cuda")
+docs /= docs.norm(dim=1, keepdim=True)
+q = torch.randn((nq, dim), generator=g, device="cuda")
+q /= q.norm(dim=1, keepdim=True)
+scale = xb.estimate_scale(docs[:100000].cpu().numpy(), 0.98)
+idx = xb.build_index(docs, xb.QuantParams(dim=dim, scale=scale, doc_bits=4, query_bits=4), keep_originals=False)
+del docs
+for _ in range(2):
+    xb.search(idx, q, k)
+prof = torch.zeros((148 * 12,), dtype=torch.int64, device="cuda")
+_native.check(_native.lib().xfbq_debug_profile(prof.data_ptr()))
+_native.set_timing(True)
+xb.search(idx, q, k)
+ms = _native.last_scan_ms()
+_native.set_timing(False)
+_native.check(_native.lib().xfbq_debug_profile(0))
+allc = prof.cpu().numpy().astype(np.float64)
+c = allc[:148 * 8].reshape(148, 8)
+x = allc[148 * 8:].reshape(148, 4)
+tot = c[:, 6].mean()
+st = c[:, 7].mean()
+print(f"kernel {ms:.3f} ms; per CTA: {tot / 1e6:.2f} Mclk, {st:.0f} stages, {tot / st:.0f} clk/stage")
+names = ["epi wait acc_full", "epi slow-path chunks (warp 0)", "mma wait b_full", "mma wait acc_empty", "prod wait b_empty",
+         "prod store time"]
+for i, nm in enumerate(names):
+    if i == 1:
+        print(f"  {nm:34s} {c[:, i].mean():12.0f}  ({c[:, i].mean() / (st * 4) * 100:.1f}% of chunks)")
+    else:
+        print(f"  {nm:34s} {c[:, i].mean() / 1e6:9.2f} Mclk  {c[:, i].mean() / tot * 100:5.1f}%  min {c[:, i].min() / tot * 100:5.1f}% max {c[:, i].max() / tot * 100:5.1f}%")
+print(f"  epi warp0 compactions {x[:, 2].mean():.0f}")
