@@ -889,6 +889,7 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
 // ----------------------------------------------------------------------------------------------
 struct UmmaShape {
     int MT = 2, DW = 1, groups = 1, grid = 1, slots = 1, parts = 1, cap = 0, NS = 0;
+    bool queue = false;  // scan_queue_kernel (main scans) vs scan_kernel (sample scans: open thresholds)
     int64_t stages = 0, nq_pad = 0, n_pad = 0;
     size_t smem = 0, lists_bytes = 0, parts_bytes = 0, mscratch_bytes = 0;
 };
@@ -902,17 +903,24 @@ struct UmmaPlan {
 
 typedef void (*UmmaKernel)(const umma::Params);
 
-UmmaKernel pick_umma_kernel(int C, int MT) {
+UmmaKernel pick_umma_kernel(int C, int MT, bool queue) {
+    if (queue) {
+        if (C == 1) return MT == 2 ? umma::scan_queue_kernel<1, 2> : umma::scan_queue_kernel<1, 1>;
+        if (C == 2) return MT == 2 ? umma::scan_queue_kernel<2, 2> : umma::scan_queue_kernel<2, 1>;
+        if (C == 4 && MT == 1) return umma::scan_queue_kernel<4, 1>;
+        return nullptr;
+    }
     if (C == 1) return MT == 2 ? umma::scan_kernel<1, 2> : umma::scan_kernel<1, 1>;
     if (C == 2) return MT == 2 ? umma::scan_kernel<2, 2> : umma::scan_kernel<2, 1>;
     if (C == 4 && MT == 1) return umma::scan_kernel<4, 1>;
     return nullptr;
 }
 
-void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &info, UmmaShape *out) {
+void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &info, UmmaShape *out, bool seed_scan = false) {
     UmmaShape sh;
     sh.MT = MT;
-    sh.DW = MT == 2 ? 1 : 2;
+    sh.queue = !seed_scan && env_int("XFBQ_UMMA_QUEUE", 1) != 0;
+    sh.DW = (MT == 2 || sh.queue) ? 1 : 2;
     int cap = 64;
     while (cap < 2 * k) cap <<= 1;
     sh.cap = cap;
@@ -923,6 +931,13 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
     sh.stages = (sh.n_pad + umma::STAGE_DOCS - 1) / umma::STAGE_DOCS;
     const int64_t W = static_cast<int64_t>(sh.groups) * sh.stages;
     int64_t grid = env_int("XFBQ_GRID", 0) > 0 ? env_int("XFBQ_GRID", 0) : info.sms;
+    // The sample scan that seeds the thresholds starts from open lists, so its cost grows with the number of
+    // lists, not with the documents: give every query group to as few CTAs as keep the chip busy.
+    if (seed_scan && env_int("XFBQ_GRID", 0) <= 0) {
+        const int64_t per_group = (info.sms + sh.groups - 1) / sh.groups;
+        const int64_t cap_grid = sh.groups * (per_group < env_int("XFBQ_SEED_SPLIT", 1) ? per_group : env_int("XFBQ_SEED_SPLIT", 1));
+        if (grid > cap_grid) grid = cap_grid;
+    }
     if (grid > W) grid = W;
     sh.grid = static_cast<int>(grid);
     int slots = 1;
@@ -940,9 +955,10 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
     sh.parts = slots * sh.DW;
     int NS = env_int("XFBQ_UMMA_STAGES", 6);
     const size_t budget = static_cast<size_t>(info.smem_optin);
-    while (NS > 2 && umma::smem_layout(C, MT, NS).total > budget) --NS;
-    sh.NS = umma::smem_layout(C, MT, NS).total <= budget ? NS : 0;
-    sh.smem = umma::smem_layout(C, MT, NS).total;
+    auto smem_need = [&](int ns) { return static_cast<size_t>(sh.queue ? umma::q_smem_layout(C, ns).total : umma::smem_layout(C, MT, ns).total); };
+    while (NS > 2 && smem_need(NS) > budget) --NS;
+    sh.NS = smem_need(NS) <= budget ? NS : 0;
+    sh.smem = smem_need(NS);
     sh.lists_bytes = static_cast<size_t>(sh.grid) * umma::EPI_WARPS * 32 * cap * 8;
     sh.parts_bytes = static_cast<size_t>(sh.parts) * nq * k * 8;
     sh.mscratch_bytes = static_cast<size_t>(merge_scratch_parts(sh.parts, k, nq)) * nq * k * 8;
@@ -970,7 +986,7 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     if (sample < 0) sample = 131072;
     if (sample > 0 && (n < 16 * sample || sample < 4 * k)) sample = 0;
     pl.sample = sample;
-    if (sample) umma_shape(sample, C, nq, k, MT, info, &pl.pre);
+    if (sample) umma_shape(sample, C, nq, k, MT, info, &pl.pre, true);
     size_t off = 0;
     pl.off_qimg = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 128 * C);
     pl.off_qconst = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 4);
@@ -987,7 +1003,7 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
 
 int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, const void *nib, int64_t n, int C,
                   int64_t nq, int k, int64_t row_offset, const int32_t *tau_init, uint64_t *keys_out, cudaStream_t st) {
-    UmmaKernel kern = pick_umma_kernel(C, sh.MT);
+    UmmaKernel kern = pick_umma_kernel(C, sh.MT, sh.queue);
     if (!kern) return fail(XFBQ_E_UNSUPPORTED, "no tcgen05 kernel for C=%d MT=%d", C, sh.MT);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh.smem));
     if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "umma scan smem opt-in (%zu bytes): %s", sh.smem, cudaGetErrorString(e));
@@ -1010,7 +1026,7 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     }
     const bool timed = g_timing && &sh == &pl.main;
     if (timed) cudaEventRecord(g_ev0, st);
-    kern<<<static_cast<unsigned>(sh.grid), umma::THREADS, sh.smem, st>>>(p);
+    kern<<<static_cast<unsigned>(sh.grid), sh.queue ? umma::Q_THREADS : umma::THREADS, sh.smem, st>>>(p);
     if (timed) { cudaEventRecord(g_ev1, st); g_ev_valid = true; }
     if (int rc = check_launch("umma::scan_kernel")) return rc;
     return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st, true);

@@ -455,9 +455,17 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
 
             const uint32_t u0 = s_run * MT + mt;
             Ring ac{static_cast<int>(u0 % ACC_BUFS), (u0 / ACC_BUFS) & 1u};
+            // thresholds other CTAs found for this query: fetched four stages ahead of their use, so the L2 round
+            // trip never sits on a stage's critical path
+            const bool fetch_shared = p.theta_g && valid;
+            int shared_next = TAU_OPEN;
             for (int i = 0; i < sg.cnt; ++i) {
                 const uint32_t buf = ac.idx;
-                const int shared_theta = (p.theta_g && valid) ? __ldcg(p.theta_g + myq) : TAU_OPEN;  // in flight during the wait
+                int shared_theta = TAU_OPEN;
+                if ((i & 3) == 0) {
+                    shared_theta = shared_next;
+                    if (fetch_shared) shared_next = __ldcg(p.theta_g + myq);
+                }
                 mbar_wait_prof(&acc_full[buf], ac.phase, prof, w0);
                 fence_after();
                 const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + buf * STAGE_DOCS + col0;
@@ -568,6 +576,362 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
             cta_sync();
         }
         if (prof && lane == 0) { p.prof[blockIdx.x * 8 + 4] = w0; p.prof[blockIdx.x * 8 + 5] = 0; }
+    }
+    fence_before();
+    cta_sync();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+// ================================================================================================
+// Queue variant (main scans): the drain warps never maintain lists.  A score row whose maximum passes
+// its query's threshold is parked in a shared-memory ring (8 STS.128 + a ticket) and two resolver warps
+// turn parked rows into list entries, compact lists and publish tighter thresholds.  With only three
+// accumulators in flight, any data-dependent pause of a drain warp used to stall the tensor pipe (the
+// kernel above, still used for the open-threshold sample scans, ran at a third of its no-hit speed);
+// here the accumulator hand-off takes the same time whatever the scores are.
+// ================================================================================================
+constexpr int Q_DRAIN = 8, Q_MMA_WARP = 8, Q_TMA_WARP = 9, Q_RES0 = 10, Q_RESOLVERS = 2;
+constexpr int Q_THREADS = (Q_DRAIN + 2 + Q_RESOLVERS) * 32;  // 12 warps -> 168 registers per thread
+constexpr int RING_ROWS = 64;                                 // parked rows per resolver (power of two)
+constexpr int STASH_WORDS = 36;                               // a parked row: 32 scores, query, first document, ticket, pad (144 B)
+
+struct QSmemLayout {
+    uint32_t b_off, ring_off, state_off, hist_off, bar_off, total;
+};
+__host__ __device__ inline QSmemLayout q_smem_layout(int C, int NS) {
+    QSmemLayout L;
+    uint32_t off = 0;
+    L.b_off = off; off += static_cast<uint32_t>(NS) * STAGE_DOCS * 128 * C;
+    L.ring_off = off; off += Q_RESOLVERS * RING_ROWS * STASH_WORDS * 4;
+    L.state_off = off; off += 4 * 256 * 4 + 64;  // per query: count, threshold, Dq, claim; ring heads / tails / done
+    L.hist_off = off; off += Q_RESOLVERS * 256 * 4;
+    L.bar_off = off; off += (2 * NS + 2 * ACC_BUFS) * 8 + 16;
+    L.total = off + 1024;
+    return L;
+}
+__device__ __forceinline__ int ld_volatile(const int *p) { return *reinterpret_cast<const volatile int *>(p); }
+__device__ __forceinline__ void st_volatile(int *p, int v) { *reinterpret_cast<volatile int *>(p) = v; }
+
+template <int C, int MT>
+__global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p) {
+    constexpr int B_STAGE = STAGE_DOCS * 128 * C;
+    constexpr int KSTEPS = 4 * C;
+    constexpr int COLS = MT == 2 ? 128 : 64;
+    constexpr int EPI_PER_BUF = MT == 2 ? 4 : 8;
+    constexpr int A_COLS = 32 * C;
+    constexpr int NQ_CTA = 128 * MT;                  // queries of one group
+    extern __shared__ unsigned char smem_unaligned[];
+    const uint32_t pad = (1024u - (smem_u32(smem_unaligned) & 1023u)) & 1023u;
+    unsigned char *smem = smem_unaligned + pad;
+    const int NS = p.NS;
+    const QSmemLayout L = q_smem_layout(C, NS);
+    unsigned char *sB = smem + L.b_off;
+    uint32_t *rings = reinterpret_cast<uint32_t *>(smem + L.ring_off);
+    int *cnt_s = reinterpret_cast<int *>(smem + L.state_off), *theta_s = cnt_s + 256, *dq_s = cnt_s + 512, *claim_s = cnt_s + 768;
+    int *head_s = cnt_s + 1024, *tail_s = head_s + Q_RESOLVERS, *done_s = tail_s + Q_RESOLVERS;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L.bar_off);
+    uint64_t *b_full = bars, *b_empty = bars + NS, *acc_full = bars + 2 * NS, *acc_empty = bars + 2 * NS + ACC_BUFS;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 2 * ACC_BUFS);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    const int64_t T = p.stages;
+    const int64_t W = static_cast<int64_t>(p.groups) * T;
+    const int64_t G = gridDim.x;
+    Segments sg{static_cast<int64_t>(blockIdx.x) * W / G, (static_cast<int64_t>(blockIdx.x) + 1) * W / G, T, 0, 0, 0};
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NS; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
+        for (int i = 0; i < ACC_BUFS; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], EPI_PER_BUF); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int r = 0; r < Q_RESOLVERS; ++r) { head_s[r] = 0; tail_s[r] = 0; done_s[r] = 0; }
+    }
+    for (int i = threadIdx.x; i < Q_RESOLVERS * RING_ROWS; i += Q_THREADS) rings[i * STASH_WORDS + 34] = 0u;  // no ticket yet
+    if (warp == 0) tmem_alloc(tmem_slot, 512);
+    fence_before();
+    cta_sync();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+    uint32_t s_run = 0;
+    const bool prof = p.prof != nullptr;
+    long long w0 = 0, w1 = 0;
+    int w2 = 0;
+    const long long t_begin = prof ? clock64() : 0;
+    uint64_t *group_lists = p.lists + static_cast<int64_t>(blockIdx.x) * NQ_CTA * static_cast<int64_t>(p.cap);
+
+    if (warp < Q_DRAIN) {
+        // ================================ drain ================================
+        const int q4 = warp & 3, idx = warp >> 2;
+        const int mt = MT == 2 ? idx : 0;
+        const int col0 = MT == 2 ? 0 : idx * COLS;
+        const int qloc = mt * 128 + q4 * 32 + lane;   // this thread's query inside the group
+        const int res = warp & 1;                     // the resolver that owns these queries' lists
+        uint32_t *ring = rings + res * (RING_ROWS * STASH_WORDS);
+        while (sg.next()) {
+            const int64_t myq = static_cast<int64_t>(sg.gr) * NQ_CTA + qloc;
+            const bool valid = myq < p.nq;
+            if (MT == 2 || idx == 0) {  // query row -> tensor memory; the query's shared state
+                const uint4 *src = reinterpret_cast<const uint4 *>(p.qimg + myq * (128 * C));
+                const uint32_t ta = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + A_COL0 + mt * A_COLS;
+#pragma unroll
+                for (int c = 0; c < A_COLS / 8; ++c) tmem_st8(ta + c * 8, __ldg(src + 2 * c), __ldg(src + 2 * c + 1));
+                tmem_st_wait();
+                cnt_s[qloc] = 0;
+                dq_s[qloc] = valid ? p.qconst[myq] : 0;
+                theta_s[qloc] = valid ? (p.tau_init ? max(TAU_OPEN, p.tau_init[myq]) : TAU_OPEN) : TAU_NEVER;
+            }
+            fence_before();
+            cta_sync();
+            int theta = theta_s[qloc];
+
+            // 32 scores of this thread's query row: 3-input max tree, one compare, one vote; a row whose
+            // maximum passes is parked for the resolver (its scores, its query, its first document, a ticket)
+            auto filter = [&](const int (&v)[32], uint32_t doc0) {
+                const int m = max(max(max8(v), max8(v + 8)), max(max8(v + 16), max8(v + 24)));
+                const bool hit = m >= theta;
+                const unsigned hm = __ballot_sync(0xffffffffu, hit);
+                if (hm) {
+                    ++w1;
+                    const int n = __popc(hm);
+                    int t0 = 0;
+                    if (lane == 0) t0 = atomicAdd(&head_s[res], n);
+                    t0 = __shfl_sync(0xffffffffu, t0, 0);
+                    while (t0 + n - ld_volatile(&tail_s[res]) > RING_ROWS) __nanosleep(40);  // ring full: the resolver is behind
+                    if (hit) {
+                        const int t = t0 + __popc(hm & ((1u << lane) - 1u));
+                        uint32_t *row = ring + (t & (RING_ROWS - 1)) * STASH_WORDS;
+#pragma unroll
+                        for (int c = 0; c < 8; ++c)
+                            *reinterpret_cast<uint4 *>(row + 4 * c) = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+                        row[32] = qloc;
+                        row[33] = doc0;
+                        __threadfence_block();
+                        st_volatile(reinterpret_cast<int *>(row + 34), t + 1);
+                    }
+                }
+            };
+
+            const uint32_t u0 = s_run * MT + mt;
+            Ring ac{static_cast<int>(u0 % ACC_BUFS), (u0 / ACC_BUFS) & 1u};
+            const bool fetch_shared = p.theta_g && valid && (MT == 2 || idx == 0);
+            int shared_next = TAU_OPEN;
+            constexpr int HC = COLS / 64;  // 32-column chunks per half accumulator slice
+            int va[HC][32], vb[HC][32];
+            auto taddr_of = [&](uint32_t buf) { return tmem + (static_cast<uint32_t>(q4 * 32) << 16) + buf * STAGE_DOCS + col0; };
+            if (sg.cnt > 0) {
+                mbar_wait_prof(&acc_full[ac.idx], ac.phase, prof, w0);
+                fence_after();
+#pragma unroll
+                for (int c = 0; c < HC; ++c) tmem_ld32(taddr_of(ac.idx) + c * 32, va[c]);
+            }
+            // software pipeline over half slices: one half is filtered while the other is in flight from tensor
+            // memory; the buffer goes back to the issuer as soon as its second half is in registers
+            for (int i = 0; i < sg.cnt; ++i) {
+                const uint32_t buf = ac.idx;
+                const uint32_t taddr = taddr_of(buf);
+                const uint32_t doc0 = static_cast<uint32_t>(sg.sd0 + i) * STAGE_DOCS + col0;
+                if ((i & 3) == 0) {  // thresholds other CTAs found: fetched four stages ahead of their use
+                    if (shared_next > theta) atomicMax(&theta_s[qloc], shared_next);
+                    if (fetch_shared) shared_next = __ldcg(p.theta_g + myq);
+                }
+                theta = theta_s[qloc];
+                tmem_ld_wait();
+#pragma unroll
+                for (int c = 0; c < HC; ++c) tmem_ld32(taddr + (HC + c) * 32, vb[c]);
+                if (!(p.debug & 4)) {
+#pragma unroll
+                    for (int c = 0; c < HC; ++c) filter(va[c], doc0 + c * 32);
+                }
+                tmem_ld_wait();
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[buf]);
+#pragma unroll
+                for (int a = 0; a < MT; ++a) ac.advance(ACC_BUFS);
+                if (i + 1 < sg.cnt) {
+                    mbar_wait_prof(&acc_full[ac.idx], ac.phase, prof, w0);
+                    fence_after();
+#pragma unroll
+                    for (int c = 0; c < HC; ++c) tmem_ld32(taddr_of(ac.idx) + c * 32, va[c]);
+                }
+                if (!(p.debug & 4)) {
+#pragma unroll
+                    for (int c = 0; c < HC; ++c) filter(vb[c], doc0 + (HC + c) * 32);
+                }
+            }
+            tmem_ld_wait();
+            __syncwarp();
+            if (lane == 0) { __threadfence_block(); atomicAdd(&done_s[res], 1); }
+            s_run += static_cast<uint32_t>(sg.cnt);
+            cta_sync();
+        }
+        if (prof && threadIdx.x == 0) {
+            unsigned long long *o = p.prof + blockIdx.x * 8;
+            o[0] = w0; o[1] = w1; o[6] = clock64() - t_begin; o[7] = s_run;
+        }
+    } else if (warp == Q_MMA_WARP) {
+        // ================================ MMA issuer ================================
+        const uint32_t b_lo0 = desc_lo(smem_u32(sB));
+        const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+        while (sg.next()) {
+            cta_sync();
+            fence_after();
+            Ring rb{static_cast<int>(s_run % NS), (s_run / NS) & 1u};
+            const uint32_t u0 = s_run * MT;
+            Ring ac{static_cast<int>(u0 % ACC_BUFS), ((u0 / ACC_BUFS) & 1u) ^ 1u};
+            for (int i = 0; i < sg.cnt; ++i) {
+                mbar_wait_prof(&b_full[rb.idx], rb.phase, prof, w0);
+                fence_after();
+                const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const uint32_t buf = ac.idx;
+                    mbar_wait_prof(&acc_empty[buf], ac.phase, prof, w1);
+                    fence_after();
+                    if (elect_one()) {
+                        const uint32_t d = tm + buf * STAGE_DOCS;
+#pragma unroll
+                        for (int ks = 0; ks < KSTEPS; ++ks) {
+                            const uint32_t ta = tm + A_COL0 + mt * A_COLS + ks * 8;
+                            const uint32_t bo = ((ks >> 2) * (STAGE_DOCS * 128) + (ks & 3) * 32) >> 4;
+                            if (ks == 0) umma_i8<false>(d, ta, b_lo + bo);
+                            else umma_i8<true>(d, ta, b_lo + bo);
+                        }
+                        umma_commit(&acc_full[buf]);
+                    }
+                    __syncwarp();
+                    ac.advance(ACC_BUFS);
+                }
+                if (elect_one()) umma_commit(&b_empty[rb.idx]);
+                __syncwarp();
+                rb.advance(NS);
+            }
+            s_run += static_cast<uint32_t>(sg.cnt);
+            cta_sync();
+        }
+        if (prof && lane == 0) { p.prof[blockIdx.x * 8 + 2] = w0; p.prof[blockIdx.x * 8 + 3] = w1; }
+    } else if (warp == Q_TMA_WARP) {
+        // ================================ loader ================================
+        const unsigned char *db = reinterpret_cast<const unsigned char *>(p.db);
+        while (sg.next()) {
+            cta_sync();
+            if (lane == 0) {
+                Ring rb{static_cast<int>(s_run % NS), ((s_run / NS) & 1u) ^ 1u};
+                for (int i = 0; i < sg.cnt; ++i) {
+                    mbar_wait_prof(&b_empty[rb.idx], rb.phase, prof, w0);
+                    mma::mbar_arrive_expect_tx(&b_full[rb.idx], B_STAGE);
+                    mma::tma_bulk_g2s(sB + static_cast<size_t>(rb.idx) * B_STAGE, db + static_cast<int64_t>(sg.sd0 + i) * B_STAGE, B_STAGE, &b_full[rb.idx]);
+                    rb.advance(NS);
+                }
+            }
+            __syncwarp();
+            s_run += static_cast<uint32_t>(sg.cnt);
+            cta_sync();
+        }
+        if (prof && lane == 0) { p.prof[blockIdx.x * 8 + 4] = w0; p.prof[blockIdx.x * 8 + 5] = 0; }
+    } else {
+        // ================================ resolvers ================================
+        const int res = warp - Q_RES0;
+        uint32_t *ring = rings + res * (RING_ROWS * STASH_WORDS);
+        int *hist = reinterpret_cast<int *>(smem + L.hist_off) + res * 256;
+        const uint32_t n_docs = static_cast<uint32_t>(p.n);
+        const uint32_t id_off = static_cast<uint32_t>(p.row_offset);
+        const int cap = p.cap, k = p.k;
+        constexpr int FEEDERS = Q_DRAIN / Q_RESOLVERS;
+        int tail = 0;
+        while (sg.next()) {
+            cta_sync();
+            const int64_t gq0 = static_cast<int64_t>(sg.gr) * NQ_CTA;
+            while (true) {
+                // rows tail .. tail + n - 1 are ready (tickets are handed out in order, rows may land out of order)
+                const int t = tail + lane;
+                const uint32_t *row = ring + (t & (RING_ROWS - 1)) * STASH_WORDS;
+                const bool ready = ld_volatile(reinterpret_cast<const int *>(row + 34)) == t + 1;
+                const unsigned rm = __ballot_sync(0xffffffffu, ready);
+                const int n = rm == 0xffffffffu ? 32 : __ffs(~rm) - 1;
+                if (n == 0) {
+                    if (ld_volatile(&done_s[res]) == FEEDERS && ld_volatile(&head_s[res]) == tail) break;
+                    __nanosleep(100);
+                    continue;
+                }
+                __threadfence_block();
+                bool pend = lane < n;
+                const int q = pend ? static_cast<int>(row[32]) : 0;
+                const uint32_t doc0 = pend ? row[33] : 0u;
+                while (__any_sync(0xffffffffu, pend)) {
+                    // one row per query and round (last claim wins), so a round adds at most 32 keys to a list
+                    if (pend) claim_s[q] = lane;
+                    __syncwarp();
+                    const bool go = pend && claim_s[q] == lane;
+                    if (go) {
+                        const int th = theta_s[q], dqe = dq_s[q];
+                        uint32_t below = 0;  // bit j: score j < threshold
+#pragma unroll
+                        for (int c = 7; c >= 0; --c) {
+                            const uint4 w = *reinterpret_cast<const uint4 *>(row + 4 * c);
+                            below = __funnelshift_l(w.w - static_cast<uint32_t>(th), below, 1);
+                            below = __funnelshift_l(w.z - static_cast<uint32_t>(th), below, 1);
+                            below = __funnelshift_l(w.y - static_cast<uint32_t>(th), below, 1);
+                            below = __funnelshift_l(w.x - static_cast<uint32_t>(th), below, 1);
+                        }
+                        uint32_t hits = ~below;
+                        uint64_t *list = group_lists + static_cast<int64_t>(q) * cap;
+                        int c = cnt_s[q];
+                        while (hits) {
+                            const int j = __ffs(hits) - 1;
+                            hits &= hits - 1;
+                            const uint32_t doc = doc0 + j;
+                            if (doc < n_docs)
+                                list[c++] = (static_cast<uint64_t>(static_cast<uint32_t>(dqe - static_cast<int>(row[j]))) << 32) | (id_off + doc);
+                        }
+                        cnt_s[q] = c;
+                        pend = false;
+                    }
+                    __syncwarp();
+                    unsigned need = __ballot_sync(0xffffffffu, go && cnt_s[q] > cap - 32);
+                    while (need) {  // a list that another row could overflow: keep its k best, tighten its threshold
+                        const int src = __ffs(need) - 1;
+                        need &= need - 1;
+                        const int qc = __shfl_sync(0xffffffffu, q, src);
+                        ++w2;
+                        const uint64_t kth = select_any(group_lists + static_cast<int64_t>(qc) * cap, cnt_s[qc], k, hist, lane);
+                        if (lane == src) {
+                            cnt_s[qc] = k;
+                            const int th = dq_s[qc] - static_cast<int>(kth >> 32);
+                            atomicMax(&theta_s[qc], th);
+                            if (p.theta_g && gq0 + qc < p.nq) atomicMax(p.theta_g + gq0 + qc, th);  // every CTA scanning this query tightens with us
+                        }
+                        __syncwarp();
+                    }
+                }
+                tail += n;
+                if (lane == 0) st_volatile(&tail_s[res], tail);
+            }
+            // ---- emit the lists this resolver owns: <= k best keys each (unsorted), KEY_INF padded
+            {
+                int64_t c_first = (static_cast<int64_t>(sg.gr) * T * G) / W;
+                while (c_first > 0 && c_first * W / G > static_cast<int64_t>(sg.gr) * T) --c_first;
+                while ((c_first + 1) * W / G <= static_cast<int64_t>(sg.gr) * T) ++c_first;
+                const int64_t part = static_cast<int64_t>(blockIdx.x) - c_first;
+                for (int blk = res; blk < NQ_CTA / 32; blk += Q_RESOLVERS) {  // drain warp w feeds resolver w & 1: blocks of 32 queries
+                    for (int ql = 0; ql < 32; ++ql) {
+                        const int qc = blk * 32 + ql;
+                        const int64_t qq = gq0 + qc;
+                        if (qq >= p.nq) break;
+                        int c = cnt_s[qc];
+                        uint64_t *lrow = group_lists + static_cast<int64_t>(qc) * cap;
+                        if (c > k) { select_any(lrow, c, k, hist, lane); c = k; }
+                        __syncwarp();
+                        uint64_t *dst = p.out + (part * p.nq + qq) * k;
+                        for (int e = lane; e < k; e += 32) dst[e] = e < c ? __ldcg(lrow + e) : KEY_INF;
+                    }
+                }
+                __syncwarp();
+            }
+            if (lane == 0) st_volatile(&done_s[res], 0);
+            s_run += static_cast<uint32_t>(sg.cnt);
+            cta_sync();
+        }
+        if (prof && lane == 0 && res == 0) { p.prof[gridDim.x * 8 + blockIdx.x * 4 + 2] = w2; }
     }
     fence_before();
     cta_sync();
