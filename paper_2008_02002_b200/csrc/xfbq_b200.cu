@@ -935,7 +935,7 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
     // lists, not with the documents: give every query group to as few CTAs as keep the chip busy.
     if (seed_scan && env_int("XFBQ_GRID", 0) <= 0) {
         const int64_t per_group = (info.sms + sh.groups - 1) / sh.groups;
-        const int64_t cap_grid = sh.groups * (per_group < env_int("XFBQ_SEED_SPLIT", 1) ? per_group : env_int("XFBQ_SEED_SPLIT", 1));
+        const int64_t cap_grid = sh.groups * (per_group < env_int("XFBQ_SEED_SPLIT", 4) ? per_group : env_int("XFBQ_SEED_SPLIT", 4));
         if (grid > cap_grid) grid = cap_grid;
     }
     if (grid > W) grid = W;
@@ -982,8 +982,11 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     const int MT = (C == 4 || nq <= 128) ? 1 : 2;
     umma_shape(n, C, nq, k, MT, info, &pl.main);
     if (pl.main.NS == 0) return XFBQ_OK;
+    // Sample scan that seeds the thresholds (measured on 10M x 256, 10k queries: 16k documents split over at
+    // most 4 CTAs per query group balance its cost -- it starts from open lists -- against the rows the main
+    // scan's resolvers then have to handle).
     int64_t sample = env_int("XFBQ_SAMPLE", -1);
-    if (sample < 0) sample = 131072;
+    if (sample < 0) { sample = 16384; while (sample < 64 * static_cast<int64_t>(k)) sample <<= 1; }
     if (sample > 0 && (n < 16 * sample || sample < 4 * k)) sample = 0;
     pl.sample = sample;
     if (sample) umma_shape(sample, C, nq, k, MT, info, &pl.pre, true);
