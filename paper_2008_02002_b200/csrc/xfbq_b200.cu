@@ -953,7 +953,7 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
     }
     sh.slots = slots;
     sh.parts = slots * sh.DW;
-    int NS = env_int("XFBQ_UMMA_STAGES", 6);
+    int NS = env_int("XFBQ_UMMA_STAGES", 5);
     const size_t budget = static_cast<size_t>(info.smem_optin);
     auto smem_need = [&](int ns) { return static_cast<size_t>(sh.queue ? umma::q_smem_layout(C, ns).total : umma::smem_layout(C, MT, ns).total); };
     while (NS > 2 && smem_need(NS) > budget) --NS;

@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
 // ================================================================================================
 constexpr int Q_DRAIN = 8, Q_MMA_WARP = 8, Q_TMA_WARP = 9, Q_RES0 = 10, Q_RESOLVERS = 2;
 constexpr int Q_THREADS = (Q_DRAIN + 2 + Q_RESOLVERS) * 32;  // 12 warps -> 168 registers per thread
-constexpr int RING_ROWS = 64;                                 // parked rows per resolver (power of two)
+constexpr int RING_ROWS = 32;                                 // parked rows per drain warp (one vote can park 32)
 constexpr int STASH_WORDS = 36;                               // a parked row: 32 scores, query, first document, ticket, pad (144 B)
 
 struct QSmemLayout {
@@ -602,7 +602,7 @@ __host__ __device__ inline QSmemLayout q_smem_layout(int C, int NS) {
     QSmemLayout L;
     uint32_t off = 0;
     L.b_off = off; off += static_cast<uint32_t>(NS) * STAGE_DOCS * 128 * C;
-    L.ring_off = off; off += Q_RESOLVERS * RING_ROWS * STASH_WORDS * 4;
+    L.ring_off = off; off += Q_DRAIN * RING_ROWS * STASH_WORDS * 4;
     L.state_off = off; off += 4 * 256 * 4 + 64;  // per query: count, threshold, Dq, claim; ring heads / tails / done
     L.hist_off = off; off += Q_RESOLVERS * 256 * 4;
     L.bar_off = off; off += (2 * NS + 2 * ACC_BUFS) * 8 + 16;
@@ -628,7 +628,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
     unsigned char *sB = smem + L.b_off;
     uint32_t *rings = reinterpret_cast<uint32_t *>(smem + L.ring_off);
     int *cnt_s = reinterpret_cast<int *>(smem + L.state_off), *theta_s = cnt_s + 256, *dq_s = cnt_s + 512, *claim_s = cnt_s + 768;
-    int *head_s = cnt_s + 1024, *tail_s = head_s + Q_RESOLVERS, *done_s = tail_s + Q_RESOLVERS;
+    int *tail_s = cnt_s + 1024, *fin_s = tail_s + Q_DRAIN;  // per drain warp: rows consumed by its resolver; final ticket of a segment
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L.bar_off);
     uint64_t *b_full = bars, *b_empty = bars + NS, *acc_full = bars + 2 * NS, *acc_empty = bars + 2 * NS + ACC_BUFS;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 2 * ACC_BUFS);
@@ -643,9 +643,9 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
         for (int i = 0; i < NS; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
         for (int i = 0; i < ACC_BUFS; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], EPI_PER_BUF); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int r = 0; r < Q_RESOLVERS; ++r) { head_s[r] = 0; tail_s[r] = 0; done_s[r] = 0; }
+        for (int w = 0; w < Q_DRAIN; ++w) { tail_s[w] = 0; fin_s[w] = -1; }
     }
-    for (int i = threadIdx.x; i < Q_RESOLVERS * RING_ROWS; i += Q_THREADS) rings[i * STASH_WORDS + 34] = 0u;  // no ticket yet
+    for (int i = threadIdx.x; i < Q_DRAIN * RING_ROWS; i += Q_THREADS) rings[i * STASH_WORDS + 34] = 0u;  // no ticket yet
     if (warp == 0) tmem_alloc(tmem_slot, 512);
     fence_before();
     cta_sync();
@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
     const uint32_t tmem = *tmem_slot;
     uint32_t s_run = 0;
     const bool prof = p.prof != nullptr;
-    long long w0 = 0, w1 = 0;
+    long long w0 = 0, w1 = 0, w3 = 0;
     int w2 = 0;
     const long long t_begin = prof ? clock64() : 0;
     uint64_t *group_lists = p.lists + static_cast<int64_t>(blockIdx.x) * NQ_CTA * static_cast<int64_t>(p.cap);
@@ -664,8 +664,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
         const int mt = MT == 2 ? idx : 0;
         const int col0 = MT == 2 ? 0 : idx * COLS;
         const int qloc = mt * 128 + q4 * 32 + lane;   // this thread's query inside the group
-        const int res = warp & 1;                     // the resolver that owns these queries' lists
-        uint32_t *ring = rings + res * (RING_ROWS * STASH_WORDS);
+        uint32_t *ring = rings + warp * (RING_ROWS * STASH_WORDS);  // this warp's ring; resolver (warp & 1) owns its queries' lists
+        int head = 0, tail_seen = 0;                  // tickets handed out (warp-uniform) / consumption last observed
         while (sg.next()) {
             const int64_t myq = static_cast<int64_t>(sg.gr) * NQ_CTA + qloc;
             const bool valid = myq < p.nq;
@@ -692,10 +692,13 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                 if (hm) {
                     ++w1;
                     const int n = __popc(hm);
-                    int t0 = 0;
-                    if (lane == 0) t0 = atomicAdd(&head_s[res], n);
-                    t0 = __shfl_sync(0xffffffffu, t0, 0);
-                    while (t0 + n - ld_volatile(&tail_s[res]) > RING_ROWS) __nanosleep(40);  // ring full: the resolver is behind
+                    const int t0 = head;
+                    head += n;
+                    if (head - tail_seen > RING_ROWS) {  // maybe full: look at the resolver's progress, wait if it is behind
+                        const long long tw = prof ? clock64() : 0;
+                        while (head - (tail_seen = ld_volatile(&tail_s[warp])) > RING_ROWS) __nanosleep(40);
+                        if (prof) w3 += clock64() - tw;
+                    }
                     if (hit) {
                         const int t = t0 + __popc(hm & ((1u << lane) - 1u));
                         uint32_t *row = ring + (t & (RING_ROWS - 1)) * STASH_WORDS;
@@ -760,13 +763,13 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             }
             tmem_ld_wait();
             __syncwarp();
-            if (lane == 0) { __threadfence_block(); atomicAdd(&done_s[res], 1); }
+            if (lane == 0) { __threadfence_block(); st_volatile(&fin_s[warp], head); }  // every ticket of this segment is out
             s_run += static_cast<uint32_t>(sg.cnt);
             cta_sync();
         }
         if (prof && threadIdx.x == 0) {
             unsigned long long *o = p.prof + blockIdx.x * 8;
-            o[0] = w0; o[1] = w1; o[6] = clock64() - t_begin; o[7] = s_run;
+            o[0] = w0; o[1] = w1; o[5] = w3; o[6] = clock64() - t_begin; o[7] = s_run;
         }
     } else if (warp == Q_MMA_WARP) {
         // ================================ MMA issuer ================================
@@ -827,84 +830,92 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             s_run += static_cast<uint32_t>(sg.cnt);
             cta_sync();
         }
-        if (prof && lane == 0) { p.prof[blockIdx.x * 8 + 4] = w0; p.prof[blockIdx.x * 8 + 5] = 0; }
+        if (prof && lane == 0) { p.prof[blockIdx.x * 8 + 4] = w0; }
     } else {
         // ================================ resolvers ================================
         const int res = warp - Q_RES0;
-        uint32_t *ring = rings + res * (RING_ROWS * STASH_WORDS);
         int *hist = reinterpret_cast<int *>(smem + L.hist_off) + res * 256;
         const uint32_t n_docs = static_cast<uint32_t>(p.n);
         const uint32_t id_off = static_cast<uint32_t>(p.row_offset);
         const int cap = p.cap, k = p.k;
-        constexpr int FEEDERS = Q_DRAIN / Q_RESOLVERS;
-        int tail = 0;
         while (sg.next()) {
             cta_sync();
             const int64_t gq0 = static_cast<int64_t>(sg.gr) * NQ_CTA;
             while (true) {
-                // rows tail .. tail + n - 1 are ready (tickets are handed out in order, rows may land out of order)
-                const int t = tail + lane;
-                const uint32_t *row = ring + (t & (RING_ROWS - 1)) * STASH_WORDS;
-                const bool ready = ld_volatile(reinterpret_cast<const int *>(row + 34)) == t + 1;
-                const unsigned rm = __ballot_sync(0xffffffffu, ready);
-                const int n = rm == 0xffffffffu ? 32 : __ffs(~rm) - 1;
-                if (n == 0) {
-                    if (ld_volatile(&done_s[res]) == FEEDERS && ld_volatile(&head_s[res]) == tail) break;
-                    __nanosleep(100);
-                    continue;
-                }
-                __threadfence_block();
-                bool pend = lane < n;
-                const int q = pend ? static_cast<int>(row[32]) : 0;
-                const uint32_t doc0 = pend ? row[33] : 0u;
-                while (__any_sync(0xffffffffu, pend)) {
-                    // one row per query and round (last claim wins), so a round adds at most 32 keys to a list
-                    if (pend) claim_s[q] = lane;
-                    __syncwarp();
-                    const bool go = pend && claim_s[q] == lane;
-                    if (go) {
-                        const int th = theta_s[q], dqe = dq_s[q];
-                        uint32_t below = 0;  // bit j: score j < threshold
-#pragma unroll
-                        for (int c = 7; c >= 0; --c) {
-                            const uint4 w = *reinterpret_cast<const uint4 *>(row + 4 * c);
-                            below = __funnelshift_l(w.w - static_cast<uint32_t>(th), below, 1);
-                            below = __funnelshift_l(w.z - static_cast<uint32_t>(th), below, 1);
-                            below = __funnelshift_l(w.y - static_cast<uint32_t>(th), below, 1);
-                            below = __funnelshift_l(w.x - static_cast<uint32_t>(th), below, 1);
-                        }
-                        uint32_t hits = ~below;
-                        uint64_t *list = group_lists + static_cast<int64_t>(q) * cap;
-                        int c = cnt_s[q];
-                        while (hits) {
-                            const int j = __ffs(hits) - 1;
-                            hits &= hits - 1;
-                            const uint32_t doc = doc0 + j;
-                            if (doc < n_docs)
-                                list[c++] = (static_cast<uint64_t>(static_cast<uint32_t>(dqe - static_cast<int>(row[j]))) << 32) | (id_off + doc);
-                        }
-                        cnt_s[q] = c;
-                        pend = false;
+                bool progressed = false;
+                bool all_done = true;
+#pragma unroll 1
+                for (int w = res; w < Q_DRAIN; w += Q_RESOLVERS) {  // the rings of the drain warps this resolver serves
+                    uint32_t *ring = rings + w * (RING_ROWS * STASH_WORDS);
+                    const int tail = tail_s[w];
+                    // rows tail .. tail + n - 1 are ready (tickets are handed out in order, rows may land out of order)
+                    const int t = tail + lane;
+                    const uint32_t *row = ring + (t & (RING_ROWS - 1)) * STASH_WORDS;
+                    const bool ready = ld_volatile(reinterpret_cast<const int *>(row + 34)) == t + 1;
+                    const unsigned rm = __ballot_sync(0xffffffffu, ready);
+                    const int n = rm == 0xffffffffu ? 32 : __ffs(~rm) - 1;
+                    if (n == 0) {
+                        if (ld_volatile(&fin_s[w]) != tail) all_done = false;
+                        continue;
                     }
-                    __syncwarp();
-                    unsigned need = __ballot_sync(0xffffffffu, go && cnt_s[q] > cap - 32);
-                    while (need) {  // a list that another row could overflow: keep its k best, tighten its threshold
-                        const int src = __ffs(need) - 1;
-                        need &= need - 1;
-                        const int qc = __shfl_sync(0xffffffffu, q, src);
-                        ++w2;
-                        const uint64_t kth = select_any(group_lists + static_cast<int64_t>(qc) * cap, cnt_s[qc], k, hist, lane);
-                        if (lane == src) {
-                            cnt_s[qc] = k;
-                            const int th = dq_s[qc] - static_cast<int>(kth >> 32);
-                            atomicMax(&theta_s[qc], th);
-                            if (p.theta_g && gq0 + qc < p.nq) atomicMax(p.theta_g + gq0 + qc, th);  // every CTA scanning this query tightens with us
+                    progressed = true;
+                    all_done = false;
+                    __threadfence_block();
+                    bool pend = lane < n;
+                    const int q = pend ? static_cast<int>(row[32]) : 0;
+                    const uint32_t doc0 = pend ? row[33] : 0u;
+                    while (__any_sync(0xffffffffu, pend)) {
+                        // one row per query and round (last claim wins), so a round adds at most 32 keys to a list
+                        if (pend) claim_s[q] = lane;
+                        __syncwarp();
+                        const bool go = pend && claim_s[q] == lane;
+                        if (go) {
+                            const int th = theta_s[q], dqe = dq_s[q];
+                            uint32_t below = 0;  // bit j: score j < threshold
+#pragma unroll
+                            for (int c = 7; c >= 0; --c) {
+                                const uint4 sw = *reinterpret_cast<const uint4 *>(row + 4 * c);
+                                below = __funnelshift_l(sw.w - static_cast<uint32_t>(th), below, 1);
+                                below = __funnelshift_l(sw.z - static_cast<uint32_t>(th), below, 1);
+                                below = __funnelshift_l(sw.y - static_cast<uint32_t>(th), below, 1);
+                                below = __funnelshift_l(sw.x - static_cast<uint32_t>(th), below, 1);
+                            }
+                            uint32_t hits = ~below;
+                            uint64_t *list = group_lists + static_cast<int64_t>(q) * cap;
+                            int c = cnt_s[q];
+                            while (hits) {
+                                const int j = __ffs(hits) - 1;
+                                hits &= hits - 1;
+                                const uint32_t doc = doc0 + j;
+                                if (doc < n_docs)
+                                    list[c++] = (static_cast<uint64_t>(static_cast<uint32_t>(dqe - static_cast<int>(row[j]))) << 32) | (id_off + doc);
+                            }
+                            cnt_s[q] = c;
+                            pend = false;
                         }
                         __syncwarp();
+                        unsigned need = __ballot_sync(0xffffffffu, go && cnt_s[q] > cap - 32);
+                        while (need) {  // a list that another row could overflow: keep its k best, tighten its threshold
+                            const int src = __ffs(need) - 1;
+                            need &= need - 1;
+                            const int qc = __shfl_sync(0xffffffffu, q, src);
+                            ++w2;
+                            const uint64_t kth = select_any(group_lists + static_cast<int64_t>(qc) * cap, cnt_s[qc], k, hist, lane);
+                            if (lane == src) {
+                                cnt_s[qc] = k;
+                                const int th = dq_s[qc] - static_cast<int>(kth >> 32);
+                                atomicMax(&theta_s[qc], th);
+                                if (p.theta_g && gq0 + qc < p.nq) atomicMax(p.theta_g + gq0 + qc, th);  // every CTA scanning this query tightens with us
+                            }
+                            __syncwarp();
+                        }
                     }
+                    __syncwarp();
+                    if (lane == 0) st_volatile(&tail_s[w], tail + n);
+                    __syncwarp();
                 }
-                tail += n;
-                if (lane == 0) st_volatile(&tail_s[res], tail);
+                if (all_done) break;
+                if (!progressed) __nanosleep(100);
             }
             // ---- emit the lists this resolver owns: <= k best keys each (unsorted), KEY_INF padded
             {
@@ -927,7 +938,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                 }
                 __syncwarp();
             }
-            if (lane == 0) st_volatile(&done_s[res], 0);
+            if (lane < Q_DRAIN && (lane % Q_RESOLVERS) == res) st_volatile(&fin_s[lane], -1);  // next segment's tickets are not out yet
             s_run += static_cast<uint32_t>(sg.cnt);
             cta_sync();
         }

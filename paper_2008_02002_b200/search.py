@@ -145,7 +145,21 @@ def search(index: Index, queries, k: int):
     d, i = unpack_keys_device(keys)
     if _is_torch(queries) and queries.is_cuda:
         return d, i
-    return d.cpu().numpy(), i.cpu().numpy()
+    return to_host_arrays(d, i)
+
+
+def to_host_arrays(*tensors):
+    """Device tensors -> numpy arrays through pinned staging buffers (torch's caching host allocator
+    recycles them), all copies in flight together, one stream synchronisation."""
+    torch = _native.require_cuda()
+    if not tensors:
+        return ()
+    with torch.cuda.device(tensors[0].device):
+        host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in tensors]
+        for h, t in zip(host, tensors):
+            h.copy_(t, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    return tuple(h.numpy() for h in host)
 
 
 def _originals_device(index: Index):

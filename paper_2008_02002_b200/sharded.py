@@ -99,5 +99,11 @@ class ShardedIndex:
 
     def search(self, queries, k: int):
         """(scores, indices) as int64 numpy arrays [nq, min(k, n_total)], identical on all ranks."""
-        keys = self.search_keys(queries, k).cpu().numpy().view(np.uint64)
-        return (keys >> np.uint64(32)).astype(np.int64), (keys & np.uint64(0xFFFFFFFF)).astype(np.int64)
+        keys = self.search_keys(queries, k)
+        if not keys.is_cuda:  # CPU hooks (tests/test_sharded_gloo.py): unpack on the host
+            kn = keys.numpy().view(np.uint64)
+            return (kn >> np.uint64(32)).astype(np.int64), (kn & np.uint64(0xFFFFFFFF)).astype(np.int64)
+        from .search import to_host_arrays, unpack_keys_device
+        d, i = unpack_keys_device(keys)  # empty slots come back as -1
+        d, i = to_host_arrays(d, i)
+        return d, i

@@ -38,7 +38,7 @@ tot = c[:, 6].mean()
 st = c[:, 7].mean()
 print(f"kernel {ms:.3f} ms; per CTA: {tot / 1e6:.2f} Mclk, {st:.0f} stages, {tot / st:.0f} clk/stage")
 names = ["epi wait acc_full", "epi slow-path chunks (warp 0)", "mma wait b_full", "mma wait acc_empty", "prod wait b_empty",
-         "prod store time"]
+         "drain wait ring full (warp 0)"]
 for i, nm in enumerate(names):
     if i == 1:
         print(f"  {nm:34s} {c[:, i].mean():12.0f}  ({c[:, i].mean() / (st * 4) * 100:.1f}% of chunks)")
