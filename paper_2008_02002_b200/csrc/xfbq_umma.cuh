@@ -590,9 +590,9 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
 // kernel above, still used for the open-threshold sample scans, ran at a third of its no-hit speed);
 // here the accumulator hand-off takes the same time whatever the scores are.
 // ================================================================================================
-constexpr int Q_DRAIN = 8, Q_MMA_WARP = 8, Q_TMA_WARP = 9, Q_RES0 = 10, Q_RESOLVERS = 2;
-constexpr int Q_THREADS = (Q_DRAIN + 2 + Q_RESOLVERS) * 32;  // 12 warps -> 168 registers per thread
-constexpr int RING_ROWS = 32;                                 // parked rows per drain warp (one vote can park 32)
+constexpr int Q_DRAIN = 12, Q_MMA_WARP = 12, Q_TMA_WARP = 13, Q_RES0 = 14, Q_RESOLVERS = 2;
+constexpr int Q_THREADS = (Q_DRAIN + 2 + Q_RESOLVERS) * 32;  // 16 warps -> 128 registers per thread (four resolvers would cap it at 96: measured slower)
+constexpr int RING_ROWS = 64;                                 // parked rows per drain warp (one vote can park 32)
 constexpr int STASH_WORDS = 36;                               // a parked row: 32 scores, query, first document, ticket, pad (144 B)
 
 struct QSmemLayout {
@@ -603,7 +603,7 @@ __host__ __device__ inline QSmemLayout q_smem_layout(int C, int NS) {
     uint32_t off = 0;
     L.b_off = off; off += static_cast<uint32_t>(NS) * STAGE_DOCS * 128 * C;
     L.ring_off = off; off += Q_DRAIN * RING_ROWS * STASH_WORDS * 4;
-    L.state_off = off; off += 4 * 256 * 4 + 64;  // per query: count, threshold, Dq, claim; ring heads / tails / done
+    L.state_off = off; off += 4 * 256 * 4 + 2 * Q_DRAIN * 4 + 32;  // per query: count, threshold, Dq, claim; per drain warp: tail, final ticket
     L.hist_off = off; off += Q_RESOLVERS * 256 * 4;
     L.bar_off = off; off += (2 * NS + 2 * ACC_BUFS) * 8 + 16;
     L.total = off + 1024;
@@ -616,8 +616,7 @@ template <int C, int MT>
 __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p) {
     constexpr int B_STAGE = STAGE_DOCS * 128 * C;
     constexpr int KSTEPS = 4 * C;
-    constexpr int COLS = MT == 2 ? 128 : 64;
-    constexpr int EPI_PER_BUF = MT == 2 ? 4 : 8;
+    constexpr int EPI_PER_BUF = 4;                    // the four drain warps (lane quarters) of a buffer's set
     constexpr int A_COLS = 32 * C;
     constexpr int NQ_CTA = 128 * MT;                  // queries of one group
     extern __shared__ unsigned char smem_unaligned[];
@@ -660,18 +659,22 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
 
     if (warp < Q_DRAIN) {
         // ================================ drain ================================
-        const int q4 = warp & 3, idx = warp >> 2;
-        const int mt = MT == 2 ? idx : 0;
-        const int col0 = MT == 2 ? 0 : idx * COLS;
-        const int qloc = mt * 128 + q4 * 32 + lane;   // this thread's query inside the group
-        uint32_t *ring = rings + warp * (RING_ROWS * STASH_WORDS);  // this warp's ring; resolver (warp & 1) owns its queries' lists
+        // Drain warps keep no per-query state (thresholds live in shared memory, lists belong to the
+        // resolvers), so accumulators are dealt to them round-robin: the four warps (one per TMEM lane
+        // quarter) of set j serve accumulator buffer j, whichever query tile it holds.  Three sets give
+        // every warp three MMA group times per accumulator.
+        const int q4 = warp & 3, set = warp >> 2;
+        uint32_t *ring = rings + warp * (RING_ROWS * STASH_WORDS);  // this warp's ring; resolver (q4 & 1) owns its queries' lists
         int head = 0, tail_seen = 0;                  // tickets handed out (warp-uniform) / consumption last observed
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
         while (sg.next()) {
-            const int64_t myq = static_cast<int64_t>(sg.gr) * NQ_CTA + qloc;
-            const bool valid = myq < p.nq;
-            if (MT == 2 || idx == 0) {  // query row -> tensor memory; the query's shared state
+            if (warp < 4 * MT) {  // query rows -> tensor memory; the queries' shared state
+                const int mt = warp >> 2;
+                const int qloc = mt * 128 + q4 * 32 + lane;
+                const int64_t myq = static_cast<int64_t>(sg.gr) * NQ_CTA + qloc;
+                const bool valid = myq < p.nq;
                 const uint4 *src = reinterpret_cast<const uint4 *>(p.qimg + myq * (128 * C));
-                const uint32_t ta = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + A_COL0 + mt * A_COLS;
+                const uint32_t ta = lane_base + A_COL0 + mt * A_COLS;
 #pragma unroll
                 for (int c = 0; c < A_COLS / 8; ++c) tmem_st8(ta + c * 8, __ldg(src + 2 * c), __ldg(src + 2 * c + 1));
                 tmem_st_wait();
@@ -681,11 +684,10 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             }
             fence_before();
             cta_sync();
-            int theta = theta_s[qloc];
 
-            // 32 scores of this thread's query row: 3-input max tree, one compare, one vote; a row whose
-            // maximum passes is parked for the resolver (its scores, its query, its first document, a ticket)
-            auto filter = [&](const int (&v)[32], uint32_t doc0) {
+            // 32 scores of one query row: 3-input max tree, one compare, one vote; a row whose maximum passes is
+            // parked for the resolver (its scores, its query, its first document, a ticket)
+            auto filter = [&](const int (&v)[32], int theta, int qloc, uint32_t doc0) {
                 const int m = max(max(max8(v), max8(v + 8)), max(max8(v + 16), max8(v + 24)));
                 const bool hit = m >= theta;
                 const unsigned hm = __ballot_sync(0xffffffffu, hit);
@@ -696,7 +698,15 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                     head += n;
                     if (head - tail_seen > RING_ROWS) {  // maybe full: look at the resolver's progress, wait if it is behind
                         const long long tw = prof ? clock64() : 0;
-                        while (head - (tail_seen = ld_volatile(&tail_s[warp])) > RING_ROWS) __nanosleep(40);
+#ifdef XFBQ_UMMA_WATCHDOG
+                        const long long wd0 = clock64();
+#endif
+                        while (head - (tail_seen = ld_volatile(&tail_s[warp])) > RING_ROWS) {
+                            __nanosleep(40);
+#ifdef XFBQ_UMMA_WATCHDOG
+                            if (clock64() - wd0 > 4000000000ll) { if (lane == 0) printf("drain %d cta %d stuck: head %d tail %d\n", warp, blockIdx.x, head, tail_seen); __trap(); }
+#endif
+                        }
                         if (prof) w3 += clock64() - tw;
                     }
                     if (hit) {
@@ -713,55 +723,36 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                 }
             };
 
-            const uint32_t u0 = s_run * MT + mt;
-            Ring ac{static_cast<int>(u0 % ACC_BUFS), (u0 / ACC_BUFS) & 1u};
-            const bool fetch_shared = p.theta_g && valid && (MT == 2 || idx == 0);
-            int shared_next = TAU_OPEN;
-            constexpr int HC = COLS / 64;  // 32-column chunks per half accumulator slice
-            int va[HC][32], vb[HC][32];
-            auto taddr_of = [&](uint32_t buf) { return tmem + (static_cast<uint32_t>(q4 * 32) << 16) + buf * STAGE_DOCS + col0; };
-            if (sg.cnt > 0) {
-                mbar_wait_prof(&acc_full[ac.idx], ac.phase, prof, w0);
+            const uint32_t u_begin = s_run * MT, u_end = u_begin + static_cast<uint32_t>(sg.cnt) * MT;
+            uint32_t u = u_begin + (set + ACC_BUFS - u_begin % ACC_BUFS) % ACC_BUFS;  // first accumulator that lands in buffer `set`
+            for (; u < u_end; u += ACC_BUFS) {
+                const uint32_t rel = u - u_begin;
+                const int mt = MT == 2 ? static_cast<int>(rel & 1u) : 0;
+                const int qloc = mt * 128 + q4 * 32 + lane;
+                const uint32_t doc0 = (static_cast<uint32_t>(sg.sd0) + rel / MT) * STAGE_DOCS;
+                const uint32_t taddr = lane_base + set * STAGE_DOCS;
+                const int theta = theta_s[qloc];
+                mbar_wait_prof(&acc_full[set], (u / ACC_BUFS) & 1u, prof, w0);
                 fence_after();
-#pragma unroll
-                for (int c = 0; c < HC; ++c) tmem_ld32(taddr_of(ac.idx) + c * 32, va[c]);
-            }
-            // software pipeline over half slices: one half is filtered while the other is in flight from tensor
-            // memory; the buffer goes back to the issuer as soon as its second half is in registers
-            for (int i = 0; i < sg.cnt; ++i) {
-                const uint32_t buf = ac.idx;
-                const uint32_t taddr = taddr_of(buf);
-                const uint32_t doc0 = static_cast<uint32_t>(sg.sd0 + i) * STAGE_DOCS + col0;
-                if ((i & 3) == 0) {  // thresholds other CTAs found: fetched four stages ahead of their use
-                    if (shared_next > theta) atomicMax(&theta_s[qloc], shared_next);
-                    if (fetch_shared) shared_next = __ldcg(p.theta_g + myq);
-                }
-                theta = theta_s[qloc];
-                tmem_ld_wait();
-#pragma unroll
-                for (int c = 0; c < HC; ++c) tmem_ld32(taddr + (HC + c) * 32, vb[c]);
+                int v[2][32];
                 if (!(p.debug & 4)) {
-#pragma unroll
-                    for (int c = 0; c < HC; ++c) filter(va[c], doc0 + c * 32);
+                    tmem_ld32(taddr, v[0]);
+                    tmem_ld32(taddr + 32, v[1]);
+                    tmem_ld_wait();
+                    filter(v[0], theta, qloc, doc0);
+                    filter(v[1], theta, qloc, doc0 + 32);
+                    tmem_ld32(taddr + 64, v[0]);
+                    tmem_ld32(taddr + 96, v[1]);
+                    tmem_ld_wait();
                 }
-                tmem_ld_wait();
-                fence_before();
+                fence_before();  // the accumulator is in registers: hand it back
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&acc_empty[buf]);
-#pragma unroll
-                for (int a = 0; a < MT; ++a) ac.advance(ACC_BUFS);
-                if (i + 1 < sg.cnt) {
-                    mbar_wait_prof(&acc_full[ac.idx], ac.phase, prof, w0);
-                    fence_after();
-#pragma unroll
-                    for (int c = 0; c < HC; ++c) tmem_ld32(taddr_of(ac.idx) + c * 32, va[c]);
-                }
+                if (lane == 0) mbar_arrive(&acc_empty[set]);
                 if (!(p.debug & 4)) {
-#pragma unroll
-                    for (int c = 0; c < HC; ++c) filter(vb[c], doc0 + (HC + c) * 32);
+                    filter(v[0], theta, qloc, doc0 + 64);
+                    filter(v[1], theta, qloc, doc0 + 96);
                 }
             }
-            tmem_ld_wait();
             __syncwarp();
             if (lane == 0) { __threadfence_block(); st_volatile(&fin_s[warp], head); }  // every ticket of this segment is out
             s_run += static_cast<uint32_t>(sg.cnt);
@@ -841,13 +832,17 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
         while (sg.next()) {
             cta_sync();
             const int64_t gq0 = static_cast<int64_t>(sg.gr) * NQ_CTA;
+            int idle = 0;
+#ifdef XFBQ_UMMA_WATCHDOG
+            long long wd0 = clock64();
+#endif
             while (true) {
                 bool progressed = false;
                 bool all_done = true;
 #pragma unroll 1
                 for (int w = res; w < Q_DRAIN; w += Q_RESOLVERS) {  // the rings of the drain warps this resolver serves
                     uint32_t *ring = rings + w * (RING_ROWS * STASH_WORDS);
-                    const int tail = tail_s[w];
+                    const int tail = ld_volatile(&tail_s[w]);
                     // rows tail .. tail + n - 1 are ready (tickets are handed out in order, rows may land out of order)
                     const int t = tail + lane;
                     const uint32_t *row = ring + (t & (RING_ROWS - 1)) * STASH_WORDS;
@@ -915,7 +910,29 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                     __syncwarp();
                 }
                 if (all_done) break;
-                if (!progressed) __nanosleep(100);
+#ifdef XFBQ_UMMA_WATCHDOG
+                if (progressed) wd0 = clock64();
+                else if (clock64() - wd0 > 4000000000ll) {
+                    if (lane == 0) {
+                        printf("resolver %d cta %d stuck:", res, blockIdx.x);
+                        for (int w = res; w < Q_DRAIN; w += Q_RESOLVERS) printf(" [w%d tail %d fin %d flag %d addr %u]", w, tail_s[w], fin_s[w], (int)rings[(w * RING_ROWS + (tail_s[w] & (RING_ROWS - 1))) * STASH_WORDS + 34], smem_u32(&rings[(w * RING_ROWS + (tail_s[w] & (RING_ROWS - 1))) * STASH_WORDS + 34]));
+                        printf("\n");
+                    }
+                    __trap();
+                }
+#endif
+                if (!progressed) {
+                    if (p.theta_g && (++idle & 15) == 0) {  // idle: import the thresholds other CTAs found for our queries
+                        for (int blk = res; blk < NQ_CTA / 32; blk += Q_RESOLVERS) {
+                            const int qc = blk * 32 + lane;
+                            if (gq0 + qc < p.nq) {
+                                const int th = __ldcg(p.theta_g + gq0 + qc);
+                                if (th > theta_s[qc]) atomicMax(&theta_s[qc], th);
+                            }
+                        }
+                    }
+                    __nanosleep(100);
+                }
             }
             // ---- emit the lists this resolver owns: <= k best keys each (unsorted), KEY_INF padded
             {
