@@ -324,7 +324,7 @@ def run_ours(a):
         "gpu_launches": int(launches),
         "clocks": clocks,
         "roofline": {"bound": "tensor",
-                     "kernel": {"umma": "umma::scan_kernel (tcgen05.mma kind::i8, TMEM accumulators, fused top-K)",
+                     "kernel": {"umma": "umma::scan_queue_kernel (tcgen05.mma kind::i8, operands by TMA, A and accumulators in TMEM, fused top-K)",
                                 "imma": "mma::scan_kernel (batch plan: IMMA.16832 + fused top-K)"}.get(engine, "scan_topk_kernel"),
                      "achieved": round(tops, 1), "peak": round(int8_peak, 1), "unit": "TOP/s (int8, dense)",
                      "frac": round(tops / int8_peak, 4), "traffic": None,

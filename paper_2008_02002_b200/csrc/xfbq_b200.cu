@@ -890,6 +890,7 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
 struct UmmaShape {
     int MT = 2, DW = 1, groups = 1, grid = 1, slots = 1, parts = 1, cap = 0, NS = 0;
     bool queue = false;  // scan_queue_kernel (main scans) vs scan_kernel (sample scans: open thresholds)
+    int n_seg = 1, seg_stages = 0;  // queue kernel: document slices (= partial results per query) and stages per slice
     int64_t stages = 0, nq_pad = 0, n_pad = 0;
     size_t smem = 0, lists_bytes = 0, parts_bytes = 0, mscratch_bytes = 0;
 };
@@ -923,6 +924,10 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
     sh.DW = (MT == 2 || sh.queue) ? 1 : 2;
     int cap = 64;
     while (cap < 2 * k) cap <<= 1;
+    if (sh.queue) {  // resolver-owned lists: a compaction costs a resolver ~cap/32 steps, so let lists run longer
+        const int want = env_int("XFBQ_UMMA_CAP", 0);
+        if (want >= k + 40) cap = (want + 7) & ~7;
+    }
     sh.cap = cap;
     const int64_t qpg = 128 * MT;
     sh.groups = static_cast<int>((nq + qpg - 1) / qpg);
@@ -950,6 +955,29 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
         while (c_last > 0 && c_last * W / grid > hi - 1) --c_last;
         while ((c_last + 1) * W / grid <= hi - 1) ++c_last;
         if (c_last - c_first + 1 > slots) slots = static_cast<int>(c_last - c_first + 1);
+    }
+    if (sh.queue) {
+        // Work items = document slices x query groups, dealt to the CTAs round-robin (umma::Items).  Pick the
+        // slice count that fills whole waves of CTAs; slices stay long enough to amortise the per-item list
+        // start-up and emission.
+        const int64_t min_stages = env_int("XFBQ_UMMA_MIN_SLICE", 512);
+        int best = 1;
+        double best_score = -1.0;
+        for (int S = 1; S <= 256; ++S) {
+            if (S > 1 && (sh.stages + S - 1) / S < min_stages) break;
+            const int64_t items = static_cast<int64_t>(S) * sh.groups;
+            const int64_t waves = (items + grid - 1) / grid;
+            const double score = static_cast<double>(items) / static_cast<double>(waves * grid) - 0.0005 * S;
+            if (score > best_score) { best_score = score; best = S; }
+        }
+        if (env_int("XFBQ_UMMA_SLICES", 0) > 0) best = env_int("XFBQ_UMMA_SLICES", 0);
+        if (best > sh.stages) best = static_cast<int>(sh.stages);
+        sh.n_seg = best;
+        sh.seg_stages = static_cast<int>((sh.stages + best - 1) / best);
+        sh.n_seg = static_cast<int>((sh.stages + sh.seg_stages - 1) / sh.seg_stages);  // no empty slices
+        const int64_t items = static_cast<int64_t>(sh.n_seg) * sh.groups;
+        if (sh.grid > items) sh.grid = static_cast<int>(items);
+        slots = sh.n_seg;
     }
     sh.slots = slots;
     sh.parts = slots * sh.DW;
@@ -1021,9 +1049,10 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     p.out = reinterpret_cast<uint64_t *>(ws + pl.off_parts);
     p.nq = nq; p.stages = sh.stages; p.groups = sh.groups;
     p.k = k; p.cap = sh.cap; p.NS = sh.NS;
+    p.n_seg = sh.n_seg; p.seg_stages = sh.seg_stages;
     p.prof = (&sh == &pl.main) ? g_prof : nullptr;
     p.debug = env_int("XFBQ_UMMA_DEBUG", 0);
-    if (sh.slots > 1) {  // slots a group does not use stay KEY_INF
+    if (sh.slots > 1 && !sh.queue) {  // slots a group does not use stay KEY_INF (the queue kernel writes every slice)
         e = cudaMemsetAsync(p.out, 0xFF, sh.parts_bytes, st);
         if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
     }
