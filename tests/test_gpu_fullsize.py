@@ -73,3 +73,24 @@ def test_single_query_and_other_plans_agree(corpus, monkeypatch):
     monkeypatch.setenv("XFBQ_SPLITS", "5")
     s2, i2 = xb.search(idx, queries, K)
     assert torch.equal(s2, base_s) and torch.equal(i2, base_i)
+
+
+def test_batch_engines_agree_at_full_size(corpus, monkeypatch):
+    """640 queries at full n: the tcgen05 engine (sample scan + queue kernel over document slices) equals the
+    mma.sync engine and the POPC route checked above, bit for bit."""
+    import torch
+    idx, queries, params, rows, sample = corpus
+    g = torch.Generator(device="cuda").manual_seed(4100)
+    q = torch.randn((640, DIM), generator=g, device="cuda", dtype=torch.float32)
+    q /= q.norm(dim=1, keepdim=True)
+    monkeypatch.setenv("XFBQ_ENGINE", "umma")
+    su, iu = xb.search(idx, q, K)
+    monkeypatch.setenv("XFBQ_ENGINE", "imma")
+    si, ii = xb.search(idx, q, K)
+    assert torch.equal(su, si) and torch.equal(iu, ii)
+    k64 = (su << 32) | iu
+    assert bool((k64[:, 1:] > k64[:, :-1]).all())
+    base_s, base_i = xb.search(idx, queries, K)
+    monkeypatch.setenv("XFBQ_ENGINE", "umma")
+    s2, i2 = xb.search(idx, queries, K)
+    assert torch.equal(s2, base_s) and torch.equal(i2, base_i)

@@ -135,7 +135,10 @@ def test_synthetic_configs_match_reference(name):
 @pytest.mark.parametrize("env", [{"XFBQ_FORCE_GENERIC": "1"}, {"XFBQ_GRID": "1"}, {"XFBQ_GRID": "7"},
                                  {"XFBQ_SAMPLE": "0"}, {"XFBQ_SAMPLE": "2048"}, {"XFBQ_SAMPLE": "2048", "XFBQ_GRID": "3"},
                                  {"XFBQ_ENGINE": "popc"}, {"XFBQ_ENGINE": "popc", "XFBQ_TQ": "1"},
-                                 {"XFBQ_ENGINE": "popc", "XFBQ_TQ": "5", "XFBQ_SPLITS": "3"}])
+                                 {"XFBQ_ENGINE": "popc", "XFBQ_TQ": "5", "XFBQ_SPLITS": "3"},
+                                 {"XFBQ_ENGINE": "imma"}, {"XFBQ_ENGINE": "umma"}, {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE": "0"},
+                                 {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_SLICES": "7"}, {"XFBQ_ENGINE": "umma", "XFBQ_SAMPLE": "0"},
+                                 {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_STAGES": "2", "XFBQ_GRID": "5"}])
 def test_scan_plans_agree(env, monkeypatch):
     """Every launch plan (generic/specialised kernel, query-tile size, document splits) yields the
     same keys: the order on (distance, id) is total, so the result is partition independent."""
@@ -161,6 +164,27 @@ def test_batch_mode_many_queries(name, nq, k):
     scores, ids = xb.search(idx, queries, k)
     planes = xo.c_quantize_matrix(c["docs"], c["wd"], c["scale"])
     qp = xo.c_quantize_matrix(queries.astype(np.float64), c["wq"], c["scale"]).transpose(2, 0, 1)
+    want_d, want_i = xo.c_search(planes, qp, k)
+    assert np.array_equal(scores.astype(np.uint64), want_d) and np.array_equal(ids, want_i)
+
+
+@pytest.mark.parametrize("engine", ["umma", "imma"])
+@pytest.mark.parametrize("n,dim,wd,nq,k", [(5000, 256, 4, 40, 10), (33333, 128, 3, 130, 7), (12345, 200, 4, 257, 33),
+                                           (9000, 512, 4, 150, 100), (3000, 100, 4, 20, 1000), (40000, 64, 2, 600, 1),
+                                           (70000, 256, 4, 1000, 100)])
+def test_tensor_engines_ragged_shapes(engine, n, dim, wd, nq, k, monkeypatch):
+    """Both tensor engines (tcgen05 with TMEM accumulators / mma.sync IMMA) on ragged shapes: n not a multiple of
+    the 128-document stage, dims that pad to 128, every (C, query-tile) kernel variant, k from 1 to 1000; every
+    query against the CPU oracle."""
+    docs = xo.synthetic_unit_rows(n, dim, 11 + n)
+    queries = xo.synthetic_unit_rows(nq, dim, 12 + n)
+    scale = xo.estimate_scale(docs, 0.98)
+    params = xb.QuantParams(dim=dim, scale=scale, doc_bits=wd, query_bits=4)
+    idx = xb.build_index(docs, params, keep_originals=False)
+    monkeypatch.setenv("XFBQ_ENGINE", engine)
+    scores, ids = xb.search(idx, queries, k)
+    planes = xo.c_quantize_matrix(docs, wd, scale)
+    qp = xo.c_quantize_matrix(queries.astype(np.float64), 4, scale).transpose(2, 0, 1)
     want_d, want_i = xo.c_search(planes, qp, k)
     assert np.array_equal(scores.astype(np.uint64), want_d) and np.array_equal(ids, want_i)
 
