@@ -298,6 +298,18 @@ def run_ours(a):
         return
 
     hbm_peak, bf16_peak, peak_src = peaks()
+    traffic = None  # DRAM bytes of the dominant kernel per launch, from the committed ncu --set full capture of this workload
+    if (a.n, a.dim, a.nq, a.k, a.doc_bits, world) == (10_000_000, 256, 10000, 100, 4, 1):
+        try:
+            import csv
+            with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_full_umma_queue_r1_v10.csv")) as f:
+                rows = list(csv.reader(f))
+            col = {h: i for i, h in enumerate(rows[0])}
+            unit = {h: u for h, u in zip(rows[0], rows[1])}
+            scale_of = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+            traffic = sum(float(rows[2][col[m]]) * scale_of[unit[m]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        except Exception:
+            traffic = None
     launches_per_step = -(-a.nq // xsearch._QUERY_BATCH)
     q_tiles_total = sum(-(-min(xsearch._QUERY_BATCH, a.nq - q0) // int(plan[0])) for q0 in range(0, a.nq, xsearch._QUERY_BATCH))
     algo_bytes_per_launch = db_bytes_local * q_tiles_total / launches_per_step
@@ -327,7 +339,9 @@ def run_ours(a):
                      "kernel": {"umma": "umma::scan_queue_kernel (tcgen05.mma kind::i8, operands by TMA, A and accumulators in TMEM, fused top-K)",
                                 "imma": "mma::scan_kernel (batch plan: IMMA.16832 + fused top-K)"}.get(engine, "scan_topk_kernel"),
                      "achieved": round(tops, 1), "peak": round(int8_peak, 1), "unit": "TOP/s (int8, dense)",
-                     "frac": round(tops / int8_peak, 4), "traffic": None,
+                     "frac": round(tops / int8_peak, 4), "traffic": traffic,
+                     "traffic_source": "profiles/ncu_full_umma_queue_r1_v10.csv (dram__bytes_read.sum + dram__bytes_write.sum of this launch)" if traffic else None,
+                     "frac_of_hw_int8_pipe": round(tops / (2 * 8192 * 148 * 1.965e9 / 1e12), 4),
                      "peak_source": peak_src + ": 2 x dense bf16 burst = int8 rate of the tcgen05 path",
                      "launch_ms": round(kernel_ms, 3), "macs_per_launch": int(macs_per_launch),
                      "legacy_imma_pipe_peak_TOPs": 1163.7, "frac_of_legacy_imma_pipe": round(tops / 1163.7, 4),

@@ -95,9 +95,15 @@ int xfbq_bundles_to_planes(const void *db_dev, int64_t n, int64_t dim, int width
                            uint64_t *planes_out_dev, void *stream);
 
 /*
- * Nibble layout ("tensor layout"): row-major 4-bit codes, 64*C bytes per document (documents
- * rounded up to 32), one 16-byte word per group of 32 dims whose 32-bit word e holds in nibble m
- * the code of dimension 4m + e.  Derived from the bundle layout on the GPU; doc_bits <= 4.
+ * Derived layouts for the tensor-core engines (doc_bits <= 4), one buffer of xfbq_nibble_bytes(n, dim)
+ * bytes filled by xfbq_planes_to_nibbles from the bundle layout on the GPU:
+ *   [nibble layout] row-major 4-bit codes, 64*C bytes per document (documents rounded up to 32), one
+ *                   16-byte word per group of 32 dims whose 32-bit word e holds in nibble m the code of
+ *                   dimension 4m + e (streamed by the mma.sync engine: <= 16 queries, HBM-bound);
+ *   [byte tiles]    (C in {1, 2, 4}) tiles of 128 documents x 128*C bytes, one code per byte, K-major with
+ *                   the 128-byte swizzle: the exact shared-memory image of a tcgen05.mma B operand, copied
+ *                   by one cp.async.bulk per tile (streamed by the tcgen05 engine: >= 17 queries).
+ * The tile region starts at the nibble region's size rounded up to 1024 bytes.
  */
 int64_t xfbq_nibble_bytes(int64_t n, int64_t dim);
 int xfbq_planes_to_nibbles(const void *db_dev, int64_t n, int64_t dim, int width, void *nibbles_out_dev,
@@ -118,17 +124,18 @@ int xfbq_batch_distances(const void *db_dev, int64_t n, int64_t dim, int doc_bit
  * no-originals ranking of k_select (search.py:206-216, :159-172, :129-131).
  * workspace_dev must hold xfbq_scan_workspace_bytes(...) bytes.
  * 1 <= k <= XFBQ_MAX_K;  row_offset + n <= 2^32.
- * nibbles_dev: optional derived copy of the codes in the nibble layout (xfbq_planes_to_nibbles).
- * When given (doc_bits <= 4, query_bits <= 7, dim <= 256 or 385..512, k <= 1024) the scan runs on
- * the integer tensor path (IMMA) with identical results; when NULL, or outside those shapes, the
- * XOR/POPC kernels scan the bit planes.
+ * nibbles_dev: optional derived layouts of the codes (xfbq_planes_to_nibbles).
+ * When given (doc_bits <= 4, query_bits <= 7, dim <= 256 or 385..512, k <= 1024) the scan runs on the
+ * integer tensor path -- tcgen05.mma kind::i8 with accumulators in tensor memory for >= 17 queries,
+ * mma.sync (IMMA) below -- with identical results; when NULL, or outside those shapes, the XOR/POPC
+ * kernels scan the bit planes.  XFBQ_ENGINE=umma|imma|popc forces one engine.
  */
 int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int doc_bits, int64_t nq,
                                   int query_bits, int k, int have_nibbles);
 /* Launch plan xfbq_scan_topk will use on the current device, for reporting:
  * plan_out[0] = queries per CTA tile, [1] = query tiles, [2] = document splits (partial results
- * merged afterwards), [3] = candidate-list capacity per query, [4] = 1 if a width/dim-specialised
- * kernel is used, [5] = dynamic shared memory bytes per CTA. */
+ * merged afterwards), [3] = candidate-list capacity per query, [4] = engine: 3 tcgen05, 2 mma.sync,
+ * 1 specialised POPC kernel, 0 generic POPC kernel, [5] = dynamic shared memory bytes per CTA. */
 int xfbq_scan_plan(int64_t n, int64_t dim, int doc_bits, int64_t nq, int query_bits, int k,
                    int have_nibbles, int32_t plan_out[6]);
 int xfbq_scan_topk(const void *db_dev, const void *nibbles_dev, int64_t n, int64_t dim, int doc_bits,
