@@ -890,6 +890,7 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
 struct UmmaShape {
     int MT = 2, DW = 1, groups = 1, grid = 1, slots = 1, parts = 1, cap = 0, NS = 0;
     bool queue = false;  // scan_queue_kernel (main scans) vs scan_kernel (sample scans: open thresholds)
+    int ring_rows = 64;
     int n_seg = 1, seg_stages = 0;  // queue kernel: document slices (= partial results per query) and stages per slice
     int64_t stages = 0, nq_pad = 0, n_pad = 0;
     size_t smem = 0, lists_bytes = 0, parts_bytes = 0, mscratch_bytes = 0;
@@ -983,7 +984,8 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
     sh.parts = slots * sh.DW;
     int NS = env_int("XFBQ_UMMA_STAGES", 5);
     const size_t budget = static_cast<size_t>(info.smem_optin);
-    auto smem_need = [&](int ns) { return static_cast<size_t>(sh.queue ? umma::q_smem_layout(C, ns).total : umma::smem_layout(C, MT, ns).total); };
+    auto smem_need = [&](int ns) { return static_cast<size_t>(sh.queue ? umma::q_smem_layout(C, ns, sh.ring_rows).total : umma::smem_layout(C, MT, ns).total); };
+    if (sh.queue && smem_need(NS < 3 ? NS : 3) > budget) sh.ring_rows = 32;  // wide documents: shorter rings rather than fewer than three tiles in flight
     while (NS > 2 && smem_need(NS) > budget) --NS;
     sh.NS = smem_need(NS) <= budget ? NS : 0;
     sh.smem = smem_need(NS);
@@ -1049,7 +1051,7 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     p.out = reinterpret_cast<uint64_t *>(ws + pl.off_parts);
     p.nq = nq; p.stages = sh.stages; p.groups = sh.groups;
     p.k = k; p.cap = sh.cap; p.NS = sh.NS;
-    p.n_seg = sh.n_seg; p.seg_stages = sh.seg_stages;
+    p.n_seg = sh.n_seg; p.seg_stages = sh.seg_stages; p.ring_rows = sh.ring_rows;
     p.prof = (&sh == &pl.main) ? g_prof : nullptr;
     p.debug = env_int("XFBQ_UMMA_DEBUG", 0);
     if (sh.slots > 1 && !sh.queue) {  // slots a group does not use stay KEY_INF (the queue kernel writes every slice)

@@ -48,6 +48,7 @@ struct Params {
     uint64_t *out;             // [slots * DW][nq][k], KEY_INF pre-filled when slots > 1
     int64_t nq, stages;
     int groups, k, cap, NS;    // NS = operand stages in shared memory
+    int ring_rows;             // queue kernel: rows of a drain warp's ring (32 or 64)
     int n_seg, seg_stages;     // queue kernel: document slices and stages per slice (work items = n_seg x groups)
     int debug;                 // timing experiments (XFBQ_UMMA_DEBUG): 1 skip operand stores, 2 skip document loads, 4 skip the filter
     unsigned long long *prof;  // optional [grid][8] wait-cycle counters (xfbq_debug_profile), else nullptr
@@ -613,17 +614,17 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
 // ================================================================================================
 constexpr int Q_DRAIN = 12, Q_MMA_WARP = 12, Q_TMA_WARP = 13, Q_RES0 = 14, Q_RESOLVERS = 2;
 constexpr int Q_THREADS = (Q_DRAIN + 2 + Q_RESOLVERS) * 32;  // 16 warps -> 128 registers per thread (four resolvers would cap it at 96: measured slower)
-constexpr int RING_ROWS = 64;                                 // parked rows per drain warp (one vote can park 32)
+constexpr int RING_ROWS_MAX = 64;                             // parked rows per drain warp: Params::ring_rows = 32 or 64 (one vote can park 32)
 constexpr int STASH_WORDS = 36;                               // a parked row: 32 scores, query, first document, ticket, pad (144 B)
 
 struct QSmemLayout {
     uint32_t b_off, ring_off, state_off, hist_off, bar_off, total;
 };
-__host__ __device__ inline QSmemLayout q_smem_layout(int C, int NS) {
+__host__ __device__ inline QSmemLayout q_smem_layout(int C, int NS, int ring_rows) {
     QSmemLayout L;
     uint32_t off = 0;
     L.b_off = off; off += static_cast<uint32_t>(NS) * STAGE_DOCS * 128 * C;
-    L.ring_off = off; off += Q_DRAIN * RING_ROWS * STASH_WORDS * 4;
+    L.ring_off = off; off += Q_DRAIN * ring_rows * STASH_WORDS * 4;
     L.state_off = off; off += 4 * 256 * 4 + 2 * Q_DRAIN * 4 + 32;  // per query: count, threshold, Dq, claim; per drain warp: tail, final ticket
     L.hist_off = off; off += Q_RESOLVERS * 256 * 4;
     L.bar_off = off; off += (2 * NS + 2 * ACC_BUFS) * 8 + 16;
@@ -644,7 +645,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
     const uint32_t pad = (1024u - (smem_u32(smem_unaligned) & 1023u)) & 1023u;
     unsigned char *smem = smem_unaligned + pad;
     const int NS = p.NS;
-    const QSmemLayout L = q_smem_layout(C, NS);
+    const int RING_ROWS = p.ring_rows;
+    const QSmemLayout L = q_smem_layout(C, NS, RING_ROWS);
     unsigned char *sB = smem + L.b_off;
     uint32_t *rings = reinterpret_cast<uint32_t *>(smem + L.ring_off);
     int *cnt_s = reinterpret_cast<int *>(smem + L.state_off), *theta_s = cnt_s + 256, *dq_s = cnt_s + 512, *claim_s = cnt_s + 768;
