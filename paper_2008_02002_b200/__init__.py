@@ -9,13 +9,15 @@ from .bitplane import (PackedMatrix, PackedVector, pack_matrix, quantize_matrix,
                        quantize_vector, unpack_matrix, words_needed)
 from .distance import (batch_distances, decode_inner_product, decode_inner_product_values,
                        distance_upper_bound)
-from .errors import DimensionMismatchError, InvalidInputError, NativeLibraryError, XfbqError
-from .index import Index, QuantParams, build_index, estimate_scale
+from .errors import (BadMagicError, DimensionMismatchError, IndexFormatError, InvalidInputError, NativeLibraryError,
+                     TruncatedIndexError, UnsupportedVersionError, XfbqError)
+from .index import Index, QuantParams, build_index, estimate_scale, load_index, save_index
 from .sharded import ShardedIndex, shard_bounds
 from .search import SearchRequest, SearchResult, k_select, search, search_device
 
 __version__ = "0.1.0"
 __all__ = [
+    "BadMagicError", "IndexFormatError", "TruncatedIndexError", "UnsupportedVersionError", "load_index", "save_index",
     "DimensionMismatchError", "Index", "InvalidInputError", "NativeLibraryError", "PackedMatrix",
     "PackedVector", "QuantParams", "SearchRequest", "SearchResult", "XfbqError", "batch_distances",
     "build_index", "decode_inner_product", "decode_inner_product_values", "distance_upper_bound",
