@@ -761,8 +761,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                     tmem_ld32(taddr + 32, v[1]);
                     tmem_ld_wait();
                     filter(v[0], theta, qloc, doc0);
+                    tmem_ld32(taddr + 64, v[0]);   // in flight while the second chunk is filtered
                     filter(v[1], theta, qloc, doc0 + 32);
-                    tmem_ld32(taddr + 64, v[0]);
                     tmem_ld32(taddr + 96, v[1]);
                     tmem_ld_wait();
                 }
