@@ -725,6 +725,7 @@ MmaKernel pick_mma_kernel(int C, bool fused, int warps) {
     if (warps == mma::WARPS_WIDE) {
         if (C == 1) return mma::scan_kernel<1, 1, 2, true, mma::WARPS_WIDE>;
         if (C == 2) return mma::scan_kernel<2, 1, 2, true, mma::WARPS_WIDE>;
+        if (C == 4) return mma::scan_kernel<4, 1, 1, true, mma::WARPS_WIDE>;
         return nullptr;
     }
     if (warps == mma::WARPS_BATCH) {
@@ -747,7 +748,7 @@ void mma_shape(int64_t n, int wd, int C, int64_t nq, int k, const DeviceInfo &in
     MmaShape sh;
     sh.MT = C == 4 ? 1 : 2;
     sh.NT = C == 4 ? 1 : 2;
-    if (nq <= 16 && C <= 2 && env_int("XFBQ_NO_WIDE", 0) == 0 && env_int("XFBQ_NO_FUSED", 0) == 0) {
+    if (nq <= 16 && env_int("XFBQ_NO_WIDE", 0) == 0 && env_int("XFBQ_NO_FUSED", 0) == 0) {
         sh.MT = 1;  // <= 16 queries: one 16-row tile, 16 warps per CTA
         sh.warps = mma::WARPS_WIDE;
     }
