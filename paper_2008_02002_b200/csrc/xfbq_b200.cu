@@ -919,10 +919,11 @@ UmmaKernel pick_umma_kernel(int C, int MT, bool queue) {
     return nullptr;
 }
 
-void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &info, UmmaShape *out, bool seed_scan = false) {
+void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &info, UmmaShape *out, bool seed_scan = false,
+                bool allow_queue = true) {
     UmmaShape sh;
     sh.MT = MT;
-    sh.queue = !seed_scan && env_int("XFBQ_UMMA_QUEUE", 1) != 0;
+    sh.queue = !seed_scan && allow_queue && env_int("XFBQ_UMMA_QUEUE", 1) != 0;
     sh.DW = (MT == 2 || sh.queue) ? 1 : 2;
     int cap = 64;
     while (cap < 2 * k) cap <<= 1;
@@ -1011,14 +1012,19 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     DeviceInfo info;
     if (int rc = device_info(&info)) return rc;
     const int MT = (C == 4 || nq <= 128) ? 1 : 2;
-    umma_shape(n, C, nq, k, MT, info, &pl.main);
-    if (pl.main.NS == 0) return XFBQ_OK;
     // Sample scan that seeds the thresholds (measured on 10M x 256, 10k queries: 16k documents split over at
     // most 4 CTAs per query group balance its cost -- it starts from open lists -- against the rows the main
     // scan's resolvers then have to handle).
     int64_t sample = env_int("XFBQ_SAMPLE", -1);
     if (sample < 0) { sample = 16384; while (sample < 64 * static_cast<int64_t>(k)) sample <<= 1; }
     if (sample > 0 && (n < 16 * sample || sample < 4 * k)) sample = 0;
+    // Without seeded thresholds every score passes at first: list work dominates and the kernel whose eight
+    // epilogue warps own their lists beats the two resolvers of the queue kernel (100k x 128, 100 queries: 4x).
+    // The same holds for small problems with few query groups (1M x 128, 1000 queries: 2.5x): the lists stay hot.
+    const int64_t groups = (nq + 128 * MT - 1) / (128 * MT);
+    const bool big = n >= env_int("XFBQ_UMMA_QUEUE_MIN_N", 2000000) || groups >= 16;
+    umma_shape(n, C, nq, k, MT, info, &pl.main, false, sample > 0 && big);
+    if (pl.main.NS == 0) return XFBQ_OK;
     pl.sample = sample;
     if (sample) umma_shape(sample, C, nq, k, MT, info, &pl.pre, true);
     size_t off = 0;

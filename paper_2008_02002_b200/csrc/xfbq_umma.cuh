@@ -677,6 +677,24 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
     int w2 = 0;
     const long long t_begin = prof ? clock64() : 0;
     uint64_t *group_lists = p.lists + static_cast<int64_t>(blockIdx.x) * NQ_CTA * static_cast<int64_t>(p.cap);
+    // End of an item, after the resolvers have drained every ring: the 14 drain + resolver warps emit the
+    // group's lists round-robin (<= k best keys each, unsorted, KEY_INF padded).  With two warps doing it, short
+    // items (few query groups -> many document slices) spent more time emitting than scanning.
+    auto emit_lists = [&](int slot, int *hist, int gr, int part) {
+        const int64_t gq0 = static_cast<int64_t>(gr) * NQ_CTA;
+        const int cap = p.cap, k = p.k;
+        for (int qc = slot; qc < NQ_CTA; qc += Q_DRAIN + Q_RESOLVERS) {
+            const int64_t qq = gq0 + qc;
+            if (qq >= p.nq) break;
+            int c = cnt_s[qc];
+            uint64_t *lrow = group_lists + static_cast<int64_t>(qc) * cap;
+            if (c > k) { select_any(lrow, c, k, hist, lane); c = k; }
+            __syncwarp();
+            uint64_t *dst = p.out + (static_cast<int64_t>(part) * p.nq + qq) * k;
+            for (int e = lane; e < k; e += 32) dst[e] = e < c ? __ldcg(lrow + e) : KEY_INF;
+        }
+        __syncwarp();
+    };
 
     if (warp < Q_DRAIN) {
         // ================================ drain ================================
@@ -776,6 +794,12 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             }
             __syncwarp();
             if (lane == 0) { __threadfence_block(); st_volatile(&fin_s[warp], head); }  // every ticket of this segment is out
+            cta_sync();  // the resolvers have emptied the rings: lists are final, this warp's ring is free scratch
+            emit_lists(warp, reinterpret_cast<int *>(ring), sg.gr, sg.part);
+            __syncwarp();
+            for (int i = lane; i < RING_ROWS; i += 32) ring[i * STASH_WORDS + 34] = 0u;  // scratch use may have forged tickets
+            head = 0; tail_seen = 0;
+            if (lane == 0) { st_volatile(&tail_s[warp], 0); }
             s_run += static_cast<uint32_t>(sg.cnt);
             cta_sync();
         }
@@ -821,7 +845,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                 rb.advance(NS);
             }
             s_run += static_cast<uint32_t>(sg.cnt);
-            cta_sync();
+            cta_sync();  // lists final
+            cta_sync();  // lists emitted
         }
         if (prof && lane == 0) { p.prof[blockIdx.x * 8 + 2] = w0; p.prof[blockIdx.x * 8 + 3] = w1; }
     } else if (warp == Q_TMA_WARP) {
@@ -840,7 +865,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             }
             __syncwarp();
             s_run += static_cast<uint32_t>(sg.cnt);
-            cta_sync();
+            cta_sync();  // lists final
+            cta_sync();  // lists emitted
         }
         if (prof && lane == 0) { p.prof[blockIdx.x * 8 + 4] = w0; }
     } else {
@@ -955,24 +981,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                     __nanosleep(100);
                 }
             }
-            // ---- emit the lists this resolver owns: <= k best keys each (unsorted), KEY_INF padded
-            {
-                const int64_t part = sg.part;
-                for (int blk = res; blk < NQ_CTA / 32; blk += Q_RESOLVERS) {  // drain warp w feeds resolver w & 1: blocks of 32 queries
-                    for (int ql = 0; ql < 32; ++ql) {
-                        const int qc = blk * 32 + ql;
-                        const int64_t qq = gq0 + qc;
-                        if (qq >= p.nq) break;
-                        int c = cnt_s[qc];
-                        uint64_t *lrow = group_lists + static_cast<int64_t>(qc) * cap;
-                        if (c > k) { select_any(lrow, c, k, hist, lane); c = k; }
-                        __syncwarp();
-                        uint64_t *dst = p.out + (part * p.nq + qq) * k;
-                        for (int e = lane; e < k; e += 32) dst[e] = e < c ? __ldcg(lrow + e) : KEY_INF;
-                    }
-                }
-                __syncwarp();
-            }
+            cta_sync();  // every resolver is done: lists are final
+            emit_lists(Q_DRAIN + res, hist, sg.gr, sg.part);
             if (lane < Q_DRAIN && (lane % Q_RESOLVERS) == res) st_volatile(&fin_s[lane], -1);  // next segment's tickets are not out yet
             s_run += static_cast<uint32_t>(sg.cnt);
             cta_sync();
