@@ -145,6 +145,95 @@ quantize_pack_kernel(const T *__restrict__ x, int64_t n, int dim, int64_t ld, do
     if (bad) atomicAdd(nonfinite, bad);
 }
 
+
+// Fast quantizer for float32 rows (16-byte aligned, dim % 4 == 0).  Same result as quantize_one for every
+// input, with float64 touched only near a code boundary:
+//   yz = x * fl32(scale * 2^(w-1) * 2^16)  carries a relative error <= 2^-23 against the exact product, i.e.
+//   < 2.1 units of 2^-16 for |y| < 2^(w-1) + 2 <= 130; so when the 16 fraction bits of floor(yz) lie in
+//   [4, 65531] the float64 value the reference computes, floor((double(x) * scale) * 2^(w-1)), has the same
+//   integer part (quant.py:146).  yz is first clamped to +-(2^(w-1) + 1.5) * 2^16: saturating values land on
+//   fraction 0x8000, pass the test and are clipped like quant.py:147 does.  Anything else -- about 1 element
+//   in 10^4, plus every non-finite value -- is flagged in a per-lane bit mask and redone in float64 after the
+//   branch-free main loop.  x == 0 is exact (t = 0) and never flagged.
+// A lane owns 32 consecutive dimensions of one document (8 LDG.128 in flight), builds its word of every bit
+// plane in registers, and the warp's stores of one plane are 128 contiguous bytes of the bundle layout.
+// 4x4 bit-block transpose of four 32-bit words (delta swaps; its own inverse): plane words <-> nibble words
+__device__ __forceinline__ void transpose_4x4_blocks(uint32_t &p0, uint32_t &p1, uint32_t &p2, uint32_t &p3) {
+    uint32_t t;
+    t = ((p0 >> 1) ^ p1) & 0x55555555u; p1 ^= t; p0 ^= t << 1;
+    t = ((p2 >> 1) ^ p3) & 0x55555555u; p3 ^= t; p2 ^= t << 1;
+    t = ((p0 >> 2) ^ p2) & 0x33333333u; p2 ^= t; p0 ^= t << 2;
+    t = ((p1 >> 2) ^ p3) & 0x33333333u; p3 ^= t; p1 ^= t << 2;
+}
+
+template <int WIDTH>
+__global__ void __launch_bounds__(256)
+quantize_pack_f32_fast_kernel(const float *__restrict__ x, int64_t n, int dim, int64_t ld, double scale,
+                              int C, uint32_t *__restrict__ out, unsigned long long *__restrict__ nonfinite) {
+    const int lane = threadIdx.x & 31;
+    const int d = lane >> 2, t = lane & 3;
+    constexpr int ihalf = 1 << (WIDTH - 1);
+    const double half = static_cast<double>(ihalf);
+    const float sz = static_cast<float>(scale * half * 65536.0);
+    constexpr float satc = (static_cast<float>(ihalf) + 1.5f) * 65536.0f;
+    const int64_t nb = (n + 31) >> 5;
+    const int64_t units = nb * C * 4;  // (bundle, chunk, group of 8 documents)
+    unsigned long long bad = 0;
+    for (int64_t u = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < units;
+         u += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        const int s8 = static_cast<int>(u & 3);
+        const int64_t bc = u >> 2;
+        const int c = static_cast<int>(bc % C);
+        const int64_t b = bc / C;
+        const int64_t doc = b * 32 + s8 * 8 + d;
+        const int k0 = c * 128 + t * 32;
+        const float *src = x + doc * ld + k0;
+        // dimensions k0 .. k0 + 31 that exist (dim % 4 == 0: whole float4s), none for a padding document
+        const int nvalid = doc < n ? min(max(dim - k0, 0), 32) : 0;
+        const uint32_t valid = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
+        float4 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = 4 * j < nvalid ? __ldg(reinterpret_cast<const float4 *>(src + 4 * j)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        constexpr bool NIBBLES = WIDTH <= 4;  // codes fit a nibble: pack them first, transpose to bit planes once per 32
+        uint32_t w[NIBBLES ? 4 : WIDTH];
+#pragma unroll
+        for (int i = 0; i < (NIBBLES ? 4 : WIDTH); ++i) w[i] = 0u;
+        uint32_t redo = 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float yz = fminf(fmaxf(e[q] * sz, -satc), satc);
+                const int z = __float2int_rd(yz);
+                const bool inexact = ((static_cast<unsigned>(z) & 0xFFFFu) - 4u > 65527u && e[q] != 0.0f) || !(fabsf(e[q]) <= 3.402823466e38f);
+                redo = __funnelshift_r(redo, inexact ? 1u : 0u, 1);
+                const unsigned code = static_cast<unsigned>(ihalf - 1 - min(max(z >> 16, -ihalf), ihalf - 1));  // quant.py:147-148
+                if (NIBBLES) {
+                    w[q] = __funnelshift_r(w[q], code, 4);  // word q: nibble j = code of element 4j + q
+                } else {
+#pragma unroll
+                    for (int i = 0; i < WIDTH; ++i) w[i] = __funnelshift_r(w[i], code >> i, 1);  // after 32 elements bit p = element p
+                }
+            }
+        }
+        if (NIBBLES) transpose_4x4_blocks(w[0], w[1], w[2], w[3]);  // -> w[i] = bit plane i
+        redo &= valid;
+        while (redo) {  // rare: exact float64 path for the flagged elements (re-read through L1)
+            const int pos = __ffs(redo) - 1;
+            redo &= redo - 1;
+            const unsigned code = quantize_one<float>(src[pos], scale, half, bad);
+#pragma unroll
+            for (int i = 0; i < WIDTH; ++i) w[i] = (w[i] & ~(1u << pos)) | (((code >> i) & 1u) << pos);
+        }
+        // bundle layout: 16-byte word ((b * width + i) * C + c) * 32 + doc-in-bundle, 32-bit word t
+        const int64_t lane_word = static_cast<int64_t>(s8 * 8 + d) * 4 + t;
+#pragma unroll
+        for (int i = 0; i < WIDTH; ++i) out[(((b * WIDTH + i) * C + c) * 32) * 4 + lane_word] = w[i] & valid;
+    }
+    if (bad) atomicAdd(nonfinite, bad);
+}
+
 // Queries: one warp per query row, output uint32 [nq][width][4C].
 template <typename T>
 __global__ void __launch_bounds__(256)
@@ -1106,6 +1195,22 @@ int quantize_pack_impl(const T *x, int64_t n, int64_t dim, int64_t ld, double sc
     DeviceInfo info;
     if (int rc = device_info(&info)) return rc;
     const int64_t nb = bundles_of(n);
+    if (sizeof(T) == 4 && dim % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+        scale * static_cast<double>(1 << (width - 1)) * 65536.0 <= 1e30 && env_int("XFBQ_QUANT_SLOW", 0) == 0) {
+        const int64_t units = nb * chunks128(dim) * 4;
+        int64_t fblocks = (units + 7) / 8;
+        const int64_t fmax = static_cast<int64_t>(info.sms) * 16;
+        if (fblocks > fmax) fblocks = fmax;
+        typedef void (*FastKernel)(const float *, int64_t, int, int64_t, double, int, uint32_t *, unsigned long long *);
+        static const FastKernel kernels[XFBQ_MAX_WIDTH] = {
+            quantize_pack_f32_fast_kernel<1>, quantize_pack_f32_fast_kernel<2>, quantize_pack_f32_fast_kernel<3>,
+            quantize_pack_f32_fast_kernel<4>, quantize_pack_f32_fast_kernel<5>, quantize_pack_f32_fast_kernel<6>,
+            quantize_pack_f32_fast_kernel<7>, quantize_pack_f32_fast_kernel<8>};
+        kernels[width - 1]<<<static_cast<unsigned>(fblocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+            reinterpret_cast<const float *>(x), n, static_cast<int>(dim), ld, scale, static_cast<int>(chunks128(dim)),
+            static_cast<uint32_t *>(out), reinterpret_cast<unsigned long long *>(nonfinite));
+        return check_launch("quantize_pack_f32_fast_kernel");
+    }
     int64_t blocks = (nb + QP_WARPS - 1) / QP_WARPS;
     const int64_t max_blocks = static_cast<int64_t>(info.sms) * 8;
     if (blocks > max_blocks) blocks = max_blocks;

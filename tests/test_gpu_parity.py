@@ -189,6 +189,36 @@ def test_tensor_engines_ragged_shapes(engine, n, dim, wd, nq, k, monkeypatch):
     assert np.array_equal(scores.astype(np.uint64), want_d) and np.array_equal(ids, want_i)
 
 
+@pytest.mark.parametrize("width", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_fast_float32_quantizer_on_code_boundaries(width, monkeypatch):
+    """The float32-first quantizer (exact float64 redo near code boundaries) against the CPU oracle and the
+    all-float64 kernel: values on, one ulp and two ulps around every code boundary, saturation edges,
+    denormals, +-0, huge values, plus random data; dims that leave a ragged last float4 group of a lane."""
+    import torch
+    rng = np.random.default_rng(100 + width)
+    for scale in (1.0, 0.7310585786300049, 3.3333333333333335, 12.345, 1e-3):
+        half = 2.0 ** (width - 1)
+        g32 = (np.arange(-half - 3, half + 4) / (scale * half)).astype(np.float32)
+        up = np.nextafter(g32, np.float32(np.inf))
+        dn = np.nextafter(g32, np.float32(-np.inf))
+        special = np.array([0.0, -0.0, 1e-45, -1e-45, 1e-38, -1e-38, 3e38, -3e38, 1.0, -1.0, 0.5, -0.5], dtype=np.float32)
+        rnd = rng.uniform(-2, 2, size=6000).astype(np.float32) / np.float32(scale)
+        vals = np.concatenate([g32, up, dn, np.nextafter(up, np.float32(np.inf)), np.nextafter(dn, np.float32(-np.inf)), special, rnd])
+        dim = 200                                   # ragged: the fourth lane of a row holds 8 of its 32 dims
+        vals = np.concatenate([vals, np.zeros((-len(vals)) % dim, np.float32)]).reshape(-1, dim).astype(np.float32)
+        want = xo.c_quantize_matrix(vals, width, scale)
+        monkeypatch.delenv("XFBQ_QUANT_SLOW", raising=False)
+        fast = xb.quantize_matrix(torch.from_numpy(vals).cuda(), width, scale).planes
+        monkeypatch.setenv("XFBQ_QUANT_SLOW", "1")
+        slow = xb.quantize_matrix(torch.from_numpy(vals).cuda(), width, scale).planes
+        assert np.array_equal(fast, want) and np.array_equal(slow, want), (width, scale)
+    monkeypatch.delenv("XFBQ_QUANT_SLOW", raising=False)
+    with pytest.raises(xb.InvalidInputError):       # non-finite values are still caught (quant.py:142-143)
+        xb.quantize_matrix(torch.tensor([[1.0, float("inf"), 0.0, 0.0]], device="cuda"), width, 1.0)
+    with pytest.raises(xb.InvalidInputError):
+        xb.quantize_matrix(torch.tensor([[float("nan"), 0.0, 0.0, 0.0]], device="cuda"), width, 1.0)
+
+
 def test_edge_cases():
     """k > n, empty index, dim mismatch, non-finite, bad scale (test_search.py:205-222,
     test_distance.py:143-153)."""
