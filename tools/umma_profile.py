@@ -13,7 +13,7 @@ from paper_2008_02002_b200 import _native  # noqa: E402
 nq = int(sys.argv[1]) if len(sys.argv) > 1 else 10000
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 10_000_000
 dim = int(sys.argv[3]) if len(sys.argv) > 3 else 256
-k = 100
+k = int(sys.argv[4]) if len(sys.argv) > 4 else 100
 g = torch.Generator(device="cuda").manual_seed(1)
 docs = torch.randn((n, dim), generator=g, device="cuda")
 docs /= docs.norm(dim=1, keepdim=True)
