@@ -102,7 +102,7 @@ int xfbq_bundles_to_planes(const void *db_dev, int64_t n, int64_t dim, int width
  *                   dimension 4m + e (streamed by the mma.sync engine: <= 16 queries, HBM-bound);
  *   [byte tiles]    (C in {1, 2, 4}) tiles of 128 documents x 128*C bytes, one code per byte, K-major with
  *                   the 128-byte swizzle: the exact shared-memory image of a tcgen05.mma B operand, copied
- *                   by one cp.async.bulk per tile (streamed by the tcgen05 engine: >= 17 queries).
+ *                   by one cp.async.bulk per tile (streamed by the tcgen05 engine: >= 32 queries).
  * The tile region starts at the nibble region's size rounded up to 1024 bytes.
  */
 int64_t xfbq_nibble_bytes(int64_t n, int64_t dim);
@@ -126,7 +126,7 @@ int xfbq_batch_distances(const void *db_dev, int64_t n, int64_t dim, int doc_bit
  * 1 <= k <= XFBQ_MAX_K;  row_offset + n <= 2^32.
  * nibbles_dev: optional derived layouts of the codes (xfbq_planes_to_nibbles).
  * When given (doc_bits <= 4, query_bits <= 7, dim <= 256 or 385..512, k <= 1024) the scan runs on the
- * integer tensor path -- tcgen05.mma kind::i8 with accumulators in tensor memory for >= 17 queries,
+ * integer tensor path -- tcgen05.mma kind::i8 with accumulators in tensor memory for >= 32 queries,
  * mma.sync (IMMA) below -- with identical results; when NULL, or outside those shapes, the XOR/POPC
  * kernels scan the bit planes.  XFBQ_ENGINE=umma|imma|popc forces one engine.
  */

@@ -1028,11 +1028,10 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
     sh.stages = (sh.n_pad + umma::STAGE_DOCS - 1) / umma::STAGE_DOCS;
     const int64_t W = static_cast<int64_t>(sh.groups) * sh.stages;
     int64_t grid = env_int("XFBQ_GRID", 0) > 0 ? env_int("XFBQ_GRID", 0) : info.sms;
-    // The sample scan that seeds the thresholds starts from open lists, so its cost grows with the number of
-    // lists, not with the documents: give every query group to as few CTAs as keep the chip busy.
-    if (seed_scan && env_int("XFBQ_GRID", 0) <= 0) {
-        const int64_t per_group = (info.sms + sh.groups - 1) / sh.groups;
-        const int64_t cap_grid = sh.groups * (per_group < env_int("XFBQ_SEED_SPLIT", 4) ? per_group : env_int("XFBQ_SEED_SPLIT", 4));
+    // (The sample scan runs on every SM too: capping it at a few CTAs per query group saved list start-ups but
+    // left most of the chip idle for small batches -- 256 queries: 1.7 ms on 4 CTAs.)
+    if (seed_scan && env_int("XFBQ_SEED_SPLIT", 0) > 0 && env_int("XFBQ_GRID", 0) <= 0) {
+        const int64_t cap_grid = static_cast<int64_t>(sh.groups) * env_int("XFBQ_SEED_SPLIT", 0);
         if (grid > cap_grid) grid = cap_grid;
     }
     if (grid > W) grid = W;
@@ -1095,7 +1094,7 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     const bool forced = eng && strcmp(eng, "umma") == 0;
     if (!have_nibbles || wd > 4 || wq > 7 || !(C == 1 || C == 2 || C == 4) || k > 1024 || n < 1 || env_int("XFBQ_FORCE_GENERIC", 0))
         return XFBQ_OK;
-    if (!forced && nq < env_int("XFBQ_UMMA_MIN_NQ", 17)) return XFBQ_OK;  // tiny batches: the fused HBM-bound IMMA scan
+    if (!forced && nq < env_int("XFBQ_UMMA_MIN_NQ", 32)) return XFBQ_OK;  // small batches: the mma.sync scans (HBM-bound below 17 queries; measured crossover at 32)
     if (nq < 1) return XFBQ_OK;
     if (merge_group_max(k) == 0 || nq > 65535) return XFBQ_OK;  // lists are emitted unsorted: needs the tree merge
     DeviceInfo info;
