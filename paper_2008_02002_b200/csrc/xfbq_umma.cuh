@@ -5,7 +5,7 @@
 // run on tcgen05.mma.kind::i8 (measured 8 188 MAC/clk/SM, 4x the mma.sync IMMA pipe) with the
 // accumulators in tensor memory.
 //
-// One persistent CTA per SM, 10 warps in three roles that only meet at mbarriers:
+// Two kernels share the loader / issuer design (one persistent CTA per SM, roles meet only at mbarriers):
 //   loader (1 thread)    one cp.async.bulk per stage: the engine streams a derived "byte tile" copy of the
 //                        codes -- 128 documents x 128C bytes, K-major with the 128-byte swizzle, i.e. the
 //                        exact shared-memory image of a tcgen05 B operand -- so nothing touches the data
@@ -13,16 +13,18 @@
 //   issuer (1 thread)    per stage and per 128-query tile: 4C x tcgen05.mma (M = 128 queries, N = 128
 //                        documents, K = 32) into one of three 128-column TMEM accumulators;
 //                        tcgen05.commit releases the operand stage / publishes the accumulator
-//   epilogue (8 warps)   tcgen05.ld of the warp's 32 lanes x 128 columns into registers, accumulator handed
-//                        back at once (it is on the MMA critical path), then per 32 scores of the thread's
-//                        OWN query row: 3-input max tree, compare with the row's threshold register, vote;
-//                        only on a hit are (distance << 32 | row id) keys appended to the thread-private
-//                        candidate list; a list that could overflow is cut to its k best by a warp-level
-//                        radix select (search.py:129-131 order on the full key), which tightens the threshold.
+// and differ in who maintains the candidate lists:
+//   scan_kernel          8 epilogue warps: tcgen05.ld of 32 lanes x 128 columns, accumulator handed back, then
+//                        per 32 scores of the thread's OWN query row a 3-input max tree, one compare with the
+//                        row's threshold register, one vote; hits go to thread-private lists, compacted in place
+//                        (register radix select).  Used for the sample scans that seed the thresholds (every
+//                        score passes at first) and for small problems.
+//   scan_queue_kernel    12 stateless drain warps park passing score rows in shared-memory rings, 2 resolver
+//                        warps own the lists (see the comment above that kernel).  Used for the big scans: the
+//                        tensor pipe never waits on list work.
 // The query operand (s8 weights 2y - Aq, same K permutation as the byte tiles) lives in tensor memory too
 // (A-from-TMEM form of tcgen05.mma: lane = query row, 4 K-elements per 32-bit column), stored once per query
-// group with tcgen05.st, so shared-memory bandwidth only carries the document operand.  Work = groups x
-// stages is linearised and cut into gridDim.x equal ranges, as in the IMMA engine.
+// group with tcgen05.st, so shared-memory bandwidth only carries the document operand.
 #pragma once
 
 namespace umma {
@@ -106,11 +108,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-__device__ __forceinline__ int tmem_ld1(uint32_t taddr) {
-    int v;
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr) : "memory");
-    return v;
-}
 __device__ __forceinline__ bool elect_one() {  // one lane of a converged warp
     uint32_t pred;
     asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
