@@ -444,13 +444,24 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                         }
                     }
                     uint32_t cols = __reduce_or_sync(0xffffffffu, single ? 0u : hits);
-                    while (cols) {
-                        const int j = __ffs(cols) - 1;
-                        cols &= cols - 1;
-                        const int val = pick32(v, j);
-                        if (!single && ((hits >> j) & 1u) && doc0 + j < n_docs) {
-                            my_list[cnt] = (static_cast<uint64_t>(static_cast<uint32_t>(dq - val)) << 32) | (id_off + doc0 + j);
-                            ++cnt;
+                    if (__popc(cols) > 6) {
+                        // dense hits (open or young thresholds: the sample scans): one predicated pass over the
+                        // 32 columns beats walking their union one jump-table pick at a time
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (!single && ((hits >> j) & 1u) && doc0 + j < n_docs) {
+                                my_list[cnt] = (static_cast<uint64_t>(static_cast<uint32_t>(dq - v[j])) << 32) | (id_off + doc0 + j);
+                                ++cnt;
+                            }
+                    } else {
+                        while (cols) {
+                            const int j = __ffs(cols) - 1;
+                            cols &= cols - 1;
+                            const int val = pick32(v, j);
+                            if (!single && ((hits >> j) & 1u) && doc0 + j < n_docs) {
+                                my_list[cnt] = (static_cast<uint64_t>(static_cast<uint32_t>(dq - val)) << 32) | (id_off + doc0 + j);
+                                ++cnt;
+                            }
                         }
                     }
                     __syncwarp();
