@@ -32,7 +32,8 @@ thread_local bool g_timing = false;
 thread_local cudaEvent_t g_ev0 = nullptr, g_ev1 = nullptr;
 thread_local bool g_ev_valid = false;
 std::atomic<int64_t> g_launches{0};
-thread_local unsigned long long *g_prof = nullptr;  // debug: device buffer for the tcgen05 engine's wait counters
+thread_local unsigned long long *g_prof = nullptr;
+thread_local int g_hist_shift = 2;  // bin width of the tcgen05 engine's global candidate histogram (set per search from the distance range)  // debug: device buffer for the tcgen05 engine's wait counters
 
 int fail(int code, const char *fmt, ...) {
     va_list ap;
@@ -990,7 +991,8 @@ struct UmmaPlan {
     bool ok = false;
     UmmaShape main, pre;
     int64_t sample = 0;
-    size_t off_qimg = 0, off_qconst = 0, off_tau = 0, off_prekeys = 0, off_lists = 0, off_parts = 0, off_mscratch = 0, bytes = 0;
+    size_t off_qimg = 0, off_qconst = 0, off_tau = 0, off_prekeys = 0, off_lists = 0, off_parts = 0, off_mscratch = 0,
+           off_theta0 = 0, off_ghist = 0, bytes = 0;
 };
 
 typedef void (*UmmaKernel)(const umma::Params);
@@ -1123,6 +1125,9 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     pl.off_lists = off; off = align256(off + (pl.main.lists_bytes > pl.pre.lists_bytes ? pl.main.lists_bytes : pl.pre.lists_bytes));
     pl.off_parts = off; off = align256(off + (pl.main.parts_bytes > pl.pre.parts_bytes ? pl.main.parts_bytes : pl.pre.parts_bytes));
     pl.off_mscratch = off; off = align256(off + (pl.main.mscratch_bytes > pl.pre.mscratch_bytes ? pl.main.mscratch_bytes : pl.pre.mscratch_bytes));
+    const bool use_hist = pl.main.queue && sample > 0 && env_int("XFBQ_UMMA_HIST", 1) != 0;
+    pl.off_theta0 = off; off = align256(off + (use_hist ? static_cast<size_t>(nq) * 4 : 0));
+    pl.off_ghist = off; off = align256(off + (use_hist ? static_cast<size_t>(nq) * umma::HIST_BINS * 4 : 0));
     pl.bytes = off;
     pl.ok = true;
     *plan = pl;
@@ -1147,6 +1152,10 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     p.nq = nq; p.stages = sh.stages; p.groups = sh.groups;
     p.k = k; p.cap = sh.cap; p.NS = sh.NS;
     p.n_seg = sh.n_seg; p.seg_stages = sh.seg_stages; p.ring_rows = sh.ring_rows;
+    const bool use_hist = sh.queue && tau_init && pl.off_ghist > pl.off_theta0;
+    p.ghist = use_hist ? reinterpret_cast<uint32_t *>(ws + pl.off_ghist) : nullptr;
+    p.theta0 = use_hist ? reinterpret_cast<const int32_t *>(ws + pl.off_theta0) : nullptr;
+    p.hist_shift = g_hist_shift;
     p.prof = (&sh == &pl.main) ? g_prof : nullptr;
     p.debug = env_int("XFBQ_UMMA_DEBUG", 0);
     if (sh.slots > 1 && !sh.queue) {  // slots a group does not use stay KEY_INF (the queue kernel writes every slice)
@@ -1177,6 +1186,16 @@ int run_umma(const UmmaPlan &up, unsigned char *ws, const void *nib, int64_t n, 
         mma::tau_from_keys_kernel<<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(prekeys, qconst, nq, k, tau);
         if (int rc = check_launch("tau_from_keys_kernel")) return rc;
         tau_init = tau;
+        if (up.off_ghist > up.off_theta0) {  // global candidate histogram of the main scan, bins measured from the seeded thresholds
+            cudaError_t e = cudaMemcpyAsync(ws + up.off_theta0, tau, static_cast<size_t>(nq) * 4, cudaMemcpyDeviceToDevice, st);
+            if (e == cudaSuccess) e = cudaMemsetAsync(ws + up.off_ghist, 0, static_cast<size_t>(nq) * umma::HIST_BINS * 4, st);
+            if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "histogram setup: %s", cudaGetErrorString(e));
+            // scores of interest lie within ~1/64 of the distance range below the seed: 256 bins of width 2^shift cover it
+            const int64_t ub = xfbq_distance_upper_bound(dim, wd, wq);
+            int shift = 0;
+            while ((static_cast<int64_t>(umma::HIST_BINS) << shift) < ub / 56) ++shift;
+            g_hist_shift = env_int("XFBQ_UMMA_HIST_SHIFT", shift);
+        }
         if (env_int("XFBQ_DEBUG_TAU_NEVER", 0)) cudaMemsetAsync(tau, 0x40, static_cast<size_t>(nq) * 4, st);  // timing experiments only: nothing passes
     }
     return run_umma_scan(up.main, up, ws, nib, n, C, nq, k, row_offset, tau_init, keys_out, st);

@@ -36,6 +36,7 @@ constexpr int THREADS = 320;    // 10 warps: registers are carved per 4 warps, s
 constexpr int STAGE_DOCS = 128;  // N of one MMA
 constexpr int ACC_BUFS = 3;      // 3 x 128 accumulator columns; columns 384..511 hold the query operand
 constexpr int A_COL0 = ACC_BUFS * STAGE_DOCS;
+constexpr int HIST_BINS = 256;
 constexpr int TAU_OPEN = -(1 << 30);
 constexpr int TAU_NEVER = 1 << 30;     // |acc| <= 512 * 15 * 127 < 2^20, so acc - tau never overflows
 
@@ -46,6 +47,9 @@ struct Params {
     const int32_t *qconst;     // [nq_pad] Dq
     const int32_t *tau_init;   // [nq] or nullptr
     int *theta_g;              // [nq] thresholds shared by all CTAs (acc domain, atomicMax), or nullptr
+    uint32_t *ghist;           // [nq][HIST_BINS] global histogram of every candidate appended to any list (queue kernel), or nullptr
+    const int32_t *theta0;     // [nq] the seeded thresholds the histogram bins are measured from
+    int hist_shift;            // bin width = 1 << hist_shift score units
     uint64_t *lists;           // [grid][EPI_WARPS][32][cap]
     uint64_t *out;             // [slots * DW][nq][k], KEY_INF pre-filled when slots > 1
     int64_t nq, stages;
@@ -612,6 +616,36 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+// Global candidate histogram (queue kernel): every key appended to ANY list of a query -- by any CTA -- bumps the
+// bin of its score, measured from the query's seeded threshold.  Bins are only ever incremented for real,
+// distinct documents, so "the bins >= b hold at least k candidates" proves that the k-th best score is at
+// least theta0 + b * width: a threshold every list of the query may adopt, however few documents it has seen
+// itself.  Lane l passes its 8 bins [8l, 8l + 8); returns b, or -1 while fewer than k candidates are known.
+__device__ __forceinline__ int hist_bound(const uint4 &lo, const uint4 &hi, int k, int lane) {
+    const uint32_t c[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    uint32_t s = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s += c[e];
+    uint32_t suf = s;  // candidates in this lane's bins and all better ones
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_down_sync(0xffffffffu, suf, o);
+        if (lane + o < 32) suf += v;
+    }
+    const bool mine = suf >= static_cast<uint32_t>(k) && suf - s < static_cast<uint32_t>(k);
+    int b = -1;
+    if (mine) {
+        uint32_t acc = suf - s;
+#pragma unroll
+        for (int e = 7; e >= 0; --e) {
+            acc += c[e];
+            if (b < 0 && acc >= static_cast<uint32_t>(k)) b = 8 * lane + e;
+        }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, mine);
+    return m ? __shfl_sync(0xffffffffu, b, __ffs(m) - 1) : -1;
+}
+
 // ================================================================================================
 // Queue variant (main scans): the drain warps never maintain lists.  A score row whose maximum passes
 // its query's threshold is parked in a shared-memory ring (8 STS.128 + a ticket) and two resolver warps
@@ -633,7 +667,7 @@ __host__ __device__ inline QSmemLayout q_smem_layout(int C, int NS, int ring_row
     uint32_t off = 0;
     L.b_off = off; off += static_cast<uint32_t>(NS) * STAGE_DOCS * 128 * C;
     L.ring_off = off; off += Q_DRAIN * ring_rows * STASH_WORDS * 4;
-    L.state_off = off; off += 4 * 256 * 4 + 2 * Q_DRAIN * 4 + 32;  // per query: count, threshold, Dq, claim; per drain warp: tail, final ticket
+    L.state_off = off; off += 5 * 256 * 4 + 2 * Q_DRAIN * 4 + 32;  // per query: count, threshold, Dq, claim, seeded threshold; per drain warp: tail, final ticket
     L.hist_off = off; off += Q_RESOLVERS * 256 * 4;
     L.bar_off = off; off += (2 * NS + 2 * ACC_BUFS) * 8 + 16;
     L.total = off + 1024;
@@ -658,7 +692,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
     unsigned char *sB = smem + L.b_off;
     uint32_t *rings = reinterpret_cast<uint32_t *>(smem + L.ring_off);
     int *cnt_s = reinterpret_cast<int *>(smem + L.state_off), *theta_s = cnt_s + 256, *dq_s = cnt_s + 512, *claim_s = cnt_s + 768;
-    int *tail_s = cnt_s + 1024, *fin_s = tail_s + Q_DRAIN;  // per drain warp: rows consumed by its resolver; final ticket of a segment
+    int *theta0_s = cnt_s + 1024;
+    int *tail_s = cnt_s + 1280, *fin_s = tail_s + Q_DRAIN;  // per drain warp: rows consumed by its resolver; final ticket of a segment
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L.bar_off);
     uint64_t *b_full = bars, *b_empty = bars + NS, *acc_full = bars + 2 * NS, *acc_empty = bars + 2 * NS + ACC_BUFS;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 2 * ACC_BUFS);
@@ -728,6 +763,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                 cnt_s[qloc] = 0;
                 dq_s[qloc] = valid ? p.qconst[myq] : 0;
                 theta_s[qloc] = valid ? (p.tau_init ? max(TAU_OPEN, p.tau_init[myq]) : TAU_OPEN) : TAU_NEVER;
+                theta0_s[qloc] = (valid && p.theta0) ? max(TAU_OPEN, p.theta0[myq]) : TAU_OPEN;
             }
             fence_before();
             cta_sync();
@@ -888,10 +924,37 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             cta_sync();
             const int64_t gq0 = static_cast<int64_t>(sg.gr) * NQ_CTA;
             int idle = 0;
+            // round-robin refresh of this resolver's queries from the global histogram: the bins of the next query
+            // are fetched while the current sweep runs (one L2 round trip per sweep would double its length)
+            constexpr int OWN_Q = NQ_CTA / Q_RESOLVERS;
+            int rq = 0, rq_pending = -1;
+            uint4 hb_lo = make_uint4(0u, 0u, 0u, 0u), hb_hi = hb_lo;
 #ifdef XFBQ_UMMA_WATCHDOG
             long long wd0 = clock64();
 #endif
             while (true) {
+                if (p.ghist) {
+                    if (rq_pending >= 0) {
+                        const int b = hist_bound(hb_lo, hb_hi, k, lane);
+                        if (b > 0 && lane == 0) {
+                            const int th = theta0_s[rq_pending] + (b << p.hist_shift);
+                            if (th > theta_s[rq_pending]) {
+                                atomicMax(&theta_s[rq_pending], th);
+                                if (p.theta_g) atomicMax(p.theta_g + gq0 + rq_pending, th);
+                            }
+                        }
+                    }
+                    const int qn = (res + Q_RESOLVERS * (rq >> 5)) * 32 + (rq & 31);  // the queries of this resolver's blocks in turn
+                    rq = rq + 1 == OWN_Q ? 0 : rq + 1;
+                    if (gq0 + qn < p.nq) {
+                        const uint4 *bins = reinterpret_cast<const uint4 *>(p.ghist + (gq0 + qn) * HIST_BINS) + 2 * lane;
+                        hb_lo = __ldcg(bins);
+                        hb_hi = __ldcg(bins + 1);
+                        rq_pending = qn;
+                    } else {
+                        rq_pending = -1;
+                    }
+                }
                 bool progressed = false;
                 bool all_done = true;
 #pragma unroll 1
@@ -937,8 +1000,11 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                                 const int j = __ffs(hits) - 1;
                                 hits &= hits - 1;
                                 const uint32_t doc = doc0 + j;
-                                if (doc < n_docs)
-                                    list[c++] = (static_cast<uint64_t>(static_cast<uint32_t>(dqe - static_cast<int>(row[j]))) << 32) | (id_off + doc);
+                                if (doc < n_docs) {
+                                    const int val = static_cast<int>(row[j]);
+                                    list[c++] = (static_cast<uint64_t>(static_cast<uint32_t>(dqe - val)) << 32) | (id_off + doc);
+                                    if (p.ghist) atomicAdd(p.ghist + (gq0 + q) * HIST_BINS + min((val - theta0_s[q]) >> p.hist_shift, HIST_BINS - 1), 1u);
+                                }
                             }
                             cnt_s[q] = c;
                             pend = false;
