@@ -219,6 +219,34 @@ def test_fast_float32_quantizer_on_code_boundaries(width, monkeypatch):
         xb.quantize_matrix(torch.tensor([[float("nan"), 0.0, 0.0, 0.0]], device="cuda"), width, 1.0)
 
 
+def test_concurrent_searches_are_deterministic():
+    """test_search.py:254-265: searches from a thread pool on one shared index give exactly the serial answers
+    (the library keeps no global mutable state: thread-local error string / timing, caller-owned workspaces)."""
+    from concurrent.futures import ThreadPoolExecutor
+    c = synth_case("cfg4_40k_256_w4")
+    z = c["z"]
+    params = xb.QuantParams(dim=c["dim"], scale=c["scale"], doc_bits=c["wd"], query_bits=c["wq"])
+    idx = xb.build_index(c["docs"], params, keep_originals=False)
+    batch = xo.synthetic_unit_rows(96, c["dim"], 4242)          # tcgen05 engine
+    serial_batch = xb.search(idx, batch, 50)
+    serial_single = [xb.k_select(idx, xb.SearchRequest(query=q, k=c["k"])) for q in c["queries"][:8]]
+
+    def work(i):
+        if i % 2:
+            return xb.search(idx, batch, 50)
+        return xb.k_select(idx, xb.SearchRequest(query=c["queries"][(i // 2) % 8], k=c["k"]))
+
+    with ThreadPoolExecutor(max_workers=6) as pool:
+        results = list(pool.map(work, range(48)))
+    for i, r in enumerate(results):
+        if i % 2:
+            assert np.array_equal(r[0], serial_batch[0]) and np.array_equal(r[1], serial_batch[1])
+        else:
+            want = serial_single[(i // 2) % 8]
+            assert r.hits == want.hits and r.threshold_distance == want.threshold_distance
+    assert [h[0] for h in serial_single[0].hits] == z["ids"][0].tolist()
+
+
 def test_edge_cases():
     """k > n, empty index, dim mismatch, non-finite, bad scale (test_search.py:205-222,
     test_distance.py:143-153)."""
