@@ -45,3 +45,8 @@ for i, nm in enumerate(names):
     else:
         print(f"  {nm:34s} {c[:, i].mean() / 1e6:9.2f} Mclk  {c[:, i].mean() / tot * 100:5.1f}%  min {c[:, i].min() / tot * 100:5.1f}% max {c[:, i].max() / tot * 100:5.1f}%")
 print(f"  epi warp0 compactions {x[:, 2].mean():.0f}")
+if len(sys.argv) > 5:
+    print("per CTA: stages, total Mclk, clk/stage, mma wait acc_empty %, mma wait b_full %, drain w0 wait acc_full %, ring-full %")
+    for b in range(148):
+        print(b, int(c[b, 7]), round(c[b, 6] / 1e6, 2), int(c[b, 6] / max(c[b, 7], 1)), round(100 * c[b, 3] / c[b, 6], 1), round(100 * c[b, 2] / c[b, 6], 1),
+              round(100 * c[b, 0] / c[b, 6], 1), round(100 * c[b, 5] / c[b, 6], 1))
