@@ -981,6 +981,7 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
 struct UmmaShape {
     int MT = 2, DW = 1, groups = 1, grid = 1, slots = 1, parts = 1, cap = 0, NS = 0;
     bool queue = false;  // scan_queue_kernel (main scans) vs scan_kernel (sample scans: open thresholds)
+    bool count = false;  // sample scan that only counts scores into per-query histograms (scan_kernel<.., SEED = true>)
     int ring_rows = 64;
     int n_seg = 1, seg_stages = 0;  // queue kernel: document slices (= partial results per query) and stages per slice
     int64_t stages = 0, nq_pad = 0, n_pad = 0;
@@ -992,12 +993,18 @@ struct UmmaPlan {
     UmmaShape main, pre;
     int64_t sample = 0;
     size_t off_qimg = 0, off_qconst = 0, off_tau = 0, off_prekeys = 0, off_lists = 0, off_parts = 0, off_mscratch = 0,
-           off_theta0 = 0, off_ghist = 0, bytes = 0;
+           off_theta0 = 0, off_ghist = 0, off_seedpar = 0, off_seedhist = 0, bytes = 0;
 };
 
 typedef void (*UmmaKernel)(const umma::Params);
 
-UmmaKernel pick_umma_kernel(int C, int MT, bool queue) {
+UmmaKernel pick_umma_kernel(int C, int MT, bool queue, bool count = false) {
+    if (count) {
+        if (C == 1) return MT == 2 ? umma::scan_kernel<1, 2, true> : umma::scan_kernel<1, 1, true>;
+        if (C == 2) return MT == 2 ? umma::scan_kernel<2, 2, true> : umma::scan_kernel<2, 1, true>;
+        if (C == 4 && MT == 1) return umma::scan_kernel<4, 1, true>;
+        return nullptr;
+    }
     if (queue) {
         if (C == 1) return MT == 2 ? umma::scan_queue_kernel<1, 2> : umma::scan_queue_kernel<1, 1>;
         if (C == 2) return MT == 2 ? umma::scan_queue_kernel<2, 2> : umma::scan_queue_kernel<2, 1>;
@@ -1011,9 +1018,10 @@ UmmaKernel pick_umma_kernel(int C, int MT, bool queue) {
 }
 
 void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &info, UmmaShape *out, bool seed_scan = false,
-                bool allow_queue = true) {
+                bool allow_queue = true, bool count = false) {
     UmmaShape sh;
     sh.MT = MT;
+    sh.count = count;
     sh.queue = !seed_scan && allow_queue && env_int("XFBQ_UMMA_QUEUE", 1) != 0;
     sh.DW = (MT == 2 || sh.queue) ? 1 : 2;
     int cap = 64;
@@ -1076,7 +1084,7 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
     sh.parts = slots * sh.DW;
     int NS = env_int("XFBQ_UMMA_STAGES", 5);
     const size_t budget = static_cast<size_t>(info.smem_optin);
-    auto smem_need = [&](int ns) { return static_cast<size_t>(sh.queue ? umma::q_smem_layout(C, ns, sh.ring_rows).total : umma::smem_layout(C, MT, ns).total); };
+    auto smem_need = [&](int ns) { return static_cast<size_t>(sh.queue ? umma::q_smem_layout(C, ns, sh.ring_rows).total : umma::smem_layout(C, MT, ns, sh.count).total); };
     if (sh.queue && smem_need(NS < 3 ? NS : 3) > budget) sh.ring_rows = 32;  // wide documents: shorter rings rather than fewer than three tiles in flight
     while (NS > 2 && smem_need(NS) > budget) --NS;
     sh.NS = smem_need(NS) <= budget ? NS : 0;
@@ -1084,6 +1092,7 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
     sh.lists_bytes = static_cast<size_t>(sh.grid) * umma::EPI_WARPS * 32 * cap * 8;
     sh.parts_bytes = static_cast<size_t>(sh.parts) * nq * k * 8;
     sh.mscratch_bytes = static_cast<size_t>(merge_scratch_parts(sh.parts, k, nq)) * nq * k * 8;
+    if (count) sh.lists_bytes = sh.parts_bytes = sh.mscratch_bytes = 0;  // the counting scan keeps no lists
     *out = sh;
 }
 
@@ -1116,7 +1125,15 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     umma_shape(n, C, nq, k, MT, info, &pl.main, false, sample > 0 && big);
     if (pl.main.NS == 0) return XFBQ_OK;
     pl.sample = sample;
-    if (sample) umma_shape(sample, C, nq, k, MT, info, &pl.pre, true);
+    // Queue-kernel scans are seeded by counting (histogram of the sample's scores, no lists); the list-keeping
+    // sample scan remains for XFBQ_SEED_HIST=0.  A counted sample is nearly free, so it can be larger.
+    const bool count = sample > 0 && pl.main.queue && env_int("XFBQ_SEED_HIST", 1) != 0;
+    if (count && env_int("XFBQ_SAMPLE", -1) < 0) {
+        while (sample < 65536 && n >= 32 * sample) sample <<= 1;
+        pl.sample = sample;
+    }
+    if (sample) umma_shape(sample, C, nq, k, MT, info, &pl.pre, true, true, count);
+    if (sample && pl.pre.NS == 0) return XFBQ_OK;
     size_t off = 0;
     pl.off_qimg = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 128 * C);
     pl.off_qconst = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 4);
@@ -1128,15 +1145,28 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     const bool use_hist = pl.main.queue && sample > 0 && env_int("XFBQ_UMMA_HIST", 1) != 0;
     pl.off_theta0 = off; off = align256(off + (use_hist ? static_cast<size_t>(nq) * 4 : 0));
     pl.off_ghist = off; off = align256(off + (use_hist ? static_cast<size_t>(nq) * umma::HIST_BINS * 4 : 0));
+    pl.off_seedpar = off; off = align256(off + (count ? static_cast<size_t>(nq) * 8 : 0));
+    pl.off_seedhist = off; off = align256(off + (count ? static_cast<size_t>(nq) * umma::SEED_BINS * 4 : 0));
     pl.bytes = off;
     pl.ok = true;
     *plan = pl;
     return XFBQ_OK;
 }
 
+// z with P(N(0,1) > z) = p, by bisection on erfc (host side, once per call)
+double normal_quantile(double p) {
+    if (p >= 0.5) return 0.0;
+    double lo = 0.0, hi = 8.0;
+    for (int i = 0; i < 60; ++i) {
+        const double mid = 0.5 * (lo + hi);
+        if (0.5 * erfc(mid / 1.4142135623730951) > p) lo = mid; else hi = mid;
+    }
+    return 0.5 * (lo + hi);
+}
+
 int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, const void *nib, int64_t n, int C,
                   int64_t nq, int k, int64_t row_offset, const int32_t *tau_init, uint64_t *keys_out, cudaStream_t st) {
-    UmmaKernel kern = pick_umma_kernel(C, sh.MT, sh.queue);
+    UmmaKernel kern = pick_umma_kernel(C, sh.MT, sh.queue, sh.count);
     if (!kern) return fail(XFBQ_E_UNSUPPORTED, "no tcgen05 kernel for C=%d MT=%d", C, sh.MT);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh.smem));
     if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "umma scan smem opt-in (%zu bytes): %s", sh.smem, cudaGetErrorString(e));
@@ -1156,9 +1186,11 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     p.ghist = use_hist ? reinterpret_cast<uint32_t *>(ws + pl.off_ghist) : nullptr;
     p.theta0 = use_hist ? reinterpret_cast<const int32_t *>(ws + pl.off_theta0) : nullptr;
     p.hist_shift = g_hist_shift;
+    p.seed_par = sh.count ? reinterpret_cast<const int2 *>(ws + pl.off_seedpar) : nullptr;
+    p.seed_hist = sh.count ? reinterpret_cast<uint32_t *>(ws + pl.off_seedhist) : nullptr;
     p.prof = (&sh == &pl.main) ? g_prof : nullptr;
     p.debug = env_int("XFBQ_UMMA_DEBUG", 0);
-    if (sh.slots > 1 && !sh.queue) {  // slots a group does not use stay KEY_INF (the queue kernel writes every slice)
+    if (sh.slots > 1 && !sh.queue && !sh.count) {  // slots a group does not use stay KEY_INF (the queue kernel writes every slice)
         e = cudaMemsetAsync(p.out, 0xFF, sh.parts_bytes, st);
         if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
     }
@@ -1167,6 +1199,7 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     kern<<<static_cast<unsigned>(sh.grid), sh.queue ? umma::Q_THREADS : umma::THREADS, sh.smem, st>>>(p);
     if (timed) { cudaEventRecord(g_ev1, st); g_ev_valid = true; }
     if (int rc = check_launch("umma::scan_kernel")) return rc;
+    if (sh.count) return XFBQ_OK;  // histograms only: seed_bounds_kernel follows
     return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st, true);
 }
 
@@ -1182,9 +1215,25 @@ int run_umma(const UmmaPlan &up, unsigned char *ws, const void *nib, int64_t n, 
     if (up.sample) {
         uint64_t *prekeys = reinterpret_cast<uint64_t *>(ws + up.off_prekeys);
         int32_t *tau = reinterpret_cast<int32_t *>(ws + up.off_tau);
-        if (int rc = run_umma_scan(up.pre, up, ws, nib, up.sample, C, nq, k, row_offset, nullptr, prekeys, st)) return rc;
-        mma::tau_from_keys_kernel<<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(prekeys, qconst, nq, k, tau);
-        if (int rc = check_launch("tau_from_keys_kernel")) return rc;
+        if (up.pre.count) {
+            // thresholds by counting: frame per query from 128 sampled scores, 64-bin histogram of the whole sample
+            // on the tensor cores, threshold = lower edge of the bin where the suffix count reaches k
+            int2 *par = reinterpret_cast<int2 *>(ws + up.off_seedpar);
+            uint32_t *hist = reinterpret_cast<uint32_t *>(ws + up.off_seedhist);
+            cudaError_t e = cudaMemsetAsync(hist, 0, static_cast<size_t>(nq) * umma::SEED_BINS * 4, st);
+            if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
+            umma::seed_stats_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(static_cast<const unsigned char *>(nib), qimg, nq, C, up.pre.stages,
+                                                                            static_cast<float>(normal_quantile(static_cast<double>(k) / static_cast<double>(up.sample))),
+                                                                            0.25f * env_int("XFBQ_SEED_BELOW4", 12), par);
+            if (int rc = check_launch("umma::seed_stats_kernel")) return rc;
+            if (int rc = run_umma_scan(up.pre, up, ws, nib, up.sample, C, nq, k, row_offset, nullptr, nullptr, st)) return rc;
+            umma::seed_bounds_kernel<<<static_cast<unsigned>((nq * 32 + 255) / 256), 256, 0, st>>>(hist, par, nq, k, tau);
+            if (int rc = check_launch("umma::seed_bounds_kernel")) return rc;
+        } else {
+            if (int rc = run_umma_scan(up.pre, up, ws, nib, up.sample, C, nq, k, row_offset, nullptr, prekeys, st)) return rc;
+            mma::tau_from_keys_kernel<<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(prekeys, qconst, nq, k, tau);
+            if (int rc = check_launch("tau_from_keys_kernel")) return rc;
+        }
         tau_init = tau;
         if (up.off_ghist > up.off_theta0) {  // global candidate histogram of the main scan, bins measured from the seeded thresholds
             cudaError_t e = cudaMemcpyAsync(ws + up.off_theta0, tau, static_cast<size_t>(nq) * 4, cudaMemcpyDeviceToDevice, st);
