@@ -1128,8 +1128,9 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     // Queue-kernel scans are seeded by counting (histogram of the sample's scores, no lists); the list-keeping
     // sample scan remains for XFBQ_SEED_HIST=0.  A counted sample is nearly free, so it can be larger.
     const bool count = sample > 0 && pl.main.queue && env_int("XFBQ_SEED_HIST", 1) != 0;
-    if (count && env_int("XFBQ_SAMPLE", -1) < 0) {
-        while (sample < 65536 && n >= 32 * sample) sample <<= 1;
+    if (count) {
+        if (env_int("XFBQ_SAMPLE", -1) < 0) while (sample < 65536 && n >= 32 * sample) sample <<= 1;
+        if (sample > umma::SEED_MAX_SAMPLE) sample = umma::SEED_MAX_SAMPLE;
         pl.sample = sample;
     }
     if (sample) umma_shape(sample, C, nq, k, MT, info, &pl.pre, true, true, count);
@@ -1224,7 +1225,7 @@ int run_umma(const UmmaPlan &up, unsigned char *ws, const void *nib, int64_t n, 
             if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
             umma::seed_stats_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(static_cast<const unsigned char *>(nib), qimg, nq, C, up.pre.stages,
                                                                             static_cast<float>(normal_quantile(static_cast<double>(k) / static_cast<double>(up.sample))),
-                                                                            0.25f * env_int("XFBQ_SEED_BELOW4", 12), par);
+                                                                            0.25f * env_int("XFBQ_SEED_BELOW4", 8), par);
             if (int rc = check_launch("umma::seed_stats_kernel")) return rc;
             if (int rc = run_umma_scan(up.pre, up, ws, nib, up.sample, C, nq, k, row_offset, nullptr, nullptr, st)) return rc;
             umma::seed_bounds_kernel<<<static_cast<unsigned>((nq * 32 + 255) / 256), 256, 0, st>>>(hist, par, nq, k, tau);

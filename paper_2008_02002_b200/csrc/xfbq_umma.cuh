@@ -38,7 +38,9 @@ constexpr int ACC_BUFS = 3;      // 3 x 128 accumulator columns; columns 384..51
 constexpr int A_COL0 = ACC_BUFS * STAGE_DOCS;
 constexpr int HIST_BINS = 256;
 constexpr int SEED_BINS = 64;     // bins of the sample histogram that seeds the thresholds
-constexpr int SEED_STRIDE = EPI_WARPS * 32;  // bin-major shared-memory histogram: word b * 256 + thread, so a warp's 32 updates never share a bank
+constexpr int SEED_STRIDE = EPI_WARPS * 32;  // bin-major shared-memory histograms: counter (copy * 64 + bin) * 256 + thread
+__host__ __device__ constexpr int SEED_COPIES(int C) { return C == 4 ? 2 : 4; }  // 16-bit counters: a copy takes 32 KB
+constexpr int64_t SEED_MAX_SAMPLE = 65536;  // a 16-bit counter sees at most sample / copies documents
 constexpr int TAU_OPEN = -(1 << 30);
 constexpr int TAU_NEVER = 1 << 30;     // |acc| <= 512 * 15 * 127 < 2^20, so acc - tau never overflows
 
@@ -177,7 +179,7 @@ __host__ __device__ inline SmemLayout smem_layout(int C, int MT, int NS, bool se
     uint32_t off = 0;
     L.a_off = off; (void)MT;
     L.b_off = off; off += static_cast<uint32_t>(NS) * STAGE_DOCS * 128 * C;
-    L.hist_off = off; off += seed_hist ? SEED_STRIDE * SEED_BINS * 4 : EPI_WARPS * 256 * 4;
+    L.hist_off = off; off += seed_hist ? SEED_COPIES(C) * SEED_STRIDE * SEED_BINS * 2 : EPI_WARPS * 256 * 4;
     L.bar_off = off; off += (2 * NS + 2 * ACC_BUFS) * 8 + 16;
     L.total = off + 1024;  // slack for the manual 1024-byte alignment of the operand area
     return L;
@@ -426,9 +428,15 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
             cta_sync();
             const bool valid = myq < p.nq;
             if constexpr (SEED) {
-                // counting epilogue: this thread's 64 bins live in a shared-memory row of its own
-                uint32_t *bins = reinterpret_cast<uint32_t *>(smem + L.hist_off) + warp * 32 + lane;
-                for (int b = 0; b < SEED_BINS; ++b) bins[b * SEED_STRIDE] = 0;
+                // Counting epilogue.  This thread's bins are 16-bit counters of its own in shared memory, bin-major
+                // (word index (copy * 64 + bin) * 256 + thread: a warp's accesses never conflict), in SEED_COPIES
+                // copies: column j updates copy j % COPIES, so COPIES read-modify-writes are in flight at a time
+                // (plain LDS/ADD/STS: shared-memory atomics -- and the divergent branches ptxas wraps around
+                // predicated ones -- bounded the first version at 11k cycles per stage).
+                constexpr int COPIES = SEED_COPIES(C);
+                const uint32_t bins_s = smem_u32(smem + L.hist_off) + (warp * 32 + lane) * 2;
+                for (int b = 0; b < COPIES * SEED_BINS; ++b)
+                    asm volatile("st.shared.u16 [%0], %1;" ::"r"(bins_s + b * (SEED_STRIDE * 2)), "h"(static_cast<unsigned short>(0)) : "memory");
                 const int2 par = valid ? p.seed_par[myq] : make_int2(TAU_NEVER, 0);
                 const int origin = par.x;
                 const uint32_t magic = static_cast<uint32_t>(par.y);  // bin = floor(d * magic / 2^32): monotone in d
@@ -450,17 +458,34 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
 #pragma unroll
                     for (int c = 0; c < COLS / 32; ++c)
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const int d = v[c][j] - origin;
-                            if (d >= 0 && doc0 + c * 32 + j < n_docs)
-                                atomicAdd(bins + min(__umulhi(static_cast<uint32_t>(d), magic), static_cast<uint32_t>(SEED_BINS - 1)) * SEED_STRIDE, 1u);
+                        for (int j0 = 0; j0 < 32; j0 += COPIES) {
+                            uint32_t addr[COPIES];
+                            unsigned short cur[COPIES], hit[COPIES];
+#pragma unroll
+                            for (int u = 0; u < COPIES; ++u) {
+                                const int d = v[c][j0 + u] - origin;  // d < 0 lands in the last bin with hit = 0
+                                const uint32_t bin = min(__umulhi(static_cast<uint32_t>(d), magic), static_cast<uint32_t>(SEED_BINS - 1));
+                                hit[u] = static_cast<unsigned short>((d >= 0) & (doc0 + c * 32 + j0 + u < n_docs));
+                                addr[u] = bins_s + (u * SEED_BINS + bin) * (SEED_STRIDE * 2);
+                            }
+#pragma unroll
+                            for (int u = 0; u < COPIES; ++u) asm volatile("ld.shared.u16 %0, [%1];" : "=h"(cur[u]) : "r"(addr[u]) : "memory");
+#pragma unroll
+                            for (int u = 0; u < COPIES; ++u)
+                                asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr[u]), "h"(static_cast<unsigned short>(cur[u] + hit[u])) : "memory");
                         }
 #pragma unroll
                     for (int a = 0; a < MT; ++a) ac.advance(ACC_BUFS);
                 }
                 if (valid)
                     for (int b = 0; b < SEED_BINS; ++b) {
-                        const uint32_t c = bins[b * SEED_STRIDE];
+                        uint32_t c = 0;
+#pragma unroll
+                        for (int u = 0; u < COPIES; ++u) {
+                            unsigned short x;
+                            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(x) : "r"(bins_s + (u * SEED_BINS + b) * (SEED_STRIDE * 2)) : "memory");
+                            c += x;
+                        }
                         if (c) atomicAdd(p.seed_hist + myq * SEED_BINS + b, c);
                     }
                 s_run += static_cast<uint32_t>(sg.cnt);
