@@ -1130,7 +1130,7 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     const bool count = sample > 0 && pl.main.queue && env_int("XFBQ_SEED_HIST", 1) != 0;
     if (count) {
         if (env_int("XFBQ_SAMPLE", -1) < 0) while (sample < 65536 && n >= 32 * sample) sample <<= 1;
-        if (sample > umma::SEED_MAX_SAMPLE) sample = umma::SEED_MAX_SAMPLE;
+        if (sample > umma::SEED_MAX_SAMPLE(C)) sample = umma::SEED_MAX_SAMPLE(C);
         pl.sample = sample;
     }
     if (sample) umma_shape(sample, C, nq, k, MT, info, &pl.pre, true, true, count);

@@ -32,3 +32,14 @@ ms, _ = t(lambda: ((kn >> np.uint64(32)).astype(np.int64), (kn & np.uint64(0xFFF
 ms, _ = t(lambda: xs.unpack_keys_device(keys)); print(f"device unpack: {ms:.2f} ms")
 d, i = xs.unpack_keys_device(keys)
 ms, _ = t(lambda: (d.cpu(), i.cpu())); print(f"d.cpu(), i.cpu(): {ms:.2f} ms")
+# per-call times: outliers point at the host side (allocator, scheduler), not at the kernels
+import gc
+times = []
+for _ in range(40):
+    t0 = time.perf_counter(); r = sh.search(qp, k); times.append((time.perf_counter() - t0) * 1e3)
+print("per-call ms:", " ".join(f"{x:.1f}" for x in times))
+gc.disable()
+times = []
+for _ in range(40):
+    t0 = time.perf_counter(); r = sh.search(qp, k); times.append((time.perf_counter() - t0) * 1e3)
+print("per-call ms, gc off:", " ".join(f"{x:.1f}" for x in times))
