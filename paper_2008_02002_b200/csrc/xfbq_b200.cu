@@ -601,6 +601,60 @@ merge_tree_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k,
     for (int i = threadIdx.x; i < k; i += blockDim.x) dst[i] = buf[i];
 }
 
+
+// Bounded merge (tensor engine, seeded scans): bound[q] is a proven lower bound of query q's k-th best score
+// (the shared threshold the scan CTAs tightened), so a partial-result key with a larger distance than
+// Dq - bound cannot be in the answer.  One CTA per query drops those keys while loading -- typically ~k of
+// the parts * k survive -- and sorts only the survivors (next power of two), instead of sorting and tree-merging
+// every row (config 4: 0.47 ms -> see profiles/).  Rows may arrive unsorted.  parts * k <= BOUNDED_MERGE_MAX.
+constexpr int BOUNDED_MERGE_MAX = 4096;
+constexpr int BOUNDED_MERGE_THREADS = 128;
+__global__ void __launch_bounds__(BOUNDED_MERGE_THREADS)
+merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k, const int32_t *__restrict__ bound,
+                     const int32_t *__restrict__ qconst, uint64_t *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t *buf = reinterpret_cast<uint64_t *>(smem_raw);
+    __shared__ int s_cnt;
+    const int64_t q = blockIdx.x;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const int64_t limit = static_cast<int64_t>(qconst[q]) - static_cast<int64_t>(bound[q]);  // largest distance that can still be in the top k
+    const int total = parts * k;
+    for (int e0 = 0; e0 < total; e0 += BOUNDED_MERGE_THREADS) {
+        const int e = e0 + threadIdx.x;
+        uint64_t key = KEY_INF;
+        if (e < total) {
+            const int part = e / k, slot = e - part * k;
+            key = in[(static_cast<int64_t>(part) * nq + q) * k + slot];
+        }
+        const bool keep = key != KEY_INF && static_cast<int64_t>(key >> 32) <= limit;
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        int base = 0;
+        if (lane == 0 && m) base = atomicAdd(&s_cnt, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) buf[base + __popc(m & ((1u << lane) - 1u))] = key;
+    }
+    __syncthreads();
+    const int c = s_cnt;
+    int n2 = 32;
+    while (n2 < c) n2 <<= 1;
+    for (int i = c + threadIdx.x; i < n2; i += BOUNDED_MERGE_THREADS) buf[i] = KEY_INF;
+    __syncthreads();
+    for (int size = 2; size <= n2; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < (n2 >> 1); t += BOUNDED_MERGE_THREADS) {
+                const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t a = buf[lo], b = buf[hi];
+                if ((a > b) == up) { buf[lo] = b; buf[hi] = a; }
+            }
+            __syncthreads();
+        }
+    uint64_t *dst = out + q * k;
+    for (int i = threadIdx.x; i < k; i += BOUNDED_MERGE_THREADS) dst[i] = i < c ? buf[i] : KEY_INF;
+}
+
 }  // namespace
 #include "xfbq_mma.cuh"
 #include "xfbq_umma.cuh"
@@ -1201,6 +1255,13 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     if (timed) { cudaEventRecord(g_ev1, st); g_ev_valid = true; }
     if (int rc = check_launch("umma::scan_kernel")) return rc;
     if (sh.count) return XFBQ_OK;  // histograms only: seed_bounds_kernel follows
+    if (p.theta_g && sh.parts > 1 && sh.parts * k <= BOUNDED_MERGE_MAX && env_int("XFBQ_MERGE_BOUNDED", 1)) {
+        int n2 = 32;
+        while (n2 < sh.parts * k) n2 <<= 1;
+        merge_bounded_kernel<<<static_cast<unsigned>(nq), BOUNDED_MERGE_THREADS, static_cast<size_t>(n2) * 8, st>>>(
+            p.out, sh.parts, nq, k, p.theta_g, p.qconst, keys_out);
+        return check_launch("merge_bounded_kernel");
+    }
     return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st, true);
 }
 
