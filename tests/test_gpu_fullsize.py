@@ -94,3 +94,8 @@ def test_batch_engines_agree_at_full_size(corpus, monkeypatch):
     monkeypatch.setenv("XFBQ_ENGINE", "umma")
     s2, i2 = xb.search(idx, queries, K)
     assert torch.equal(s2, base_s) and torch.equal(i2, base_i)
+    # the pieces of the seeded route against their predecessors: list-keeping sample scan, tree merge
+    for key in ("XFBQ_SEED_HIST", "XFBQ_MERGE_BOUNDED"):
+        monkeypatch.setenv(key, "0")
+        s3, i3 = xb.search(idx, q, K)
+        assert torch.equal(s3, su) and torch.equal(i3, iu)

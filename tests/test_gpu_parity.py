@@ -189,6 +189,33 @@ def test_tensor_engines_ragged_shapes(engine, n, dim, wd, nq, k, monkeypatch):
     assert np.array_equal(scores.astype(np.uint64), want_d) and np.array_equal(ids, want_i)
 
 
+_SEEDED = {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SAMPLE": "4096"}
+
+
+@pytest.mark.parametrize("extra", [{}, {"XFBQ_SEED_BELOW4": "0"}, {"XFBQ_SEED_BELOW4": "40"}, {"XFBQ_MERGE_BOUNDED": "0"},
+                                   {"XFBQ_SEED_HIST": "0"}, {"XFBQ_UMMA_SLICES": "3", "XFBQ_GRID": "9"},
+                                   {"XFBQ_UMMA_SHARE": "0"}, {"XFBQ_UMMA_HIST": "0"}])
+@pytest.mark.parametrize("n,dim,wd,nq,k", [(70000, 256, 4, 1000, 100), (70001, 128, 3, 600, 10), (80000, 512, 4, 300, 50)])
+def test_counted_seed_queue_scan_and_bounded_merge(extra, n, dim, wd, nq, k, monkeypatch):
+    """The route full-size batches take, forced onto a corpus the CPU oracle can check: thresholds seeded by
+    counting the sample's scores into per-query histograms, the queue kernel over document slices with the
+    shared candidate histogram, and the merge that drops keys beyond the proven bound.  The variants move the
+    histogram frame to where it misses for many queries (open thresholds) or catches everything in the last
+    bin, and switch each piece back to its predecessor: thresholds only ever prune, the keys never change."""
+    docs = xo.synthetic_unit_rows(n, dim, 21 + n)
+    queries = xo.synthetic_unit_rows(nq, dim, 22 + n)
+    scale = xo.estimate_scale(docs, 0.98)
+    params = xb.QuantParams(dim=dim, scale=scale, doc_bits=wd, query_bits=4)
+    idx = xb.build_index(docs, params, keep_originals=False)
+    for key, val in {**_SEEDED, **extra}.items():
+        monkeypatch.setenv(key, val)
+    scores, ids = xb.search(idx, queries, k)
+    planes = xo.c_quantize_matrix(docs, wd, scale)
+    qp = xo.c_quantize_matrix(queries.astype(np.float64), 4, scale).transpose(2, 0, 1)
+    want_d, want_i = xo.c_search(planes, qp, k)
+    assert np.array_equal(scores.astype(np.uint64), want_d) and np.array_equal(ids, want_i)
+
+
 @pytest.mark.parametrize("width", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_fast_float32_quantizer_on_code_boundaries(width, monkeypatch):
     """The float32-first quantizer (exact float64 redo near code boundaries) against the CPU oracle and the
