@@ -604,31 +604,63 @@ merge_tree_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k,
 
 // Bounded merge (tensor engine, seeded scans): bound[q] is a proven lower bound of query q's k-th best score
 // (the shared threshold the scan CTAs tightened), so a partial-result key with a larger distance than
-// Dq - bound cannot be in the answer.  One CTA per query drops those keys while loading -- typically ~k of
-// the parts * k survive -- and sorts only the survivors (next power of two), instead of sorting and tree-merging
-// every row (config 4: 0.47 ms -> see profiles/).  Rows may arrive unsorted.  parts * k <= BOUNDED_MERGE_MAX.
-constexpr int BOUNDED_MERGE_MAX = 4096;
-constexpr int BOUNDED_MERGE_THREADS = 128;
-__global__ void __launch_bounds__(BOUNDED_MERGE_THREADS)
-merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k, const int32_t *__restrict__ bound,
+// Dq - bound cannot be in the answer.  One CTA per query drops those keys while loading -- typically little
+// more than k of the parts * k survive -- and sorts only the survivors (next power of two), instead of sorting
+// and tree-merging every row (config 4: 0.47 ms -> 0.05 ms).  Rows may arrive unsorted.  Exact for any number of
+// survivors: when the buffer of B keys could overflow it is sorted, cut back to its k best, and the bound
+// tightens to the k-th of those.  B is a power of two >= k + blockDim.x.
+__global__ void __launch_bounds__(512)
+merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k, int B, const int32_t *__restrict__ bound,
                      const int32_t *__restrict__ qconst, uint64_t *__restrict__ out) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t *buf = reinterpret_cast<uint64_t *>(smem_raw);
     __shared__ int s_cnt;
+    __shared__ long long s_limit;
     const int64_t q = blockIdx.x;
-    const int lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
-    const int64_t limit = static_cast<int64_t>(qconst[q]) - static_cast<int64_t>(bound[q]);  // largest distance that can still be in the top k
-    const int total = parts * k;
-    for (int e0 = 0; e0 < total; e0 += BOUNDED_MERGE_THREADS) {
-        const int e = e0 + threadIdx.x;
+    const int lane = threadIdx.x & 31, nt = blockDim.x;
+    if (threadIdx.x == 0) {
+        s_cnt = 0;
+        s_limit = static_cast<long long>(qconst[q]) - static_cast<long long>(bound[q]);  // largest distance that can still be in the top k
+    }
+    auto sort_prefix = [&](int c) {  // ascending sort of buf[0, c), padded to a power of two; ends on a barrier
+        int n2 = 32;
+        while (n2 < c) n2 <<= 1;
+        for (int i = c + threadIdx.x; i < n2; i += nt) buf[i] = KEY_INF;
+        __syncthreads();
+        for (int size = 2; size <= n2; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int t = threadIdx.x; t < (n2 >> 1); t += nt) {
+                    const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+                    const bool up = (lo & size) == 0;
+                    const uint64_t a = buf[lo], b = buf[hi];
+                    if ((a > b) == up) { buf[lo] = b; buf[hi] = a; }
+                }
+                __syncthreads();
+            }
+    };
+    const int64_t total = static_cast<int64_t>(parts) * k;
+    for (int64_t e0 = 0; e0 < total; e0 += nt) {
+        __syncthreads();
+        const int c = s_cnt;
+        if (c + nt > B) {  // the next round of appends could overflow: keep the k best, tighten the bound
+            sort_prefix(c);
+            if (threadIdx.x == 0) {
+                s_cnt = c < k ? c : k;
+                if (c >= k) {
+                    const long long kth = static_cast<long long>(buf[k - 1] >> 32);
+                    if (kth < s_limit) s_limit = kth;
+                }
+            }
+            __syncthreads();
+        }
+        const long long limit = s_limit;
+        const int64_t e = e0 + threadIdx.x;
         uint64_t key = KEY_INF;
         if (e < total) {
-            const int part = e / k, slot = e - part * k;
-            key = in[(static_cast<int64_t>(part) * nq + q) * k + slot];
+            const int64_t part = e / k, slot = e - part * k;
+            key = in[(part * nq + q) * k + slot];
         }
-        const bool keep = key != KEY_INF && static_cast<int64_t>(key >> 32) <= limit;
+        const bool keep = key != KEY_INF && static_cast<long long>(key >> 32) <= limit;
         const unsigned m = __ballot_sync(0xffffffffu, keep);
         int base = 0;
         if (lane == 0 && m) base = atomicAdd(&s_cnt, __popc(m));
@@ -637,22 +669,9 @@ merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int
     }
     __syncthreads();
     const int c = s_cnt;
-    int n2 = 32;
-    while (n2 < c) n2 <<= 1;
-    for (int i = c + threadIdx.x; i < n2; i += BOUNDED_MERGE_THREADS) buf[i] = KEY_INF;
-    __syncthreads();
-    for (int size = 2; size <= n2; size <<= 1)
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int t = threadIdx.x; t < (n2 >> 1); t += BOUNDED_MERGE_THREADS) {
-                const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
-                const bool up = (lo & size) == 0;
-                const uint64_t a = buf[lo], b = buf[hi];
-                if ((a > b) == up) { buf[lo] = b; buf[hi] = a; }
-            }
-            __syncthreads();
-        }
+    sort_prefix(c);
     uint64_t *dst = out + q * k;
-    for (int i = threadIdx.x; i < k; i += BOUNDED_MERGE_THREADS) dst[i] = i < c ? buf[i] : KEY_INF;
+    for (int i = threadIdx.x; i < k; i += nt) dst[i] = i < c ? buf[i] : KEY_INF;
 }
 
 }  // namespace
@@ -1255,11 +1274,18 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     if (timed) { cudaEventRecord(g_ev1, st); g_ev_valid = true; }
     if (int rc = check_launch("umma::scan_kernel")) return rc;
     if (sh.count) return XFBQ_OK;  // histograms only: seed_bounds_kernel follows
-    if (p.theta_g && sh.parts > 1 && sh.parts * k <= BOUNDED_MERGE_MAX && env_int("XFBQ_MERGE_BOUNDED", 1)) {
-        int n2 = 32;
-        while (n2 < sh.parts * k) n2 <<= 1;
-        merge_bounded_kernel<<<static_cast<unsigned>(nq), BOUNDED_MERGE_THREADS, static_cast<size_t>(n2) * 8, st>>>(
-            p.out, sh.parts, nq, k, p.theta_g, p.qconst, keys_out);
+    if (p.theta_g && sh.parts > 1 && env_int("XFBQ_MERGE_BOUNDED", 1)) {
+        int B = 512;
+        while (B < 4 * k) B <<= 1;  // k <= 1024 on this engine: at most 8192 keys = 64 KB
+        int threads = B / 4 > 512 ? 512 : B / 4;
+        const int want = env_int("XFBQ_MERGE_BUF", 0);  // tests: a small buffer forces the overflow path (power of two >= k + threads)
+        if (want >= k + threads && (want & (want - 1)) == 0) B = want;
+        const size_t smem = static_cast<size_t>(B) * 8;
+        if (smem > 48 * 1024) {
+            e = cudaFuncSetAttribute(merge_bounded_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "merge smem opt-in: %s", cudaGetErrorString(e));
+        }
+        merge_bounded_kernel<<<static_cast<unsigned>(nq), threads, smem, st>>>(p.out, sh.parts, nq, k, B, p.theta_g, p.qconst, keys_out);
         return check_launch("merge_bounded_kernel");
     }
     return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st, true);

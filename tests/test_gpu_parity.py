@@ -194,7 +194,8 @@ _SEEDED = {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SAMPLE": "
 
 @pytest.mark.parametrize("extra", [{}, {"XFBQ_SEED_BELOW4": "0"}, {"XFBQ_SEED_BELOW4": "40"}, {"XFBQ_MERGE_BOUNDED": "0"},
                                    {"XFBQ_SEED_HIST": "0"}, {"XFBQ_UMMA_SLICES": "3", "XFBQ_GRID": "9"},
-                                   {"XFBQ_UMMA_SHARE": "0"}, {"XFBQ_UMMA_HIST": "0"}])
+                                   {"XFBQ_UMMA_SHARE": "0"}, {"XFBQ_UMMA_HIST": "0"},
+                                   {"XFBQ_MERGE_BUF": "256", "XFBQ_UMMA_SLICES": "6", "XFBQ_SEED_BELOW4": "0"}])
 @pytest.mark.parametrize("n,dim,wd,nq,k", [(70000, 256, 4, 1000, 100), (70001, 128, 3, 600, 10), (80000, 512, 4, 300, 50)])
 def test_counted_seed_queue_scan_and_bounded_merge(extra, n, dim, wd, nq, k, monkeypatch):
     """The route full-size batches take, forced onto a corpus the CPU oracle can check: thresholds seeded by
