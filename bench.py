@@ -369,7 +369,7 @@ def run_ours(a):
     if (a.n, a.dim, a.nq, a.k, a.doc_bits, world) == (10_000_000, 256, 10000, 100, 4, 1):
         try:
             import csv
-            with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_full_umma_queue_r1_v12.csv")) as f:
+            with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_full_umma_queue_r1_v13.csv")) as f:
                 rows = list(csv.reader(f))
             col = {h: i for i, h in enumerate(rows[0])}
             unit = {h: u for h, u in zip(rows[0], rows[1])}
@@ -407,7 +407,7 @@ def run_ours(a):
                                 "imma": "mma::scan_kernel (batch plan: IMMA.16832 + fused top-K)"}.get(engine, "scan_topk_kernel"),
                      "achieved": round(tops, 1), "peak": round(int8_peak, 1), "unit": "TOP/s (int8, dense)",
                      "frac": round(tops / int8_peak, 4), "traffic": traffic,
-                     "traffic_source": "profiles/ncu_full_umma_queue_r1_v12.csv (dram__bytes_read.sum + dram__bytes_write.sum of this launch)" if traffic else None,
+                     "traffic_source": "profiles/ncu_full_umma_queue_r1_v13.csv (dram__bytes_read.sum + dram__bytes_write.sum of this launch)" if traffic else None,
                      "frac_of_hw_int8_pipe": round(tops / (2 * 8192 * 148 * 1.965e9 / 1e12), 4),
                      "peak_source": peak_src + ": 2 x dense bf16 burst = int8 rate of the tcgen05 path",
                      "launch_ms": round(kernel_ms, 3), "macs_per_launch": int(macs_per_launch),
