@@ -1055,6 +1055,7 @@ struct UmmaShape {
     int MT = 2, DW = 1, groups = 1, grid = 1, slots = 1, parts = 1, cap = 0, NS = 0;
     bool queue = false;  // scan_queue_kernel (main scans) vs scan_kernel (sample scans: open thresholds)
     bool count = false;  // sample scan that only counts scores into per-query histograms (scan_kernel<.., SEED = true>)
+    int64_t tile_stride = 1, n_valid = 0;  // counting scan: stage i reads tile i * tile_stride of a database of n_valid documents
     int ring_rows = 64;
     int n_seg = 1, seg_stages = 0;  // queue kernel: document slices (= partial results per query) and stages per slice
     int64_t stages = 0, nq_pad = 0, n_pad = 0;
@@ -1208,6 +1209,11 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     }
     if (sample) umma_shape(sample, C, nq, k, MT, info, &pl.pre, true, true, count);
     if (sample && pl.pre.NS == 0) return XFBQ_OK;
+    if (count) {  // the counted sample is spread over the whole database (every stride-th tile)
+        pl.pre.tile_stride = env_int("XFBQ_SEED_SPREAD", 1) ? pl.main.stages / pl.pre.stages : 1;
+        if (pl.pre.tile_stride < 1) pl.pre.tile_stride = 1;
+        pl.pre.n_valid = n;
+    }
     size_t off = 0;
     pl.off_qimg = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 128 * C);
     pl.off_qconst = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 4);
@@ -1246,7 +1252,8 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "umma scan smem opt-in (%zu bytes): %s", sh.smem, cudaGetErrorString(e));
     umma::Params p;
     p.db = nib;  // byte tiles (the caller passes the tile region of the derived buffer)
-    p.n = n; p.n_pad = sh.n_pad; p.row_offset = row_offset;
+    p.n = sh.count ? sh.n_valid : n; p.n_pad = sh.n_pad; p.row_offset = row_offset;
+    p.tile_stride = sh.count ? sh.tile_stride : 1;
     p.qimg = ws + pl.off_qimg;
     p.qconst = reinterpret_cast<const int32_t *>(ws + pl.off_qconst);
     p.tau_init = tau_init;
@@ -1310,7 +1317,7 @@ int run_umma(const UmmaPlan &up, unsigned char *ws, const void *nib, int64_t n, 
             uint32_t *hist = reinterpret_cast<uint32_t *>(ws + up.off_seedhist);
             cudaError_t e = cudaMemsetAsync(hist, 0, static_cast<size_t>(nq) * umma::SEED_BINS * 4, st);
             if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
-            umma::seed_stats_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(static_cast<const unsigned char *>(nib), qimg, nq, C, up.pre.stages,
+            umma::seed_stats_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(static_cast<const unsigned char *>(nib), qimg, nq, C, up.pre.stages, up.pre.tile_stride,
                                                                             static_cast<float>(normal_quantile(static_cast<double>(k) / static_cast<double>(up.sample))),
                                                                             0.25f * env_int("XFBQ_SEED_BELOW4", 8), par);
             if (int rc = check_launch("umma::seed_stats_kernel")) return rc;

@@ -54,7 +54,9 @@ struct Params {
     uint32_t *ghist;           // [nq][HIST_BINS] global histogram of every candidate appended to any list (queue kernel), or nullptr
     const int32_t *theta0;     // [nq] the seeded thresholds the histogram bins are measured from
     int hist_shift;            // bin width = 1 << hist_shift score units
-    const int2 *seed_par;      // sample-histogram kernel: per query (origin, shift) of its 64 score bins
+    const int2 *seed_par;      // sample-histogram kernel: per query (origin, reciprocal bin width * 2^32) of its 64 score bins
+    int64_t tile_stride;       // sample-histogram kernel: stage i reads byte tile i * tile_stride (the sample is spread over the whole database,
+                               // so an ordered or clustered database still gives representative thresholds); n counts the real documents
     uint32_t *seed_hist;       // sample-histogram kernel: [nq][SEED_BINS] counts of sample scores >= origin
     uint64_t *lists;           // [grid][EPI_WARPS][32][cap]
     uint64_t *out;             // [slots * DW][nq][k], KEY_INF pre-filled when slots > 1
@@ -447,7 +449,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                     mbar_wait_prof(&acc_full[buf], ac.phase, prof, w0);
                     fence_after();
                     const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + buf * STAGE_DOCS + col0;
-                    const uint32_t doc0 = static_cast<uint32_t>(sg.sd0 + i) * STAGE_DOCS + col0;
+                    const uint32_t doc0 = static_cast<uint32_t>((sg.sd0 + i) * p.tile_stride) * STAGE_DOCS + col0;
                     int v[COLS / 32][32];
 #pragma unroll
                     for (int c = 0; c < COLS / 32; ++c) tmem_ld32(taddr + c * 32, v[c]);
@@ -677,7 +679,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                 for (int i = 0; i < sg.cnt; ++i) {
                     mbar_wait_prof(&b_empty[rb.idx], rb.phase, prof, w0);
                     mma::mbar_arrive_expect_tx(&b_full[rb.idx], B_STAGE);
-                    mma::tma_bulk_g2s(sB + static_cast<size_t>(rb.idx) * B_STAGE, db + static_cast<int64_t>(sg.sd0 + i) * B_STAGE, B_STAGE, &b_full[rb.idx]);
+                    mma::tma_bulk_g2s(sB + static_cast<size_t>(rb.idx) * B_STAGE, db + static_cast<int64_t>(sg.sd0 + i) * (SEED ? p.tile_stride : 1) * B_STAGE, B_STAGE, &b_full[rb.idx]);
                     rb.advance(NS);
                 }
             }
@@ -694,15 +696,15 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
 
 // ------------------------------------------------------------------------------ threshold seeding by counting
 // seed_stats_kernel: one block of 128 threads per query scores 128 documents spread over the sample (row i of
-// every (tiles/128)-th byte tile) with dp4a, and turns mean and deviation of those scores into the query's bin
+// every (tiles/128)-th sampled byte tile) with dp4a, and turns mean and deviation of those scores into the query's bin
 // frame: origin = mean + (z - 3) sigma, 64 bins of sigma/16, where z is the normal quantile of the k-th best of
 // the sample.  The frame only has to bracket the k-th best sample score; any frame gives a VALID threshold
 // (bins count real documents), a poor one a loose or open threshold.
 __global__ void __launch_bounds__(128) seed_stats_kernel(const unsigned char *__restrict__ tiles, const unsigned char *__restrict__ qimg,
-                                                         int64_t nq, int C, int64_t sample_tiles, float z, float below, int2 *__restrict__ par) {
+                                                         int64_t nq, int C, int64_t sample_tiles, int64_t tile_stride, float z, float below, int2 *__restrict__ par) {
     const int64_t q = blockIdx.x;
     const int r = threadIdx.x;
-    const int64_t t = static_cast<int64_t>(r) * sample_tiles / 128;
+    const int64_t t = (static_cast<int64_t>(r) * sample_tiles / 128) * tile_stride;
     const unsigned char *tile = tiles + t * (static_cast<int64_t>(STAGE_DOCS) * 128 * C);
     const uint4 *qrow = reinterpret_cast<const uint4 *>(qimg + q * (128 * C));
     int acc = 0;
