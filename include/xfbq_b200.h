@@ -117,6 +117,17 @@ int xfbq_batch_distances(const void *db_dev, int64_t n, int64_t dim, int doc_bit
                          const uint32_t *q_dev, int query_bits, uint64_t *out_dev, void *stream);
 
 /*
+ * Candidate gather of k_select (search.py:206-216 after the histogram threshold, _kernels.py:56-69 for the
+ * distances): one pass over the codes for one packed query, no distance array.  *count_out_dev (device
+ * uint64, zeroed by the call) receives the number of documents with distance <= threshold; when
+ * ids_out_dev is not NULL the first min(count, cap) of their row ids are written to it in no particular
+ * order (the caller sorts: search.py:129-131).  count > cap means the id list is incomplete.
+ */
+int xfbq_collect_candidates(const void *db_dev, int64_t n, int64_t dim, int doc_bits, const uint32_t *q_dev,
+                            int query_bits, int64_t threshold, int64_t *ids_out_dev, int64_t cap,
+                            uint64_t *count_out_dev, void *stream);
+
+/*
  * Fused scan + top-K: for each of nq queries the k smallest keys
  * (distance << 32 | row_offset + row) over the n documents, ascending, written
  * to keys_out_dev[nq][k] (slots beyond min(k, n) hold UINT64_MAX).  No score

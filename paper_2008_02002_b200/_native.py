@@ -31,7 +31,7 @@ SYMBOLS = [
     "xfbq_abi_version", "xfbq_last_error", "xfbq_chunks128", "xfbq_db_bytes", "xfbq_query_bytes",
     "xfbq_distance_upper_bound", "xfbq_quantize_pack_f32", "xfbq_quantize_pack_f64",
     "xfbq_quantize_queries_f32", "xfbq_quantize_queries_f64", "xfbq_planes_to_bundles",
-    "xfbq_bundles_to_planes", "xfbq_nibble_bytes", "xfbq_planes_to_nibbles", "xfbq_batch_distances", "xfbq_scan_workspace_bytes",
+    "xfbq_bundles_to_planes", "xfbq_nibble_bytes", "xfbq_planes_to_nibbles", "xfbq_batch_distances", "xfbq_collect_candidates", "xfbq_scan_workspace_bytes",
     "xfbq_scan_plan", "xfbq_scan_topk", "xfbq_merge_topk", "xfbq_unpack_keys", "xfbq_set_timing", "xfbq_last_scan_ms", "xfbq_launch_count", "xfbq_debug_profile",
 ]
 
@@ -99,6 +99,7 @@ def lib():
         "xfbq_planes_to_bundles": (i32, [vp, i64, i64, i32, vp, vp]),
         "xfbq_bundles_to_planes": (i32, [vp, i64, i64, i32, vp, vp]),
         "xfbq_batch_distances": (i32, [vp, i64, i64, i32, vp, i32, vp, vp]),
+        "xfbq_collect_candidates": (i32, [vp, i64, i64, i32, vp, i32, i64, vp, i64, vp, vp]),
         "xfbq_nibble_bytes": (i64, [i64, i64]),
         "xfbq_planes_to_nibbles": (i32, [vp, i64, i64, i32, vp, vp]),
         "xfbq_scan_workspace_bytes": (i64, [i64, i64, i32, i64, i32, i32, i32]),

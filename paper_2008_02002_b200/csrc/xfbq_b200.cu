@@ -359,6 +359,34 @@ batch_distances_kernel(const uint4 *__restrict__ db, int64_t n, int wd, int C,
     }
 }
 
+// Candidate gather of k_select (search.py:206-216: histogram threshold, then every row with d <= threshold):
+// one pass over the codes, no distance array.  counts[0] += rows with d <= threshold; the first `cap` of them
+// (in no particular order) go to ids_out.
+__global__ void __launch_bounds__(256)
+collect_candidates_kernel(const uint4 *__restrict__ db, int64_t n, int wd, int C, const uint32_t *__restrict__ q, int wq,
+                          uint32_t threshold, int64_t *__restrict__ ids_out, int64_t cap, unsigned long long *__restrict__ counts) {
+    extern __shared__ __align__(16) uint32_t qs_dyn[];
+    const int qwords = wq * C * 4;
+    for (int t = threadIdx.x; t < qwords; t += blockDim.x) qs_dyn[t] = q[t];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nb = (n + 31) >> 5;
+    const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t b = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nb; b += warps) {
+        const int64_t doc = b * 32 + lane;
+        const uint32_t d = distance_generic(db + b * wd * C * 32 + lane, wd, C, qs_dyn, wq);
+        const bool hit = doc < n && d <= threshold;
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (m) {
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(counts, static_cast<unsigned long long>(__popc(m)));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            const int64_t pos = static_cast<int64_t>(base) + __popc(m & ((1u << lane) - 1u));
+            if (hit && ids_out && pos < cap) ids_out[pos] = doc;
+        }
+    }
+}
+
 // ----------------------------------------------------------------------------------------------
 // Top-K selection state of one CTA: per query slot a candidate list in shared memory, a count
 // and a threshold key.  A score enters the list only if its key (distance<<32 | row id) is below
@@ -1534,6 +1562,30 @@ XFBQ_API int xfbq_batch_distances(const void *db, int64_t n, int64_t dim, int wd
     batch_distances_kernel<<<static_cast<unsigned>(blocks), 256, smem, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const uint4 *>(db), n, wd, C, q, wq, out);
     return check_launch("batch_distances_kernel");
+}
+
+XFBQ_API int xfbq_collect_candidates(const void *db, int64_t n, int64_t dim, int wd, const uint32_t *q, int wq,
+                                     int64_t threshold, int64_t *ids_out, int64_t cap, uint64_t *count_out, void *stream) {
+    if (!width_ok(wd) || !width_ok(wq)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d/%d", wd, wq);
+    if (n < 0 || dim < 1 || cap < 0) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld cap=%lld", (long long)n, (long long)dim, (long long)cap);
+    if (!count_out) return fail(XFBQ_E_INVALID, "null pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(count_out, 0, 8, st);
+    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
+    if (n == 0 || threshold < 0) return XFBQ_OK;
+    if (!db || !q) return fail(XFBQ_E_INVALID, "null pointer");
+    DeviceInfo info;
+    if (int rc = device_info(&info)) return rc;
+    const int C = static_cast<int>(chunks128(dim));
+    const size_t smem = static_cast<size_t>(wq) * C * 16;
+    if (smem > 48 * 1024) return fail(XFBQ_E_UNSUPPORTED, "dim %lld too large for collect_candidates", (long long)dim);
+    int64_t blocks = (bundles_of(n) + 7) / 8;
+    const int64_t max_blocks = static_cast<int64_t>(info.sms) * 8;
+    if (blocks > max_blocks) blocks = max_blocks;
+    const uint32_t thr = threshold > 0xFFFFFFFFll ? 0xFFFFFFFFu : static_cast<uint32_t>(threshold);
+    collect_candidates_kernel<<<static_cast<unsigned>(blocks), 256, smem, st>>>(
+        static_cast<const uint4 *>(db), n, wd, C, q, wq, thr, ids_out, ids_out ? cap : 0, reinterpret_cast<unsigned long long *>(count_out));
+    return check_launch("collect_candidates_kernel");
 }
 
 XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, int have_nibbles) {

@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _native
 from .bitplane import PackedMatrix, _is_torch, _stream_ptr, quantize_queries, quantize_vector
-from .distance import batch_distances_device, decode_inner_product_values, distance_upper_bound
+from .distance import collect_candidates_device, decode_inner_product_values, distance_upper_bound
 from .errors import DimensionMismatchError, InvalidInputError
 from .index import Index
 
@@ -192,14 +192,14 @@ def k_select(index: Index, request: SearchRequest, collect_timing: bool = False)
     packed_query = quantize_vector(request.query, p.query_bits, p.scale)
     qwords = packed_query.device_words()
     sync(); t1 = time.perf_counter()
-    dists = batch_distances_device(index.packed, packed_query)          # int64[n] on device
     keys = scan_topk_device(index.packed, qwords.view(torch.int32), 1, p.query_bits, kk)
-    top_d, top_i = unpack_keys_device(keys)
-    top_d, top_i = top_d[0].cpu().numpy(), top_i[0].cpu().numpy()
+    top_d, top_i = to_host_arrays(*(t[0] for t in unpack_keys_device(keys)))
     sync(); t2 = time.perf_counter()
-    threshold = int(top_d[kk - 1]) + int(request.extra_distance)        # search.py:211-213
-    cand_mask = dists <= min(threshold, upper)
-    candidate_count = int(cand_mask.sum())
+    # the k-th smallest distance IS the reference's histogram threshold (search.py:206-213); the gather is one
+    # more pass over the codes (no distance array): count, and row ids when they are re-ranked
+    threshold = int(top_d[kk - 1]) + int(request.extra_distance)
+    candidate_count, cand = collect_candidates_device(index.packed, packed_query, min(threshold, upper),
+                                                      want_ids=index.originals is not None, cap=max(1 << 16, 4 * kk))
     sync(); t3 = time.perf_counter()
     if index.originals is None:
         sims = decode_inner_product_values(top_d, p.dim, p.doc_bits, p.query_bits)
@@ -207,7 +207,6 @@ def k_select(index: Index, request: SearchRequest, collect_timing: bool = False)
         hits = [(int(i), float(s)) for i, s in zip(top_i, sims)]
         approximate = True
     else:
-        cand = torch.nonzero(cand_mask).flatten()
         rows = _originals_device(index)[cand].to(torch.float64)
         q64 = torch.from_numpy(request.query).to(rows.device)
         sims = (rows @ q64).cpu().numpy()                               # search.py:153-157

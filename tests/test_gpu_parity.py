@@ -189,6 +189,29 @@ def test_tensor_engines_ragged_shapes(engine, n, dim, wd, nq, k, monkeypatch):
     assert np.array_equal(scores.astype(np.uint64), want_d) and np.array_equal(ids, want_i)
 
 
+def test_collect_candidates_matches_distance_array():
+    """The one-pass candidate gather of k_select (count + row ids of d <= threshold, no distance array) against
+    the materialised distances, for thresholds from 'nothing' to 'everything'; a small id buffer forces the
+    second pass."""
+    import torch
+    from paper_2008_02002_b200.distance import batch_distances_device, collect_candidates_device
+    c = synth_case("cfg3_50k_200_w4")
+    params = xb.QuantParams(dim=c["dim"], scale=c["scale"], doc_bits=c["wd"], query_bits=c["wq"])
+    idx = xb.build_index(c["docs"], params, keep_originals=False)
+    upper = xb.distance_upper_bound(c["dim"], c["wd"], c["wq"])
+    for qi in (0, 3):
+        pq = xb.quantize_vector(c["queries"][qi], c["wq"], c["scale"])
+        d = batch_distances_device(idx.packed, pq)
+        srt = torch.sort(d).values
+        for thr in (-1, 0, int(srt[0]) - 1, int(srt[0]), int(srt[9]), int(srt[999]), int(srt[-1]), upper):
+            count, ids = collect_candidates_device(idx.packed, pq, thr, want_ids=True, cap=16)
+            want = torch.nonzero(d <= thr).flatten()
+            assert count == want.numel()
+            assert torch.equal(torch.sort(ids).values, want)
+            count_only, none = collect_candidates_device(idx.packed, pq, thr, want_ids=False)
+            assert count_only == count and none is None
+
+
 _SEEDED = {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SAMPLE": "4096"}
 
 
