@@ -387,6 +387,36 @@ collect_candidates_kernel(const uint4 *__restrict__ db, int64_t n, int wd, int C
     }
 }
 
+// Same, for the common widths: the document's words are loaded first (WD * C independent LDG.128), the
+// weight classes accumulate in registers.
+template <int WD, int WQ, int C>
+__global__ void __launch_bounds__(256)
+collect_candidates_fast_kernel(const uint4 *__restrict__ db, int64_t n, const uint32_t *__restrict__ q, uint32_t threshold,
+                               int64_t *__restrict__ ids_out, int64_t cap, unsigned long long *__restrict__ counts) {
+    __shared__ __align__(16) uint32_t qs[WQ * C * 4];
+    for (int t = threadIdx.x; t < WQ * C * 4; t += blockDim.x) qs[t] = q[t];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nb = (n + 31) >> 5;
+    const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t b = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); b < nb; b += warps) {
+        const int64_t doc = b * 32 + lane;
+        uint4 x[WD * C];
+#pragma unroll
+        for (int e = 0; e < WD * C; ++e) x[e] = __ldg(db + (b * (WD * C) + e) * 32 + lane);
+        const uint32_t d = distance_regs<WD, WQ, C>(x, qs);
+        const bool hit = doc < n && d <= threshold;
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (m) {
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(counts, static_cast<unsigned long long>(__popc(m)));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            const int64_t pos = static_cast<int64_t>(base) + __popc(m & ((1u << lane) - 1u));
+            if (hit && ids_out && pos < cap) ids_out[pos] = doc;
+        }
+    }
+}
+
 // ----------------------------------------------------------------------------------------------
 // Top-K selection state of one CTA: per query slot a candidate list in shared memory, a count
 // and a threshold key.  A score enters the list only if its key (distance<<32 | row id) is below
@@ -1583,6 +1613,17 @@ XFBQ_API int xfbq_collect_candidates(const void *db, int64_t n, int64_t dim, int
     const int64_t max_blocks = static_cast<int64_t>(info.sms) * 8;
     if (blocks > max_blocks) blocks = max_blocks;
     const uint32_t thr = threshold > 0xFFFFFFFFll ? 0xFFFFFFFFu : static_cast<uint32_t>(threshold);
+    typedef void (*FastKernel)(const uint4 *, int64_t, const uint32_t *, uint32_t, int64_t *, int64_t, unsigned long long *);
+    FastKernel fast = nullptr;
+#define XFBQ_CASE(WD_, WQ_, C_) if (wd == WD_ && wq == WQ_ && C == C_) fast = collect_candidates_fast_kernel<WD_, WQ_, C_>;
+    XFBQ_CASE(3, 4, 1) XFBQ_CASE(3, 4, 2) XFBQ_CASE(3, 4, 4)
+    XFBQ_CASE(4, 4, 1) XFBQ_CASE(4, 4, 2) XFBQ_CASE(4, 4, 4)
+#undef XFBQ_CASE
+    if (fast && !env_int("XFBQ_FORCE_GENERIC", 0)) {
+        fast<<<static_cast<unsigned>(blocks), 256, 0, st>>>(static_cast<const uint4 *>(db), n, q, thr, ids_out, ids_out ? cap : 0,
+                                                            reinterpret_cast<unsigned long long *>(count_out));
+        return check_launch("collect_candidates_fast_kernel");
+    }
     collect_candidates_kernel<<<static_cast<unsigned>(blocks), 256, smem, st>>>(
         static_cast<const uint4 *>(db), n, wd, C, q, wq, thr, ids_out, ids_out ? cap : 0, reinterpret_cast<unsigned long long *>(count_out));
     return check_launch("collect_candidates_kernel");

@@ -189,7 +189,8 @@ def test_tensor_engines_ragged_shapes(engine, n, dim, wd, nq, k, monkeypatch):
     assert np.array_equal(scores.astype(np.uint64), want_d) and np.array_equal(ids, want_i)
 
 
-def test_collect_candidates_matches_distance_array():
+@pytest.mark.parametrize("generic", [False, True])
+def test_collect_candidates_matches_distance_array(generic, monkeypatch):
     """The one-pass candidate gather of k_select (count + row ids of d <= threshold, no distance array) against
     the materialised distances, for thresholds from 'nothing' to 'everything'; a small id buffer forces the
     second pass."""
@@ -199,6 +200,8 @@ def test_collect_candidates_matches_distance_array():
     params = xb.QuantParams(dim=c["dim"], scale=c["scale"], doc_bits=c["wd"], query_bits=c["wq"])
     idx = xb.build_index(c["docs"], params, keep_originals=False)
     upper = xb.distance_upper_bound(c["dim"], c["wd"], c["wq"])
+    if generic:
+        monkeypatch.setenv("XFBQ_FORCE_GENERIC", "1")  # the any-width kernel instead of the <WD, WQ, C> specialisation
     for qi in (0, 3):
         pq = xb.quantize_vector(c["queries"][qi], c["wq"], c["scale"])
         d = batch_distances_device(idx.packed, pq)
