@@ -1261,12 +1261,16 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     // sample scan remains for XFBQ_SEED_HIST=0.  A counted sample is nearly free, so it can be larger.
     const bool count = sample > 0 && pl.main.queue && env_int("XFBQ_SEED_HIST", 1) != 0;
     if (count) {
-        if (env_int("XFBQ_SAMPLE", -1) < 0) while (sample < 65536 && n >= 32 * sample) sample <<= 1;
+        if (env_int("XFBQ_SAMPLE", -1) < 0) {
+            while (sample < 65536 && n >= 32 * sample) sample <<= 1;
+            if (sample == 65536 && n >= 64 * sample) sample <<= 1;  // 10M rows: 128k documents, the main scan gains 0.5 ms for 0.3
+        }
         if (sample > umma::SEED_MAX_SAMPLE(C)) sample = umma::SEED_MAX_SAMPLE(C);
         pl.sample = sample;
     }
     if (sample) umma_shape(sample, C, nq, k, MT, info, &pl.pre, true, true, count);
     if (sample && pl.pre.NS == 0) return XFBQ_OK;
+    if (count && pl.main.stages < 2 * pl.pre.stages) return XFBQ_OK;  // (cannot happen: n >= 16 * sample) sampled tiles must be full tiles
     if (count) {  // the counted sample is spread over the whole database (every stride-th tile)
         pl.pre.tile_stride = env_int("XFBQ_SEED_SPREAD", 1) ? pl.main.stages / pl.pre.stages : 1;
         if (pl.pre.tile_stride < 1) pl.pre.tile_stride = 1;

@@ -431,17 +431,22 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
             const bool valid = myq < p.nq;
             if constexpr (SEED) {
                 // Counting epilogue.  This thread's bins are 16-bit counters of its own in shared memory, bin-major
-                // (word index (copy * 64 + bin) * 256 + thread: a warp's accesses never conflict), in SEED_COPIES
+                // (row (copy * 64 + bin) of 256 counters, a thread's slot chosen so that a warp never conflicts), in SEED_COPIES
                 // copies: column j updates copy j % COPIES, so COPIES read-modify-writes are in flight at a time
                 // (plain LDS/ADD/STS: shared-memory atomics -- and the divergent branches ptxas wraps around
                 // predicated ones -- bounded the first version at 11k cycles per stage).
                 constexpr int COPIES = SEED_COPIES(C);
-                const uint32_t bins_s = smem_u32(smem + L.hist_off) + (warp * 32 + lane) * 2;
+                // 16-bit counter of (bin row, thread): word (warp / 2) * 32 + lane, half warp & 1 -- a warp's 32 accesses fall in
+                // 32 different banks whatever their bins (thread-linear halves put lanes 2i, 2i + 1 in one bank: 2-way conflicts)
+                const uint32_t bins_s = smem_u32(smem + L.hist_off) + ((warp >> 1) * 32 + lane) * 4 + (warp & 1) * 2;
                 for (int b = 0; b < COPIES * SEED_BINS; ++b)
                     asm volatile("st.shared.u16 [%0], %1;" ::"r"(bins_s + b * (SEED_STRIDE * 2)), "h"(static_cast<unsigned short>(0)) : "memory");
-                const int2 par = valid ? p.seed_par[myq] : make_int2(TAU_NEVER, 0);
-                const int origin = par.x;
-                const uint32_t magic = static_cast<uint32_t>(par.y);  // bin = floor(d * magic / 2^32): monotone in d
+                // frame of this query: bin(v) = clamp(floor((v - origin) / width) + 1, 0, 63) computed as a signed
+                // multiply-high; bin 0 collects everything below the origin, so every score is one unconditional
+                // read-modify-write (sampled tiles hold real documents only: the host keeps them off the last tile)
+                const int2 par = valid ? p.seed_par[myq] : make_int2(0, 0);
+                const int c2 = par.x;   // 2 * (origin - width)
+                const int m31 = par.y;  // ceil(2^31 / width)
                 const uint32_t u0 = s_run * MT + mt;
                 Ring ac{static_cast<int>(u0 % ACC_BUFS), (u0 / ACC_BUFS) & 1u};
                 for (int i = 0; i < sg.cnt; ++i) {
@@ -449,7 +454,6 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                     mbar_wait_prof(&acc_full[buf], ac.phase, prof, w0);
                     fence_after();
                     const uint32_t taddr = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + buf * STAGE_DOCS + col0;
-                    const uint32_t doc0 = static_cast<uint32_t>((sg.sd0 + i) * p.tile_stride) * STAGE_DOCS + col0;
                     int v[COLS / 32][32];
 #pragma unroll
                     for (int c = 0; c < COLS / 32; ++c) tmem_ld32(taddr + c * 32, v[c]);
@@ -462,25 +466,24 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
 #pragma unroll
                         for (int j0 = 0; j0 < 32; j0 += COPIES) {
                             uint32_t addr[COPIES];
-                            unsigned short cur[COPIES], hit[COPIES];
+                            unsigned short cur[COPIES];
 #pragma unroll
                             for (int u = 0; u < COPIES; ++u) {
-                                const int d = v[c][j0 + u] - origin;  // d < 0 lands in the last bin with hit = 0
-                                const uint32_t bin = min(__umulhi(static_cast<uint32_t>(d), magic), static_cast<uint32_t>(SEED_BINS - 1));
-                                hit[u] = static_cast<unsigned short>((d >= 0) & (doc0 + c * 32 + j0 + u < n_docs));
-                                addr[u] = bins_s + (u * SEED_BINS + bin) * (SEED_STRIDE * 2);
+                                const int h = __mulhi(2 * v[c][j0 + u] - c2, m31);
+                                const int bin = min(max(h, 0), SEED_BINS - 1);
+                                addr[u] = bins_s + u * (SEED_BINS * SEED_STRIDE * 2) + bin * (SEED_STRIDE * 2);
                             }
 #pragma unroll
                             for (int u = 0; u < COPIES; ++u) asm volatile("ld.shared.u16 %0, [%1];" : "=h"(cur[u]) : "r"(addr[u]) : "memory");
 #pragma unroll
                             for (int u = 0; u < COPIES; ++u)
-                                asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr[u]), "h"(static_cast<unsigned short>(cur[u] + hit[u])) : "memory");
+                                asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr[u]), "h"(static_cast<unsigned short>(cur[u] + 1)) : "memory");
                         }
 #pragma unroll
                     for (int a = 0; a < MT; ++a) ac.advance(ACC_BUFS);
                 }
                 if (valid)
-                    for (int b = 0; b < SEED_BINS; ++b) {
+                    for (int b = 1; b < SEED_BINS; ++b) {  // bin 0 (below the origin) proves nothing
                         uint32_t c = 0;
 #pragma unroll
                         for (int u = 0; u < COPIES; ++u) {
@@ -731,11 +734,10 @@ __global__ void __launch_bounds__(128) seed_stats_kernel(const unsigned char *__
     __syncthreads();
     if (r == 0) {
         const float sigma = sqrtf((s_sq[0] + s_sq[1] + s_sq[2] + s_sq[3]) * (1.0f / 127.0f));
-        const float width = fmaxf(1.0f, rintf(sigma * (1.0f / 16.0f)));
+        const float width = fmaxf(2.0f, rintf(sigma * (1.0f / 16.0f)));
         const int origin = static_cast<int>(floorf(mean + (z - below) * sigma));
-        const uint32_t w = static_cast<uint32_t>(width);
-        const uint32_t magic = w <= 1 ? 0xFFFFFFFFu : static_cast<uint32_t>((0x100000000ull + w - 1) / w);
-        par[q] = make_int2(origin, static_cast<int>(magic));
+        const int w = static_cast<int>(width);
+        par[q] = make_int2(2 * (origin - w), static_cast<int>((0x80000000ll + w - 1) / w));
     }
 }
 
@@ -763,10 +765,11 @@ __global__ void __launch_bounds__(256) seed_bounds_kernel(const uint32_t *__rest
     if (lane == 0) {
         int32_t out = TAU_OPEN;
         if (m) {
+            // bin b >= 1 holds the scores v with (v - origin') * m31 >= b * 2^31, origin' = par.x / 2
             const int2 pr = par[q];
-            const uint64_t magic = static_cast<uint32_t>(pr.y);
-            const uint64_t d_b = ((static_cast<uint64_t>(bb) << 32) + magic - 1) / magic;  // smallest d with floor(d magic / 2^32) >= bb
-            out = pr.x + static_cast<int32_t>(d_b);
+            const int64_t m31 = pr.y;
+            const int64_t d_b = ((static_cast<int64_t>(bb) << 31) + m31 - 1) / m31;
+            out = pr.x / 2 + static_cast<int32_t>(d_b);
         }
         tau[q] = out;
     }
