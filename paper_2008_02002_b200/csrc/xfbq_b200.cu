@@ -666,7 +666,8 @@ merge_tree_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k,
 // more than k of the parts * k survive -- and sorts only the survivors (next power of two), instead of sorting
 // and tree-merging every row (config 4: 0.47 ms -> 0.05 ms).  Rows may arrive unsorted.  Exact for any number of
 // survivors: when the buffer of B keys could overflow it is sorted, cut back to its k best, and the bound
-// tightens to the k-th of those.  B is a power of two >= k + blockDim.x.
+// tightens to the k-th of those.  B is a power of two >= k + blockDim.x.  With bound == nullptr the rows must be
+// sorted and the bound comes from the rows themselves (see below).
 __global__ void __launch_bounds__(512)
 merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k, int B, const int32_t *__restrict__ bound,
                      const int32_t *__restrict__ qconst, uint64_t *__restrict__ out) {
@@ -678,7 +679,21 @@ merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int
     const int lane = threadIdx.x & 31, nt = blockDim.x;
     if (threadIdx.x == 0) {
         s_cnt = 0;
-        s_limit = static_cast<long long>(qconst[q]) - static_cast<long long>(bound[q]);  // largest distance that can still be in the top k
+        // largest distance that can still be in the top k
+        s_limit = bound ? static_cast<long long>(qconst[q]) - static_cast<long long>(bound[q]) : -1;
+    }
+    if (!bound) {
+        // Sorted rows without a shared threshold (last level of a tree merge): the m-th keys of all rows, m = ceil(k / parts),
+        // bound the answer -- parts * m >= k keys are no larger than the largest of them.
+        __syncthreads();
+        const int m = (k + parts - 1) / parts;
+        long long mine = -1;
+        for (int part = threadIdx.x; part < parts; part += nt) {
+            const uint64_t key = in[(static_cast<int64_t>(part) * nq + q) * k + (m - 1)];
+            const long long d = key == KEY_INF ? 0x7FFFFFFFFFFFFFFFll : static_cast<long long>(key >> 32);
+            mine = d > mine ? d : mine;
+        }
+        atomicMax(&s_limit, mine);
     }
     auto sort_prefix = [&](int c) {  // ascending sort of buf[0, c), padded to a power of two; ends on a barrier
         int n2 = 32;
@@ -908,6 +923,12 @@ int launch_merge(const uint64_t *in, int parts, int64_t nq, int k, uint64_t *out
             if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "merge smem opt-in: %s", cudaGetErrorString(e));
         }
         uint64_t *dst = groups == 1 ? out : scratch;
+        if (groups == 1 && rows >= 16 && !(sort_input && l == 0) && k <= 1024 && env_int("XFBQ_MERGE_BOUNDED", 1)) {
+            // last level over many sorted rows (single queries: 74 rows of 100): keep what the rows' own m-th keys allow
+            // and sort those few hundred keys, instead of log2(rows) rounds of bitonic merges in one CTA (28.6 -> see profiles)
+            merge_bounded_kernel<<<static_cast<unsigned>(nq), 512, 4096 * 8, st>>>(in, parts, nq, k, 4096, nullptr, nullptr, out);
+            return check_launch("merge_bounded_kernel");
+        }
         int threads = active * K2 / 4;
         threads = threads < 64 ? 64 : (threads > 512 ? 512 : threads);
         kern<<<dim3(static_cast<unsigned>(groups), static_cast<unsigned>(nq)), threads, smem, st>>>(in, parts, nq, k, G, dst);
@@ -938,6 +959,9 @@ struct MmaPlan {
     int64_t sample = 0;      // documents in the sample scan, 0 = none
     size_t off_qop = 0, off_qconst = 0, off_tau = 0, off_prekeys = 0, off_lists = 0, off_parts = 0,
            off_mscratch = 0, bytes = 0;
+    // thresholds seeded by counting on the tcgen05 path (run_counted_seed) instead of the list-keeping sample scan
+    bool count = false;
+    size_t off_uqimg = 0, off_uqconst = 0, off_seedpar = 0, off_seedhist = 0;
 };
 
 typedef void (*MmaKernel)(const mma::Params);
@@ -1031,6 +1055,11 @@ void mma_shape(int64_t n, int wd, int C, int64_t nq, int k, const DeviceInfo &in
     *out = sh;
 }
 
+// Thresholds by counting (defined with the tcgen05 planning below; shared by both tensor engines).
+int run_counted_seed(unsigned char *ws, const void *tiles, int64_t n, int64_t dim, int wd, const uint32_t *q, int64_t nq, int wq,
+                     int k, int64_t sample, bool prep, size_t off_qimg, size_t off_qconst, size_t off_par, size_t off_hist,
+                     int32_t *tau, cudaStream_t st);
+
 int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bool have_nibbles, MmaPlan *plan) {
     MmaPlan pl;
     const int C = static_cast<int>(chunks128(dim));
@@ -1058,8 +1087,10 @@ int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, boo
     // of the sample scan floods from an open threshold -- so only small batches use it.)
     if (sample < 0) sample = pl.main.groups == 1 ? (nq <= 4 ? 32768 : 65536) : 131072;
     if (sample > 0 && (n < 16 * sample || sample < 4 * k)) sample = 0;
+    pl.count = sample > 0 && env_int("XFBQ_SEED_HIST", 1) != 0;
+    if (pl.count && sample > umma::SEED_MAX_SAMPLE(C)) sample = umma::SEED_MAX_SAMPLE(C);
     pl.sample = sample;
-    if (sample) mma_shape(sample, wd, C, nq, k, info, &pl.pre);
+    if (sample && !pl.count) mma_shape(sample, wd, C, nq, k, info, &pl.pre);
     size_t off = 0;
     pl.off_qop = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 32 * C * 4);
     pl.off_qconst = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 4);
@@ -1068,6 +1099,14 @@ int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, boo
     pl.off_lists = off; off = align256(off + (pl.main.lists_bytes > pl.pre.lists_bytes ? pl.main.lists_bytes : pl.pre.lists_bytes));
     pl.off_parts = off; off = align256(off + (pl.main.parts_bytes > pl.pre.parts_bytes ? pl.main.parts_bytes : pl.pre.parts_bytes));
     pl.off_mscratch = off; off = align256(off + (pl.main.mscratch_bytes > pl.pre.mscratch_bytes ? pl.main.mscratch_bytes : pl.pre.mscratch_bytes));
+    if (pl.count) {
+        const int64_t uq = 128 * ((C == 4 || nq <= 128) ? 1 : 2);  // queries per group of the counting kernel
+        const int64_t nq_pad = (nq + uq - 1) / uq * uq;
+        pl.off_uqimg = off; off = align256(off + static_cast<size_t>(nq_pad) * 128 * C);
+        pl.off_uqconst = off; off = align256(off + static_cast<size_t>(nq_pad) * 4);
+        pl.off_seedpar = off; off = align256(off + static_cast<size_t>(nq) * 8);
+        pl.off_seedhist = off; off = align256(off + static_cast<size_t>(nq) * umma::SEED_BINS * 4);
+    }
     pl.bytes = off;
     *plan = pl;
     return XFBQ_OK;
@@ -1360,6 +1399,43 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st, true);
 }
 
+// Thresholds by counting: frame per query from 128 sampled scores, 64-bin histogram of the whole sample on the
+// tensor cores (every stride-th byte tile of the database), threshold = lower edge of the bin where the suffix
+// count reaches k.  tau[q] is in the accumulator domain both tensor engines use (Dq - distance).
+int run_counted_seed(unsigned char *ws, const void *tiles, int64_t n, int64_t dim, int wd, const uint32_t *q, int64_t nq, int wq,
+                     int k, int64_t sample, bool prep, size_t off_qimg, size_t off_qconst, size_t off_par, size_t off_hist,
+                     int32_t *tau, cudaStream_t st) {
+    const int C = static_cast<int>(chunks128(dim));
+    DeviceInfo info;
+    if (int rc = device_info(&info)) return rc;
+    const int MT = (C == 4 || nq <= 128) ? 1 : 2;
+    UmmaPlan pl;
+    umma_shape(sample, C, nq, k, MT, info, &pl.pre, true, true, true);
+    const int64_t total_stages = (bundles_of(n) * 32 + umma::STAGE_DOCS - 1) / umma::STAGE_DOCS;
+    if (pl.pre.NS == 0 || total_stages < 2 * pl.pre.stages)
+        return fail(XFBQ_E_UNSUPPORTED, "counted seed: sample %lld does not fit n=%lld dim=%lld", (long long)sample, (long long)n, (long long)dim);
+    pl.pre.tile_stride = env_int("XFBQ_SEED_SPREAD", 1) ? total_stages / pl.pre.stages : 1;
+    pl.pre.n_valid = n;
+    pl.off_qimg = off_qimg; pl.off_qconst = off_qconst; pl.off_seedpar = off_par; pl.off_seedhist = off_hist;
+    unsigned char *qimg = ws + off_qimg;
+    if (prep) {
+        umma::prep_queries_kernel<<<static_cast<unsigned>((pl.pre.nq_pad * 32 + 255) / 256), 256, 0, st>>>(
+            q, nq, pl.pre.nq_pad, static_cast<int>(dim), wq, wd, C, MT, qimg, reinterpret_cast<int32_t *>(ws + off_qconst));
+        if (int rc = check_launch("umma::prep_queries_kernel")) return rc;
+    }
+    int2 *par = reinterpret_cast<int2 *>(ws + off_par);
+    uint32_t *hist = reinterpret_cast<uint32_t *>(ws + off_hist);
+    cudaError_t e = cudaMemsetAsync(hist, 0, static_cast<size_t>(nq) * umma::SEED_BINS * 4, st);
+    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
+    umma::seed_stats_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(static_cast<const unsigned char *>(tiles), qimg, nq, C, pl.pre.stages, pl.pre.tile_stride,
+                                                                    static_cast<float>(normal_quantile(static_cast<double>(k) / static_cast<double>(sample))),
+                                                                    0.25f * env_int("XFBQ_SEED_BELOW4", 8), par);
+    if (int rc = check_launch("umma::seed_stats_kernel")) return rc;
+    if (int rc = run_umma_scan(pl.pre, pl, ws, tiles, sample, C, nq, k, 0, nullptr, nullptr, st)) return rc;
+    umma::seed_bounds_kernel<<<static_cast<unsigned>((nq * 32 + 255) / 256), 256, 0, st>>>(hist, par, nq, k, tau);
+    return check_launch("umma::seed_bounds_kernel");
+}
+
 int run_umma(const UmmaPlan &up, unsigned char *ws, const void *nib, int64_t n, int64_t dim, int wd, const uint32_t *q,
              int64_t nq, int wq, int k, int64_t row_offset, uint64_t *keys_out, cudaStream_t st) {
     const int C = static_cast<int>(chunks128(dim));
@@ -1373,19 +1449,8 @@ int run_umma(const UmmaPlan &up, unsigned char *ws, const void *nib, int64_t n, 
         uint64_t *prekeys = reinterpret_cast<uint64_t *>(ws + up.off_prekeys);
         int32_t *tau = reinterpret_cast<int32_t *>(ws + up.off_tau);
         if (up.pre.count) {
-            // thresholds by counting: frame per query from 128 sampled scores, 64-bin histogram of the whole sample
-            // on the tensor cores, threshold = lower edge of the bin where the suffix count reaches k
-            int2 *par = reinterpret_cast<int2 *>(ws + up.off_seedpar);
-            uint32_t *hist = reinterpret_cast<uint32_t *>(ws + up.off_seedhist);
-            cudaError_t e = cudaMemsetAsync(hist, 0, static_cast<size_t>(nq) * umma::SEED_BINS * 4, st);
-            if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
-            umma::seed_stats_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(static_cast<const unsigned char *>(nib), qimg, nq, C, up.pre.stages, up.pre.tile_stride,
-                                                                            static_cast<float>(normal_quantile(static_cast<double>(k) / static_cast<double>(up.sample))),
-                                                                            0.25f * env_int("XFBQ_SEED_BELOW4", 8), par);
-            if (int rc = check_launch("umma::seed_stats_kernel")) return rc;
-            if (int rc = run_umma_scan(up.pre, up, ws, nib, up.sample, C, nq, k, row_offset, nullptr, nullptr, st)) return rc;
-            umma::seed_bounds_kernel<<<static_cast<unsigned>((nq * 32 + 255) / 256), 256, 0, st>>>(hist, par, nq, k, tau);
-            if (int rc = check_launch("umma::seed_bounds_kernel")) return rc;
+            if (int rc = run_counted_seed(ws, nib, n, dim, wd, q, nq, wq, k, up.sample, false, up.off_qimg, up.off_qconst, up.off_seedpar,
+                                          up.off_seedhist, tau, st)) return rc;
         } else {
             if (int rc = run_umma_scan(up.pre, up, ws, nib, up.sample, C, nq, k, row_offset, nullptr, prekeys, st)) return rc;
             mma::tau_from_keys_kernel<<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(prekeys, qconst, nq, k, tau);
@@ -1714,7 +1779,12 @@ XFBQ_API int xfbq_scan_topk(const void *db, const void *nib, int64_t n, int64_t 
             q, nq, mp.main.nq_pad, static_cast<int>(dim), wq, wd, C, qop, qconst);
         if (int rc = check_launch("prep_queries_kernel")) return rc;
         const int32_t *tau_init = nullptr;
-        if (mp.sample) {
+        if (mp.sample && mp.count) {
+            int32_t *tau = reinterpret_cast<int32_t *>(ws + mp.off_tau);
+            if (int rc = run_counted_seed(ws, static_cast<const unsigned char *>(nib) + nibble_region_bytes(n, dim), n, dim, wd, q, nq, wq, k, mp.sample,
+                                          true, mp.off_uqimg, mp.off_uqconst, mp.off_seedpar, mp.off_seedhist, tau, st)) return rc;
+            tau_init = tau;
+        } else if (mp.sample) {
             uint64_t *prekeys = reinterpret_cast<uint64_t *>(ws + mp.off_prekeys);
             int32_t *tau = reinterpret_cast<int32_t *>(ws + mp.off_tau);
             if (int rc = run_mma_scan(mp.pre, mp, ws, nib, mp.sample, C, nq, k, row_offset, nullptr, prekeys, st)) return rc;

@@ -243,6 +243,27 @@ def test_counted_seed_queue_scan_and_bounded_merge(extra, n, dim, wd, nq, k, mon
     assert np.array_equal(scores.astype(np.uint64), want_d) and np.array_equal(ids, want_i)
 
 
+@pytest.mark.parametrize("extra", [{}, {"XFBQ_SEED_BELOW4": "0"}, {"XFBQ_SEED_BELOW4": "40"}, {"XFBQ_SEED_HIST": "0"}])
+@pytest.mark.parametrize("n,dim,wd,nq,k", [(70000, 256, 4, 1, 100), (70001, 128, 3, 5, 10), (80000, 512, 4, 16, 50),
+                                           (66000, 200, 4, 2, 1000)])
+def test_small_batches_counted_seed(extra, n, dim, wd, nq, k, monkeypatch):
+    """Small batches (mma.sync engine, the documents split over every warp of the chip) take their thresholds from
+    the counting kernel of the tcgen05 path; frames that miss or catch everything, and the list-keeping sample scan
+    it replaced, give the same keys."""
+    docs = xo.synthetic_unit_rows(n, dim, 31 + n)
+    queries = xo.synthetic_unit_rows(nq, dim, 32 + n)
+    scale = xo.estimate_scale(docs, 0.98)
+    params = xb.QuantParams(dim=dim, scale=scale, doc_bits=wd, query_bits=4)
+    idx = xb.build_index(docs, params, keep_originals=False)
+    for key, val in {"XFBQ_SAMPLE": "4096", **extra}.items():
+        monkeypatch.setenv(key, val)
+    scores, ids = xb.search(idx, queries, k)
+    planes = xo.c_quantize_matrix(docs, wd, scale)
+    qp = xo.c_quantize_matrix(queries.astype(np.float64), 4, scale).transpose(2, 0, 1)
+    want_d, want_i = xo.c_search(planes, qp, k)
+    assert np.array_equal(scores.astype(np.uint64), want_d) and np.array_equal(ids, want_i)
+
+
 @pytest.mark.parametrize("width", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_fast_float32_quantizer_on_code_boundaries(width, monkeypatch):
     """The float32-first quantizer (exact float64 redo near code boundaries) against the CPU oracle and the
