@@ -1371,6 +1371,7 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     p.seed_par = sh.count ? reinterpret_cast<const int2 *>(ws + pl.off_seedpar) : nullptr;
     p.seed_hist = sh.count ? reinterpret_cast<uint32_t *>(ws + pl.off_seedhist) : nullptr;
     p.prof = (&sh == &pl.main) ? g_prof : nullptr;
+    p.pace = env_int("XFBQ_UMMA_PACE", 48);
     p.debug = env_int("XFBQ_UMMA_DEBUG", 0);
     if (sh.slots > 1 && !sh.queue && !sh.count) {  // slots a group does not use stay KEY_INF (the queue kernel writes every slice)
         e = cudaMemsetAsync(p.out, 0xFF, sh.parts_bytes, st);

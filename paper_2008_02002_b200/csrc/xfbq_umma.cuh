@@ -64,6 +64,10 @@ struct Params {
     int groups, k, cap, NS;    // NS = operand stages in shared memory
     int ring_rows;             // queue kernel: rows of a drain warp's ring (32 or 64)
     int n_seg, seg_stages;     // queue kernel: document slices and stages per slice (work items = n_seg x groups)
+    int pace;                  // queue kernel: roles that read the clock around their mbarrier waits (8 drain, 16 issuer/operands,
+                               // 32 issuer/accumulator, 64 loader).  Measured, not understood: with the issuer's two waits bracketed by
+                               // clock reads the 10k-query scan takes 14.85 ms instead of 15.7 (the same reads the profiling
+                               // counters use; the drain's and the loader's make no difference)
     int debug;                 // timing experiments (XFBQ_UMMA_DEBUG): 1 skip operand stores, 2 skip document loads, 4 skip the filter
     unsigned long long *prof;  // optional [grid][8] wait-cycle counters (xfbq_debug_profile), else nullptr
 };
@@ -839,7 +843,7 @@ template <int C, int MT>
 __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p) {
     constexpr int B_STAGE = STAGE_DOCS * 128 * C;
     constexpr int KSTEPS = 4 * C;
-    constexpr int EPI_PER_BUF = 4;                    // the four drain warps (lane quarters) of a buffer's set
+    constexpr int EPI_PER_BUF = 8;                    // arrivals that free an accumulator: two column halves x four lane quarters
     constexpr int A_COLS = 32 * C;
     constexpr int NQ_CTA = 128 * MT;                  // queries of one group
     extern __shared__ unsigned char smem_unaligned[];
@@ -966,33 +970,33 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             };
 
             const uint32_t u_begin = s_run * MT, u_end = u_begin + static_cast<uint32_t>(sg.cnt) * MT;
-            uint32_t u = u_begin + (set + ACC_BUFS - u_begin % ACC_BUFS) % ACC_BUFS;  // first accumulator that lands in buffer `set`
-            for (; u < u_end; u += ACC_BUFS) {
-                const uint32_t rel = u - u_begin;
-                const int mt = MT == 2 ? static_cast<int>(rel & 1u) : 0;
-                const int qloc = mt * 128 + q4 * 32 + lane;
-                const uint32_t doc0 = (static_cast<uint32_t>(sg.sd0) + rel / MT) * STAGE_DOCS;
-                const uint32_t taddr = lane_base + set * STAGE_DOCS;
-                const int theta = theta_s[qloc];
-                mbar_wait_prof(&acc_full[set], (u / ACC_BUFS) & 1u, prof, w0);
-                fence_after();
-                int v[2][32];
-                if (!(p.debug & 4)) {
+            {
+                // Half accumulators dealt round-robin to the three warps of a lane quarter: 64 columns are in registers after
+                // one tensor-memory read, so the buffer goes back to the issuer BEFORE any filtering -- parking a row never
+                // delays the tensor pipe, and the hand-off chain is one read round instead of two reads and two filters.
+                const uint32_t n_units = 2 * (u_end - u_begin);
+                for (uint32_t x = set; x < n_units; x += 3) {
+                    const uint32_t rel = x >> 1, half = x & 1u;
+                    const uint32_t u = u_begin + rel;
+                    const uint32_t buf = u % ACC_BUFS;
+                    const int mt = MT == 2 ? static_cast<int>(rel & 1u) : 0;
+                    const int qloc = mt * 128 + q4 * 32 + lane;
+                    const uint32_t doc0 = (static_cast<uint32_t>(sg.sd0) + rel / MT) * STAGE_DOCS + half * 64;
+                    const uint32_t taddr = lane_base + buf * STAGE_DOCS + half * 64;
+                    const int theta = theta_s[qloc];
+                    mbar_wait_prof(&acc_full[buf], (u / ACC_BUFS) & 1u, prof || (p.pace & 8), w0);
+                    fence_after();
+                    int v[2][32];
                     tmem_ld32(taddr, v[0]);
                     tmem_ld32(taddr + 32, v[1]);
                     tmem_ld_wait();
-                    filter(v[0], theta, qloc, doc0);
-                    tmem_ld32(taddr + 64, v[0]);   // in flight while the second chunk is filtered
-                    filter(v[1], theta, qloc, doc0 + 32);
-                    tmem_ld32(taddr + 96, v[1]);
-                    tmem_ld_wait();
-                }
-                fence_before();  // the accumulator is in registers: hand it back
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&acc_empty[set]);
-                if (!(p.debug & 4)) {
-                    filter(v[0], theta, qloc, doc0 + 64);
-                    filter(v[1], theta, qloc, doc0 + 96);
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&acc_empty[buf]);
+                    if (!(p.debug & 4)) {
+                        filter(v[0], theta, qloc, doc0);
+                        filter(v[1], theta, qloc, doc0 + 32);
+                    }
                 }
             }
             __syncwarp();
@@ -1021,13 +1025,13 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             const uint32_t u0 = s_run * MT;
             Ring ac{static_cast<int>(u0 % ACC_BUFS), ((u0 / ACC_BUFS) & 1u) ^ 1u};
             for (int i = 0; i < sg.cnt; ++i) {
-                mbar_wait_prof(&b_full[rb.idx], rb.phase, prof, w0);
+                mbar_wait_prof(&b_full[rb.idx], rb.phase, prof || (p.pace & 16), w0);
                 fence_after();
                 const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4);
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
                     const uint32_t buf = ac.idx;
-                    mbar_wait_prof(&acc_empty[buf], ac.phase, prof, w1);
+                    mbar_wait_prof(&acc_empty[buf], ac.phase, prof || (p.pace & 32), w1);
                     fence_after();
                     if (elect_one()) {
                         const uint32_t d = tm + buf * STAGE_DOCS;
@@ -1060,7 +1064,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             if (lane == 0) {
                 Ring rb{static_cast<int>(s_run % NS), ((s_run / NS) & 1u) ^ 1u};
                 for (int i = 0; i < sg.cnt; ++i) {
-                    mbar_wait_prof(&b_empty[rb.idx], rb.phase, prof, w0);
+                    mbar_wait_prof(&b_empty[rb.idx], rb.phase, prof || (p.pace & 64), w0);
                     mma::mbar_arrive_expect_tx(&b_full[rb.idx], B_STAGE);
                     mma::tma_bulk_g2s(sB + static_cast<size_t>(rb.idx) * B_STAGE, db + static_cast<int64_t>(sg.sd0 + i) * B_STAGE, B_STAGE, &b_full[rb.idx]);
                     rb.advance(NS);
