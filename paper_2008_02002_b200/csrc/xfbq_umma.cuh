@@ -222,6 +222,23 @@ __device__ __forceinline__ void mbar_wait_prof(uint64_t *bar, uint32_t parity, b
     acc += clock64() - t0;
 }
 
+// mbarrier wait with the retry loop inside the asm block.  Around a C++ loop the compiler places a YIELD in front of
+// every try_wait, the first one included: the warp hands its issue slot to the other warps of its scheduler even when
+// the barrier has already completed.  For the MMA issuer (one warp, on the critical path of the tensor pipe, sharing
+// a scheduler with three busy drain warps) that cost 5 % of the scan (found through the profiling counters: their
+// clock reads happened to move the first try_wait out of the yielding loop).
+__device__ __forceinline__ void mbar_wait_tight(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@p bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n\t"
+        "DONE_%=:\n\t}"
+        ::"r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+
 // v[j] for a warp-uniform j without dynamic register indexing (a jump table of 32 moves)
 __device__ __forceinline__ int pick32(const int (&v)[32], int j) {
     int r = v[0];
@@ -984,7 +1001,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                     const uint32_t doc0 = (static_cast<uint32_t>(sg.sd0) + rel / MT) * STAGE_DOCS + half * 64;
                     const uint32_t taddr = lane_base + buf * STAGE_DOCS + half * 64;
                     const int theta = theta_s[qloc];
-                    mbar_wait_prof(&acc_full[buf], (u / ACC_BUFS) & 1u, prof || (p.pace & 8), w0);
+                    if (prof) mbar_wait_prof(&acc_full[buf], (u / ACC_BUFS) & 1u, true, w0); else mbar_wait_tight(&acc_full[buf], (u / ACC_BUFS) & 1u);
                     fence_after();
                     int v[2][32];
                     tmem_ld32(taddr, v[0]);
@@ -1025,13 +1042,13 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             const uint32_t u0 = s_run * MT;
             Ring ac{static_cast<int>(u0 % ACC_BUFS), ((u0 / ACC_BUFS) & 1u) ^ 1u};
             for (int i = 0; i < sg.cnt; ++i) {
-                mbar_wait_prof(&b_full[rb.idx], rb.phase, prof || (p.pace & 16), w0);
+                if (prof) mbar_wait_prof(&b_full[rb.idx], rb.phase, true, w0); else mbar_wait_tight(&b_full[rb.idx], rb.phase);
                 fence_after();
                 const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4);
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
                     const uint32_t buf = ac.idx;
-                    mbar_wait_prof(&acc_empty[buf], ac.phase, prof || (p.pace & 32), w1);
+                    if (prof) mbar_wait_prof(&acc_empty[buf], ac.phase, true, w1); else mbar_wait_tight(&acc_empty[buf], ac.phase);
                     fence_after();
                     if (elect_one()) {
                         const uint32_t d = tm + buf * STAGE_DOCS;
@@ -1064,7 +1081,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             if (lane == 0) {
                 Ring rb{static_cast<int>(s_run % NS), ((s_run / NS) & 1u) ^ 1u};
                 for (int i = 0; i < sg.cnt; ++i) {
-                    mbar_wait_prof(&b_empty[rb.idx], rb.phase, prof || (p.pace & 64), w0);
+                    mbar_wait_prof(&b_empty[rb.idx], rb.phase, prof, w0);
                     mma::mbar_arrive_expect_tx(&b_full[rb.idx], B_STAGE);
                     mma::tma_bulk_g2s(sB + static_cast<size_t>(rb.idx) * B_STAGE, db + static_cast<int64_t>(sg.sd0 + i) * B_STAGE, B_STAGE, &b_full[rb.idx]);
                     rb.advance(NS);

@@ -16,7 +16,7 @@ import os
 if os.environ.get('PROF'):
     prof = torch.zeros((148 * 12,), dtype=torch.int64, device='cuda')
     _native.check(_native.lib().xfbq_debug_profile(prof.data_ptr()))
-for dbg in (48, 0, 48, 16, 32, 120, 48):
+for dbg in (0, 0):
     os.environ["XFBQ_UMMA_PACE"] = str(dbg)
     ts = []
     for i in range(5):
