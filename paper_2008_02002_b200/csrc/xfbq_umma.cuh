@@ -64,10 +64,8 @@ struct Params {
     int groups, k, cap, NS;    // NS = operand stages in shared memory
     int ring_rows;             // queue kernel: rows of a drain warp's ring (32 or 64)
     int n_seg, seg_stages;     // queue kernel: document slices and stages per slice (work items = n_seg x groups)
-    int pace;                  // queue kernel: roles that read the clock around their mbarrier waits (8 drain, 16 issuer/operands,
-                               // 32 issuer/accumulator, 64 loader).  Measured, not understood: with the issuer's two waits bracketed by
-                               // clock reads the 10k-query scan takes 14.85 ms instead of 15.7 (the same reads the profiling
-                               // counters use; the drain's and the loader's make no difference)
+    int pace;                  // experiments: roles that read the clock around their mbarrier waits when not profiling (8 drain,
+                               // 16 issuer/operands, 32 issuer/accumulator, 64 loader) -- how the yielding wait loop was found
     int debug;                 // timing experiments (XFBQ_UMMA_DEBUG): 1 skip operand stores, 2 skip document loads, 4 skip the filter
     unsigned long long *prof;  // optional [grid][8] wait-cycle counters (xfbq_debug_profile), else nullptr
 };
