@@ -271,22 +271,6 @@ def run_ours(a):
     db_bytes_local = index.packed.nbytes                      # algorithmic bytes of this rank's shard
     db_bytes_total = a.n * a.doc_bits * ((a.dim + 63) // 64) * 8
 
-    # ---- extras that need the float originals (N = 1 only): recall@K vs float cosine
-    recall = None
-    if world == 1 and not a.no_extras:
-        nr = min(64, a.nq)
-        keys = shard.search_keys(q_dev[:nr], a.k)
-        ids_q = (keys & 0xFFFFFFFF)
-        sims = q_dev[:nr] @ docs.T                           # float32 cosine (unit rows)
-        ids_f = torch.topk(sims, min(a.k, a.n), dim=1).indices
-        hit = 0
-        for r in range(nr):
-            hit += int(torch.isin(ids_q[r], ids_f[r]).sum())
-        recall = hit / float(nr * min(a.k, a.n))
-        del sims, ids_f
-    del docs
-    torch.cuda.empty_cache()
-
     plan = (np.zeros(6, dtype=np.int32))
     _native.check(_native.lib().xfbq_scan_plan(index.n, a.dim, a.doc_bits, min(a.nq, xsearch._QUERY_BATCH),
                                                a.query_bits, min(a.k, index.n), 1, plan.ctypes.data))
@@ -332,6 +316,24 @@ def run_ours(a):
     barrier()
     e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / a.steps)
     clocks = sampler.stop() if rank == 0 else None
+
+    # ---- extras that need the float originals (N = 1 only): recall@K vs float cosine (after the timed regions: the
+    # 64 x 10M float GEMM + top-K would otherwise push the board into its power cap right before they start)
+    recall = None
+    if world == 1 and not a.no_extras:
+        nr = min(64, a.nq)
+        keys = shard.search_keys(q_dev[:nr], a.k)
+        ids_q = (keys & 0xFFFFFFFF)
+        sims = q_dev[:nr] @ docs.T                           # float32 cosine (unit rows)
+        ids_f = torch.topk(sims, min(a.k, a.n), dim=1).indices
+        hit = 0
+        for r in range(nr):
+            hit += int(torch.isin(ids_q[r], ids_f[r]).sum())
+        recall = hit / float(nr * min(a.k, a.n))
+        del sims, ids_f
+    del docs
+    torch.cuda.empty_cache()
+
 
     # ---- small-batch regime: single-query latency and achieved HBM bandwidth
     single = None
