@@ -211,10 +211,12 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
-def quantize_to_device(values, width: int, scale: float, queries: bool):
+def quantize_to_device(values, width: int, scale: float, queries: bool, defer_check: bool = False):
     """Run the quantizer kernel.  `values`: host array or CUDA tensor, (n, dim) f32/f64.
     Returns (device buffer, n, dim).  Raises InvalidInputError on non-finite scaled values
-    (quant.py:142-143) exactly as the reference does."""
+    (quant.py:142-143) exactly as the reference does.  With `defer_check` the device counter of
+    non-finite values is returned as a fourth item instead of being read here (the read is a
+    stream synchronisation): the caller enqueues the work that follows and checks it afterwards."""
     torch = _native.require_cuda()
     L = _native.lib()
     width = check_width(width)
@@ -224,7 +226,7 @@ def quantize_to_device(values, width: int, scale: float, queries: bool):
         if values.dtype not in (torch.float32, torch.float64):
             values = values.to(torch.float64)
         if not values.is_cuda:
-            values = values.cuda()
+            values = values.cuda(non_blocking=values.is_pinned())  # pinned: the host goes on to enqueue the kernels
         if values.stride(-1) != 1:
             values = values.contiguous()
         n, dim = values.shape
@@ -261,6 +263,8 @@ def quantize_to_device(values, width: int, scale: float, queries: bool):
             chunk = torch.from_numpy(values[row0:row0 + _ROW_CHUNK]).cuda()
             run(chunk, row0)
             del chunk
+    if defer_check:
+        return out, n, dim, bad
     if n and int(bad.item()):
         raise InvalidInputError("cannot quantize non-finite values")
     return out, n, dim
@@ -278,12 +282,16 @@ def quantize_matrix(values, width: int, scale: float = 1.0) -> PackedMatrix:
     return PackedMatrix(None, dim, _codes=codes, _count=n, _width=check_width(width))
 
 
-def quantize_queries(values, width: int, scale: float = 1.0):
-    """Batched query quantizer: (nq, dim) -> device int32 buffer in the query layout."""
+def quantize_queries(values, width: int, scale: float = 1.0, defer_check: bool = False):
+    """Batched query quantizer: (nq, dim) -> device int32 buffer in the query layout
+    (defer_check: -> (buffer, device counter of non-finite values), see quantize_to_device)."""
     if scale <= 0:
         raise InvalidInputError(f"scale must be positive, got {scale}")
     if values.ndim != 2:
         raise InvalidInputError("quantize_queries expects an (nq, dim) matrix")
+    if defer_check:
+        out, _, _, bad = quantize_to_device(values, width, scale, queries=True, defer_check=True)
+        return out, bad
     out, _, _ = quantize_to_device(values, width, scale, queries=True)
     return out
 

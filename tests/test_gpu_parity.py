@@ -352,6 +352,15 @@ def test_edge_cases():
         xb.quantize_matrix(np.array([[1e300, 1.0]]), 3, 1e300)  # scaled value overflows to inf
     with pytest.raises(xb.InvalidInputError):
         xb.search(idx, np.zeros((1, 5)), 0)
+    # non-finite queries raise whether they arrive from the host (check read after the scan is enqueued), from
+    # pinned memory or from the device (check read right after the quantizer): quant.py:142-143
+    import torch
+    bad_q = np.array([[0.0, np.nan, 0.0, 0.0, 0.0], [0.0, 0.0, 0.0, 0.0, 0.0]])
+    for q in (bad_q, bad_q.astype(np.float32), torch.from_numpy(bad_q).pin_memory(), torch.from_numpy(bad_q).cuda()):
+        with pytest.raises(xb.InvalidInputError):
+            xb.search(idx, q, 2)
+    s_ok, i_ok = xb.search(idx, torch.zeros((2, 5), dtype=torch.float64).pin_memory(), 2)
+    assert i_ok.tolist() == [[0, 1], [0, 1]]
     with pytest.raises(xb.InvalidInputError):
         xb.PackedMatrix(np.full((3, 1, 2), 1 << 40, dtype=np.uint64), 5)  # padding bits set
 
