@@ -64,8 +64,9 @@ struct Params {
     int groups, k, cap, NS;    // NS = operand stages in shared memory
     int ring_rows;             // queue kernel: rows of a drain warp's ring (32 or 64)
     int n_seg, seg_stages;     // queue kernel: document slices and stages per slice (work items = n_seg x groups)
-    int pace;                  // experiments: roles that read the clock around their mbarrier waits when not profiling (8 drain,
-                               // 16 issuer/operands, 32 issuer/accumulator, 64 loader) -- how the yielding wait loop was found
+    int pace;                  // no longer read by the kernels (it selected the roles whose waits were bracketed by clock reads in the
+                               // experiment that exposed the yielding wait loop); left in the block because the build without it
+                               // ran the main scan 3 % slower -- the code-shape sensitivity described in DESIGN.md section 8, next (1)
     int debug;                 // timing experiments (XFBQ_UMMA_DEBUG): 1 skip operand stores, 2 skip document loads, 4 skip the filter
     unsigned long long *prof;  // optional [grid][8] wait-cycle counters (xfbq_debug_profile), else nullptr
 };
