@@ -1287,7 +1287,7 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     // scan's resolvers then have to handle).
     int64_t sample = env_int("XFBQ_SAMPLE", -1);
     if (sample < 0) { sample = 16384; while (sample < 64 * static_cast<int64_t>(k)) sample <<= 1; }
-    if (sample > 0 && (n < 16 * sample || sample < 4 * k)) sample = 0;
+    if (sample > 0 && (n < 8 * sample || sample < 4 * k)) sample = 0;
     // Without seeded thresholds every score passes at first: list work dominates and the kernel whose eight
     // epilogue warps own their lists beats the two resolvers of the queue kernel (100k x 128, 100 queries: 4x).
     // The same holds for small problems with few query groups (1M x 128, 1000 queries: 2.5x): the lists stay hot.
@@ -1301,11 +1301,12 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     const bool count = sample > 0 && pl.main.queue && env_int("XFBQ_SEED_HIST", 1) != 0;
     if (count) {
         if (env_int("XFBQ_SAMPLE", -1) < 0) {
-            // a counted sample may be 1/16 of the database; what it saves grows with k (list insertions ~ k ln(n / sample)).
+            // a counted sample may be 1/8 of the database; what it saves grows with k (list insertions ~ k ln(n / sample)).
             // Measured per 10k queries: top-100 over 2.5M rows 5.41 ms with 64k documents, 5.05 with 128k; 1.25M rows 4.51 ms
-            // with 16k, 3.61 with 64k; top-10 over 1.2M rows 2.35 ms with 64k, 2.26 with 32k.
+            // with 16k, 3.61 with 64k, 3.38 with 128k; 1M x 128: 3.53 ms with 32k, 3.27 with 64k; top-10 over 1.2M rows 2.35 ms
+            // with 64k, 2.26 with 32k.
             const int64_t cap_k = k >= 64 ? 131072 : (k >= 16 ? 65536 : 32768);
-            while (sample < cap_k && n >= 32 * sample) sample <<= 1;
+            while (sample < cap_k && n >= 16 * sample) sample <<= 1;
         }
         if (sample > umma::SEED_MAX_SAMPLE(C)) sample = umma::SEED_MAX_SAMPLE(C);
         pl.sample = sample;
