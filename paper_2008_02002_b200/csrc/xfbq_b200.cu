@@ -715,6 +715,7 @@ merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int
     for (int64_t e0 = 0; e0 < total; e0 += nt) {
         __syncthreads();
         const int c = s_cnt;
+        __syncthreads();  // every thread has read the count before any warp appends: the branch below is block-uniform
         if (c + nt > B) {  // the next round of appends could overflow: keep the k best, tighten the bound
             sort_prefix(c);
             if (threadIdx.x == 0) {
