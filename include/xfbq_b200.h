@@ -128,6 +128,32 @@ int xfbq_collect_candidates(const void *db_dev, int64_t n, int64_t dim, int doc_
                             uint64_t *count_out_dev, void *stream);
 
 /*
+ * estimate_scale (index.py:123-138: 1 / np.quantile(|x|, p)).  numpy's "linear" quantile interpolates between two
+ * order statistics of the flattened array; this call finds them exactly: out2_dev[0] / out2_dev[1] receive the
+ * rank_lo-th and rank_hi-th smallest |x| (0-based ranks over the `count` contiguous elements at x_dev;
+ * 0 <= rank_lo <= rank_hi < count), *nan_count_dev the number of NaN entries (they take no rank: numpy returns NaN
+ * when there is one).  Most-significant-digit radix select on the float bit patterns, 11 bits per pass.
+ * workspace_dev: xfbq_select_workspace_bytes() bytes, 8-byte aligned.
+ */
+int64_t xfbq_select_workspace_bytes(void);
+int xfbq_abs_order_stats_f32(const float *x_dev, int64_t count, int64_t rank_lo, int64_t rank_hi, void *workspace_dev,
+                             int64_t workspace_bytes, float *out2_dev, uint64_t *nan_count_dev, void *stream);
+int xfbq_abs_order_stats_f64(const double *x_dev, int64_t count, int64_t rank_lo, int64_t rank_hi, void *workspace_dev,
+                             int64_t workspace_bytes, double *out2_dev, uint64_t *nan_count_dev, void *stream);
+
+/*
+ * Float re-rank of k_select's candidates (refine, search.py:153-157 + _rank_hits :129-131; originals widened to
+ * float64 as index.py:106-120): sims[c] = sum_k double(rows[r_c][k]) * q_dev[k] accumulated in float64, then the k
+ * best (similarity desc, id asc) to sims_out_dev[k] / ids_out_dev[k] (slots beyond `count` hold 0.0 / -1).
+ * r_c = ids_dev[c], or c when rows_gathered != 0 (rows_dev then holds the candidates' rows in candidate order and n
+ * is ignored).  ids_dev[c] are the row ids reported and used as tie-break.  1 <= k <= XFBQ_MAX_K.
+ */
+int64_t xfbq_refine_workspace_bytes(int64_t count, int k);
+int xfbq_refine_f32(const float *rows_dev, int64_t n, int64_t dim, int64_t ld, int rows_gathered, const int64_t *ids_dev,
+                    int64_t count, const double *q_dev, int k, double *sims_out_dev, int64_t *ids_out_dev,
+                    void *workspace_dev, int64_t workspace_bytes, void *stream);
+
+/*
  * Fused scan + top-K: for each of nq queries the k smallest keys
  * (distance << 32 | row_offset + row) over the n documents, ascending, written
  * to keys_out_dev[nq][k] (slots beyond min(k, n) hold UINT64_MAX).  No score

@@ -751,6 +751,7 @@ merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int
 }  // namespace
 #include "xfbq_mma.cuh"
 #include "xfbq_umma.cuh"
+#include "xfbq_select.cuh"
 namespace {
 
 __global__ void unpack_keys_kernel(const uint64_t *__restrict__ keys, int64_t count,
@@ -1702,6 +1703,120 @@ XFBQ_API int xfbq_collect_candidates(const void *db, int64_t n, int64_t dim, int
     collect_candidates_kernel<<<static_cast<unsigned>(blocks), 256, smem, st>>>(
         static_cast<const uint4 *>(db), n, wd, C, q, wq, thr, ids_out, ids_out ? cap : 0, reinterpret_cast<unsigned long long *>(count_out));
     return check_launch("collect_candidates_kernel");
+}
+
+
+namespace {
+
+template <typename T>
+int abs_order_stats_impl(const T *x, int64_t count, int64_t rank_lo, int64_t rank_hi, void *ws, int64_t ws_bytes, T *out2,
+                         uint64_t *nan_count, void *stream) {
+    if (count < 1) return fail(XFBQ_E_INVALID, "cannot take order statistics of an empty array");
+    if (rank_lo < 0 || rank_hi < rank_lo || rank_hi >= count)
+        return fail(XFBQ_E_INVALID, "bad ranks %lld, %lld for %lld elements", (long long)rank_lo, (long long)rank_hi, (long long)count);
+    if (!x || !ws || !out2 || !nan_count) return fail(XFBQ_E_INVALID, "null pointer");
+    if (ws_bytes < static_cast<int64_t>(sizeof(sel::State))) return fail(XFBQ_E_INVALID, "workspace too small: need %zu bytes", sizeof(sel::State));
+    if ((reinterpret_cast<uintptr_t>(ws) & 7) != 0) return fail(XFBQ_E_INVALID, "workspace must be 8-byte aligned");
+    DeviceInfo info;
+    if (int rc = device_info(&info)) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    sel::State *state = static_cast<sel::State *>(ws);
+    sel::init_state_kernel<<<1, 256, 0, st>>>(state, rank_lo, rank_hi);
+    if (int rc = check_launch("sel::init_state_kernel")) return rc;
+    const size_t smem = static_cast<size_t>(sel::COPIES) * sel::BINS * 4;
+    cudaError_t e = cudaFuncSetAttribute(sel::hist_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(sel::hist_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "select smem opt-in: %s", cudaGetErrorString(e));
+    constexpr int V = 16 / sizeof(T);
+    int64_t blocks = (count / V + 255) / 256;
+    const int64_t max_blocks = static_cast<int64_t>(info.sms) * 3;  // 64 KB of histogram copies per block: three blocks per SM
+    if (blocks > max_blocks) blocks = max_blocks;
+    if (blocks < 1) blocks = 1;
+    int hi_bit = static_cast<int>(sizeof(T)) * 8;
+    bool first = true;
+    while (hi_bit > 0) {
+        const int nbits = hi_bit >= sel::DIGIT_BITS ? sel::DIGIT_BITS : hi_bit;
+        const int lo_bit = hi_bit - nbits;
+        if (first) sel::hist_kernel<T, true><<<static_cast<unsigned>(blocks), 256, smem, st>>>(x, count, lo_bit, nbits, state);
+        else sel::hist_kernel<T, false><<<static_cast<unsigned>(blocks), 256, smem, st>>>(x, count, lo_bit, nbits, state);
+        if (int rc = check_launch("sel::hist_kernel")) return rc;
+        sel::pick_kernel<<<1, 1024, 0, st>>>(state, nbits);
+        if (int rc = check_launch("sel::pick_kernel")) return rc;
+        hi_bit = lo_bit;
+        first = false;
+    }
+    sel::finish_kernel<T><<<1, 32, 0, st>>>(state, out2, reinterpret_cast<unsigned long long *>(nan_count));
+    return check_launch("sel::finish_kernel");
+}
+
+int refine_k2(int k) {
+    int K2 = 256;
+    while (K2 < k) K2 <<= 1;
+    return K2;
+}
+int refine_blocks(int64_t count, int sms) {
+    int64_t g = (count + 8191) / 8192;
+    if (g > 2 * static_cast<int64_t>(sms)) g = 2 * sms;
+    return g < 1 ? 1 : static_cast<int>(g);
+}
+
+template <typename T>
+int refine_impl(const T *rows, int64_t n, int64_t dim, int64_t ld, int gathered, const int64_t *ids, int64_t count, const double *q, int k,
+                double *sims_out, int64_t *ids_out, void *ws, int64_t ws_bytes, void *stream) {
+    if (n < 0 || dim < 1 || ld < dim || count < 0) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld ld=%lld count=%lld", (long long)n, (long long)dim, (long long)ld, (long long)count);
+    if (k < 1) return fail(XFBQ_E_INVALID, "k must be >= 1, got %d", k);
+    if (k > XFBQ_MAX_K) return fail(XFBQ_E_UNSUPPORTED, "k=%d exceeds XFBQ_MAX_K=%d", k, XFBQ_MAX_K);
+    if (!sims_out || !ids_out) return fail(XFBQ_E_INVALID, "null pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    DeviceInfo info;
+    if (int rc = device_info(&info)) return rc;
+    if (!rows || !ids || !q || !ws) return fail(XFBQ_E_INVALID, "null pointer");
+    const int G = refine_blocks(count, info.sms);
+    const int64_t need = xfbq_refine_workspace_bytes(count, k);
+    if (ws_bytes < need) return fail(XFBQ_E_INVALID, "workspace too small: need %lld bytes, got %lld", (long long)need, (long long)ws_bytes);
+    double *sims = static_cast<double *>(ws);
+    sel::RankPair *part = reinterpret_cast<sel::RankPair *>(static_cast<unsigned char *>(ws) + align256(static_cast<size_t>(count) * 8));
+    if (count > 0) {
+        sel::gather_dot_kernel<T><<<static_cast<unsigned>((count * 32 + 255) / 256), 256, 0, st>>>(rows, ld, static_cast<int>(dim), gathered ? nullptr : ids, count, q, sims);
+        if (int rc = check_launch("sel::gather_dot_kernel")) return rc;
+    }
+    const int K2 = refine_k2(k);
+    const size_t smem = static_cast<size_t>(2) * K2 * sizeof(sel::RankPair);
+    cudaError_t e = cudaFuncSetAttribute(sel::rank_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(sel::rank_final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "refine smem opt-in: %s", cudaGetErrorString(e));
+    sel::rank_partial_kernel<<<static_cast<unsigned>(G), 256, smem, st>>>(sims, ids, count, k, K2, part);
+    if (int rc = check_launch("sel::rank_partial_kernel")) return rc;
+    sel::rank_final_kernel<<<1, 256, smem, st>>>(part, static_cast<int64_t>(G) * k, k, K2, sims_out, ids_out);
+    return check_launch("sel::rank_final_kernel");
+}
+
+}  // namespace
+
+XFBQ_API int64_t xfbq_select_workspace_bytes(void) { return static_cast<int64_t>(align256(sizeof(sel::State))); }
+
+XFBQ_API int xfbq_abs_order_stats_f32(const float *x, int64_t count, int64_t rank_lo, int64_t rank_hi, void *ws, int64_t ws_bytes,
+                                      float *out2, uint64_t *nan_count, void *stream) {
+    return abs_order_stats_impl<float>(x, count, rank_lo, rank_hi, ws, ws_bytes, out2, nan_count, stream);
+}
+
+XFBQ_API int xfbq_abs_order_stats_f64(const double *x, int64_t count, int64_t rank_lo, int64_t rank_hi, void *ws, int64_t ws_bytes,
+                                      double *out2, uint64_t *nan_count, void *stream) {
+    return abs_order_stats_impl<double>(x, count, rank_lo, rank_hi, ws, ws_bytes, out2, nan_count, stream);
+}
+
+XFBQ_API int64_t xfbq_refine_workspace_bytes(int64_t count, int k) {
+    if (count < 0 || k < 1) return -1;
+    DeviceInfo info;
+    int sms = 148;
+    if (device_info(&info) == XFBQ_OK) sms = info.sms;
+    return static_cast<int64_t>(align256(static_cast<size_t>(count) * 8) +
+                                align256(static_cast<size_t>(refine_blocks(count, sms)) * k * sizeof(sel::RankPair)));
+}
+
+XFBQ_API int xfbq_refine_f32(const float *rows, int64_t n, int64_t dim, int64_t ld, int gathered, const int64_t *ids, int64_t count, const double *q, int k,
+                             double *sims_out, int64_t *ids_out, void *ws, int64_t ws_bytes, void *stream) {
+    return refine_impl<float>(rows, n, dim, ld, gathered, ids, count, q, k, sims_out, ids_out, ws, ws_bytes, stream);
 }
 
 XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, int have_nibbles) {

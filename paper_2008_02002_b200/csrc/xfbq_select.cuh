@@ -1,0 +1,285 @@
+// xfbq_select.cuh -- exact order statistics of |x| (estimate_scale, index.py:123-138) and the float re-rank of
+// k_select's candidates (search.py:153-157, index.py:106-120) -- included by xfbq_b200.cu.
+//
+// estimate_scale = 1 / np.quantile(|x|, p): numpy's "linear" method interpolates between TWO order statistics of
+// the flattened array (ranks floor((n-1)p) and the next one).  The data-sized part -- finding those two values
+// exactly -- is a most-significant-digit radix select on the bit patterns of |x| (non-negative IEEE floats order
+// like unsigned integers), 11 bits per pass: a histogram pass over every element that still matches the prefix
+// found so far, then a one-block pick of the digit that holds the rank.  Three passes for float32, six for
+// float64; both ranks are tracked at once (they nearly always share every digit but the last).  The interpolation
+// itself is a handful of scalar operations on the host (paper_2008_02002_b200/index.py restates numpy's).
+#pragma once
+
+namespace sel {
+
+constexpr int DIGIT_BITS = 11;
+constexpr int BINS = 1 << DIGIT_BITS;
+constexpr int COPIES = 8;  // shared-memory histogram copies (lane & 7): unit-norm data puts most first digits in a few bins
+
+struct State {              // device-resident, one per call (workspace)
+    unsigned long long hist[2][BINS];
+    unsigned long long prefix[2];   // digits found so far, right-aligned
+    long long rank[2];              // rank still to find among the elements matching prefix[t]
+    unsigned long long nan_count;
+    int same;                       // both targets share prefix[0]: one histogram serves both
+    int pad;
+};
+
+template <typename T> struct KeyOf;
+template <> struct KeyOf<float> {
+    typedef uint32_t type;
+    static constexpr int BITS = 32;
+    static __device__ __forceinline__ uint32_t key(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
+    static __device__ __forceinline__ bool is_nan(uint32_t k) { return k > 0x7F800000u; }
+};
+template <> struct KeyOf<double> {
+    typedef unsigned long long type;
+    static constexpr int BITS = 64;
+    static __device__ __forceinline__ unsigned long long key(double v) {
+        return static_cast<unsigned long long>(__double_as_longlong(v)) & 0x7FFFFFFFFFFFFFFFull;
+    }
+    static __device__ __forceinline__ bool is_nan(unsigned long long k) { return k > 0x7FF0000000000000ull; }
+};
+
+__global__ void init_state_kernel(State *st, long long rank_lo, long long rank_hi) {
+    for (int i = threadIdx.x; i < 2 * BINS; i += blockDim.x) (&st->hist[0][0])[i] = 0ull;
+    if (threadIdx.x == 0) {
+        st->prefix[0] = st->prefix[1] = 0ull;
+        st->rank[0] = rank_lo; st->rank[1] = rank_hi;
+        st->nan_count = 0ull; st->same = 1; st->pad = 0;
+    }
+}
+
+// Histogram of digit [lo_bit, lo_bit + nbits) over the elements whose higher bits equal the prefix of a target.
+// FIRST: no prefix yet (every element counts; NaNs are counted on the side -- numpy's quantile returns NaN then).
+template <typename T, bool FIRST>
+__global__ void __launch_bounds__(256) hist_kernel(const T *__restrict__ x, int64_t count, int lo_bit, int nbits, State *st) {
+    typedef typename KeyOf<T>::type K;
+    extern __shared__ uint32_t sh[];  // [COPIES][BINS]
+    for (int i = threadIdx.x; i < COPIES * BINS; i += blockDim.x) sh[i] = 0u;
+    __syncthreads();
+    const int same = FIRST ? 1 : st->same;
+    const K p0 = static_cast<K>(st->prefix[0]), p1 = static_cast<K>(st->prefix[1]);
+    const int hi_bit = lo_bit + nbits;
+    const uint32_t mask = (1u << nbits) - 1u;
+    const int lane = threadIdx.x & 31;
+    // same prefix: 8 copies by lane; different prefixes: target t owns copies 4t .. 4t + 3
+    uint32_t *h0 = sh + (same ? (lane & 7) : (lane & 3)) * BINS;
+    uint32_t *h1 = sh + (4 + (lane & 3)) * BINS;
+    unsigned long long nans = 0;
+    constexpr int V = 16 / sizeof(T);  // elements per 16-byte load
+    const int64_t nvec = ((reinterpret_cast<uintptr_t>(x) & 15) == 0) ? count / V : 0;
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    auto visit = [&](T v) {
+        const K k = KeyOf<T>::key(v);
+        if (FIRST) {
+            if (KeyOf<T>::is_nan(k)) { ++nans; return; }
+            atomicAdd(&h0[static_cast<uint32_t>(k >> lo_bit) & mask], 1u);
+        } else {
+            const K hi = hi_bit >= KeyOf<T>::BITS ? static_cast<K>(0) : static_cast<K>(k >> hi_bit);
+            const uint32_t d = static_cast<uint32_t>(k >> lo_bit) & mask;
+            if (hi == p0) atomicAdd(&h0[d], 1u);
+            if (!same && hi == p1) atomicAdd(&h1[d], 1u);
+        }
+    };
+    const uint4 *xv = reinterpret_cast<const uint4 *>(x);
+#pragma unroll 2
+    for (int64_t i = tid; i < nvec; i += nthreads) {
+        const uint4 w = __ldg(xv + i);
+        T e[V];
+        memcpy(e, &w, 16);
+#pragma unroll
+        for (int j = 0; j < V; ++j) visit(e[j]);
+    }
+    for (int64_t i = nvec * V + tid; i < count; i += nthreads) visit(x[i]);
+    __syncthreads();
+    for (int b = threadIdx.x; b < BINS; b += blockDim.x) {
+        uint32_t c0 = 0, c1 = 0;
+        if (same) {
+#pragma unroll
+            for (int c = 0; c < COPIES; ++c) c0 += sh[c * BINS + b];
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { c0 += sh[c * BINS + b]; c1 += sh[(4 + c) * BINS + b]; }
+        }
+        if (c0) atomicAdd(&st->hist[0][b], static_cast<unsigned long long>(c0));
+        if (c1) atomicAdd(&st->hist[1][b], static_cast<unsigned long long>(c1));
+    }
+    if (FIRST) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) nans += __shfl_xor_sync(0xffffffffu, nans, o);
+        if (lane == 0 && nans) atomicAdd(&st->nan_count, nans);
+    }
+}
+
+// One block: for each target, the digit whose bin holds the rank; prefix and rank move on, histograms are cleared.
+__global__ void __launch_bounds__(1024) pick_kernel(State *st, int nbits) {
+    __shared__ int s_digit[2];
+    __shared__ long long s_below[2];
+    const int same = st->same;
+    for (int t = 0; t < 2; ++t) {
+        const unsigned long long *h = st->hist[same ? 0 : t];
+        const long long want = st->rank[t];
+        // inclusive prefix sums of the bins (2048 bins, 1024 threads: two bins per thread, block scan)
+        const int b0 = 2 * threadIdx.x;
+        const unsigned long long a = h[b0], b = h[b0 + 1];
+        unsigned long long sum = a + b;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        unsigned long long inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        __shared__ unsigned long long s_warp[32];
+        if (lane == 31) s_warp[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            unsigned long long w = s_warp[lane], wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long v = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += v;
+            }
+            s_warp[lane] = wi - w;  // exclusive
+        }
+        __syncthreads();
+        const unsigned long long exc = s_warp[warp] + inc - sum;  // elements in bins below b0
+        // the digit: smallest bin with inclusive count > want
+        const unsigned long long w = static_cast<unsigned long long>(want);
+        if (exc <= w && w < exc + a) { s_digit[t] = b0; s_below[t] = static_cast<long long>(exc); }
+        else if (exc + a <= w && w < exc + a + b) { s_digit[t] = b0 + 1; s_below[t] = static_cast<long long>(exc + a); }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        for (int t = 0; t < 2; ++t) {
+            st->prefix[t] = (st->prefix[t] << nbits) | static_cast<unsigned long long>(s_digit[t]);
+            st->rank[t] -= s_below[t];
+        }
+        st->same = st->prefix[0] == st->prefix[1];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2 * BINS; i += blockDim.x) (&st->hist[0][0])[i] = 0ull;
+}
+
+template <typename T>
+__global__ void finish_kernel(const State *st, T *out2, unsigned long long *nan_out) {
+    typedef typename KeyOf<T>::type K;
+    if (threadIdx.x < 2) {
+        const K k = static_cast<K>(st->prefix[threadIdx.x]);
+        T v;
+        memcpy(&v, &k, sizeof(T));
+        out2[threadIdx.x] = v;
+    }
+    if (threadIdx.x == 0) *nan_out = st->nan_count;
+}
+
+// ------------------------------------------------------------------------------ float re-rank (search.py:153-157)
+// sims[c] = sum_k double(rows[ids[c]][k]) * q[k], accumulated in float64 IN DIMENSION ORDER by pairwise halves the way
+// a BLAS dot would not promise -- the reference's `rows @ q` goes through numpy's float64 matmul (pairwise / SIMD
+// order unspecified), so the comparison with it is to 1e-12 relative, not bit-exact (tests state the tolerance).
+// One warp per candidate: lanes stride the row (coalesced float32 loads), butterfly reduction.
+template <typename T>
+__global__ void __launch_bounds__(256) gather_dot_kernel(const T *__restrict__ rows, int64_t ld, int dim, const int64_t *__restrict__ ids,
+                                                         int64_t count, const double *__restrict__ q, double *__restrict__ sims) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (c >= count) return;
+    const T *row = rows + (ids ? ids[c] : c) * ld;  // ids == nullptr: the rows were gathered by the caller
+    double acc = 0.0;
+    for (int k = lane; k < dim; k += 32) acc = fma(static_cast<double>(row[k]), __ldg(q + k), acc);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) sims[c] = acc;
+}
+
+// Rank keys of the re-rank: (similarity desc, id asc) == ascending (monotone key of -sim, id).  The float64 similarity
+// maps to a uint64 whose unsigned order is the numeric order of -sim (search.py:129-131 lexsort((ids, -sims))).
+__device__ __forceinline__ unsigned long long order_key_desc(double sim) {
+    const double neg = 0.0 - sim;  // -0.0 and 0.0 rank equal, like numpy's comparison
+    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(neg));
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double sim_of_key(unsigned long long key) {
+    const unsigned long long b = (key & 0x8000000000000000ull) ? (key & 0x7FFFFFFFFFFFFFFFull) : ~key;
+    return 0.0 - __longlong_as_double(static_cast<long long>(b));
+}
+
+struct RankPair { unsigned long long key; long long id; };
+constexpr long long RANK_EMPTY = 0x7FFFFFFFFFFFFFFFll;
+__device__ __forceinline__ bool pair_less(const RankPair &a, const RankPair &b) {
+    return a.key < b.key || (a.key == b.key && a.id < b.id);
+}
+
+// Block-wide bounded top-k over a stream of pairs: buf[0, K2) holds the best so far (sorted after every flush),
+// buf[K2, 2 K2) collects the pairs that beat the current k-th; a full upper half is folded in by one bitonic sort of
+// the 2 K2 entries.  K2 = power of two >= max(k, blockDim.x).  Every thread of the block calls it with the same arguments.
+template <typename Fetch>
+__device__ void bounded_topk(RankPair *buf, int K2, int k, int64_t begin, int64_t end, Fetch fetch) {
+    __shared__ int s_cnt;
+    const RankPair inf{~0ull, RANK_EMPTY};
+    for (int t = threadIdx.x; t < 2 * K2; t += blockDim.x) buf[t] = inf;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    auto fold = [&]() {  // sort buf[0, 2 K2): the K2 best end up in the lower half; ends on a barrier
+        const int P = 2 * K2;
+        for (int size = 2; size <= P; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int t = threadIdx.x; t < (P >> 1); t += blockDim.x) {
+                    const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+                    const bool up = (lo & size) == 0;
+                    const RankPair a = buf[lo], b = buf[hi];
+                    if (pair_less(b, a) == up) { buf[lo] = b; buf[hi] = a; }
+                }
+                __syncthreads();
+            }
+        for (int t = threadIdx.x; t < K2; t += blockDim.x) buf[K2 + t] = inf;
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+    };
+    for (int64_t e0 = begin; e0 < end; e0 += blockDim.x) {
+        const int c = s_cnt;
+        __syncthreads();  // everyone has read the count: the branch is block-uniform
+        if (c + static_cast<int>(blockDim.x) > K2) fold();
+        const RankPair kth = buf[k - 1];  // inf until k pairs have been folded in
+        const int64_t e = e0 + threadIdx.x;
+        RankPair mine = inf;
+        if (e < end) mine = fetch(e);
+        const bool keep = mine.id != RANK_EMPTY && pair_less(mine, kth);
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        int base = 0;
+        const int lane = threadIdx.x & 31;
+        if (lane == 0 && m) base = atomicAdd(&s_cnt, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) buf[K2 + base + __popc(m & ((1u << lane) - 1u))] = mine;
+        __syncthreads();
+    }
+    fold();
+}
+
+// Stage 1: block b ranks its contiguous share of the candidates and writes its k best pairs (RANK_EMPTY padded).
+__global__ void __launch_bounds__(256) rank_partial_kernel(const double *__restrict__ sims, const int64_t *__restrict__ ids, int64_t count,
+                                                          int k, int K2, RankPair *__restrict__ part) {
+    extern __shared__ __align__(16) unsigned char raw[];
+    RankPair *buf = reinterpret_cast<RankPair *>(raw);
+    const int64_t per = (count + gridDim.x - 1) / gridDim.x;
+    const int64_t begin = static_cast<int64_t>(blockIdx.x) * per, end = min(count, begin + per);
+    bounded_topk(buf, K2, k, begin, end, [&](int64_t e) { return RankPair{order_key_desc(sims[e]), ids[e]}; });
+    for (int t = threadIdx.x; t < k; t += blockDim.x) part[static_cast<int64_t>(blockIdx.x) * k + t] = buf[t];
+}
+
+// Stage 2: one block ranks the partial results; hits leave as (id, float64 similarity), best first.
+__global__ void __launch_bounds__(256) rank_final_kernel(const RankPair *__restrict__ part, int64_t count, int k, int K2,
+                                                        double *__restrict__ out_sims, int64_t *__restrict__ out_ids) {
+    extern __shared__ __align__(16) unsigned char raw[];
+    RankPair *buf = reinterpret_cast<RankPair *>(raw);
+    bounded_topk(buf, K2, k, 0, count, [&](int64_t e) { return part[e]; });
+    for (int t = threadIdx.x; t < k; t += blockDim.x) {
+        const bool real = buf[t].id != RANK_EMPTY;
+        out_sims[t] = real ? sim_of_key(buf[t].key) : 0.0;
+        out_ids[t] = real ? buf[t].id : -1;
+    }
+}
+
+}  // namespace sel

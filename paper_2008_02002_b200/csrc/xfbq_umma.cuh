@@ -128,7 +128,12 @@ __device__ __forceinline__ bool elect_one() {  // one lane of a converged warp
     asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
     return pred != 0;
 }
-__device__ __forceinline__ void cta_sync() { asm volatile("bar.sync 0;" ::: "memory"); }
+// bar.sync is the .aligned barrier: every thread of a warp must arrive converged.  Role branches end in lane-dependent code
+// (`if (lane == 0)`, `if (valid)`), and reconvergence after those is not guaranteed without a warp barrier (synccheck).
+__device__ __forceinline__ void cta_sync() {
+    __syncwarp();
+    asm volatile("bar.sync 0;" ::: "memory");
+}
 __device__ __forceinline__ int max8(const int *v) {
     return max(max(max(v[0], v[1]), v[2]), max(max(max(v[3], v[4]), v[5]), max(v[6], v[7])));
 }
@@ -839,7 +844,7 @@ constexpr int RING_ROWS_MAX = 64;                             // parked rows per
 constexpr int STASH_WORDS = 36;                               // a parked row: 32 scores, query, first document, ticket, pad (144 B)
 
 struct QSmemLayout {
-    uint32_t b_off, ring_off, state_off, hist_off, bar_off, total;
+    uint32_t b_off, ring_off, state_off, hist_off, slotbar_off, bar_off, total;
 };
 __host__ __device__ inline QSmemLayout q_smem_layout(int C, int NS, int ring_rows) {
     QSmemLayout L;
@@ -848,12 +853,11 @@ __host__ __device__ inline QSmemLayout q_smem_layout(int C, int NS, int ring_row
     L.ring_off = off; off += Q_DRAIN * ring_rows * STASH_WORDS * 4;
     L.state_off = off; off += 5 * 256 * 4 + 2 * Q_DRAIN * 4 + 32;  // per query: count, threshold, Dq, claim, seeded threshold; per drain warp: tail, final ticket
     L.hist_off = off; off += Q_RESOLVERS * 256 * 4;
+    L.slotbar_off = off; off += (2 * Q_DRAIN * ring_rows + Q_DRAIN) * 8;  // per ring slot: row-full and row-free mbarriers; per drain warp: segment end
     L.bar_off = off; off += (2 * NS + 2 * ACC_BUFS) * 8 + 16;
     L.total = off + 1024;
     return L;
 }
-__device__ __forceinline__ int ld_volatile(const int *p) { return *reinterpret_cast<const volatile int *>(p); }
-__device__ __forceinline__ void st_volatile(int *p, int v) { *reinterpret_cast<volatile int *>(p) = v; }
 
 template <int C, int MT>
 __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p) {
@@ -870,9 +874,15 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
     const QSmemLayout L = q_smem_layout(C, NS, RING_ROWS);
     unsigned char *sB = smem + L.b_off;
     uint32_t *rings = reinterpret_cast<uint32_t *>(smem + L.ring_off);
-    int *cnt_s = reinterpret_cast<int *>(smem + L.state_off), *theta_s = cnt_s + 256, *dq_s = cnt_s + 512, *claim_s = cnt_s + 768;
+    int *cnt_s = reinterpret_cast<int *>(smem + L.state_off), *theta_s = cnt_s + 256, *dq_s = cnt_s + 512;
     int *theta0_s = cnt_s + 1024;
-    int *tail_s = cnt_s + 1280, *fin_s = tail_s + Q_DRAIN;  // per drain warp: rows consumed by its resolver; final ticket of a segment
+    int *tail_s = cnt_s + 1280, *fin_s = tail_s + Q_DRAIN;  // per drain warp: rows consumed so far (resolver-private); last ticket of the segment
+    // Ring hand-offs are mbarriers (release on arrive, acquire on the test): slot_full[w][s] completes a phase every time
+    // drain warp w parks a row in slot s, slot_free[w][s] every time its resolver has consumed it, seg_done[w] when the
+    // warp has parked the last row of a work item.  Tickets run on across work items, so the phase of ticket t is t / RING_ROWS.
+    uint64_t *slot_full = reinterpret_cast<uint64_t *>(smem + L.slotbar_off), *slot_free = slot_full + Q_DRAIN * RING_ROWS;
+    uint64_t *seg_done = slot_free + Q_DRAIN * RING_ROWS;
+    const int LOG_R = RING_ROWS == 64 ? 6 : 5;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L.bar_off);
     uint64_t *b_full = bars, *b_empty = bars + NS, *acc_full = bars + 2 * NS, *acc_empty = bars + 2 * NS + ACC_BUFS;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 2 * ACC_BUFS);
@@ -885,9 +895,9 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
         for (int i = 0; i < NS; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
         for (int i = 0; i < ACC_BUFS; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], EPI_PER_BUF); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int w = 0; w < Q_DRAIN; ++w) { tail_s[w] = 0; fin_s[w] = -1; }
+        for (int w = 0; w < Q_DRAIN; ++w) { tail_s[w] = 0; fin_s[w] = 0; mbar_init(&seg_done[w], 1); }
     }
-    for (int i = threadIdx.x; i < Q_DRAIN * RING_ROWS; i += Q_THREADS) rings[i * STASH_WORDS + 34] = 0u;  // no ticket yet
+    for (int i = threadIdx.x; i < 2 * Q_DRAIN * RING_ROWS; i += Q_THREADS) mbar_init(&slot_full[i], 1);  // slot_free follows slot_full
     if (warp == 0) tmem_alloc(tmem_slot, 512);
     fence_before();
     cta_sync();
@@ -926,7 +936,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
         // every warp three MMA group times per accumulator.
         const int q4 = warp & 3, set = warp >> 2;
         uint32_t *ring = rings + warp * (RING_ROWS * STASH_WORDS);  // this warp's ring; resolver (q4 & 1) owns its queries' lists
-        int head = 0, tail_seen = 0;                  // tickets handed out (warp-uniform) / consumption last observed
+        int head = 0;                                 // tickets handed out so far (warp-uniform; never reset)
+        uint64_t *my_full = slot_full + warp * RING_ROWS, *my_free = slot_free + warp * RING_ROWS;
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
         while (sg.next()) {
             if (warp < 4 * MT) {  // query rows -> tensor memory; the queries' shared state
@@ -958,29 +969,24 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                     const int n = __popc(hm);
                     const int t0 = head;
                     head += n;
-                    if (head - tail_seen > RING_ROWS) {  // maybe full: look at the resolver's progress, wait if it is behind
-                        const long long tw = prof ? clock64() : 0;
-#ifdef XFBQ_UMMA_WATCHDOG
-                        const long long wd0 = clock64();
-#endif
-                        while (head - (tail_seen = ld_volatile(&tail_s[warp])) > RING_ROWS) {
-                            __nanosleep(40);
-#ifdef XFBQ_UMMA_WATCHDOG
-                            if (clock64() - wd0 > 4000000000ll) { if (lane == 0) printf("drain %d cta %d stuck: head %d tail %d\n", warp, blockIdx.x, head, tail_seen); __trap(); }
-#endif
-                        }
-                        if (prof) w3 += clock64() - tw;
-                    }
                     if (hit) {
                         const int t = t0 + __popc(hm & ((1u << lane) - 1u));
-                        uint32_t *row = ring + (t & (RING_ROWS - 1)) * STASH_WORDS;
+                        const int slot = t & (RING_ROWS - 1);
+                        // the slot is free once the resolver has consumed ticket t - RING_ROWS (phase t / RING_ROWS - 1 of its
+                        // row-free barrier; a fresh barrier reads as "previous phase complete")
+                        const uint32_t free_parity = ((static_cast<uint32_t>(t) >> LOG_R) & 1u) ^ 1u;
+                        if (!mma::mbar_test(&my_free[slot], free_parity)) {
+                            const long long tw = prof ? clock64() : 0;
+                            mbar_wait(&my_free[slot], free_parity);
+                            if (prof) w3 += clock64() - tw;
+                        }
+                        uint32_t *row = ring + slot * STASH_WORDS;
 #pragma unroll
                         for (int c = 0; c < 8; ++c)
                             *reinterpret_cast<uint4 *>(row + 4 * c) = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
                         row[32] = qloc;
                         row[33] = doc0;
-                        __threadfence_block();
-                        st_volatile(reinterpret_cast<int *>(row + 34), t + 1);
+                        mbar_arrive(&my_full[slot]);  // release: the row is visible to whoever sees the phase complete
                     }
                 }
             };
@@ -1016,13 +1022,10 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                 }
             }
             __syncwarp();
-            if (lane == 0) { __threadfence_block(); st_volatile(&fin_s[warp], head); }  // every ticket of this segment is out
+            if (lane == 0) { fin_s[warp] = head; mbar_arrive(&seg_done[warp]); }  // every ticket of this work item is out
             cta_sync();  // the resolvers have emptied the rings: lists are final, this warp's ring is free scratch
             emit_lists(warp, reinterpret_cast<int *>(ring), sg.gr, sg.part);
             __syncwarp();
-            for (int i = lane; i < RING_ROWS; i += 32) ring[i * STASH_WORDS + 34] = 0u;  // scratch use may have forged tickets
-            head = 0; tail_seen = 0;
-            if (lane == 0) { st_volatile(&tail_s[warp], 0); }
             s_run += static_cast<uint32_t>(sg.cnt);
             cta_sync();
         }
@@ -1099,6 +1102,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
         const uint32_t n_docs = static_cast<uint32_t>(p.n);
         const uint32_t id_off = static_cast<uint32_t>(p.row_offset);
         const int cap = p.cap, k = p.k;
+        uint32_t seg_parity = 0;  // work items this CTA has finished, mod 2 (phase of seg_done)
         while (sg.next()) {
             cta_sync();
             const int64_t gq0 = static_cast<int64_t>(sg.gr) * NQ_CTA;
@@ -1139,28 +1143,29 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
 #pragma unroll 1
                 for (int w = res; w < Q_DRAIN; w += Q_RESOLVERS) {  // the rings of the drain warps this resolver serves
                     uint32_t *ring = rings + w * (RING_ROWS * STASH_WORDS);
-                    const int tail = ld_volatile(&tail_s[w]);
+                    const int tail = tail_s[w];  // resolver-private (written by lane 0 below, behind a warp barrier)
                     // rows tail .. tail + n - 1 are ready (tickets are handed out in order, rows may land out of order)
                     const int t = tail + lane;
-                    const uint32_t *row = ring + (t & (RING_ROWS - 1)) * STASH_WORDS;
-                    const bool ready = ld_volatile(reinterpret_cast<const int *>(row + 34)) == t + 1;
+                    const int slot = t & (RING_ROWS - 1);
+                    const uint32_t *row = ring + slot * STASH_WORDS;
+                    const bool ready = mma::mbar_test(&slot_full[w * RING_ROWS + slot], (static_cast<uint32_t>(t) >> LOG_R) & 1u);  // acquire
                     const unsigned rm = __ballot_sync(0xffffffffu, ready);
                     const int n = rm == 0xffffffffu ? 32 : __ffs(~rm) - 1;
                     if (n == 0) {
-                        if (ld_volatile(&fin_s[w]) != tail) all_done = false;
+                        // nothing parked: done with this ring once its warp has announced its last ticket and we have consumed it
+                        if (!(mma::mbar_test(&seg_done[w], seg_parity) && fin_s[w] == tail)) all_done = false;
                         continue;
                     }
                     progressed = true;
                     all_done = false;
-                    __threadfence_block();
                     bool pend = lane < n;
                     const int q = pend ? static_cast<int>(row[32]) : 0;
                     const uint32_t doc0 = pend ? row[33] : 0u;
                     while (__any_sync(0xffffffffu, pend)) {
-                        // one row per query and round (last claim wins), so a round adds at most 32 keys to a list
-                        if (pend) claim_s[q] = lane;
-                        __syncwarp();
-                        const bool go = pend && claim_s[q] == lane;
+                        // one row per query and round (the highest lane holding a row of the query goes), so a round adds at
+                        // most 32 keys to a list
+                        const unsigned peers = __match_any_sync(0xffffffffu, pend ? q : 0x10000 + lane);
+                        const bool go = pend && lane == 31 - __clz(peers);
                         if (go) {
                             const int th = theta_s[q], dqe = dq_s[q];
                             uint32_t below = 0;  // bit j: score j < threshold
@@ -1206,7 +1211,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                         }
                     }
                     __syncwarp();
-                    if (lane == 0) st_volatile(&tail_s[w], tail + n);
+                    if (lane < n) mbar_arrive(&slot_free[w * RING_ROWS + slot]);  // the row has been read: its slot may be reused
+                    if (lane == 0) tail_s[w] = tail + n;
                     __syncwarp();
                 }
                 if (all_done) break;
@@ -1215,7 +1221,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                 else if (clock64() - wd0 > 4000000000ll) {
                     if (lane == 0) {
                         printf("resolver %d cta %d stuck:", res, blockIdx.x);
-                        for (int w = res; w < Q_DRAIN; w += Q_RESOLVERS) printf(" [w%d tail %d fin %d flag %d addr %u]", w, tail_s[w], fin_s[w], (int)rings[(w * RING_ROWS + (tail_s[w] & (RING_ROWS - 1))) * STASH_WORDS + 34], smem_u32(&rings[(w * RING_ROWS + (tail_s[w] & (RING_ROWS - 1))) * STASH_WORDS + 34]));
+                        for (int w = res; w < Q_DRAIN; w += Q_RESOLVERS) printf(" [w%d tail %d fin %d]", w, tail_s[w], fin_s[w]);
                         printf("\n");
                     }
                     __trap();
@@ -1236,7 +1242,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             }
             cta_sync();  // every resolver is done: lists are final
             emit_lists(Q_DRAIN + res, hist, sg.gr, sg.part);
-            if (lane < Q_DRAIN && (lane % Q_RESOLVERS) == res) st_volatile(&fin_s[lane], -1);  // next segment's tickets are not out yet
+            seg_parity ^= 1u;
             s_run += static_cast<uint32_t>(sg.cnt);
             cta_sync();
         }

@@ -72,14 +72,26 @@ def scan_topk_device(packed: PackedMatrix, qwords, nq: int, query_bits: int, k: 
         C = (packed.dim + 127) // 128
         words_per_query = query_bits * 4 * C  # int32 elements
         st = _stream_ptr(torch)
-        nib = packed.nibbles if query_bits <= 7 and k <= 1024 else None
+        if k > MAX_K:
+            # Wider than the fused selector (XFBQ_MAX_K lists per query): the reference accepts any k (search.py:212), so
+            # fall back to the distance kernel + a full device sort of the (distance << 32 | id) keys, one query at a time.
+            # torch.sort is library code (CUB): this regime (k > 4096) is outside the fused hot path.
+            ids = torch.arange(packed.count, dtype=torch.int64, device=dev) + int(row_offset)
+            d = torch.empty(packed.count, dtype=torch.int64, device=dev)
+            for qi in range(nq):
+                _native.check(L.xfbq_batch_distances(packed.codes.data_ptr(), packed.count, packed.dim, packed.width,
+                                                     qwords.data_ptr() + qi * words_per_query * 4, query_bits, d.data_ptr(), st))
+                keys[qi] = torch.sort((d << 32) | ids).values[:k]
+            return keys
+        # derived layouts only where a tensor engine will read them (C in {1, 2, 4}): other shapes take the POPC kernels
+        nib = packed.nibbles if query_bits <= 7 and k <= 1024 and C in (1, 2, 4) else None
         nib_ptr = nib.data_ptr() if nib is not None else None
         for q0 in range(0, nq, _QUERY_BATCH):
             qn = min(_QUERY_BATCH, nq - q0)
             ws_bytes = int(L.xfbq_scan_workspace_bytes(packed.count, packed.dim, packed.width, qn, query_bits, k,
                                                        1 if nib is not None else 0))
             if ws_bytes < 0:
-                _native.check(_native.E_UNSUPPORTED if k > MAX_K else _native.E_INVALID)
+                _native.check(_native.E_INVALID)
             ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
             qptr = qwords.data_ptr() + q0 * words_per_query * 4
             if SCAN_EVENTS is not None:
@@ -173,14 +185,53 @@ def to_host_arrays(*tensors):
     return tuple(h.numpy() for h in host)
 
 
-def _originals_device(index: Index):
+def _refine_device(index: Index, query: np.ndarray, cand, k: int):
+    """refine with originals (search.py:153-157 + _rank_hits :129-131): float64 dot products of the candidates' float32
+    rows with the query and the k best by (similarity desc, id asc), in xfbq_refine_f32 (gather-dot kernel + bounded
+    block top-k).  `cand`: device int64 row ids, any order.  Originals that live in HBM (CUDA tensor: build_index from a
+    CUDA tensor, or Index.originals_to_device()) are gathered by the kernel; host-resident originals are gathered on the
+    host (count rows, a memory move) and only those rows are uploaded -- the whole matrix (10 GB at 10M x 256) never is."""
     torch = _native.require_cuda()
-    cached = getattr(index, "_originals_dev", None)
-    if cached is None:
-        o = index.originals
-        cached = o if _is_torch(o) else torch.from_numpy(np.asarray(o)).to(index.packed.codes.device)
-        object.__setattr__(index, "_originals_dev", cached)
-    return cached
+    L = _native.lib()
+    dev = index.packed.codes.device
+    count = int(cand.numel())
+    kk = min(int(k), count)
+    if kk == 0:
+        return []
+    orig = getattr(index, "_originals_dev", None)
+    if orig is None and _is_torch(index.originals) and index.originals.is_cuda:
+        orig = index.originals
+    with torch.cuda.device(dev):
+        st = _stream_ptr(torch)
+        q_dev = torch.from_numpy(np.ascontiguousarray(query, dtype=np.float64)).to(dev)
+        if orig is not None:
+            rows, gathered, n_rows = orig, 0, index.n
+        else:
+            ids_host = cand.cpu().numpy()
+            host_rows = index.originals.numpy() if _is_torch(index.originals) else np.asarray(index.originals)
+            rows = torch.from_numpy(np.ascontiguousarray(host_rows[ids_host], dtype=np.float32)).to(dev)
+            gathered, n_rows = 1, count
+        if rows.dtype != torch.float32 or rows.stride(-1) != 1:
+            rows = rows.to(torch.float32).contiguous()
+        if kk > MAX_K:
+            # library fallback beyond XFBQ_MAX_K (no hand-written selector that wide): float64 GEMV + two stable sorts
+            sel_rows = rows if gathered else rows[cand]
+            sims = sel_rows.to(torch.float64) @ q_dev
+            by_id = torch.sort(cand, stable=True)
+            by_sim = torch.sort(-sims[by_id.indices], stable=True)
+            order = by_id.indices[by_sim.indices][:kk]
+            sims_out, ids_out = sims[order], cand[order]
+        else:
+            ws_bytes = int(L.xfbq_refine_workspace_bytes(count, kk))
+            ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
+            sims_out = torch.empty(kk, dtype=torch.float64, device=dev)
+            ids_out = torch.empty(kk, dtype=torch.int64, device=dev)
+            ld = rows.stride(0) if rows.shape[0] > 1 else rows.shape[1]
+            _native.check(L.xfbq_refine_f32(rows.data_ptr(), n_rows, rows.shape[1], ld, gathered, cand.data_ptr(), count,
+                                            q_dev.data_ptr(), kk, sims_out.data_ptr(), ids_out.data_ptr(), ws.data_ptr(),
+                                            ws_bytes, st))
+        sims_h, ids_h = to_host_arrays(sims_out, ids_out)
+    return [(int(i), float(s)) for i, s in zip(ids_h, sims_h)]
 
 
 def k_select(index: Index, request: SearchRequest, collect_timing: bool = False) -> SearchResult:
@@ -218,12 +269,7 @@ def k_select(index: Index, request: SearchRequest, collect_timing: bool = False)
         hits = [(int(i), float(s)) for i, s in zip(top_i, sims)]
         approximate = True
     else:
-        rows = _originals_device(index)[cand].to(torch.float64)
-        q64 = torch.from_numpy(request.query).to(rows.device)
-        sims = (rows @ q64).cpu().numpy()                               # search.py:153-157
-        ids = cand.cpu().numpy()
-        order = np.lexsort((ids, -sims))[: request.k]                   # search.py:129-131
-        hits = [(int(ids[i]), float(sims[i])) for i in order]
+        hits = _refine_device(index, request.query, cand, request.k)
         approximate = False
     sync(); t4 = time.perf_counter()
     if index.ids is not None:
