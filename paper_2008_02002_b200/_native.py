@@ -80,10 +80,11 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    if needs_build():
+    override = os.environ.get("XFBQ_LIB")  # A/B experiments: another build of the same ABI (missing symbols fail loudly below)
+    if override is None and needs_build():
         build()
     try:
-        L = ctypes.CDLL(str(LIB))
+        L = ctypes.CDLL(override or str(LIB))
     except OSError as exc:  # pragma: no cover
         raise NativeLibraryError(f"cannot load {LIB}: {exc}") from exc
     i64, i32, vp, dbl = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_double
@@ -120,6 +121,8 @@ def lib():
         "xfbq_launch_count": (i64, []),
     }
     for name in SYMBOLS:
+        if override and not hasattr(L, name):
+            continue
         fn = getattr(L, name)
         fn.restype, fn.argtypes = sig[name]
     if L.xfbq_abi_version() != 1:

@@ -668,15 +668,44 @@ merge_tree_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k,
 // survivors: when the buffer of B keys could overflow it is sorted, cut back to its k best, and the bound
 // tightens to the k-th of those.  B is a power of two >= k + blockDim.x.  With bound == nullptr the rows must be
 // sorted and the bound comes from the rows themselves (see below).
+// With `src.counts` the partial results are the scan CTAs' candidate lists where they lie (single-wave plans of the queue
+// kernel: CTA part * groups + group holds, for each of its nq_cta queries, src.counts[...] <= cap unsorted keys): the rows
+// have different lengths, entry e of the query maps to (part, slot) through a prefix sum of the lengths.
+struct ListSrc {
+    const int *counts = nullptr;  // [parts * groups][nq_cta]
+    int nq_cta = 0, cap = 0, groups = 0;
+};
 __global__ void __launch_bounds__(512)
 merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k, int B, const int32_t *__restrict__ bound,
-                     const int32_t *__restrict__ qconst, uint64_t *__restrict__ out) {
+                     const int32_t *__restrict__ qconst, uint64_t *__restrict__ out, const ListSrc src = ListSrc()) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t *buf = reinterpret_cast<uint64_t *>(smem_raw);
     __shared__ int s_cnt;
     __shared__ long long s_limit;
+    __shared__ int s_pre[257];  // list mode: entries of the query in parts < i (parts <= 256)
     const int64_t q = blockIdx.x;
     const int lane = threadIdx.x & 31, nt = blockDim.x;
+    const bool lists = src.counts != nullptr;
+    const int gr = lists ? static_cast<int>(q / src.nq_cta) : 0, ql = lists ? static_cast<int>(q - static_cast<int64_t>(gr) * src.nq_cta) : 0;
+    if (lists) {
+        if (threadIdx.x < 32) {  // warp scan over the parts' list lengths
+            int run = 0;
+            for (int p0 = 0; p0 < parts; p0 += 32) {
+                const int part = p0 + lane;
+                const int c = part < parts ? src.counts[(static_cast<int64_t>(part) * src.groups + gr) * src.nq_cta + ql] : 0;
+                int inc = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += v;
+                }
+                if (part < parts) s_pre[part] = run + inc - c;
+                run += __shfl_sync(0xffffffffu, inc, 31);
+            }
+            if (lane == 0) s_pre[parts] = run;
+        }
+        __syncthreads();
+    }
     if (threadIdx.x == 0) {
         s_cnt = 0;
         // largest distance that can still be in the top k
@@ -711,7 +740,7 @@ merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int
                 __syncthreads();
             }
     };
-    const int64_t total = static_cast<int64_t>(parts) * k;
+    const int64_t total = lists ? s_pre[parts] : static_cast<int64_t>(parts) * k;
     for (int64_t e0 = 0; e0 < total; e0 += nt) {
         __syncthreads();
         const int c = s_cnt;
@@ -731,8 +760,17 @@ merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int
         const int64_t e = e0 + threadIdx.x;
         uint64_t key = KEY_INF;
         if (e < total) {
-            const int64_t part = e / k, slot = e - part * k;
-            key = in[(part * nq + q) * k + slot];
+            if (lists) {
+                int lo = 0, hi = parts;  // largest part with s_pre[part] <= e
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_pre[mid] <= static_cast<int>(e)) lo = mid; else hi = mid;
+                }
+                key = __ldcg(in + ((static_cast<int64_t>(lo) * src.groups + gr) * src.nq_cta + ql) * src.cap + (e - s_pre[lo]));
+            } else {
+                const int64_t part = e / k, slot = e - part * k;
+                key = in[(part * nq + q) * k + slot];
+            }
         }
         const bool keep = key != KEY_INF && static_cast<long long>(key >> 32) <= limit;
         const unsigned m = __ballot_sync(0xffffffffu, keep);
@@ -1153,6 +1191,7 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
 struct UmmaShape {
     int MT = 2, DW = 1, groups = 1, grid = 1, slots = 1, parts = 1, cap = 0, NS = 0;
     bool queue = false;  // scan_queue_kernel (main scans) vs scan_kernel (sample scans: open thresholds)
+    bool direct = false; // queue kernel with one work item per CTA: lists stay in place, the bounded merge reads them (no emission)
     bool count = false;  // sample scan that only counts scores into per-query histograms (scan_kernel<.., SEED = true>)
     int64_t tile_stride = 1, n_valid = 0;  // counting scan: stage i reads tile i * tile_stride of a database of n_valid documents
     int ring_rows = 64;
@@ -1166,7 +1205,7 @@ struct UmmaPlan {
     UmmaShape main, pre;
     int64_t sample = 0;
     size_t off_qimg = 0, off_qconst = 0, off_tau = 0, off_prekeys = 0, off_lists = 0, off_parts = 0, off_mscratch = 0,
-           off_theta0 = 0, off_ghist = 0, off_seedpar = 0, off_seedhist = 0, bytes = 0;
+           off_theta0 = 0, off_ghist = 0, off_seedpar = 0, off_seedhist = 0, off_counts = 0, bytes = 0;
 };
 
 typedef void (*UmmaKernel)(const umma::Params);
@@ -1252,6 +1291,8 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
         const int64_t items = static_cast<int64_t>(sh.n_seg) * sh.groups;
         if (sh.grid > items) sh.grid = static_cast<int>(items);
         slots = sh.n_seg;
+        sh.direct = items <= sh.grid && sh.n_seg > 1 && sh.n_seg <= 256 && env_int("XFBQ_UMMA_DIRECT", 1) != 0 && env_int("XFBQ_MERGE_BOUNDED", 1) != 0 &&
+                    env_int("XFBQ_UMMA_SHARE", 1) != 0;
     }
     sh.slots = slots;
     sh.parts = slots * sh.DW;
@@ -1278,7 +1319,7 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     const bool forced = eng && strcmp(eng, "umma") == 0;
     if (!have_nibbles || wd > 4 || wq > 7 || !(C == 1 || C == 2 || C == 4) || k > 1024 || n < 1 || env_int("XFBQ_FORCE_GENERIC", 0))
         return XFBQ_OK;
-    if (!forced && nq < env_int("XFBQ_UMMA_MIN_NQ", 32)) return XFBQ_OK;  // small batches: the mma.sync scans (HBM-bound below 17 queries; measured crossover at 32)
+    if (!forced && nq < env_int("XFBQ_UMMA_MIN_NQ", 17)) return XFBQ_OK;  // <= 16 queries: the mma.sync scans (HBM-bound on the nibble layout; a 24-query batch took 0.72 ms there, 0.55 ms here)
     if (nq < 1) return XFBQ_OK;
     if (merge_group_max(k) == 0 || nq > 65535) return XFBQ_OK;  // lists are emitted unsorted: needs the tree merge
     DeviceInfo info;
@@ -1334,6 +1375,8 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     pl.off_ghist = off; off = align256(off + (use_hist ? static_cast<size_t>(nq) * umma::HIST_BINS * 4 : 0));
     pl.off_seedpar = off; off = align256(off + (count ? static_cast<size_t>(nq) * 8 : 0));
     pl.off_seedhist = off; off = align256(off + (count ? static_cast<size_t>(nq) * umma::SEED_BINS * 4 : 0));
+    if (!(sample > 0)) pl.main.direct = false;  // the bounded merge needs the seeded, shared thresholds
+    pl.off_counts = off; off = align256(off + (pl.main.direct ? static_cast<size_t>(pl.main.grid) * 128 * pl.main.MT * 4 : 0));
     pl.bytes = off;
     pl.ok = true;
     *plan = pl;
@@ -1376,6 +1419,8 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     p.hist_shift = g_hist_shift;
     p.seed_par = sh.count ? reinterpret_cast<const int2 *>(ws + pl.off_seedpar) : nullptr;
     p.seed_hist = sh.count ? reinterpret_cast<uint32_t *>(ws + pl.off_seedhist) : nullptr;
+    const bool direct = sh.direct && &sh == &pl.main && tau_init != nullptr;
+    p.list_counts = direct ? reinterpret_cast<int *>(ws + pl.off_counts) : nullptr;
     p.prof = (&sh == &pl.main) ? g_prof : nullptr;
     p.pace = env_int("XFBQ_UMMA_PACE", 48);
     p.debug = env_int("XFBQ_UMMA_DEBUG", 0);
@@ -1400,7 +1445,13 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
             e = cudaFuncSetAttribute(merge_bounded_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "merge smem opt-in: %s", cudaGetErrorString(e));
         }
-        merge_bounded_kernel<<<static_cast<unsigned>(nq), threads, smem, st>>>(p.out, sh.parts, nq, k, B, p.theta_g, p.qconst, keys_out);
+        if (direct) {
+            ListSrc src;
+            src.counts = p.list_counts; src.nq_cta = 128 * sh.MT; src.cap = sh.cap; src.groups = sh.groups;
+            merge_bounded_kernel<<<static_cast<unsigned>(nq), threads, smem, st>>>(p.lists, sh.parts, nq, k, B, p.theta_g, p.qconst, keys_out, src);
+        } else {
+            merge_bounded_kernel<<<static_cast<unsigned>(nq), threads, smem, st>>>(p.out, sh.parts, nq, k, B, p.theta_g, p.qconst, keys_out);
+        }
         return check_launch("merge_bounded_kernel");
     }
     return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st, true);

@@ -60,6 +60,8 @@ struct Params {
     uint32_t *seed_hist;       // sample-histogram kernel: [nq][SEED_BINS] counts of sample scores >= origin
     uint64_t *lists;           // [grid][EPI_WARPS][32][cap]
     uint64_t *out;             // [slots * DW][nq][k], KEY_INF pre-filled when slots > 1
+    int *list_counts;          // queue kernel, single-wave plans: [grid][queries per CTA] final list lengths -- the lists are not
+                               // cut to k and copied out, merge_bounded_kernel reads them where they are; nullptr: emit to `out`
     int64_t nq, stages;
     int groups, k, cap, NS;    // NS = operand stages in shared memory
     int ring_rows;             // queue kernel: rows of a drain warp's ring (32 or 64)
@@ -844,7 +846,7 @@ constexpr int RING_ROWS_MAX = 64;                             // parked rows per
 constexpr int STASH_WORDS = 36;                               // a parked row: 32 scores, query, first document, ticket, pad (144 B)
 
 struct QSmemLayout {
-    uint32_t b_off, ring_off, state_off, hist_off, slotbar_off, bar_off, total;
+    uint32_t b_off, ring_off, state_off, hist_off, bar_off, total;
 };
 __host__ __device__ inline QSmemLayout q_smem_layout(int C, int NS, int ring_rows) {
     QSmemLayout L;
@@ -853,10 +855,22 @@ __host__ __device__ inline QSmemLayout q_smem_layout(int C, int NS, int ring_row
     L.ring_off = off; off += Q_DRAIN * ring_rows * STASH_WORDS * 4;
     L.state_off = off; off += 5 * 256 * 4 + 2 * Q_DRAIN * 4 + 32;  // per query: count, threshold, Dq, claim, seeded threshold; per drain warp: tail, final ticket
     L.hist_off = off; off += Q_RESOLVERS * 256 * 4;
-    L.slotbar_off = off; off += (2 * Q_DRAIN * ring_rows + Q_DRAIN) * 8;  // per ring slot: row-full and row-free mbarriers; per drain warp: segment end
     L.bar_off = off; off += (2 * NS + 2 * ACC_BUFS) * 8 + 16;
     L.total = off + 1024;
     return L;
+}
+// Ring hand-off words (tickets, consumption counters): release stores / acquire loads at CTA scope -- the PTX memory
+// model's own ordering of the row payload against the word that publishes it (no volatile + fence pairs).  An mbarrier
+// per ring slot (arrive.release / test_wait.acquire) was measured: same guarantees, but the resolvers' 32 barrier tests
+// per ring and sweep cost 23 % of the 10k-query scan (14.55 -> 17.85 ms), and compute-sanitizer's racecheck flags the
+// mbarrier form of this protocol as well (tools/sanitizer_probe.cu variant 5, profiles/README.md).
+__device__ __forceinline__ int ld_acquire(const int *p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v) {
+    asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
 template <int C, int MT>
@@ -874,15 +888,9 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
     const QSmemLayout L = q_smem_layout(C, NS, RING_ROWS);
     unsigned char *sB = smem + L.b_off;
     uint32_t *rings = reinterpret_cast<uint32_t *>(smem + L.ring_off);
-    int *cnt_s = reinterpret_cast<int *>(smem + L.state_off), *theta_s = cnt_s + 256, *dq_s = cnt_s + 512;
+    int *cnt_s = reinterpret_cast<int *>(smem + L.state_off), *theta_s = cnt_s + 256, *dq_s = cnt_s + 512, *claim_s = cnt_s + 768;
     int *theta0_s = cnt_s + 1024;
-    int *tail_s = cnt_s + 1280, *fin_s = tail_s + Q_DRAIN;  // per drain warp: rows consumed so far (resolver-private); last ticket of the segment
-    // Ring hand-offs are mbarriers (release on arrive, acquire on the test): slot_full[w][s] completes a phase every time
-    // drain warp w parks a row in slot s, slot_free[w][s] every time its resolver has consumed it, seg_done[w] when the
-    // warp has parked the last row of a work item.  Tickets run on across work items, so the phase of ticket t is t / RING_ROWS.
-    uint64_t *slot_full = reinterpret_cast<uint64_t *>(smem + L.slotbar_off), *slot_free = slot_full + Q_DRAIN * RING_ROWS;
-    uint64_t *seg_done = slot_free + Q_DRAIN * RING_ROWS;
-    const int LOG_R = RING_ROWS == 64 ? 6 : 5;
+    int *tail_s = cnt_s + 1280, *fin_s = tail_s + Q_DRAIN;  // per drain warp: rows consumed by its resolver; final ticket of a segment
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L.bar_off);
     uint64_t *b_full = bars, *b_empty = bars + NS, *acc_full = bars + 2 * NS, *acc_empty = bars + 2 * NS + ACC_BUFS;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 2 * ACC_BUFS);
@@ -895,9 +903,9 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
         for (int i = 0; i < NS; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
         for (int i = 0; i < ACC_BUFS; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], EPI_PER_BUF); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int w = 0; w < Q_DRAIN; ++w) { tail_s[w] = 0; fin_s[w] = 0; mbar_init(&seg_done[w], 1); }
+        for (int w = 0; w < Q_DRAIN; ++w) { tail_s[w] = 0; fin_s[w] = -1; }
     }
-    for (int i = threadIdx.x; i < 2 * Q_DRAIN * RING_ROWS; i += Q_THREADS) mbar_init(&slot_full[i], 1);  // slot_free follows slot_full
+    for (int i = threadIdx.x; i < Q_DRAIN * RING_ROWS; i += Q_THREADS) rings[i * STASH_WORDS + 34] = 0u;  // no ticket yet
     if (warp == 0) tmem_alloc(tmem_slot, 512);
     fence_before();
     cta_sync();
@@ -915,6 +923,11 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
     auto emit_lists = [&](int slot, int *hist, int gr, int part) {
         const int64_t gq0 = static_cast<int64_t>(gr) * NQ_CTA;
         const int cap = p.cap, k = p.k;
+        if (p.list_counts) {  // one work item per CTA: leave the lists in place, publish their lengths
+            for (int qc = slot * 32 + lane; qc < NQ_CTA; qc += (Q_DRAIN + Q_RESOLVERS) * 32)
+                p.list_counts[static_cast<int64_t>(blockIdx.x) * NQ_CTA + qc] = gq0 + qc < p.nq ? cnt_s[qc] : 0;
+            return;
+        }
         for (int qc = slot; qc < NQ_CTA; qc += Q_DRAIN + Q_RESOLVERS) {
             const int64_t qq = gq0 + qc;
             if (qq >= p.nq) break;
@@ -936,8 +949,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
         // every warp three MMA group times per accumulator.
         const int q4 = warp & 3, set = warp >> 2;
         uint32_t *ring = rings + warp * (RING_ROWS * STASH_WORDS);  // this warp's ring; resolver (q4 & 1) owns its queries' lists
-        int head = 0;                                 // tickets handed out so far (warp-uniform; never reset)
-        uint64_t *my_full = slot_full + warp * RING_ROWS, *my_free = slot_free + warp * RING_ROWS;
+        int head = 0, tail_seen = 0;                  // tickets handed out (warp-uniform) / consumption last observed
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(q4 * 32) << 16);
         while (sg.next()) {
             if (warp < 4 * MT) {  // query rows -> tensor memory; the queries' shared state
@@ -969,24 +981,28 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                     const int n = __popc(hm);
                     const int t0 = head;
                     head += n;
+                    if (head - tail_seen > RING_ROWS) {  // maybe full: look at the resolver's progress, wait if it is behind
+                        const long long tw = prof ? clock64() : 0;
+#ifdef XFBQ_UMMA_WATCHDOG
+                        const long long wd0 = clock64();
+#endif
+                        while (head - (tail_seen = ld_acquire(&tail_s[warp])) > RING_ROWS) {
+                            __nanosleep(40);
+#ifdef XFBQ_UMMA_WATCHDOG
+                            if (clock64() - wd0 > 4000000000ll) { if (lane == 0) printf("drain %d cta %d stuck: head %d tail %d\n", warp, blockIdx.x, head, tail_seen); __trap(); }
+#endif
+                        }
+                        if (prof) w3 += clock64() - tw;
+                    }
                     if (hit) {
                         const int t = t0 + __popc(hm & ((1u << lane) - 1u));
-                        const int slot = t & (RING_ROWS - 1);
-                        // the slot is free once the resolver has consumed ticket t - RING_ROWS (phase t / RING_ROWS - 1 of its
-                        // row-free barrier; a fresh barrier reads as "previous phase complete")
-                        const uint32_t free_parity = ((static_cast<uint32_t>(t) >> LOG_R) & 1u) ^ 1u;
-                        if (!mma::mbar_test(&my_free[slot], free_parity)) {
-                            const long long tw = prof ? clock64() : 0;
-                            mbar_wait(&my_free[slot], free_parity);
-                            if (prof) w3 += clock64() - tw;
-                        }
-                        uint32_t *row = ring + slot * STASH_WORDS;
+                        uint32_t *row = ring + (t & (RING_ROWS - 1)) * STASH_WORDS;
 #pragma unroll
                         for (int c = 0; c < 8; ++c)
                             *reinterpret_cast<uint4 *>(row + 4 * c) = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
                         row[32] = qloc;
                         row[33] = doc0;
-                        mbar_arrive(&my_full[slot]);  // release: the row is visible to whoever sees the phase complete
+                        st_release(reinterpret_cast<int *>(row + 34), t + 1);  // publishes the row
                     }
                 }
             };
@@ -1022,10 +1038,13 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                 }
             }
             __syncwarp();
-            if (lane == 0) { fin_s[warp] = head; mbar_arrive(&seg_done[warp]); }  // every ticket of this work item is out
+            if (lane == 0) st_release(&fin_s[warp], head);  // every ticket of this segment is out
             cta_sync();  // the resolvers have emptied the rings: lists are final, this warp's ring is free scratch
             emit_lists(warp, reinterpret_cast<int *>(ring), sg.gr, sg.part);
             __syncwarp();
+            for (int i = lane; i < RING_ROWS; i += 32) ring[i * STASH_WORDS + 34] = 0u;  // scratch use may have forged tickets
+            head = 0; tail_seen = 0;
+            if (lane == 0) { st_release(&tail_s[warp], 0); }
             s_run += static_cast<uint32_t>(sg.cnt);
             cta_sync();
         }
@@ -1102,7 +1121,6 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
         const uint32_t n_docs = static_cast<uint32_t>(p.n);
         const uint32_t id_off = static_cast<uint32_t>(p.row_offset);
         const int cap = p.cap, k = p.k;
-        uint32_t seg_parity = 0;  // work items this CTA has finished, mod 2 (phase of seg_done)
         while (sg.next()) {
             cta_sync();
             const int64_t gq0 = static_cast<int64_t>(sg.gr) * NQ_CTA;
@@ -1110,7 +1128,13 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             // round-robin refresh of this resolver's queries from the global histogram: the bins of the next query
             // are fetched while the current sweep runs (one L2 round trip per sweep would double its length)
             constexpr int OWN_Q = NQ_CTA / Q_RESOLVERS;
-            int rq = 0, rq_pending = -1;
+            // The CTAs that scan this query group at the same time (one per document slice) start their rounds at different
+            // queries, so between them every query's histogram is read every few sweeps; what one CTA proves it publishes
+            // through theta_g, and every CTA imports theta_g for all its queries every few sweeps (below).  A lone CTA
+            // gets round to a query only every OWN_Q sweeps: with one query group (<= 256 queries, 148 slices of 0.6 ms)
+            // thresholds lagged so far behind that 31 % of the 32 x 32 score chunks parked a row.
+            int rq = static_cast<int>((static_cast<int64_t>(sg.part) * OWN_Q) / (p.n_seg > 0 ? p.n_seg : 1)) % OWN_Q, rq_pending = -1;
+            int sweeps = 0;
             uint4 hb_lo = make_uint4(0u, 0u, 0u, 0u), hb_hi = hb_lo;
 #ifdef XFBQ_UMMA_WATCHDOG
             long long wd0 = clock64();
@@ -1143,17 +1167,15 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
 #pragma unroll 1
                 for (int w = res; w < Q_DRAIN; w += Q_RESOLVERS) {  // the rings of the drain warps this resolver serves
                     uint32_t *ring = rings + w * (RING_ROWS * STASH_WORDS);
-                    const int tail = tail_s[w];  // resolver-private (written by lane 0 below, behind a warp barrier)
+                    const int tail = ld_acquire(&tail_s[w]);
                     // rows tail .. tail + n - 1 are ready (tickets are handed out in order, rows may land out of order)
                     const int t = tail + lane;
-                    const int slot = t & (RING_ROWS - 1);
-                    const uint32_t *row = ring + slot * STASH_WORDS;
-                    const bool ready = mma::mbar_test(&slot_full[w * RING_ROWS + slot], (static_cast<uint32_t>(t) >> LOG_R) & 1u);  // acquire
+                    const uint32_t *row = ring + (t & (RING_ROWS - 1)) * STASH_WORDS;
+                    const bool ready = ld_acquire(reinterpret_cast<const int *>(row + 34)) == t + 1;
                     const unsigned rm = __ballot_sync(0xffffffffu, ready);
                     const int n = rm == 0xffffffffu ? 32 : __ffs(~rm) - 1;
                     if (n == 0) {
-                        // nothing parked: done with this ring once its warp has announced its last ticket and we have consumed it
-                        if (!(mma::mbar_test(&seg_done[w], seg_parity) && fin_s[w] == tail)) all_done = false;
+                        if (ld_acquire(&fin_s[w]) != tail) all_done = false;
                         continue;
                     }
                     progressed = true;
@@ -1162,10 +1184,12 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                     const int q = pend ? static_cast<int>(row[32]) : 0;
                     const uint32_t doc0 = pend ? row[33] : 0u;
                     while (__any_sync(0xffffffffu, pend)) {
-                        // one row per query and round (the highest lane holding a row of the query goes), so a round adds at
-                        // most 32 keys to a list
-                        const unsigned peers = __match_any_sync(0xffffffffu, pend ? q : 0x10000 + lane);
-                        const bool go = pend && lane == 31 - __clz(peers);
+                        // a round adds at most 32 keys to a list:
+// one row per query and round: the last lane to claim the query's word goes (an atomic exchange, so the lanes' writes
+                        // are ordered; __match_any_sync picks the same kind of winner but cost 2 % of the 10k-query scan)
+                        if (pend) atomicExch(&claim_s[q], lane);
+                        __syncwarp();
+                        const bool go = pend && claim_s[q] == lane;
                         if (go) {
                             const int th = theta_s[q], dqe = dq_s[q];
                             uint32_t below = 0;  // bit j: score j < threshold
@@ -1211,8 +1235,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                         }
                     }
                     __syncwarp();
-                    if (lane < n) mbar_arrive(&slot_free[w * RING_ROWS + slot]);  // the row has been read: its slot may be reused
-                    if (lane == 0) tail_s[w] = tail + n;
+                    if (lane == 0) st_release(&tail_s[w], tail + n);
                     __syncwarp();
                 }
                 if (all_done) break;
@@ -1221,28 +1244,27 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                 else if (clock64() - wd0 > 4000000000ll) {
                     if (lane == 0) {
                         printf("resolver %d cta %d stuck:", res, blockIdx.x);
-                        for (int w = res; w < Q_DRAIN; w += Q_RESOLVERS) printf(" [w%d tail %d fin %d]", w, tail_s[w], fin_s[w]);
+                        for (int w = res; w < Q_DRAIN; w += Q_RESOLVERS) printf(" [w%d tail %d fin %d flag %d addr %u]", w, tail_s[w], fin_s[w], (int)rings[(w * RING_ROWS + (tail_s[w] & (RING_ROWS - 1))) * STASH_WORDS + 34], smem_u32(&rings[(w * RING_ROWS + (tail_s[w] & (RING_ROWS - 1))) * STASH_WORDS + 34]));
                         printf("\n");
                     }
                     __trap();
                 }
 #endif
-                if (!progressed) {
-                    if (p.theta_g && (++idle & 15) == 0) {  // idle: import the thresholds other CTAs found for our queries
-                        for (int blk = res; blk < NQ_CTA / 32; blk += Q_RESOLVERS) {
-                            const int qc = blk * 32 + lane;
-                            if (gq0 + qc < p.nq) {
-                                const int th = __ldcg(p.theta_g + gq0 + qc);
-                                if (th > theta_s[qc]) atomicMax(&theta_s[qc], th);
-                            }
+                if (p.theta_g && ((++sweeps & 7) == 0 || (!progressed && (++idle & 15) == 0))) {
+                    // import the thresholds other CTAs found for our queries (4 coalesced loads per resolver)
+                    for (int blk = res; blk < NQ_CTA / 32; blk += Q_RESOLVERS) {
+                        const int qc = blk * 32 + lane;
+                        if (gq0 + qc < p.nq) {
+                            const int th = __ldcg(p.theta_g + gq0 + qc);
+                            if (th > theta_s[qc]) atomicMax(&theta_s[qc], th);
                         }
                     }
-                    __nanosleep(100);
                 }
+                if (!progressed) __nanosleep(100);
             }
             cta_sync();  // every resolver is done: lists are final
             emit_lists(Q_DRAIN + res, hist, sg.gr, sg.part);
-            seg_parity ^= 1u;
+            if (lane < Q_DRAIN && (lane % Q_RESOLVERS) == res) st_release(&fin_s[lane], -1);  // next segment's tickets are not out yet
             s_run += static_cast<uint32_t>(sg.cnt);
             cta_sync();
         }
