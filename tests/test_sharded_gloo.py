@@ -36,12 +36,12 @@ def _oracle_merge(stacked, k):
     return torch.from_numpy(np.sort(a.transpose(1, 0, 2).reshape(nq, parts * kk), axis=1)[:, :kk].view(np.int64).copy())
 
 
-def _worker(rank, world, port, case, k, out_dir):
+def _worker(rank, world, port, case, k, out_dir, query_shards=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle import xfbq_oracle as xo
-        from paper_2008_02002_b200.sharded import ShardedIndex, shard_bounds
+        from paper_2008_02002_b200.sharded import ShardedIndex, grid_of, shard_bounds
         from tests._golden import synth_case, small_cases
         if case == "tiny":
             c = next(x for x in small_cases() if x["n"] >= 3 and x["dim"] == 65 and x["wd"] == 4)
@@ -51,10 +51,11 @@ def _worker(rank, world, port, case, k, out_dir):
             c = synth_case(case)
             docs, queries, n = c["docs"], c["queries"][:6], c["n"]
             want_d, want_i = c["z"]["dists"][:6], c["z"]["ids"][:6]
-        lo, hi = shard_bounds(n, world, rank)
+        R, r, _ = grid_of(world, rank, query_shards)   # R row shards x query_shards query blocks
+        lo, hi = shard_bounds(n, R, r)
         planes = xo.c_quantize_matrix(docs[lo:hi], c["wd"], c["scale"]) if hi > lo else np.zeros((c["wd"], (c["dim"] + 63) // 64, 0), np.uint64)
         shard = ShardedIndex(local=_HostShard(planes, c["dim"], c["wq"], c["scale"]), row_offset=lo, n_total=n,
-                             world=world, rank=rank, scan_fn=_oracle_scan, merge_fn=_oracle_merge)
+                             world=world, rank=rank, scan_fn=_oracle_scan, merge_fn=_oracle_merge, query_shards=query_shards)
         scores, ids = shard.search(queries, k)
         if want_d is None:
             full = xo.c_quantize_matrix(docs, c["wd"], c["scale"])
@@ -74,11 +75,27 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,case,k", [(2, "cfg1_100k_128_w4", 10), (3, "cfg2_60k_128_w3", 100), (2, "tiny", 50)])
-def test_sharded_search_gloo(world, case, k, tmp_path):
-    mp.spawn(_worker, args=(world, _free_port(), case, k, str(tmp_path)), nprocs=world, join=True)
+@pytest.mark.parametrize("world,query_shards,case,k", [
+    (2, 1, "cfg1_100k_128_w4", 10), (3, 1, "cfg2_60k_128_w3", 100), (2, 1, "tiny", 50),   # rows only
+    (2, 2, "cfg1_100k_128_w4", 10),                                                         # queries only (replicated database, no merge)
+    (4, 2, "cfg2_60k_128_w3", 100), (4, 2, "tiny", 50),                                     # 2 row shards x 2 query blocks (6 and 3 queries: ragged blocks)
+])
+def test_sharded_search_gloo(world, query_shards, case, k, tmp_path):
+    mp.spawn(_worker, args=(world, _free_port(), case, k, str(tmp_path), query_shards), nprocs=world, join=True)
     for r in range(world):
         assert Path(tmp_path, f"rank{r}.txt").read_text() == "ok"
+
+
+def test_grid_and_layout_choice():
+    from paper_2008_02002_b200.errors import InvalidInputError
+    from paper_2008_02002_b200.sharded import choose_query_shards, grid_of
+    assert grid_of(8, 5, 4) == (2, 1, 1) and grid_of(8, 7, 1) == (8, 7, 0) and grid_of(8, 3, 8) == (1, 0, 3)
+    with pytest.raises(InvalidInputError):
+        grid_of(8, 0, 3)
+    assert choose_query_shards(8, 10_000_000, 256, 4, 10_000) == 8        # config 4: replicate, 1 250 queries per GPU
+    assert choose_query_shards(8, 10_000_000, 256, 4, 1) == 1             # single queries: split the rows
+    assert choose_query_shards(8, 100_000_000, 512, 4, 10_000) == 4       # config 5: a replica does not fit in half of HBM
+    assert choose_query_shards(1, 10_000_000, 256, 4, 10_000) == 1
 
 
 def test_shard_bounds_cover_rows_exactly():
