@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the cpu_baseline leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip recall / single-query extras")
+    ap.add_argument("--layout", default="auto",
+                    help="multi-GPU grid: 'rows' (database split N ways), 'queries' (database replicated, batch split N ways), "
+                         "an integer Q (N/Q row shards x Q query blocks) or 'auto' (sharded.choose_query_shards)")
     return ap.parse_args()
 
 
@@ -188,23 +191,46 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ corpus
-def gen_chunk_gpu(torch, c, rows, dim):
-    g = torch.Generator(device="cuda").manual_seed(4000 + c)
-    x = torch.randn((rows, dim), generator=g, device="cuda", dtype=torch.float32)
-    return x / x.norm(dim=1, keepdim=True)
+def gen_chunk_host(c, rows, dim):
+    """Chunk c of the global corpus = the reference generator's recipe (dataio.py:104-124 generate_synthetic: PCG64,
+    normal(0, 1/sqrt(dim)), float64 row normalisation, cast to float32) with seed 4000 + c, `rows` rows.  Both arms call
+    this function, so the GPU path and the CPU reference see identical bytes (tests/test_oracle_golden.py pins the recipe
+    to the reference's own output)."""
+    rng = np.random.Generator(np.random.PCG64(4000 + c))
+    data = rng.normal(0.0, 1.0 / np.sqrt(dim), size=(rows, dim))
+    data /= np.linalg.norm(data, axis=1, keepdims=True)
+    return data.astype(np.float32)
+
+
+def gen_rows_host(lo, hi, n, dim, sink, workers=4):
+    """Rows [lo, hi) of the global corpus (identical for every sharding), chunk by chunk through `sink(first_row, rows)`;
+    chunks are generated by a few threads (numpy's generators release the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+    chunks = list(range(lo // CHUNK, -(-hi // CHUNK)))
+
+    def make(c):
+        c_lo, c_hi = c * CHUNK, min(n, (c + 1) * CHUNK)
+        x = gen_chunk_host(c, c_hi - c_lo, dim)
+        a, b = max(lo, c_lo), min(hi, c_hi)
+        return a, x[a - c_lo:b - c_lo]
+
+    with ThreadPoolExecutor(max_workers=workers) as pool:
+        for a, x in pool.map(make, chunks):
+            sink(a, x)
 
 
 def gen_rows_gpu(torch, lo, hi, n, dim):
-    """Rows [lo, hi) of the global synthetic corpus (identical for every sharding)."""
     out = torch.empty((hi - lo, dim), dtype=torch.float32, device="cuda")
-    c = lo // CHUNK
-    while c * CHUNK < hi:
-        c_lo, c_hi = c * CHUNK, min(n, (c + 1) * CHUNK)
-        x = gen_chunk_gpu(torch, c, c_hi - c_lo, dim)
-        a, b = max(lo, c_lo), min(hi, c_hi)
-        out[a - lo:b - lo] = x[a - c_lo:b - c_lo]
-        c += 1
+
+    def sink(a, x):
+        out[a - lo:a - lo + x.shape[0]].copy_(torch.from_numpy(x))
+
+    gen_rows_host(lo, hi, n, dim, sink)
     return out
+
+
+def gen_chunk_gpu(torch, c, rows, dim):  # tools/: one chunk on the device
+    return torch.from_numpy(gen_chunk_host(c, rows, dim)).cuda()
 
 
 def gen_queries(nq, dim):
@@ -245,15 +271,26 @@ def run_ours(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    # ---- the grid: R row shards x Q query blocks (sharded.py)
+    from paper_2008_02002_b200.sharded import choose_query_shards, grid_of
+    if a.layout == "auto":
+        Q = choose_query_shards(world, a.n, a.dim, a.doc_bits, a.nq)
+    elif a.layout == "rows":
+        Q = 1
+    elif a.layout == "queries":
+        Q = world
+    else:
+        Q = int(a.layout)
+    R, row_shard, _ = grid_of(world, rank, Q)
     # ---- build this rank's shard
-    lo, hi = xb.shard_bounds(a.n, world, rank)
-    head = gen_chunk_gpu(torch, 0, min(CHUNK, a.n), a.dim)[:100_000].cpu().numpy()
-    scale = xb.estimate_scale(head, 0.98)
-    params = xb.QuantParams(dim=a.dim, scale=scale, doc_bits=a.doc_bits, query_bits=a.query_bits)
+    lo, hi = xb.shard_bounds(a.n, R, row_shard)
     docs = gen_rows_gpu(torch, lo, hi, a.n, a.dim)
+    head = gen_chunk_host(0, min(CHUNK, a.n), a.dim)[:100_000] if lo > 0 else docs[:100_000]
+    scale = xb.estimate_scale(head, 0.98)   # GPU order statistics; bit-identical to the reference's np.quantile (tests)
+    params = xb.QuantParams(dim=a.dim, scale=scale, doc_bits=a.doc_bits, query_bits=a.query_bits)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    shard = xb.ShardedIndex.build(docs, params, n_total=a.n, row_offset=lo, world=world, rank=rank)
+    shard = xb.ShardedIndex.build(docs, params, n_total=a.n, row_offset=lo, world=world, rank=rank, query_shards=Q)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -271,8 +308,9 @@ def run_ours(a):
     db_bytes_local = index.packed.nbytes                      # algorithmic bytes of this rank's shard
     db_bytes_total = a.n * a.doc_bits * ((a.dim + 63) // 64) * 8
 
+    nq_local = -(-a.nq // Q)   # queries this rank scans per step
     plan = (np.zeros(6, dtype=np.int32))
-    _native.check(_native.lib().xfbq_scan_plan(index.n, a.dim, a.doc_bits, min(a.nq, xsearch._QUERY_BATCH),
+    _native.check(_native.lib().xfbq_scan_plan(index.n, a.dim, a.doc_bits, min(nq_local, xsearch._QUERY_BATCH),
                                                a.query_bits, min(a.k, index.n), 1, plan.ctypes.data))
 
     def step_device():
@@ -302,7 +340,8 @@ def run_ours(a):
     ms_step = max_over_ranks(e0.elapsed_time(e1) / a.steps)
     scan_ms = [s.elapsed_time(e) for s, e in scan_events]
     scan_ms_avg = sum(scan_ms) / len(scan_ms)          # whole xfbq_scan_topk call (prep + sample + scan + merge)
-    kernel_ms = _native.last_scan_ms()                  # the dominant kernel alone (last launch of the timed region)
+    kernel_ms, kernel_launches = _native.scan_ms_mean()  # the dominant kernel alone: mean over the launches of the timed region
+    kernel_ms = max_over_ranks(kernel_ms)
     _native.set_timing(False)
 
     # ---- end-to-end through the public API with host buffers
@@ -335,31 +374,43 @@ def run_ours(a):
     torch.cuda.empty_cache()
 
 
-    # ---- small-batch regime: single-query latency and achieved HBM bandwidth
+    # ---- batch-size sweep: call latency (device-resident queries), the dominant kernel's time and the fraction of the
+    # roofline that binds each size: HBM (one pass over the packed codes, n x doc_bits x ceil(dim/64) x 8 bytes) up to 16 queries,
+    # max(HBM pass, tensor time of nq x n x dim_padded int8 MACs) above
     single = None
     if not a.no_extras:
         single = {}
-        for nq1 in (1, 4, 8, 16):
+        hbm_peak_, _, _ = peaks()
+        hw_int8 = 2 * 8188 * 148 * 1.965e9
+        dim_pad_ = ((a.dim + 127) // 128) * 128
+        for nq1 in (1, 4, 8, 16, 32, 64, 256, 1024):
+            if nq1 > a.nq:
+                continue
             for _ in range(3):
                 shard.search_keys(q_dev[:nq1], a.k)
             barrier()
-            reps = 20
+            reps = 20 if nq1 <= 64 else 8
             e0.record()
             for r in range(reps):
-                shard.search_keys(q_dev[r * nq1:(r + 1) * nq1], a.k)
+                off = (r * nq1) % max(1, a.nq - nq1 + 1)
+                shard.search_keys(q_dev[off:off + nq1], a.k)
             e1.record()
             barrier()
             ms = max_over_ranks(e0.elapsed_time(e1) / reps)
             _native.set_timing(True)
-            kms = []
             for r in range(5):
-                shard.search_keys(q_dev[r * nq1:(r + 1) * nq1], a.k)
-                kms.append(_native.last_scan_ms())
+                off = (r * nq1) % max(1, a.nq - nq1 + 1)
+                shard.search_keys(q_dev[off:off + nq1], a.k)
+            kms = max_over_ranks(_native.scan_ms_mean()[0])
             _native.set_timing(False)
-            kms = max_over_ranks(statistics.median(kms))
+            nq_rank = -(-nq1 // Q)
+            bound_ms = max(db_bytes_local / (hbm_peak_ * 1e9), 2.0 * index.n * nq_rank * dim_pad_ / hw_int8) * 1e3
             single[f"nq{nq1}"] = {"latency_us": round(ms * 1e3, 1), "qps": round(nq1 / ms * 1e3, 1),
                                   "scan_kernel_us": round(kms * 1e3, 1),
-                                  "scan_kernel_GBps": round(db_bytes_local / kms / 1e6, 1)}
+                                  "scan_kernel_GBps": round(db_bytes_local / kms / 1e6, 1),
+                                  "bound": "hbm" if db_bytes_local / (hbm_peak_ * 1e9) * 1e3 >= bound_ms else "tensor",
+                                  "bound_us": round(bound_ms * 1e3, 1), "kernel_frac_of_bound": round(bound_ms / kms, 3),
+                                  "call_frac_of_bound": round(bound_ms / ms, 3)}
 
     if rank != 0:
         if world > 1:
@@ -368,10 +419,11 @@ def run_ours(a):
 
     hbm_peak, bf16_peak, peak_src = peaks()
     traffic = None  # DRAM bytes of the dominant kernel per launch, from the committed ncu --set full capture of this workload
+    traffic_file = "ncu_full_umma_queue_r2.csv" if (ROOT / "profiles" / "ncu_full_umma_queue_r2.csv").exists() else "ncu_full_umma_queue_r1_v13.csv"
     if (a.n, a.dim, a.nq, a.k, a.doc_bits, world) == (10_000_000, 256, 10000, 100, 4, 1):
         try:
             import csv
-            with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_full_umma_queue_r1_v13.csv")) as f:
+            with open(ROOT / "profiles" / traffic_file) as f:
                 rows = list(csv.reader(f))
             col = {h: i for i, h in enumerate(rows[0])}
             unit = {h: u for h, u in zip(rows[0], rows[1])}
@@ -379,13 +431,13 @@ def run_ours(a):
             traffic = sum(float(rows[2][col[m]]) * scale_of[unit[m]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         except Exception:
             traffic = None
-    launches_per_step = -(-a.nq // xsearch._QUERY_BATCH)
-    q_tiles_total = sum(-(-min(xsearch._QUERY_BATCH, a.nq - q0) // int(plan[0])) for q0 in range(0, a.nq, xsearch._QUERY_BATCH))
+    launches_per_step = -(-nq_local // xsearch._QUERY_BATCH)
+    q_tiles_total = sum(-(-min(xsearch._QUERY_BATCH, nq_local - q0) // int(plan[0])) for q0 in range(0, nq_local, xsearch._QUERY_BATCH))
     algo_bytes_per_launch = db_bytes_local * q_tiles_total / launches_per_step
     engine = {3: "umma", 2: "imma", 1: "popc-specialised", 0: "popc-generic"}[int(plan[4])]
     # integer work of one launch: nq x n_local x dim_padded multiply-accumulates (u8 x s8 -> s32)
     dim_pad = ((a.dim + 127) // 128) * 128
-    macs_per_launch = float(index.n) * min(a.nq, xsearch._QUERY_BATCH) * dim_pad
+    macs_per_launch = float(index.n) * min(nq_local, xsearch._QUERY_BATCH) * dim_pad
     tops = 2.0 * macs_per_launch / (kernel_ms * 1e-3) / 1e12
     int8_peak = 2.0 * bf16_peak  # dense int8 tensor rate = 2 x dense bf16 on B200 (tcgen05 path)
     sb = (single or {}).get("nq4") or {}   # a small query batch; nq1 / nq8 / nq16 are listed under small_batch
@@ -397,12 +449,13 @@ def run_ours(a):
         "data": "synthetic",
         "config": {"workload": workload_name(a), "n": a.n, "dim": a.dim, "doc_bits": a.doc_bits,
                    "query_bits": a.query_bits, "nq": a.nq, "k": a.k,
-                   "sharding": f"rows/{world}" if world > 1 else "none",
+                   "sharding": f"{R} row shards x {Q} query blocks" if world > 1 else "none",
                    "l2": "inputs larger than L2 (packed DB %.0f MB per GPU streamed every scan)" % (db_bytes_local / 1e6),
                    "plan": {"engine": engine, "queries_per_cta": int(plan[0]), "query_groups": int(plan[1]), "partial_results": int(plan[2]),
                             "cand_capacity": int(plan[3]), "smem_bytes": int(plan[5])}},
         "e2e": {"value": round(a.nq / e2e_ms * 1e3, 2), "unit": "queries/s", "ms_per_step": round(e2e_ms, 3),
-                "h2d_bytes_per_step": int(q_pinned.numel() * 4), "d2h_bytes_per_step": int(a.nq * min(a.k, a.n) * 8)},
+                "h2d_bytes_per_step": int(q_pinned.numel() * 4), "d2h_bytes_per_step": int(a.nq * min(a.k, a.n) * 16),
+                "note": "ShardedIndex.search: pinned float32 queries in, (scores, indices) int64 numpy arrays out"},
         "gpu_launches": int(launches),
         "clocks": clocks,
         "roofline": {"bound": "tensor",
@@ -410,13 +463,14 @@ def run_ours(a):
                                 "imma": "mma::scan_kernel (batch plan: IMMA.16832 + fused top-K)"}.get(engine, "scan_topk_kernel"),
                      "achieved": round(tops, 1), "peak": round(hw_int8_peak, 1), "unit": "TOP/s (int8, dense)",
                      "frac": round(tops / hw_int8_peak, 4), "traffic": traffic,
-                     "traffic_source": "profiles/ncu_full_umma_queue_r1_v13.csv (dram__bytes_read.sum + dram__bytes_write.sum of this launch)" if traffic else None,
+                     "traffic_source": f"profiles/{traffic_file}: dram__bytes_read.sum + dram__bytes_write.sum of this launch in a committed ncu --set full "
+                                       "capture of the same command (a constant read from the file, not measured in this run)" if traffic else None,
                      "peak_2x_measured_bf16": round(int8_peak, 1), "frac_of_2x_measured_bf16": round(tops / int8_peak, 4),
                      "peak_source": "measured on this pool's B200: tcgen05.mma kind::i8 issues 8188 MAC/clk/SM (tools/umma_probe.cu, "
                                     "profiles/umma_probe_r1.jsonl) x 148 SMs x 1965 MHz.  MEASURED_PEAKS.json holds no int8 figure: twice its "
                                     "dense bf16 burst (" + peak_src + ") is peak_2x_measured_bf16, which this kernel exceeds, so the "
                                     "stricter hardware rate is the denominator",
-                     "launch_ms": round(kernel_ms, 3), "macs_per_launch": int(macs_per_launch),
+                     "launch_ms": round(kernel_ms, 3), "launches_averaged": int(kernel_launches), "macs_per_launch": int(macs_per_launch),
                      "legacy_imma_pipe_peak_TOPs": 1163.7, "frac_of_legacy_imma_pipe": round(tops / 1163.7, 4),
                      "note": "tcgen05.mma kind::i8 measured at 8188 MAC/clk/SM (tools/umma_probe.cu) = 4.76 POP/s at 1965 MHz; "
                              "mma.sync int8 (IMMA.16832) pipe peak is 4096 op/clk/SM (ncu) = 1164 TOP/s"},
@@ -431,6 +485,10 @@ def run_ours(a):
                        "algorithmic_GBps": round(algo_bytes_per_launch / (kernel_ms * 1e-3) / 1e9, 1)},
         "small_batch": single,
         "recall_at_k_vs_float_cosine": recall,
+        "device_bytes": {"packed_codes": int(index.packed.device_nbytes),
+                         "derived_layouts": int(index.packed.nibbles.numel()) if index.packed.nibbles is not None else 0,
+                         "algorithmic": int(db_bytes_local),
+                         "ratio_to_algorithmic": round((index.packed.device_nbytes + (index.packed.nibbles.numel() if index.packed.nibbles is not None else 0)) / db_bytes_local, 2)},
         "build": {"rows_per_s": round((hi - lo) / build_s, 1), "seconds": round(build_s, 3),
                   "quantize_kernel_ms": round(quant_ms, 3),
                   "quantize_read_GBps": round((hi - lo) * a.dim * 4 / (quant_ms * 1e-3) / 1e9, 1)},
@@ -477,14 +535,12 @@ def run_reference(a):
     W64 = (a.dim + 63) // 64
     planes = np.empty((a.doc_bits, W64, a.n), dtype=np.uint64)
     scale = None
-    for c in range(-(-a.n // CHUNK)):
-        lo, hi = c * CHUNK, min(a.n, (c + 1) * CHUNK)
-        g = torch.Generator().manual_seed(4000 + c)
-        x = torch.randn((hi - lo, a.dim), generator=g, dtype=torch.float32)
-        x = (x / x.norm(dim=1, keepdim=True)).numpy()
-        if scale is None:
-            scale = xo.estimate_scale(x[:100_000], 0.98)
-        planes[:, :, lo:hi] = xo.c_quantize_matrix(x, a.doc_bits, scale)
+    scale = xo.estimate_scale(gen_chunk_host(0, min(CHUNK, a.n), a.dim)[:100_000], 0.98)
+
+    def sink(first, x):   # the same corpus bytes as the GPU arm (gen_chunk_host), quantized by the oracle
+        planes[:, :, first:first + x.shape[0]] = xo.c_quantize_matrix(x, a.doc_bits, scale)
+
+    gen_rows_host(0, a.n, a.n, a.dim, sink)
     q_host = gen_queries(a.nq, a.dim)
     qp = xo.c_quantize_matrix(q_host.astype(np.float64), a.query_bits, scale).transpose(2, 0, 1)
     t0 = time.perf_counter()

@@ -198,6 +198,8 @@ int xfbq_unpack_keys(const uint64_t *keys_dev, int64_t count, int64_t *dist_out_
  * or the merge); xfbq_last_scan_ms synchronises on the last one and returns its duration. */
 int xfbq_set_timing(int enable);
 int xfbq_last_scan_ms(float *ms_out);
+/* Mean duration of the dominant kernel over the timed launches since xfbq_set_timing(1) (the last 64 are kept). */
+int xfbq_scan_ms_mean(float *mean_ms_out, int *launches_out);
 /* Debug hook (per host thread): device buffer of gridDim.x * 12 uint64 counters that the tcgen05 scan
  * kernel of the following xfbq_scan_topk calls fills with cycles spent waiting per role
  * (tools/umma_profile.py); NULL switches it off. */

@@ -34,7 +34,7 @@ SYMBOLS = [
     "xfbq_bundles_to_planes", "xfbq_nibble_bytes", "xfbq_planes_to_nibbles", "xfbq_batch_distances", "xfbq_collect_candidates",
     "xfbq_select_workspace_bytes", "xfbq_abs_order_stats_f32", "xfbq_abs_order_stats_f64", "xfbq_refine_workspace_bytes", "xfbq_refine_f32",
     "xfbq_scan_workspace_bytes",
-    "xfbq_scan_plan", "xfbq_scan_topk", "xfbq_merge_topk", "xfbq_unpack_keys", "xfbq_set_timing", "xfbq_last_scan_ms", "xfbq_launch_count", "xfbq_debug_profile",
+    "xfbq_scan_plan", "xfbq_scan_topk", "xfbq_merge_topk", "xfbq_unpack_keys", "xfbq_set_timing", "xfbq_last_scan_ms", "xfbq_scan_ms_mean", "xfbq_launch_count", "xfbq_debug_profile",
 ]
 
 
@@ -117,6 +117,7 @@ def lib():
         "xfbq_unpack_keys": (i32, [vp, i64, vp, vp, vp]),
         "xfbq_set_timing": (i32, [i32]),
         "xfbq_last_scan_ms": (i32, [vp]),
+        "xfbq_scan_ms_mean": (i32, [vp, vp]),
         "xfbq_debug_profile": (i32, [vp]),
         "xfbq_launch_count": (i64, []),
     }
@@ -155,6 +156,13 @@ def last_scan_ms() -> float:
     out = ctypes.c_float(0.0)
     check(lib().xfbq_last_scan_ms(ctypes.byref(out)))
     return float(out.value)
+
+
+def scan_ms_mean() -> tuple[float, int]:
+    """(mean device time of the dominant kernel, launches averaged) over the timed scans since set_timing(True)."""
+    ms, cnt = ctypes.c_float(0.0), ctypes.c_int(0)
+    check(lib().xfbq_scan_ms_mean(ctypes.byref(ms), ctypes.byref(cnt)))
+    return float(ms.value), int(cnt.value)
 
 
 def launch_count() -> int:

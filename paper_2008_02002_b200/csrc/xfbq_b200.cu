@@ -29,11 +29,17 @@ constexpr int SCAN_WARPS = SCAN_THREADS / 32;
 thread_local char g_err[512] = "";
 // optional device timing of the main scan kernel (xfbq_set_timing): events live per host thread
 thread_local bool g_timing = false;
-thread_local cudaEvent_t g_ev0 = nullptr, g_ev1 = nullptr;
-thread_local bool g_ev_valid = false;
+// a ring of event pairs: every timed launch since xfbq_set_timing(1) takes the next pair (the last TIMING_PAIRS are kept),
+// so a bench reads the MEAN launch time of its timed region, not the last launch only
+constexpr int TIMING_PAIRS = 64;
+thread_local cudaEvent_t g_evs[TIMING_PAIRS][2] = {};
+thread_local int g_ev_count = 0;   // timed launches recorded since timing was switched on
 std::atomic<int64_t> g_launches{0};
 thread_local unsigned long long *g_prof = nullptr;
 thread_local int g_hist_shift = 2;  // bin width of the tcgen05 engine's global candidate histogram (set per search from the distance range)  // debug: device buffer for the tcgen05 engine's wait counters
+
+void timing_begin(cudaStream_t st) { cudaEventRecord(g_evs[g_ev_count % TIMING_PAIRS][0], st); }
+void timing_end(cudaStream_t st) { cudaEventRecord(g_evs[g_ev_count % TIMING_PAIRS][1], st); ++g_ev_count; }
 
 int fail(int code, const char *fmt, ...) {
     va_list ap;
@@ -1010,18 +1016,20 @@ MmaKernel pick_mma_kernel(int C, bool fused, int warps) {
     if (warps == mma::WARPS_WIDE) {
         if (C == 1) return mma::scan_kernel<1, 1, 2, true, mma::WARPS_WIDE>;
         if (C == 2) return mma::scan_kernel<2, 1, 2, true, mma::WARPS_WIDE>;
+        if (C == 3) return mma::scan_kernel<3, 1, 1, true, mma::WARPS_WIDE>;
         if (C == 4) return mma::scan_kernel<4, 1, 1, true, mma::WARPS_WIDE>;
         return nullptr;
     }
     if (warps == mma::WARPS_BATCH) {
         if (C == 1) return mma::scan_kernel<1, 2, 2, false, mma::WARPS_BATCH>;
         if (C == 2) return mma::scan_kernel<2, 2, 2, false, mma::WARPS_BATCH>;
+        if (C == 3) return mma::scan_kernel<3, 1, 1, false, mma::WARPS_BATCH>;
         if (C == 4) return mma::scan_kernel<4, 1, 1, false, mma::WARPS_BATCH>;
         return nullptr;
     }
 #define XFBQ_MMA_CASE(C_, MT_, NT_) \
     if (C == C_) return fused ? mma::scan_kernel<C_, MT_, NT_, true, mma::WARPS> : mma::scan_kernel<C_, MT_, NT_, false, mma::WARPS>;
-    XFBQ_MMA_CASE(1, 2, 2) XFBQ_MMA_CASE(2, 2, 2) XFBQ_MMA_CASE(4, 1, 1)
+    XFBQ_MMA_CASE(1, 2, 2) XFBQ_MMA_CASE(2, 2, 2) XFBQ_MMA_CASE(3, 1, 1) XFBQ_MMA_CASE(4, 1, 1)
 #undef XFBQ_MMA_CASE
     return nullptr;
 }
@@ -1031,8 +1039,8 @@ inline size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255);
 void mma_shape(int64_t n, int wd, int C, int64_t nq, int k, const DeviceInfo &info, MmaShape *out) {
     const int sms = info.sms;
     MmaShape sh;
-    sh.MT = C == 4 ? 1 : 2;
-    sh.NT = C == 4 ? 1 : 2;
+    sh.MT = C >= 3 ? 1 : 2;
+    sh.NT = C >= 3 ? 1 : 2;
     if (nq <= 16 && env_int("XFBQ_NO_WIDE", 0) == 0 && env_int("XFBQ_NO_FUSED", 0) == 0) {
         sh.MT = 1;  // <= 16 queries: one 16-row tile, 16 warps per CTA
         sh.warps = mma::WARPS_WIDE;
@@ -1105,7 +1113,7 @@ int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, boo
     const int C = static_cast<int>(chunks128(dim));
     const char *eng = getenv("XFBQ_ENGINE");
     const bool forced_popc = eng && strcmp(eng, "popc") == 0;
-    if (!have_nibbles || forced_popc || wd > 4 || wq > 7 || !(C == 1 || C == 2 || C == 4) || k > 1024 || nq < 1 || n < 1 ||
+    if (!have_nibbles || forced_popc || wd > 4 || wq > 7 || C < 1 || C > 4 || k > 1024 || nq < 1 || n < 1 ||
         env_int("XFBQ_FORCE_GENERIC", 0)) {
         *plan = pl;
         return XFBQ_OK;
@@ -1140,7 +1148,7 @@ int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, boo
     pl.off_parts = off; off = align256(off + (pl.main.parts_bytes > pl.pre.parts_bytes ? pl.main.parts_bytes : pl.pre.parts_bytes));
     pl.off_mscratch = off; off = align256(off + (pl.main.mscratch_bytes > pl.pre.mscratch_bytes ? pl.main.mscratch_bytes : pl.pre.mscratch_bytes));
     if (pl.count) {
-        const int64_t uq = 128 * ((C == 4 || nq <= 128) ? 1 : 2);  // queries per group of the counting kernel
+        const int64_t uq = 128 * ((C >= 3 || nq <= 128) ? 1 : 2);  // queries per group of the counting kernel
         const int64_t nq_pad = (nq + uq - 1) / uq * uq;
         pl.off_uqimg = off; off = align256(off + static_cast<size_t>(nq_pad) * 128 * C);
         pl.off_uqconst = off; off = align256(off + static_cast<size_t>(nq_pad) * 4);
@@ -1175,9 +1183,9 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
         if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
     }
     const bool timed = g_timing && &sh == &pl.main;
-    if (timed) cudaEventRecord(g_ev0, st);
+    if (timed) timing_begin(st);
     kern<<<static_cast<unsigned>(sh.grid), sh.warps * 32, sh.smem, st>>>(p);
-    if (timed) { cudaEventRecord(g_ev1, st); g_ev_valid = true; }
+    if (timed) timing_end(st);
     if (int rc = check_launch("mma::scan_kernel")) return rc;
     if (direct) return XFBQ_OK;
     return launch_merge(p.out, sh.parts, nq, k, keys_out, reinterpret_cast<uint64_t *>(ws + pl.off_mscratch), st,
@@ -1214,17 +1222,20 @@ UmmaKernel pick_umma_kernel(int C, int MT, bool queue, bool count = false) {
     if (count) {
         if (C == 1) return MT == 2 ? umma::scan_kernel<1, 2, true> : umma::scan_kernel<1, 1, true>;
         if (C == 2) return MT == 2 ? umma::scan_kernel<2, 2, true> : umma::scan_kernel<2, 1, true>;
+        if (C == 3 && MT == 1) return umma::scan_kernel<3, 1, true>;
         if (C == 4 && MT == 1) return umma::scan_kernel<4, 1, true>;
         return nullptr;
     }
     if (queue) {
         if (C == 1) return MT == 2 ? umma::scan_queue_kernel<1, 2> : umma::scan_queue_kernel<1, 1>;
         if (C == 2) return MT == 2 ? umma::scan_queue_kernel<2, 2> : umma::scan_queue_kernel<2, 1>;
+        if (C == 3 && MT == 1) return umma::scan_queue_kernel<3, 1>;
         if (C == 4 && MT == 1) return umma::scan_queue_kernel<4, 1>;
         return nullptr;
     }
     if (C == 1) return MT == 2 ? umma::scan_kernel<1, 2> : umma::scan_kernel<1, 1>;
     if (C == 2) return MT == 2 ? umma::scan_kernel<2, 2> : umma::scan_kernel<2, 1>;
+    if (C == 3 && MT == 1) return umma::scan_kernel<3, 1>;
     if (C == 4 && MT == 1) return umma::scan_kernel<4, 1>;
     return nullptr;
 }
@@ -1317,14 +1328,14 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     const char *eng = getenv("XFBQ_ENGINE");
     if (eng && *eng && strcmp(eng, "umma") != 0) return XFBQ_OK;  // another engine was asked for
     const bool forced = eng && strcmp(eng, "umma") == 0;
-    if (!have_nibbles || wd > 4 || wq > 7 || !(C == 1 || C == 2 || C == 4) || k > 1024 || n < 1 || env_int("XFBQ_FORCE_GENERIC", 0))
+    if (!have_nibbles || wd > 4 || wq > 7 || C < 1 || C > 4 || k > 1024 || n < 1 || env_int("XFBQ_FORCE_GENERIC", 0))
         return XFBQ_OK;
     if (!forced && nq < env_int("XFBQ_UMMA_MIN_NQ", 17)) return XFBQ_OK;  // <= 16 queries: the mma.sync scans (HBM-bound on the nibble layout; a 24-query batch took 0.72 ms there, 0.55 ms here)
     if (nq < 1) return XFBQ_OK;
     if (merge_group_max(k) == 0 || nq > 65535) return XFBQ_OK;  // lists are emitted unsorted: needs the tree merge
     DeviceInfo info;
     if (int rc = device_info(&info)) return rc;
-    const int MT = (C == 4 || nq <= 128) ? 1 : 2;
+    const int MT = (C >= 3 || nq <= 128) ? 1 : 2;
     // Sample scan that seeds the thresholds (measured on 10M x 256, 10k queries: 16k documents split over at
     // most 4 CTAs per query group balance its cost -- it starts from open lists -- against the rows the main
     // scan's resolvers then have to handle).
@@ -1429,9 +1440,9 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
         if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
     }
     const bool timed = g_timing && &sh == &pl.main;
-    if (timed) cudaEventRecord(g_ev0, st);
+    if (timed) timing_begin(st);
     kern<<<static_cast<unsigned>(sh.grid), sh.queue ? umma::Q_THREADS : umma::THREADS, sh.smem, st>>>(p);
-    if (timed) { cudaEventRecord(g_ev1, st); g_ev_valid = true; }
+    if (timed) timing_end(st);
     if (int rc = check_launch("umma::scan_kernel")) return rc;
     if (sh.count) return XFBQ_OK;  // histograms only: seed_bounds_kernel follows
     if (p.theta_g && sh.parts > 1 && env_int("XFBQ_MERGE_BOUNDED", 1)) {
@@ -1466,7 +1477,7 @@ int run_counted_seed(unsigned char *ws, const void *tiles, int64_t n, int64_t di
     const int C = static_cast<int>(chunks128(dim));
     DeviceInfo info;
     if (int rc = device_info(&info)) return rc;
-    const int MT = (C == 4 || nq <= 128) ? 1 : 2;
+    const int MT = (C >= 3 || nq <= 128) ? 1 : 2;
     UmmaPlan pl;
     umma_shape(sample, C, nq, k, MT, info, &pl.pre, true, true, true);
     const int64_t total_stages = (bundles_of(n) * 32 + umma::STAGE_DOCS - 1) / umma::STAGE_DOCS;
@@ -1589,12 +1600,13 @@ int quantize_queries_impl(const T *x, int64_t nq, int64_t dim, int64_t ld, doubl
 XFBQ_API int xfbq_abi_version(void) { return XFBQ_ABI_VERSION; }
 XFBQ_API const char *xfbq_last_error(void) { return g_err; }
 XFBQ_API int xfbq_set_timing(int enable) {
-    if (enable && !g_ev0) {
-        if (cudaEventCreate(&g_ev0) != cudaSuccess || cudaEventCreate(&g_ev1) != cudaSuccess)
-            return fail(XFBQ_E_CUDA, "cudaEventCreate failed");
+    if (enable && !g_evs[0][0]) {
+        for (int i = 0; i < TIMING_PAIRS; ++i)
+            if (cudaEventCreate(&g_evs[i][0]) != cudaSuccess || cudaEventCreate(&g_evs[i][1]) != cudaSuccess)
+                return fail(XFBQ_E_CUDA, "cudaEventCreate failed");
     }
     g_timing = enable != 0;
-    g_ev_valid = false;
+    g_ev_count = 0;
     return XFBQ_OK;
 }
 
@@ -1605,10 +1617,29 @@ XFBQ_API int xfbq_debug_profile(void *device_counters) {
 
 XFBQ_API int xfbq_last_scan_ms(float *ms_out) {
     if (!ms_out) return fail(XFBQ_E_INVALID, "null pointer");
-    if (!g_ev_valid) return fail(XFBQ_E_INVALID, "no timed scan recorded (call xfbq_set_timing(1) first)");
-    cudaError_t e = cudaEventSynchronize(g_ev1);
-    if (e == cudaSuccess) e = cudaEventElapsedTime(ms_out, g_ev0, g_ev1);
+    if (g_ev_count == 0) return fail(XFBQ_E_INVALID, "no timed scan recorded (call xfbq_set_timing(1) first)");
+    cudaEvent_t *pair = g_evs[(g_ev_count - 1) % TIMING_PAIRS];
+    cudaError_t e = cudaEventSynchronize(pair[1]);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(ms_out, pair[0], pair[1]);
     if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "event timing: %s", cudaGetErrorString(e));
+    return XFBQ_OK;
+}
+
+XFBQ_API int xfbq_scan_ms_mean(float *mean_ms_out, int *launches_out) {
+    if (!mean_ms_out || !launches_out) return fail(XFBQ_E_INVALID, "null pointer");
+    if (g_ev_count == 0) return fail(XFBQ_E_INVALID, "no timed scan recorded (call xfbq_set_timing(1) first)");
+    const int kept = g_ev_count < TIMING_PAIRS ? g_ev_count : TIMING_PAIRS;
+    double sum = 0.0;
+    for (int i = 0; i < kept; ++i) {
+        cudaEvent_t *pair = g_evs[(g_ev_count - 1 - i) % TIMING_PAIRS];
+        float ms = 0.f;
+        cudaError_t e = cudaEventSynchronize(pair[1]);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, pair[0], pair[1]);
+        if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "event timing: %s", cudaGetErrorString(e));
+        sum += ms;
+    }
+    *mean_ms_out = static_cast<float>(sum / kept);
+    *launches_out = kept;
     return XFBQ_OK;
 }
 
@@ -1678,7 +1709,7 @@ inline int64_t nibble_region_bytes(int64_t n, int64_t dim) {
     return ((bundles_of(n) * 32 * chunks128(dim) * 64 + 1023) / 1024) * 1024;
 }
 inline int64_t tile_count(int64_t n) { return (n + umma::STAGE_DOCS - 1) / umma::STAGE_DOCS; }
-inline bool tiles_supported(int64_t dim) { const int64_t C = chunks128(dim); return C == 1 || C == 2 || C == 4; }
+inline bool tiles_supported(int64_t dim) { const int64_t C = chunks128(dim); return C >= 1 && C <= 4; }
 
 XFBQ_API int64_t xfbq_nibble_bytes(int64_t n, int64_t dim) {
     return nibble_region_bytes(n, dim) + (tiles_supported(dim) ? tile_count(n) * umma::STAGE_DOCS * chunks128(dim) * 128 : 0);
@@ -1988,9 +2019,9 @@ XFBQ_API int xfbq_scan_topk(const void *db, const void *nib, int64_t n, int64_t 
     p.k = k; p.cap = pl.cap; p.tq = pl.tq;
     dim3 grid(static_cast<unsigned>(pl.splits), static_cast<unsigned>(pl.q_tiles));
     if (pl.q_tiles > 65535) return fail(XFBQ_E_UNSUPPORTED, "too many query tiles (%d); split the batch", pl.q_tiles);
-    if (g_timing) cudaEventRecord(g_ev0, st);
+    if (g_timing) timing_begin(st);
     kern<<<grid, SCAN_THREADS, pl.smem, st>>>(p);
-    if (g_timing) { cudaEventRecord(g_ev1, st); g_ev_valid = true; }
+    if (g_timing) timing_end(st);
     if (int rc = check_launch("scan_topk_kernel")) return rc;
     if (pl.splits > 1)
         return launch_merge(static_cast<const uint64_t *>(workspace), pl.splits, nq, k, keys_out,

@@ -39,7 +39,7 @@ constexpr int A_COL0 = ACC_BUFS * STAGE_DOCS;
 constexpr int HIST_BINS = 256;
 constexpr int SEED_BINS = 64;     // bins of the sample histogram that seeds the thresholds
 constexpr int SEED_STRIDE = EPI_WARPS * 32;  // bin-major shared-memory histograms: counter (copy * 64 + bin) * 256 + thread
-__host__ __device__ constexpr int SEED_COPIES(int C) { return C == 4 ? 2 : 4; }  // 16-bit counters: a copy takes 32 KB
+__host__ __device__ constexpr int SEED_COPIES(int C) { return C >= 3 ? 2 : 4; }  // 16-bit counters: a copy takes 32 KB
 __host__ __device__ constexpr int64_t SEED_MAX_SAMPLE(int C) { return 32768 * SEED_COPIES(C); }  // a 16-bit counter sees at most sample / copies documents
 constexpr int TAU_OPEN = -(1 << 30);
 constexpr int TAU_NEVER = 1 << 30;     // |acc| <= 512 * 15 * 127 < 2^20, so acc - tau never overflows

@@ -137,3 +137,14 @@ def test_edge_cases():
         xo.np_quantize_values(np.array([0.1, np.nan]), 3)
     with pytest.raises(ValueError):
         xo.c_quantize_matrix(np.array([[0.1, np.inf]], dtype=np.float32), 3, 1.0)
+
+
+def test_bench_corpus_generator_is_the_reference_recipe():
+    """bench.py's corpus chunks (both arms) = generate_synthetic's recipe (dataio.py:104-124), which
+    synthetic_unit_rows restates and the golden hashes above pin to the reference's own output."""
+    import bench
+    for c, rows, dim in ((0, 1000, 256), (3, 257, 200)):
+        assert np.array_equal(bench.gen_chunk_host(c, rows, dim), xo.synthetic_unit_rows(rows, dim, 4000 + c))
+    got = []
+    bench.gen_rows_host(5, 2_000_050, 3_000_000, 8, lambda first, x: got.append((first, x.shape[0])), workers=2)
+    assert got == [(5, 999_995), (1_000_000, 1_000_000), (2_000_000, 50)]
