@@ -105,6 +105,9 @@ int xfbq_bundles_to_planes(const void *db_dev, int64_t n, int64_t dim, int width
  *                   by one cp.async.bulk per tile (streamed by the tcgen05 engine: >= 32 queries).
  * The tile region starts at the nibble region's size rounded up to 1024 bytes.
  */
+int64_t xfbq_derived_bytes(int64_t n, int64_t dim, int width);  /* width > 4: byte tiles only (no nibble region) */
+int xfbq_build_derived(const void *db_dev, int64_t n, int64_t dim, int width, void *derived_out_dev, void *stream);
+/* the same for width <= 4 (kept for callers of ABI revision 1) */
 int64_t xfbq_nibble_bytes(int64_t n, int64_t dim);
 int xfbq_planes_to_nibbles(const void *db_dev, int64_t n, int64_t dim, int width, void *nibbles_out_dev,
                            void *stream);

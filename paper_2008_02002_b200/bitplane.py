@@ -169,19 +169,20 @@ class PackedMatrix:
 
     @property
     def nibbles(self):
-        """Derived nibble-layout copy of the codes for the tensor-core scan (doc_bits <= 4), built
-        on the GPU on first use and cached; None for wider codes."""
-        if self._width > 4 or self._count == 0:
+        """Derived layouts of the codes for the tensor-core scans, built on the GPU on first use and cached: the nibble
+        layout (doc_bits <= 4: mma.sync engine, <= 16 queries) followed by the byte tiles (any width: tcgen05 engine);
+        None when the dimension has no tensor path (dim > 512)."""
+        if self._count == 0 or self._dim > 512:
             return None
         cached = getattr(self, "_nibbles", None)
         if cached is None:
             torch = _native.require_cuda()
             L = _native.lib()
             with torch.cuda.device(self._codes.device):
-                cached = torch.empty(int(L.xfbq_nibble_bytes(self._count, self._dim)), dtype=torch.uint8,
+                cached = torch.empty(int(L.xfbq_derived_bytes(self._count, self._dim, self._width)), dtype=torch.uint8,
                                      device=self._codes.device)
-                _native.check(L.xfbq_planes_to_nibbles(self._codes.data_ptr(), self._count, self._dim, self._width,
-                                                       cached.data_ptr(), _stream_ptr(torch)))
+                _native.check(L.xfbq_build_derived(self._codes.data_ptr(), self._count, self._dim, self._width,
+                                                   cached.data_ptr(), _stream_ptr(torch)))
             self._nibbles = cached
         return cached
 

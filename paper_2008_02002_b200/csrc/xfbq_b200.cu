@@ -1218,7 +1218,14 @@ struct UmmaPlan {
 
 typedef void (*UmmaKernel)(const umma::Params);
 
-UmmaKernel pick_umma_kernel(int C, int MT, bool queue, bool count = false) {
+UmmaKernel pick_umma_kernel(int C, int MT, bool queue, bool count = false, bool direct = false) {
+    if (queue && direct) {
+        if (C == 1) return MT == 2 ? umma::scan_queue_kernel<1, 2, true> : umma::scan_queue_kernel<1, 1, true>;
+        if (C == 2) return MT == 2 ? umma::scan_queue_kernel<2, 2, true> : umma::scan_queue_kernel<2, 1, true>;
+        if (C == 3 && MT == 1) return umma::scan_queue_kernel<3, 1, true>;
+        if (C == 4 && MT == 1) return umma::scan_queue_kernel<4, 1, true>;
+        return nullptr;
+    }
     if (count) {
         if (C == 1) return MT == 2 ? umma::scan_kernel<1, 2, true> : umma::scan_kernel<1, 1, true>;
         if (C == 2) return MT == 2 ? umma::scan_kernel<2, 2, true> : umma::scan_kernel<2, 1, true>;
@@ -1328,7 +1335,7 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     const char *eng = getenv("XFBQ_ENGINE");
     if (eng && *eng && strcmp(eng, "umma") != 0) return XFBQ_OK;  // another engine was asked for
     const bool forced = eng && strcmp(eng, "umma") == 0;
-    if (!have_nibbles || wd > 4 || wq > 7 || C < 1 || C > 4 || k > 1024 || n < 1 || env_int("XFBQ_FORCE_GENERIC", 0))
+    if (!have_nibbles || wq > 7 || C < 1 || C > 4 || k > 1024 || n < 1 || env_int("XFBQ_FORCE_GENERIC", 0))  // any document width: the B operand is u8
         return XFBQ_OK;
     if (!forced && nq < env_int("XFBQ_UMMA_MIN_NQ", 17)) return XFBQ_OK;  // <= 16 queries: the mma.sync scans (HBM-bound on the nibble layout; a 24-query batch took 0.72 ms there, 0.55 ms here)
     if (nq < 1) return XFBQ_OK;
@@ -1407,7 +1414,8 @@ double normal_quantile(double p) {
 
 int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, const void *nib, int64_t n, int C,
                   int64_t nq, int k, int64_t row_offset, const int32_t *tau_init, uint64_t *keys_out, cudaStream_t st) {
-    UmmaKernel kern = pick_umma_kernel(C, sh.MT, sh.queue, sh.count);
+    const bool direct = sh.direct && &sh == &pl.main && tau_init != nullptr;
+    UmmaKernel kern = pick_umma_kernel(C, sh.MT, sh.queue, sh.count, direct);
     if (!kern) return fail(XFBQ_E_UNSUPPORTED, "no tcgen05 kernel for C=%d MT=%d", C, sh.MT);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh.smem));
     if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "umma scan smem opt-in (%zu bytes): %s", sh.smem, cudaGetErrorString(e));
@@ -1430,7 +1438,6 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     p.hist_shift = g_hist_shift;
     p.seed_par = sh.count ? reinterpret_cast<const int2 *>(ws + pl.off_seedpar) : nullptr;
     p.seed_hist = sh.count ? reinterpret_cast<uint32_t *>(ws + pl.off_seedhist) : nullptr;
-    const bool direct = sh.direct && &sh == &pl.main && tau_init != nullptr;
     p.list_counts = direct ? reinterpret_cast<int *>(ws + pl.off_counts) : nullptr;
     p.prof = (&sh == &pl.main) ? g_prof : nullptr;
     p.pace = env_int("XFBQ_UMMA_PACE", 48);
@@ -1705,32 +1712,42 @@ XFBQ_API int xfbq_bundles_to_planes(const void *db, int64_t n, int64_t dim, int 
 }
 
 // Derived layouts of one index, in one buffer: [nibble layout][byte tiles].
-inline int64_t nibble_region_bytes(int64_t n, int64_t dim) {
+inline int64_t nibble_region_bytes(int64_t n, int64_t dim, int wd = 4) {
+    if (wd > 4) return 0;  // wider codes do not fit a nibble: the derived buffer holds the byte tiles only
     return ((bundles_of(n) * 32 * chunks128(dim) * 64 + 1023) / 1024) * 1024;
 }
 inline int64_t tile_count(int64_t n) { return (n + umma::STAGE_DOCS - 1) / umma::STAGE_DOCS; }
 inline bool tiles_supported(int64_t dim) { const int64_t C = chunks128(dim); return C >= 1 && C <= 4; }
 
-XFBQ_API int64_t xfbq_nibble_bytes(int64_t n, int64_t dim) {
-    return nibble_region_bytes(n, dim) + (tiles_supported(dim) ? tile_count(n) * umma::STAGE_DOCS * chunks128(dim) * 128 : 0);
+XFBQ_API int64_t xfbq_derived_bytes(int64_t n, int64_t dim, int width) {
+    return nibble_region_bytes(n, dim, width) + (tiles_supported(dim) ? tile_count(n) * umma::STAGE_DOCS * chunks128(dim) * 128 : 0);
+}
+XFBQ_API int64_t xfbq_nibble_bytes(int64_t n, int64_t dim) { return xfbq_derived_bytes(n, dim, 4); }
+
+XFBQ_API int xfbq_build_derived(const void *db, int64_t n, int64_t dim, int width, void *out, void *stream) {
+    if (!width_ok(width)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d", width);
+    if (n < 0 || dim < 1) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld", (long long)n, (long long)dim);
+    if (n == 0) return XFBQ_OK;
+    if (!db || !out) return fail(XFBQ_E_INVALID, "null pointer");
+    const int C = static_cast<int>(chunks128(dim));
+    const int64_t n_pad = bundles_of(n) * 32;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (width <= 4) {
+        const int64_t total = n_pad * 4 * C;
+        mma::planes_to_nibbles_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+            static_cast<const uint32_t *>(db), n_pad, width, C, static_cast<uint4 *>(out));
+        if (int rc = check_launch("planes_to_nibbles_kernel")) return rc;
+    }
+    if (!tiles_supported(dim)) return XFBQ_OK;
+    const int64_t tiles = tile_count(n), groups = tiles * umma::STAGE_DOCS * 4 * C;
+    umma::planes_to_tiles_kernel<<<static_cast<unsigned>((groups + 255) / 256), 256, 0, st>>>(
+        static_cast<const uint32_t *>(db), n_pad, tiles, width, C, static_cast<unsigned char *>(out) + nibble_region_bytes(n, dim, width));
+    return check_launch("planes_to_tiles_kernel");
 }
 
 XFBQ_API int xfbq_planes_to_nibbles(const void *db, int64_t n, int64_t dim, int width, void *nib_out, void *stream) {
     if (width < 1 || width > 4) return fail(XFBQ_E_UNSUPPORTED, "nibble layout holds codes of at most 4 bits, got %d", width);
-    if (n < 0 || dim < 1) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld", (long long)n, (long long)dim);
-    if (n == 0) return XFBQ_OK;
-    if (!db || !nib_out) return fail(XFBQ_E_INVALID, "null pointer");
-    const int C = static_cast<int>(chunks128(dim));
-    const int64_t n_pad = bundles_of(n) * 32;
-    const int64_t total = n_pad * 4 * C;
-    mma::planes_to_nibbles_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const uint32_t *>(db), n_pad, width, C, static_cast<uint4 *>(nib_out));
-    if (int rc = check_launch("planes_to_nibbles_kernel")) return rc;
-    if (!tiles_supported(dim)) return XFBQ_OK;
-    const int64_t tiles = tile_count(n), groups = tiles * umma::STAGE_DOCS * 4 * C;
-    umma::nibbles_to_tiles_kernel<<<static_cast<unsigned>((groups + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        static_cast<const uint4 *>(nib_out), n_pad, tiles, C, static_cast<unsigned char *>(nib_out) + nibble_region_bytes(n, dim));
-    return check_launch("nibbles_to_tiles_kernel");
+    return xfbq_build_derived(db, n, dim, width, nib_out, stream);
 }
 
 XFBQ_API int xfbq_batch_distances(const void *db, int64_t n, int64_t dim, int wd, const uint32_t *q, int wq,
@@ -1966,7 +1983,7 @@ XFBQ_API int xfbq_scan_topk(const void *db, const void *nib, int64_t n, int64_t 
     if (up.ok) {
         if (!workspace || workspace_bytes < static_cast<int64_t>(up.bytes))
             return fail(XFBQ_E_INVALID, "workspace too small: need %zu bytes, got %lld", up.bytes, (long long)workspace_bytes);
-        return run_umma(up, static_cast<unsigned char *>(workspace), static_cast<const unsigned char *>(nib) + nibble_region_bytes(n, dim),
+        return run_umma(up, static_cast<unsigned char *>(workspace), static_cast<const unsigned char *>(nib) + nibble_region_bytes(n, dim, wd),
                         n, dim, wd, q, nq, wq, k, row_offset, keys_out, st);
     }
     MmaPlan mp;

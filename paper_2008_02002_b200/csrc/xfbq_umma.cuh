@@ -98,8 +98,12 @@ __device__ __forceinline__ void umma_commit(uint64_t *bar) {
 // overflow: shared memory ends below 256 KB)
 __device__ __forceinline__ uint32_t desc_lo(uint32_t saddr) { return ((saddr >> 4) & 0x3FFFu) | (1u << 16); }
 constexpr uint32_t DESC_HI = (1024u >> 4) | (1u << 14) | (2u << 29);
-// Instruction descriptor: D = s32, A = B = signed 8-bit, both K-major, N >> 3 at bit 17, M >> 4 at bit 24.
-constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(STAGE_DOCS >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
+// Instruction descriptor: D = s32 (bits 4-5 = 2), A = signed 8-bit (bits 7-9 = 1: the query weights 2y - Aq), B = UNSIGNED
+// 8-bit (bits 10-12 = 0: the document codes, up to 255 for 8-bit codes), both K-major, N >> 3 at bit 17, M >> 4 at bit 24.
+#ifndef XFBQ_B_FORMAT
+#define XFBQ_B_FORMAT 0u
+#endif
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (XFBQ_B_FORMAT << 10) | (static_cast<uint32_t>(STAGE_DOCS >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
 
 template <bool ACC>
 __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo) {
@@ -217,6 +221,34 @@ nibbles_to_tiles_kernel(const uint4 *__restrict__ nib, int64_t n_pad, int64_t n_
         make_uint4(w.x & 0x0F0F0F0Fu, (w.x >> 4) & 0x0F0F0F0Fu, w.y & 0x0F0F0F0Fu, (w.y >> 4) & 0x0F0F0F0Fu);
     *reinterpret_cast<uint4 *>(rowp + (((2 * gg + 1) ^ (r & 7)) << 4)) =
         make_uint4(w.z & 0x0F0F0F0Fu, (w.z >> 4) & 0x0F0F0F0Fu, w.w & 0x0F0F0F0Fu, (w.w >> 4) & 0x0F0F0F0Fu);
+}
+
+// bundle layout (bit planes) -> byte tiles directly, any code width 1..8; one thread per (document, group of 32 dims).
+// Plane i's 32-bit word of the group holds dim d in bit d, so ((P_i >> (e + 4 hi)) & 0x01010101) << i places bit i of the
+// codes of dims e + 4 hi + {0, 8, 16, 24} into bytes j = 0..3 of output word (e, hi): the same K order as above.
+__global__ void __launch_bounds__(256)
+planes_to_tiles_kernel(const uint32_t *__restrict__ db, int64_t n_pad, int64_t n_tiles, int wd, int C, unsigned char *__restrict__ tiles) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int G = 4 * C;
+    if (e >= n_tiles * STAGE_DOCS * G) return;
+    const int64_t doc = e / G;
+    const int g = static_cast<int>(e - doc * G);
+    uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // w[2 e + hi]
+    if (doc < n_pad) {
+        const int64_t b = doc >> 5;
+        const int l = static_cast<int>(doc & 31), c = g >> 2;
+        for (int i = 0; i < wd; ++i) {
+            const uint32_t pw = __ldg(db + ((((b * wd + i) * C + c) * 32 + l) << 2) + (g & 3));
+#pragma unroll
+            for (int x = 0; x < 8; ++x) w[x] |= ((pw >> ((x >> 1) + 4 * (x & 1))) & 0x01010101u) << i;
+        }
+    }
+    const int64_t tile = doc / STAGE_DOCS;
+    const int r = static_cast<int>(doc - tile * STAGE_DOCS);
+    const int kb = g >> 2, gg = g & 3;
+    unsigned char *rowp = tiles + tile * (static_cast<int64_t>(STAGE_DOCS) * 128 * C) + kb * (STAGE_DOCS * 128) + (r >> 3) * 1024 + (r & 7) * 128;
+    *reinterpret_cast<uint4 *>(rowp + (((2 * gg) ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4 *>(rowp + (((2 * gg + 1) ^ (r & 7)) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
 }
 
 // mbarrier wait (every lane polls: measured far faster than one polling lane + warp barrier) that adds the
@@ -730,6 +762,11 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
 // frame: origin = mean + (z - 3) sigma, 64 bins of sigma/16, where z is the normal quantile of the k-th best of
 // the sample.  The frame only has to bracket the k-th best sample score; any frame gives a VALID threshold
 // (bins count real documents), a poor one a loose or open threshold.
+__device__ __forceinline__ int dp4a_su(uint32_t a_s8x4, uint32_t b_u8x4, int c) {
+    int d;
+    asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a_s8x4), "r"(b_u8x4), "r"(c));
+    return d;
+}
 __global__ void __launch_bounds__(128) seed_stats_kernel(const unsigned char *__restrict__ tiles, const unsigned char *__restrict__ qimg,
                                                          int64_t nq, int C, int64_t sample_tiles, int64_t tile_stride, float z, float below, int2 *__restrict__ par) {
     const int64_t q = blockIdx.x;
@@ -741,10 +778,10 @@ __global__ void __launch_bounds__(128) seed_stats_kernel(const unsigned char *__
     for (int u = 0; u < 8 * C; ++u) {
         const uint4 a = __ldg(qrow + u);
         const uint4 b = __ldg(reinterpret_cast<const uint4 *>(tile + sw128_offset(r, u * 16, STAGE_DOCS)));
-        acc = __dp4a(static_cast<int>(a.x), static_cast<int>(b.x), acc);
-        acc = __dp4a(static_cast<int>(a.y), static_cast<int>(b.y), acc);
-        acc = __dp4a(static_cast<int>(a.z), static_cast<int>(b.z), acc);
-        acc = __dp4a(static_cast<int>(a.w), static_cast<int>(b.w), acc);
+        acc = dp4a_su(a.x, b.x, acc);  // signed query weights x unsigned document codes
+        acc = dp4a_su(a.y, b.y, acc);
+        acc = dp4a_su(a.z, b.z, acc);
+        acc = dp4a_su(a.w, b.w, acc);
     }
     __shared__ float s_sum[4], s_sq[4];
     float s = static_cast<float>(acc);
@@ -873,7 +910,7 @@ __device__ __forceinline__ void st_release(int *p, int v) {
     asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
-template <int C, int MT>
+template <int C, int MT, bool DIRECT = false>
 __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p) {
     constexpr int B_STAGE = STAGE_DOCS * 128 * C;
     constexpr int KSTEPS = 4 * C;
@@ -923,7 +960,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
     auto emit_lists = [&](int slot, int *hist, int gr, int part) {
         const int64_t gq0 = static_cast<int64_t>(gr) * NQ_CTA;
         const int cap = p.cap, k = p.k;
-        if (p.list_counts) {  // one work item per CTA: leave the lists in place, publish their lengths
+        if constexpr (DIRECT) {  // one work item per CTA: leave the lists in place, publish their lengths
             for (int qc = slot * 32 + lane; qc < NQ_CTA; qc += (Q_DRAIN + Q_RESOLVERS) * 32)
                 p.list_counts[static_cast<int64_t>(blockIdx.x) * NQ_CTA + qc] = gq0 + qc < p.nq ? cnt_s[qc] : 0;
             return;

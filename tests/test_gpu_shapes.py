@@ -40,3 +40,49 @@ def test_dims_on_tensor_engines(dim, wd, monkeypatch):
             assert np.array_equal(ids, want_i[:nq]), (dim, env, nq)
         for key in env:
             monkeypatch.delenv(key)
+
+
+@pytest.mark.parametrize("wd,wq,dim", [(5, 3, 200), (8, 4, 256), (6, 7, 128), (8, 7, 512), (1, 7, 300), (7, 1, 96), (3, 7, 384)])
+def test_wide_codes_on_the_tcgen05_engine(wd, wq, dim, monkeypatch):
+    """doc_bits up to 8 (document codes are the UNSIGNED 8-bit operand of tcgen05.mma kind::i8) and query_bits up to 7
+    (|2y - Aq| <= 127 fits the signed operand) at >= 50k rows with the tensor engine forced -- the widths of
+    pkg/tests/test_distance.py:127-140 that fit it; query_bits = 8 (weights up to +-255) stays on the POPC kernels."""
+    n, k = 60_000, 40
+    docs = xo.synthetic_unit_rows(n, dim, 500 + 10 * wd + wq)
+    queries = xo.synthetic_unit_rows(150, dim, 501 + 10 * wd + wq)
+    scale = xo.estimate_scale(docs[:20_000], 0.98)
+    params = xb.QuantParams(dim=dim, scale=scale, doc_bits=wd, query_bits=wq)
+    idx = xb.build_index(docs, params, keep_originals=False)
+    planes = xo.c_quantize_matrix(docs, wd, scale)
+    assert np.array_equal(idx.packed.planes, planes)
+    qp = xo.c_quantize_matrix(queries.astype(np.float64), wq, scale).transpose(2, 0, 1)
+    want_d, want_i = xo.c_search(planes, qp, k)
+    assert _engine(n, dim, wd, 150, wq, k) == 3
+    for env in ({}, {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SAMPLE": "4096"}, {"XFBQ_ENGINE": "popc"}):
+        for key, val in env.items():
+            monkeypatch.setenv(key, val)
+        scores, ids = xb.search(idx, queries, k)
+        assert np.array_equal(scores.astype(np.uint64), want_d), (wd, wq, env)
+        assert np.array_equal(ids, want_i), (wd, wq, env)
+        for key in env:
+            monkeypatch.delenv(key)
+    # small batches: mma.sync engine for codes that fit a nibble, POPC kernels above
+    assert (_engine(n, dim, wd, 3, wq, k) == 2) if wd <= 4 else (_engine(n, dim, wd, 3, wq, k) <= 1)
+    scores, ids = xb.search(idx, queries[:3], k)
+    assert np.array_equal(scores.astype(np.uint64), want_d[:3]) and np.array_equal(ids, want_i[:3])
+
+
+def test_query_bits_8_stays_exact_on_popc():
+    n, dim, k = 50_000, 128, 20
+    docs = xo.synthetic_unit_rows(n, dim, 808)
+    queries = xo.synthetic_unit_rows(40, dim, 809)
+    scale = xo.estimate_scale(docs[:20_000], 0.98)
+    for wd in (8, 1):
+        params = xb.QuantParams(dim=dim, scale=scale, doc_bits=wd, query_bits=8)
+        idx = xb.build_index(docs, params, keep_originals=False)
+        planes = xo.c_quantize_matrix(docs, wd, scale)
+        qp = xo.c_quantize_matrix(queries.astype(np.float64), 8, scale).transpose(2, 0, 1)
+        want_d, want_i = xo.c_search(planes, qp, k)
+        assert _engine(n, dim, wd, 40, 8, k) <= 1
+        scores, ids = xb.search(idx, queries, k)
+        assert np.array_equal(scores.astype(np.uint64), want_d) and np.array_equal(ids, want_i)
