@@ -171,8 +171,8 @@ class PackedMatrix:
     def nibbles(self):
         """Derived layouts of the codes for the tensor-core scans, built on the GPU on first use and cached: the nibble
         layout (doc_bits <= 4: mma.sync engine, <= 16 queries) followed by the byte tiles (any width: tcgen05 engine);
-        None when the dimension has no tensor path (dim > 512)."""
-        if self._count == 0 or self._dim > 512:
+        None when the dimension has no tensor path (dim > 1024)."""
+        if self._count == 0 or self._dim > 1024:
             return None
         cached = getattr(self, "_nibbles", None)
         if cached is None:

@@ -987,6 +987,18 @@ int launch_merge(const uint64_t *in, int parts, int64_t nq, int k, uint64_t *out
     return XFBQ_OK;
 }
 
+// Byte-tile geometry of a dimension: CP chunks of 128 dims in the bit planes, CT >= CP chunks per tile (dims above 512 are
+// padded to an even chunk count and streamed as KP = 2 K parts of Cp chunks that accumulate into one accumulator).
+struct TileGeom { int CP, CT, KP, Cp; };
+inline TileGeom tile_geom(int64_t dim) {
+    TileGeom g;
+    g.CP = static_cast<int>(chunks128(dim));
+    g.KP = g.CP > 4 ? 2 : 1;
+    g.CT = g.KP == 2 ? (g.CP + 1) & ~1 : g.CP;
+    g.Cp = g.CT / g.KP;
+    return g;
+}
+
 // ----------------------------------------------------------------------------------------------
 // Integer-MMA engine planning (kernels in xfbq_mma.cuh).
 // ----------------------------------------------------------------------------------------------
@@ -1198,6 +1210,7 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
 // ----------------------------------------------------------------------------------------------
 struct UmmaShape {
     int MT = 2, DW = 1, groups = 1, grid = 1, slots = 1, parts = 1, cap = 0, NS = 0;
+    int C = 1, KP = 1;   // chunks of 128 dims per operand stage, K parts per tile
     bool queue = false;  // scan_queue_kernel (main scans) vs scan_kernel (sample scans: open thresholds)
     bool direct = false; // queue kernel with one work item per CTA: lists stay in place, the bounded merge reads them (no emission)
     bool count = false;  // sample scan that only counts scores into per-query histograms (scan_kernel<.., SEED = true>)
@@ -1218,7 +1231,14 @@ struct UmmaPlan {
 
 typedef void (*UmmaKernel)(const umma::Params);
 
-UmmaKernel pick_umma_kernel(int C, int MT, bool queue, bool count = false, bool direct = false) {
+UmmaKernel pick_umma_kernel(int C, int MT, bool queue, bool count = false, bool direct = false, int KP = 1) {
+    if (KP == 2) {  // 513..1024 dims: two K parts of 3 or 4 chunks, one query tile
+        if (MT != 1 || (C != 3 && C != 4)) return nullptr;
+        if (count) return C == 3 ? umma::scan_kernel<3, 1, true, 2> : umma::scan_kernel<4, 1, true, 2>;
+        if (queue && direct) return C == 3 ? umma::scan_queue_kernel<3, 1, true, 2> : umma::scan_queue_kernel<4, 1, true, 2>;
+        if (queue) return C == 3 ? umma::scan_queue_kernel<3, 1, false, 2> : umma::scan_queue_kernel<4, 1, false, 2>;
+        return C == 3 ? umma::scan_kernel<3, 1, false, 2> : umma::scan_kernel<4, 1, false, 2>;
+    }
     if (queue && direct) {
         if (C == 1) return MT == 2 ? umma::scan_queue_kernel<1, 2, true> : umma::scan_queue_kernel<1, 1, true>;
         if (C == 2) return MT == 2 ? umma::scan_queue_kernel<2, 2, true> : umma::scan_queue_kernel<2, 1, true>;
@@ -1248,9 +1268,10 @@ UmmaKernel pick_umma_kernel(int C, int MT, bool queue, bool count = false, bool 
 }
 
 void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &info, UmmaShape *out, bool seed_scan = false,
-                bool allow_queue = true, bool count = false) {
+                bool allow_queue = true, bool count = false, int KP = 1) {
     UmmaShape sh;
     sh.MT = MT;
+    sh.C = C; sh.KP = KP;
     sh.count = count;
     sh.queue = !seed_scan && allow_queue && env_int("XFBQ_UMMA_QUEUE", 1) != 0;
     sh.DW = (MT == 2 || sh.queue) ? 1 : 2;
@@ -1331,18 +1352,22 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
 int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bool have_nibbles, UmmaPlan *plan) {
     UmmaPlan pl;
     *plan = pl;
-    const int C = static_cast<int>(chunks128(dim));
+    const TileGeom tg = tile_geom(dim);
+    const int C = tg.Cp, KP = tg.KP;
     const char *eng = getenv("XFBQ_ENGINE");
     if (eng && *eng && strcmp(eng, "umma") != 0) return XFBQ_OK;  // another engine was asked for
     const bool forced = eng && strcmp(eng, "umma") == 0;
-    if (!have_nibbles || wq > 7 || C < 1 || C > 4 || k > 1024 || n < 1 || env_int("XFBQ_FORCE_GENERIC", 0))  // any document width: the B operand is u8
+    if (!have_nibbles || wq > 7 || tg.CP < 1 || tg.CP > 8 || k > 1024 || n < 1 || env_int("XFBQ_FORCE_GENERIC", 0))  // any document width: the B operand is u8
         return XFBQ_OK;
-    if (!forced && nq < env_int("XFBQ_UMMA_MIN_NQ", 17)) return XFBQ_OK;  // <= 16 queries: the mma.sync scans (HBM-bound on the nibble layout; a 24-query batch took 0.72 ms there, 0.55 ms here)
+    // where the mma.sync engine cannot go (codes wider than a nibble, more than 512 dims) this engine also takes the small
+    // batches: from two queries on it beats the POPC kernels (1 POPC per code byte and query)
+    const bool no_imma = wd > 4 || tg.CP > 4;
+    if (!forced && nq < env_int("XFBQ_UMMA_MIN_NQ", no_imma ? 2 : 17)) return XFBQ_OK;  // <= 16 queries: the mma.sync scans (HBM-bound on the nibble layout; a 24-query batch took 0.72 ms there, 0.55 ms here)
     if (nq < 1) return XFBQ_OK;
     if (merge_group_max(k) == 0 || nq > 65535) return XFBQ_OK;  // lists are emitted unsorted: needs the tree merge
     DeviceInfo info;
     if (int rc = device_info(&info)) return rc;
-    const int MT = (C >= 3 || nq <= 128) ? 1 : 2;
+    const int MT = (C >= 3 || KP == 2 || nq <= 128) ? 1 : 2;
     // Sample scan that seeds the thresholds (measured on 10M x 256, 10k queries: 16k documents split over at
     // most 4 CTAs per query group balance its cost -- it starts from open lists -- against the rows the main
     // scan's resolvers then have to handle).
@@ -1354,7 +1379,7 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     // The same holds for small problems with few query groups (1M x 128, 1000 queries: 2.5x): the lists stay hot.
     const int64_t groups = (nq + 128 * MT - 1) / (128 * MT);
     const bool big = n >= env_int("XFBQ_UMMA_QUEUE_MIN_N", 2000000) || groups >= 16;
-    umma_shape(n, C, nq, k, MT, info, &pl.main, false, sample > 0 && big);
+    umma_shape(n, C, nq, k, MT, info, &pl.main, false, sample > 0 && big, false, KP);
     if (pl.main.NS == 0) return XFBQ_OK;
     pl.sample = sample;
     // Queue-kernel scans are seeded by counting (histogram of the sample's scores, no lists); the list-keeping
@@ -1372,7 +1397,7 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
         if (sample > umma::SEED_MAX_SAMPLE(C)) sample = umma::SEED_MAX_SAMPLE(C);
         pl.sample = sample;
     }
-    if (sample) umma_shape(sample, C, nq, k, MT, info, &pl.pre, true, true, count);
+    if (sample) umma_shape(sample, C, nq, k, MT, info, &pl.pre, true, true, count, KP);
     if (sample && pl.pre.NS == 0) return XFBQ_OK;
     if (count && pl.main.stages < 2 * pl.pre.stages) return XFBQ_OK;  // (cannot happen: n >= 16 * sample) sampled tiles must be full tiles
     if (count) {  // the counted sample is spread over the whole database (every stride-th tile)
@@ -1381,7 +1406,7 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
         pl.pre.n_valid = n;
     }
     size_t off = 0;
-    pl.off_qimg = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 128 * C);
+    pl.off_qimg = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 128 * tg.CT);
     pl.off_qconst = off; off = align256(off + static_cast<size_t>(pl.main.nq_pad) * 4);
     pl.off_tau = off; off = align256(off + (sample ? static_cast<size_t>(nq) * 4 : 0));
     pl.off_prekeys = off; off = align256(off + (sample ? static_cast<size_t>(nq) * k * 8 : 0));
@@ -1415,8 +1440,9 @@ double normal_quantile(double p) {
 int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, const void *nib, int64_t n, int C,
                   int64_t nq, int k, int64_t row_offset, const int32_t *tau_init, uint64_t *keys_out, cudaStream_t st) {
     const bool direct = sh.direct && &sh == &pl.main && tau_init != nullptr;
-    UmmaKernel kern = pick_umma_kernel(C, sh.MT, sh.queue, sh.count, direct);
-    if (!kern) return fail(XFBQ_E_UNSUPPORTED, "no tcgen05 kernel for C=%d MT=%d", C, sh.MT);
+    (void)C;
+    UmmaKernel kern = pick_umma_kernel(sh.C, sh.MT, sh.queue, sh.count, direct, sh.KP);
+    if (!kern) return fail(XFBQ_E_UNSUPPORTED, "no tcgen05 kernel for C=%d MT=%d KP=%d", sh.C, sh.MT, sh.KP);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sh.smem));
     if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "umma scan smem opt-in (%zu bytes): %s", sh.smem, cudaGetErrorString(e));
     umma::Params p;
@@ -1481,12 +1507,13 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
 int run_counted_seed(unsigned char *ws, const void *tiles, int64_t n, int64_t dim, int wd, const uint32_t *q, int64_t nq, int wq,
                      int k, int64_t sample, bool prep, size_t off_qimg, size_t off_qconst, size_t off_par, size_t off_hist,
                      int32_t *tau, cudaStream_t st) {
-    const int C = static_cast<int>(chunks128(dim));
+    const TileGeom tg = tile_geom(dim);
+    const int C = tg.Cp;
     DeviceInfo info;
     if (int rc = device_info(&info)) return rc;
-    const int MT = (C >= 3 || nq <= 128) ? 1 : 2;
+    const int MT = (C >= 3 || tg.KP == 2 || nq <= 128) ? 1 : 2;
     UmmaPlan pl;
-    umma_shape(sample, C, nq, k, MT, info, &pl.pre, true, true, true);
+    umma_shape(sample, C, nq, k, MT, info, &pl.pre, true, true, true, tg.KP);
     const int64_t total_stages = (bundles_of(n) * 32 + umma::STAGE_DOCS - 1) / umma::STAGE_DOCS;
     if (pl.pre.NS == 0 || total_stages < 2 * pl.pre.stages)
         return fail(XFBQ_E_UNSUPPORTED, "counted seed: sample %lld does not fit n=%lld dim=%lld", (long long)sample, (long long)n, (long long)dim);
@@ -1496,14 +1523,14 @@ int run_counted_seed(unsigned char *ws, const void *tiles, int64_t n, int64_t di
     unsigned char *qimg = ws + off_qimg;
     if (prep) {
         umma::prep_queries_kernel<<<static_cast<unsigned>((pl.pre.nq_pad * 32 + 255) / 256), 256, 0, st>>>(
-            q, nq, pl.pre.nq_pad, static_cast<int>(dim), wq, wd, C, MT, qimg, reinterpret_cast<int32_t *>(ws + off_qconst));
+            q, nq, pl.pre.nq_pad, static_cast<int>(dim), wq, wd, tg.CT, MT, qimg, reinterpret_cast<int32_t *>(ws + off_qconst));
         if (int rc = check_launch("umma::prep_queries_kernel")) return rc;
     }
     int2 *par = reinterpret_cast<int2 *>(ws + off_par);
     uint32_t *hist = reinterpret_cast<uint32_t *>(ws + off_hist);
     cudaError_t e = cudaMemsetAsync(hist, 0, static_cast<size_t>(nq) * umma::SEED_BINS * 4, st);
     if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
-    umma::seed_stats_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(static_cast<const unsigned char *>(tiles), qimg, nq, C, pl.pre.stages, pl.pre.tile_stride,
+    umma::seed_stats_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(static_cast<const unsigned char *>(tiles), qimg, nq, tg.CT, pl.pre.stages, pl.pre.tile_stride,
                                                                     static_cast<float>(normal_quantile(static_cast<double>(k) / static_cast<double>(sample))),
                                                                     0.25f * env_int("XFBQ_SEED_BELOW4", 8), par);
     if (int rc = check_launch("umma::seed_stats_kernel")) return rc;
@@ -1514,11 +1541,11 @@ int run_counted_seed(unsigned char *ws, const void *tiles, int64_t n, int64_t di
 
 int run_umma(const UmmaPlan &up, unsigned char *ws, const void *nib, int64_t n, int64_t dim, int wd, const uint32_t *q,
              int64_t nq, int wq, int k, int64_t row_offset, uint64_t *keys_out, cudaStream_t st) {
-    const int C = static_cast<int>(chunks128(dim));
+    const int C = up.main.C;
     unsigned char *qimg = ws + up.off_qimg;
     int32_t *qconst = reinterpret_cast<int32_t *>(ws + up.off_qconst);
     umma::prep_queries_kernel<<<static_cast<unsigned>((up.main.nq_pad * 32 + 255) / 256), 256, 0, st>>>(
-        q, nq, up.main.nq_pad, static_cast<int>(dim), wq, wd, C, up.main.MT, qimg, qconst);
+        q, nq, up.main.nq_pad, static_cast<int>(dim), wq, wd, tile_geom(dim).CT, up.main.MT, qimg, qconst);
     if (int rc = check_launch("umma::prep_queries_kernel")) return rc;
     const int32_t *tau_init = nullptr;
     if (up.sample) {
@@ -1713,14 +1740,14 @@ XFBQ_API int xfbq_bundles_to_planes(const void *db, int64_t n, int64_t dim, int 
 
 // Derived layouts of one index, in one buffer: [nibble layout][byte tiles].
 inline int64_t nibble_region_bytes(int64_t n, int64_t dim, int wd = 4) {
-    if (wd > 4) return 0;  // wider codes do not fit a nibble: the derived buffer holds the byte tiles only
+    if (wd > 4 || chunks128(dim) > 4) return 0;  // no mma.sync engine for these: the derived buffer holds the byte tiles only
     return ((bundles_of(n) * 32 * chunks128(dim) * 64 + 1023) / 1024) * 1024;
 }
 inline int64_t tile_count(int64_t n) { return (n + umma::STAGE_DOCS - 1) / umma::STAGE_DOCS; }
-inline bool tiles_supported(int64_t dim) { const int64_t C = chunks128(dim); return C >= 1 && C <= 4; }
+inline bool tiles_supported(int64_t dim) { const int64_t C = chunks128(dim); return C >= 1 && C <= 8; }
 
 XFBQ_API int64_t xfbq_derived_bytes(int64_t n, int64_t dim, int width) {
-    return nibble_region_bytes(n, dim, width) + (tiles_supported(dim) ? tile_count(n) * umma::STAGE_DOCS * chunks128(dim) * 128 : 0);
+    return nibble_region_bytes(n, dim, width) + (tiles_supported(dim) ? tile_count(n) * umma::STAGE_DOCS * tile_geom(dim).CT * 128 : 0);
 }
 XFBQ_API int64_t xfbq_nibble_bytes(int64_t n, int64_t dim) { return xfbq_derived_bytes(n, dim, 4); }
 
@@ -1732,16 +1759,17 @@ XFBQ_API int xfbq_build_derived(const void *db, int64_t n, int64_t dim, int widt
     const int C = static_cast<int>(chunks128(dim));
     const int64_t n_pad = bundles_of(n) * 32;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (width <= 4) {
+    if (nibble_region_bytes(n, dim, width) > 0) {
         const int64_t total = n_pad * 4 * C;
         mma::planes_to_nibbles_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
             static_cast<const uint32_t *>(db), n_pad, width, C, static_cast<uint4 *>(out));
         if (int rc = check_launch("planes_to_nibbles_kernel")) return rc;
     }
     if (!tiles_supported(dim)) return XFBQ_OK;
-    const int64_t tiles = tile_count(n), groups = tiles * umma::STAGE_DOCS * 4 * C;
+    const int CT = tile_geom(dim).CT;
+    const int64_t tiles = tile_count(n), groups = tiles * umma::STAGE_DOCS * 4 * CT;
     umma::planes_to_tiles_kernel<<<static_cast<unsigned>((groups + 255) / 256), 256, 0, st>>>(
-        static_cast<const uint32_t *>(db), n_pad, tiles, width, C, static_cast<unsigned char *>(out) + nibble_region_bytes(n, dim, width));
+        static_cast<const uint32_t *>(db), n_pad, tiles, width, C, CT, static_cast<unsigned char *>(out) + nibble_region_bytes(n, dim, width));
     return check_launch("planes_to_tiles_kernel");
 }
 

@@ -34,8 +34,7 @@ constexpr int MMA_WARP = 8;
 constexpr int TMA_WARP = 9;
 constexpr int THREADS = 320;    // 10 warps: registers are carved per 4 warps, so 12 warps' worth -> 168 per thread
 constexpr int STAGE_DOCS = 128;  // N of one MMA
-constexpr int ACC_BUFS = 3;      // 3 x 128 accumulator columns; columns 384..511 hold the query operand
-constexpr int A_COL0 = ACC_BUFS * STAGE_DOCS;
+constexpr int ACC_BUFS_MAX = 3;  // 3 x 128 accumulator columns, the query operand behind them (two accumulators for two-part tiles)
 constexpr int HIST_BINS = 256;
 constexpr int SEED_BINS = 64;     // bins of the sample histogram that seeds the thresholds
 constexpr int SEED_STRIDE = EPI_WARPS * 32;  // bin-major shared-memory histograms: counter (copy * 64 + bin) * 256 + thread
@@ -160,7 +159,7 @@ prep_queries_kernel(const uint32_t *__restrict__ q, int64_t nq, int64_t nq_pad, 
     const int lane = threadIdx.x & 31;
     const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (row >= nq_pad) return;
-    const int W = 4 * C;
+    const int W = 4 * ((dim + 127) >> 7);  // words per plane of the query layout (C may be padded to an even chunk count)
     const int Aq = (1 << wq) - 1, Ad = (1 << wd) - 1;
     unsigned char *img = qimg + row * (static_cast<int64_t>(C) * 128);
     (void)MT;
@@ -173,10 +172,11 @@ prep_queries_kernel(const uint32_t *__restrict__ q, int64_t nq, int64_t nq_pad, 
             for (int j = 0; j < 4; ++j) {
                 const int d = 32 * g + e + 4 * hi + 8 * j;
                 const int word = d >> 5, bit = d & 31;
-                int y = 0;
-                for (int jq = 0; jq < wq; ++jq) y |= static_cast<int>((q[(row * wq + jq) * W + word] >> bit) & 1u) << jq;
-                int w = 0;
-                if (d < dim) { w = 2 * y - Aq; sy += y; }
+                int y = 0, w = 0;
+                if (d < dim) {
+                    for (int jq = 0; jq < wq; ++jq) y |= static_cast<int>((q[(row * wq + jq) * W + word] >> bit) & 1u) << jq;
+                    w = 2 * y - Aq; sy += y;
+                }
                 packed |= (static_cast<uint32_t>(w) & 0xFFu) << (8 * j);
             }
         }
@@ -196,7 +196,7 @@ __host__ __device__ inline SmemLayout smem_layout(int C, int MT, int NS, bool se
     L.a_off = off; (void)MT;
     L.b_off = off; off += static_cast<uint32_t>(NS) * STAGE_DOCS * 128 * C;
     L.hist_off = off; off += seed_hist ? SEED_COPIES(C) * SEED_STRIDE * SEED_BINS * 2 : EPI_WARPS * 256 * 4;
-    L.bar_off = off; off += (2 * NS + 2 * ACC_BUFS) * 8 + 16;
+    L.bar_off = off; off += (2 * NS + 2 * ACC_BUFS_MAX) * 8 + 16;
     L.total = off + 1024;  // slack for the manual 1024-byte alignment of the operand area
     return L;
 }
@@ -227,18 +227,19 @@ nibbles_to_tiles_kernel(const uint4 *__restrict__ nib, int64_t n_pad, int64_t n_
 // Plane i's 32-bit word of the group holds dim d in bit d, so ((P_i >> (e + 4 hi)) & 0x01010101) << i places bit i of the
 // codes of dims e + 4 hi + {0, 8, 16, 24} into bytes j = 0..3 of output word (e, hi): the same K order as above.
 __global__ void __launch_bounds__(256)
-planes_to_tiles_kernel(const uint32_t *__restrict__ db, int64_t n_pad, int64_t n_tiles, int wd, int C, unsigned char *__restrict__ tiles) {
+planes_to_tiles_kernel(const uint32_t *__restrict__ db, int64_t n_pad, int64_t n_tiles, int wd, int CP, int C, unsigned char *__restrict__ tiles) {
+    // CP = chunks of the bundle layout (ceil(dim / 128)), C >= CP = chunks of a tile (padded to an even count above 4)
     const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int G = 4 * C;
     if (e >= n_tiles * STAGE_DOCS * G) return;
     const int64_t doc = e / G;
     const int g = static_cast<int>(e - doc * G);
     uint32_t w[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // w[2 e + hi]
-    if (doc < n_pad) {
+    if (doc < n_pad && (g >> 2) < CP) {
         const int64_t b = doc >> 5;
         const int l = static_cast<int>(doc & 31), c = g >> 2;
         for (int i = 0; i < wd; ++i) {
-            const uint32_t pw = __ldg(db + ((((b * wd + i) * C + c) * 32 + l) << 2) + (g & 3));
+            const uint32_t pw = __ldg(db + ((((b * wd + i) * CP + c) * 32 + l) << 2) + (g & 3));
 #pragma unroll
             for (int x = 0; x < 8; ++x) w[x] |= ((pw >> ((x >> 1) + 4 * (x & 1))) & 0x01010101u) << i;
         }
@@ -421,13 +422,18 @@ struct Items {
 // histogram of the query when the CTA leaves the group).  seed_bounds_kernel then reads a valid threshold off
 // the histogram: "the bins >= b hold k real documents".  Seeding by list maintenance from open thresholds cost
 // 2.2 ms per 10k queries, two thirds of it in list compactions.
-template <int C, int MT, bool SEED = false>
+// KP = 2: documents of 513..1024 dims as tiles of two K parts (C chunks each, streamed as two operand stages that
+// accumulate into one accumulator); two accumulators, one query tile.
+template <int C, int MT, bool SEED = false, int KP = 1>
 __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     constexpr int B_STAGE = STAGE_DOCS * 128 * C;     // one document stage = one byte tile
     constexpr int KSTEPS = 4 * C;                     // K = 32 per MMA
     constexpr int COLS = MT == 2 ? 128 : 64;          // accumulator columns an epilogue warp drains
     constexpr int EPI_PER_BUF = MT == 2 ? 4 : 8;      // epilogue warps reading one accumulator
-    constexpr int A_COLS = 32 * C;                    // tensor-memory columns of one 128-query operand tile
+    constexpr int A_COLS = 32 * C * KP;               // tensor-memory columns of one 128-query operand tile (all K parts)
+    constexpr int AB = KP == 1 ? ACC_BUFS_MAX : 2;    // accumulators: the operand of a two-part tile takes up to 256 columns
+    constexpr int ACOL0 = AB * STAGE_DOCS;
+    static_assert(KP == 1 || MT == 1, "two-part tiles leave room for one query tile");                    // tensor-memory columns of one 128-query operand tile
     extern __shared__ unsigned char smem_unaligned[];
     const uint32_t pad = (1024u - (smem_u32(smem_unaligned) & 1023u)) & 1023u;
     unsigned char *smem = smem_unaligned + pad;
@@ -435,8 +441,8 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
     const SmemLayout L = smem_layout(C, MT, NS, SEED);
     unsigned char *sB = smem + L.b_off;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L.bar_off);
-    uint64_t *b_full = bars, *b_empty = bars + NS, *acc_full = bars + 2 * NS, *acc_empty = bars + 2 * NS + ACC_BUFS;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 2 * ACC_BUFS);
+    uint64_t *b_full = bars, *b_empty = bars + NS, *acc_full = bars + 2 * NS, *acc_empty = bars + 2 * NS + AB;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 2 * AB);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     const int64_t T = p.stages;
@@ -446,7 +452,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NS; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
-        for (int i = 0; i < ACC_BUFS; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], EPI_PER_BUF); }
+        for (int i = 0; i < AB; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], EPI_PER_BUF); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) tmem_alloc(tmem_slot, 512);
@@ -479,8 +485,8 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
             const int64_t q0 = (static_cast<int64_t>(sg.gr) * MT + mt) * 128 + q4 * 32;  // first query row of this warp
             const int64_t myq = q0 + lane;
             if (MT == 2 || idx == 0) {  // this thread's query row -> lane (32 q4 + lane), columns of tile mt
-                const uint4 *src = reinterpret_cast<const uint4 *>(p.qimg + myq * (128 * C));
-                const uint32_t ta = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + A_COL0 + mt * A_COLS;
+                const uint4 *src = reinterpret_cast<const uint4 *>(p.qimg + myq * (128 * C * KP));
+                const uint32_t ta = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + ACOL0 + mt * A_COLS;
 #pragma unroll
                 for (int c = 0; c < A_COLS / 8; ++c) tmem_st8(ta + c * 8, __ldg(src + 2 * c), __ldg(src + 2 * c + 1));
                 tmem_st_wait();
@@ -507,7 +513,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                 const int c2 = par.x;   // 2 * (origin - width)
                 const int m31 = par.y;  // ceil(2^31 / width)
                 const uint32_t u0 = s_run * MT + mt;
-                Ring ac{static_cast<int>(u0 % ACC_BUFS), (u0 / ACC_BUFS) & 1u};
+                Ring ac{static_cast<int>(u0 % AB), (u0 / AB) & 1u};
                 for (int i = 0; i < sg.cnt; ++i) {
                     const uint32_t buf = ac.idx;
                     mbar_wait_prof(&acc_full[buf], ac.phase, prof, w0);
@@ -539,7 +545,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                                 asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr[u]), "h"(static_cast<unsigned short>(cur[u] + 1)) : "memory");
                         }
 #pragma unroll
-                    for (int a = 0; a < MT; ++a) ac.advance(ACC_BUFS);
+                    for (int a = 0; a < MT; ++a) ac.advance(AB);
                 }
                 if (valid)
                     for (int b = 1; b < SEED_BINS; ++b) {  // bin 0 (below the origin) proves nothing
@@ -628,7 +634,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
             };
 
             const uint32_t u0 = s_run * MT + mt;
-            Ring ac{static_cast<int>(u0 % ACC_BUFS), (u0 / ACC_BUFS) & 1u};
+            Ring ac{static_cast<int>(u0 % AB), (u0 / AB) & 1u};
             // thresholds other CTAs found for this query: fetched four stages ahead of their use, so the L2 round
             // trip never sits on a stage's critical path
             const bool fetch_shared = p.theta_g && valid;
@@ -661,7 +667,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                     for (int c = 0; c < COLS / 32; ++c) filter(v[c], doc0 + c * 32);
                 }
 #pragma unroll
-                for (int a = 0; a < MT; ++a) ac.advance(ACC_BUFS);
+                for (int a = 0; a < MT; ++a) ac.advance(AB);
             }
             // ---- emit: every query row of this warp, its <= k best keys (unsorted), KEY_INF padded
             {
@@ -697,10 +703,37 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
         while (sg.next()) {
             cta_sync();
             fence_after();  // the query operand stored by the epilogue warps is in tensor memory
-            Ring rb{static_cast<int>(s_run % NS), (s_run / NS) & 1u};
+            Ring rb{static_cast<int>((s_run * KP) % NS), ((s_run * KP) / NS) & 1u};
             const uint32_t u0 = s_run * MT;
-            Ring ac{static_cast<int>(u0 % ACC_BUFS), ((u0 / ACC_BUFS) & 1u) ^ 1u};  // "empty" waits: completed phase first
+            Ring ac{static_cast<int>(u0 % AB), ((u0 / AB) & 1u) ^ 1u};  // "empty" waits: completed phase first
             for (int i = 0; i < sg.cnt; ++i) {  // the whole warp walks the pipeline, one elected lane issues
+                if constexpr (KP > 1) {  // one accumulator per tile, fed by KP operand stages
+                    const uint32_t buf = ac.idx;
+                    mbar_wait_prof(&acc_empty[buf], ac.phase, prof, w1);
+                    fence_after();
+#pragma unroll
+                    for (int part = 0; part < KP; ++part) {
+                        mbar_wait_prof(&b_full[rb.idx], rb.phase, prof, w0);
+                        fence_after();
+                        const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4);
+                        if (elect_one()) {
+                            const uint32_t d = tm + buf * STAGE_DOCS;
+#pragma unroll
+                            for (int ks = 0; ks < KSTEPS; ++ks) {
+                                const uint32_t ta = tm + ACOL0 + (part * KSTEPS + ks) * 8;
+                                const uint32_t bo = ((ks >> 2) * (STAGE_DOCS * 128) + (ks & 3) * 32) >> 4;
+                                if (part == 0 && ks == 0) umma_i8<false>(d, ta, b_lo + bo);
+                                else umma_i8<true>(d, ta, b_lo + bo);
+                            }
+                            umma_commit(&b_empty[rb.idx]);
+                            if (part == KP - 1) umma_commit(&acc_full[buf]);
+                        }
+                        __syncwarp();
+                        rb.advance(NS);
+                    }
+                    ac.advance(AB);
+                    continue;
+                }
                 mbar_wait_prof(&b_full[rb.idx], rb.phase, prof, w0);
                 fence_after();
                 const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4);
@@ -713,7 +746,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                         const uint32_t d = tm + buf * STAGE_DOCS;
 #pragma unroll
                         for (int ks = 0; ks < KSTEPS; ++ks) {
-                            const uint32_t ta = tm + A_COL0 + mt * A_COLS + ks * 8;  // K = 32 signed bytes = 8 columns
+                            const uint32_t ta = tm + ACOL0 + mt * A_COLS + ks * 8;  // K = 32 signed bytes = 8 columns
                             const uint32_t bo = ((ks >> 2) * (STAGE_DOCS * 128) + (ks & 3) * 32) >> 4;
                             if (ks == 0) umma_i8<false>(d, ta, b_lo + bo);
                             else umma_i8<true>(d, ta, b_lo + bo);
@@ -721,7 +754,7 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
                         umma_commit(&acc_full[buf]);
                     }
                     __syncwarp();
-                    ac.advance(ACC_BUFS);
+                    ac.advance(AB);
                 }
                 if (elect_one()) umma_commit(&b_empty[rb.idx]);
                 __syncwarp();
@@ -737,12 +770,16 @@ __global__ void __launch_bounds__(THREADS, 1) scan_kernel(const Params p) {
         while (sg.next()) {
             cta_sync();
             if (lane == 0) {
-                Ring rb{static_cast<int>(s_run % NS), ((s_run / NS) & 1u) ^ 1u};  // "empty" waits start on the completed phase
+                Ring rb{static_cast<int>((s_run * KP) % NS), (((s_run * KP) / NS) & 1u) ^ 1u};  // "empty" waits start on the completed phase
                 for (int i = 0; i < sg.cnt; ++i) {
-                    mbar_wait_prof(&b_empty[rb.idx], rb.phase, prof, w0);
-                    mma::mbar_arrive_expect_tx(&b_full[rb.idx], B_STAGE);
-                    mma::tma_bulk_g2s(sB + static_cast<size_t>(rb.idx) * B_STAGE, db + static_cast<int64_t>(sg.sd0 + i) * (SEED ? p.tile_stride : 1) * B_STAGE, B_STAGE, &b_full[rb.idx]);
-                    rb.advance(NS);
+#pragma unroll
+                    for (int part = 0; part < KP; ++part) {
+                        mbar_wait_prof(&b_empty[rb.idx], rb.phase, prof, w0);
+                        mma::mbar_arrive_expect_tx(&b_full[rb.idx], B_STAGE);
+                        mma::tma_bulk_g2s(sB + static_cast<size_t>(rb.idx) * B_STAGE,
+                                          db + (static_cast<int64_t>(sg.sd0 + i) * (SEED ? p.tile_stride : 1) * KP + part) * B_STAGE, B_STAGE, &b_full[rb.idx]);
+                        rb.advance(NS);
+                    }
                 }
             }
             __syncwarp();
@@ -892,7 +929,7 @@ __host__ __device__ inline QSmemLayout q_smem_layout(int C, int NS, int ring_row
     L.ring_off = off; off += Q_DRAIN * ring_rows * STASH_WORDS * 4;
     L.state_off = off; off += 5 * 256 * 4 + 2 * Q_DRAIN * 4 + 32;  // per query: count, threshold, Dq, claim, seeded threshold; per drain warp: tail, final ticket
     L.hist_off = off; off += Q_RESOLVERS * 256 * 4;
-    L.bar_off = off; off += (2 * NS + 2 * ACC_BUFS) * 8 + 16;
+    L.bar_off = off; off += (2 * NS + 2 * ACC_BUFS_MAX) * 8 + 16;
     L.total = off + 1024;
     return L;
 }
@@ -910,12 +947,15 @@ __device__ __forceinline__ void st_release(int *p, int v) {
     asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 
-template <int C, int MT, bool DIRECT = false>
+template <int C, int MT, bool DIRECT = false, int KP = 1>
 __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p) {
     constexpr int B_STAGE = STAGE_DOCS * 128 * C;
     constexpr int KSTEPS = 4 * C;
     constexpr int EPI_PER_BUF = 8;                    // arrivals that free an accumulator: two column halves x four lane quarters
-    constexpr int A_COLS = 32 * C;
+    constexpr int A_COLS = 32 * C * KP;               // tensor-memory columns of one 128-query operand tile (all K parts)
+    constexpr int AB = KP == 1 ? ACC_BUFS_MAX : 2;    // accumulators: the operand of a two-part tile takes up to 256 columns
+    constexpr int ACOL0 = AB * STAGE_DOCS;
+    static_assert(KP == 1 || MT == 1, "two-part tiles leave room for one query tile");
     constexpr int NQ_CTA = 128 * MT;                  // queries of one group
     extern __shared__ unsigned char smem_unaligned[];
     const uint32_t pad = (1024u - (smem_u32(smem_unaligned) & 1023u)) & 1023u;
@@ -929,8 +969,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
     int *theta0_s = cnt_s + 1024;
     int *tail_s = cnt_s + 1280, *fin_s = tail_s + Q_DRAIN;  // per drain warp: rows consumed by its resolver; final ticket of a segment
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L.bar_off);
-    uint64_t *b_full = bars, *b_empty = bars + NS, *acc_full = bars + 2 * NS, *acc_empty = bars + 2 * NS + ACC_BUFS;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 2 * ACC_BUFS);
+    uint64_t *b_full = bars, *b_empty = bars + NS, *acc_full = bars + 2 * NS, *acc_empty = bars + 2 * NS + AB;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * NS + 2 * AB);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     Items sg{static_cast<int64_t>(blockIdx.x), static_cast<int64_t>(p.n_seg) * p.groups, static_cast<int64_t>(gridDim.x),
@@ -938,7 +978,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NS; ++i) { mbar_init(&b_full[i], 1); mbar_init(&b_empty[i], 1); }
-        for (int i = 0; i < ACC_BUFS; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], EPI_PER_BUF); }
+        for (int i = 0; i < AB; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], EPI_PER_BUF); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int w = 0; w < Q_DRAIN; ++w) { tail_s[w] = 0; fin_s[w] = -1; }
     }
@@ -994,8 +1034,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                 const int qloc = mt * 128 + q4 * 32 + lane;
                 const int64_t myq = static_cast<int64_t>(sg.gr) * NQ_CTA + qloc;
                 const bool valid = myq < p.nq;
-                const uint4 *src = reinterpret_cast<const uint4 *>(p.qimg + myq * (128 * C));
-                const uint32_t ta = lane_base + A_COL0 + mt * A_COLS;
+                const uint4 *src = reinterpret_cast<const uint4 *>(p.qimg + myq * (128 * C * KP));
+                const uint32_t ta = lane_base + ACOL0 + mt * A_COLS;
 #pragma unroll
                 for (int c = 0; c < A_COLS / 8; ++c) tmem_st8(ta + c * 8, __ldg(src + 2 * c), __ldg(src + 2 * c + 1));
                 tmem_st_wait();
@@ -1053,13 +1093,13 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                 for (uint32_t x = set; x < n_units; x += 3) {
                     const uint32_t rel = x >> 1, half = x & 1u;
                     const uint32_t u = u_begin + rel;
-                    const uint32_t buf = u % ACC_BUFS;
+                    const uint32_t buf = u % AB;
                     const int mt = MT == 2 ? static_cast<int>(rel & 1u) : 0;
                     const int qloc = mt * 128 + q4 * 32 + lane;
                     const uint32_t doc0 = (static_cast<uint32_t>(sg.sd0) + rel / MT) * STAGE_DOCS + half * 64;
                     const uint32_t taddr = lane_base + buf * STAGE_DOCS + half * 64;
                     const int theta = theta_s[qloc];
-                    if (prof) mbar_wait_prof(&acc_full[buf], (u / ACC_BUFS) & 1u, true, w0); else mbar_wait_tight(&acc_full[buf], (u / ACC_BUFS) & 1u);
+                    if (prof) mbar_wait_prof(&acc_full[buf], (u / AB) & 1u, true, w0); else mbar_wait_tight(&acc_full[buf], (u / AB) & 1u);
                     fence_after();
                     int v[2][32];
                     tmem_ld32(taddr, v[0]);
@@ -1096,10 +1136,37 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
         while (sg.next()) {
             cta_sync();
             fence_after();
-            Ring rb{static_cast<int>(s_run % NS), (s_run / NS) & 1u};
+            Ring rb{static_cast<int>((s_run * KP) % NS), ((s_run * KP) / NS) & 1u};
             const uint32_t u0 = s_run * MT;
-            Ring ac{static_cast<int>(u0 % ACC_BUFS), ((u0 / ACC_BUFS) & 1u) ^ 1u};
+            Ring ac{static_cast<int>(u0 % AB), ((u0 / AB) & 1u) ^ 1u};
             for (int i = 0; i < sg.cnt; ++i) {
+                if constexpr (KP > 1) {  // one accumulator per tile, fed by KP operand stages
+                    const uint32_t buf = ac.idx;
+                    mbar_wait_prof(&acc_empty[buf], ac.phase, prof, w1);
+                    fence_after();
+#pragma unroll
+                    for (int part = 0; part < KP; ++part) {
+                        if (prof) mbar_wait_prof(&b_full[rb.idx], rb.phase, true, w0); else mbar_wait_tight(&b_full[rb.idx], rb.phase);
+                        fence_after();
+                        const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4);
+                        if (elect_one()) {
+                            const uint32_t d = tm + buf * STAGE_DOCS;
+#pragma unroll
+                            for (int ks = 0; ks < KSTEPS; ++ks) {
+                                const uint32_t ta = tm + ACOL0 + (part * KSTEPS + ks) * 8;
+                                const uint32_t bo = ((ks >> 2) * (STAGE_DOCS * 128) + (ks & 3) * 32) >> 4;
+                                if (part == 0 && ks == 0) umma_i8<false>(d, ta, b_lo + bo);
+                                else umma_i8<true>(d, ta, b_lo + bo);
+                            }
+                            umma_commit(&b_empty[rb.idx]);
+                            if (part == KP - 1) umma_commit(&acc_full[buf]);
+                        }
+                        __syncwarp();
+                        rb.advance(NS);
+                    }
+                    ac.advance(AB);
+                    continue;
+                }
                 if (prof) mbar_wait_prof(&b_full[rb.idx], rb.phase, true, w0); else mbar_wait_tight(&b_full[rb.idx], rb.phase);
                 fence_after();
                 const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4);
@@ -1112,7 +1179,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                         const uint32_t d = tm + buf * STAGE_DOCS;
 #pragma unroll
                         for (int ks = 0; ks < KSTEPS; ++ks) {
-                            const uint32_t ta = tm + A_COL0 + mt * A_COLS + ks * 8;
+                            const uint32_t ta = tm + ACOL0 + mt * A_COLS + ks * 8;
                             const uint32_t bo = ((ks >> 2) * (STAGE_DOCS * 128) + (ks & 3) * 32) >> 4;
                             if (ks == 0) umma_i8<false>(d, ta, b_lo + bo);
                             else umma_i8<true>(d, ta, b_lo + bo);
@@ -1120,7 +1187,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                         umma_commit(&acc_full[buf]);
                     }
                     __syncwarp();
-                    ac.advance(ACC_BUFS);
+                    ac.advance(AB);
                 }
                 if (elect_one()) umma_commit(&b_empty[rb.idx]);
                 __syncwarp();
@@ -1137,12 +1204,16 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
         while (sg.next()) {
             cta_sync();
             if (lane == 0) {
-                Ring rb{static_cast<int>(s_run % NS), ((s_run / NS) & 1u) ^ 1u};
+                Ring rb{static_cast<int>((s_run * KP) % NS), (((s_run * KP) / NS) & 1u) ^ 1u};
                 for (int i = 0; i < sg.cnt; ++i) {
-                    mbar_wait_prof(&b_empty[rb.idx], rb.phase, prof, w0);
-                    mma::mbar_arrive_expect_tx(&b_full[rb.idx], B_STAGE);
-                    mma::tma_bulk_g2s(sB + static_cast<size_t>(rb.idx) * B_STAGE, db + static_cast<int64_t>(sg.sd0 + i) * B_STAGE, B_STAGE, &b_full[rb.idx]);
-                    rb.advance(NS);
+#pragma unroll
+                    for (int part = 0; part < KP; ++part) {
+                        mbar_wait_prof(&b_empty[rb.idx], rb.phase, prof, w0);
+                        mma::mbar_arrive_expect_tx(&b_full[rb.idx], B_STAGE);
+                        mma::tma_bulk_g2s(sB + static_cast<size_t>(rb.idx) * B_STAGE,
+                                          db + (static_cast<int64_t>(sg.sd0 + i) * KP + part) * B_STAGE, B_STAGE, &b_full[rb.idx]);
+                        rb.advance(NS);
+                    }
                 }
             }
             __syncwarp();

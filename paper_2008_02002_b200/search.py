@@ -83,8 +83,8 @@ def scan_topk_device(packed: PackedMatrix, qwords, nq: int, query_bits: int, k: 
                                                      qwords.data_ptr() + qi * words_per_query * 4, query_bits, d.data_ptr(), st))
                 keys[qi] = torch.sort((d << 32) | ids).values[:k]
             return keys
-        # derived layouts only where a tensor engine will read them (dim <= 512): other shapes take the POPC kernels
-        nib = packed.nibbles if query_bits <= 7 and k <= 1024 and C <= 4 else None
+        # derived layouts only where a tensor engine will read them (dim <= 1024): other shapes take the POPC kernels
+        nib = packed.nibbles if query_bits <= 7 and k <= 1024 and C <= 8 else None
         nib_ptr = nib.data_ptr() if nib is not None else None
         for q0 in range(0, nq, _QUERY_BATCH):
             qn = min(_QUERY_BATCH, nq - q0)

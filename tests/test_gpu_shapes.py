@@ -66,10 +66,13 @@ def test_wide_codes_on_the_tcgen05_engine(wd, wq, dim, monkeypatch):
         assert np.array_equal(ids, want_i), (wd, wq, env)
         for key in env:
             monkeypatch.delenv(key)
-    # small batches: mma.sync engine for codes that fit a nibble, POPC kernels above
-    assert (_engine(n, dim, wd, 3, wq, k) == 2) if wd <= 4 else (_engine(n, dim, wd, 3, wq, k) <= 1)
-    scores, ids = xb.search(idx, queries[:3], k)
-    assert np.array_equal(scores.astype(np.uint64), want_d[:3]) and np.array_equal(ids, want_i[:3])
+    # small batches: the mma.sync engine for codes that fit a nibble; wider codes stay on the tcgen05 engine down to two
+    # queries, a single query takes the POPC kernels
+    assert _engine(n, dim, wd, 3, wq, k) == (2 if wd <= 4 else 3)
+    assert _engine(n, dim, wd, 1, wq, k) == (2 if wd <= 4 else _engine(n, dim, wd, 1, wq, k)) and (wd <= 4 or _engine(n, dim, wd, 1, wq, k) <= 1)
+    for nb in (3, 1):
+        scores, ids = xb.search(idx, queries[:nb], k)
+        assert np.array_equal(scores.astype(np.uint64), want_d[:nb]) and np.array_equal(ids, want_i[:nb])
 
 
 def test_query_bits_8_stays_exact_on_popc():
@@ -86,3 +89,30 @@ def test_query_bits_8_stays_exact_on_popc():
         assert _engine(n, dim, wd, 40, 8, k) <= 1
         scores, ids = xb.search(idx, queries, k)
         assert np.array_equal(scores.astype(np.uint64), want_d) and np.array_equal(ids, want_i)
+
+
+@pytest.mark.parametrize("dim,wd", [(513, 4), (640, 3), (768, 4), (1000, 4), (1024, 4), (768, 8)])
+def test_dims_513_to_1024_on_two_part_tiles(dim, wd, monkeypatch):
+    """513..1024 dims: byte tiles of two K parts (3 or 4 chunks of 128 dims each, padded to an even chunk count) that
+    accumulate into one tensor-memory accumulator; the reference accepts any dim (pkg/tests/test_distance.py:50-59 goes to 513)."""
+    n, k, wq = 60_000, 30, 4
+    docs = xo.synthetic_unit_rows(n, dim, 700 + dim)
+    queries = xo.synthetic_unit_rows(160, dim, 701 + dim)
+    scale = xo.estimate_scale(docs[:10_000], 0.98)
+    params = xb.QuantParams(dim=dim, scale=scale, doc_bits=wd, query_bits=wq)
+    idx = xb.build_index(docs, params, keep_originals=False)
+    planes = xo.c_quantize_matrix(docs, wd, scale)
+    assert np.array_equal(idx.packed.planes, planes)
+    qp = xo.c_quantize_matrix(queries.astype(np.float64), wq, scale).transpose(2, 0, 1)
+    want_d, want_i = xo.c_search(planes, qp, k)
+    assert _engine(n, dim, wd, 160, wq, k) == 3 and _engine(n, dim, wd, 2, wq, k) == 3 and _engine(n, dim, wd, 1, wq, k) <= 1
+    for env in ({}, {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SAMPLE": "4096"},
+                {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SAMPLE": "4096", "XFBQ_UMMA_SLICES": "3"}):
+        for key, val in env.items():
+            monkeypatch.setenv(key, val)
+        for nq in (160, 5, 1):
+            scores, ids = xb.search(idx, queries[:nq], k)
+            assert np.array_equal(scores.astype(np.uint64), want_d[:nq]), (dim, wd, env, nq)
+            assert np.array_equal(ids, want_i[:nq]), (dim, wd, env, nq)
+        for key in env:
+            monkeypatch.delenv(key)
