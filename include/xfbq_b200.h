@@ -184,6 +184,25 @@ int xfbq_scan_topk(const void *db_dev, const void *nibbles_dev, int64_t n, int64
                    void *stream);
 
 /*
+ * Single-launch search for small batches (1 <= nq <= 16, doc_bits <= 4, query_bits <= 7, dim <= 512, k <= 1024, databases of
+ * a million rows and more): float queries in, keys out, ONE cooperative kernel -- the query quantizer (quantize_vector,
+ * bitplane.py:214-222), query preparation, threshold seeding, the HBM-bound scan and the merge (k_select's no-originals
+ * ranking, search.py:159-172, :129-131) with grid-wide barriers in between, instead of ten launches.
+ * xfbq_search_small_workspace_bytes returns 0 for shapes it does not take (use xfbq_quantize_queries_* + xfbq_scan_topk).
+ * *nonfinite_dev (device uint64, NOT zeroed by the call) += the non-finite scaled query values found; a query holding one is
+ * answered with empty keys (UINT64_MAX) -- the reference raises InvalidInputError (quant.py:142-143), which the caller does
+ * when it reads the counter.  nibbles_dev: xfbq_build_derived / xfbq_planes_to_nibbles output.  Results are identical to
+ * xfbq_scan_topk on the quantized queries.
+ */
+int64_t xfbq_search_small_workspace_bytes(int64_t n, int64_t dim, int doc_bits, int64_t nq, int query_bits, int k);
+int xfbq_search_small_f32(const void *db_dev, const void *nibbles_dev, int64_t n, int64_t dim, int doc_bits, const float *queries_dev,
+                          int64_t nq, int64_t ld, double scale, int query_bits, int k, int64_t row_offset, uint64_t *keys_out_dev,
+                          uint64_t *nonfinite_dev, void *workspace_dev, int64_t workspace_bytes, void *stream);
+int xfbq_search_small_f64(const void *db_dev, const void *nibbles_dev, int64_t n, int64_t dim, int doc_bits, const double *queries_dev,
+                          int64_t nq, int64_t ld, double scale, int query_bits, int k, int64_t row_offset, uint64_t *keys_out_dev,
+                          uint64_t *nonfinite_dev, void *workspace_dev, int64_t workspace_bytes, void *stream);
+
+/*
  * Merge `parts` partial results keys_in_dev[parts][nq][k] (each row ascending,
  * UINT64_MAX padded) into keys_out_dev[nq][k]: the exchange step after the
  * per-GPU scans (no reference code; semantics of search.py:129-131: total order

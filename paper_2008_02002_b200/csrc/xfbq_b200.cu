@@ -674,62 +674,16 @@ merge_tree_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k,
 // survivors: when the buffer of B keys could overflow it is sorted, cut back to its k best, and the bound
 // tightens to the k-th of those.  B is a power of two >= k + blockDim.x.  With bound == nullptr the rows must be
 // sorted and the bound comes from the rows themselves (see below).
-// With `src.counts` the partial results are the scan CTAs' candidate lists where they lie (single-wave plans of the queue
-// kernel: CTA part * groups + group holds, for each of its nq_cta queries, src.counts[...] <= cap unsorted keys): the rows
-// have different lengths, entry e of the query maps to (part, slot) through a prefix sum of the lengths.
-struct ListSrc {
-    const int *counts = nullptr;  // [parts * groups][nq_cta]
-    int nq_cta = 0, cap = 0, groups = 0;
-};
-__global__ void __launch_bounds__(512)
-merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k, int B, const int32_t *__restrict__ bound,
-                     const int32_t *__restrict__ qconst, uint64_t *__restrict__ out, const ListSrc src = ListSrc()) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint64_t *buf = reinterpret_cast<uint64_t *>(smem_raw);
+// Block-wide bounded merge: keeps, of `total` keys delivered by fetch(e) (KEY_INF = no key), those with distance <= limit in a
+// shared-memory buffer of B keys (a power of two >= k + blockDim.x), sorts the survivors and writes the k best to dst
+// (KEY_INF padded).  Exact for any number of survivors: when the buffer could overflow it is sorted, cut back to its k best,
+// and the limit tightens to the k-th of those.  Every thread of the block calls it with the same arguments.
+template <class Fetch>
+__device__ void merge_bounded_block(uint64_t *buf, int B, int k, int64_t total, long long limit0, Fetch fetch, uint64_t *dst) {
     __shared__ int s_cnt;
     __shared__ long long s_limit;
-    __shared__ int s_pre[257];  // list mode: entries of the query in parts < i (parts <= 256)
-    const int64_t q = blockIdx.x;
     const int lane = threadIdx.x & 31, nt = blockDim.x;
-    const bool lists = src.counts != nullptr;
-    const int gr = lists ? static_cast<int>(q / src.nq_cta) : 0, ql = lists ? static_cast<int>(q - static_cast<int64_t>(gr) * src.nq_cta) : 0;
-    if (lists) {
-        if (threadIdx.x < 32) {  // warp scan over the parts' list lengths
-            int run = 0;
-            for (int p0 = 0; p0 < parts; p0 += 32) {
-                const int part = p0 + lane;
-                const int c = part < parts ? src.counts[(static_cast<int64_t>(part) * src.groups + gr) * src.nq_cta + ql] : 0;
-                int inc = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int v = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= o) inc += v;
-                }
-                if (part < parts) s_pre[part] = run + inc - c;
-                run += __shfl_sync(0xffffffffu, inc, 31);
-            }
-            if (lane == 0) s_pre[parts] = run;
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        s_cnt = 0;
-        // largest distance that can still be in the top k
-        s_limit = bound ? static_cast<long long>(qconst[q]) - static_cast<long long>(bound[q]) : -1;
-    }
-    if (!bound) {
-        // Sorted rows without a shared threshold (last level of a tree merge): the m-th keys of all rows, m = ceil(k / parts),
-        // bound the answer -- parts * m >= k keys are no larger than the largest of them.
-        __syncthreads();
-        const int m = (k + parts - 1) / parts;
-        long long mine = -1;
-        for (int part = threadIdx.x; part < parts; part += nt) {
-            const uint64_t key = in[(static_cast<int64_t>(part) * nq + q) * k + (m - 1)];
-            const long long d = key == KEY_INF ? 0x7FFFFFFFFFFFFFFFll : static_cast<long long>(key >> 32);
-            mine = d > mine ? d : mine;
-        }
-        atomicMax(&s_limit, mine);
-    }
+    if (threadIdx.x == 0) { s_cnt = 0; s_limit = limit0; }
     auto sort_prefix = [&](int c) {  // ascending sort of buf[0, c), padded to a power of two; ends on a barrier
         int n2 = 32;
         while (n2 < c) n2 <<= 1;
@@ -746,7 +700,6 @@ merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int
                 __syncthreads();
             }
     };
-    const int64_t total = lists ? s_pre[parts] : static_cast<int64_t>(parts) * k;
     for (int64_t e0 = 0; e0 < total; e0 += nt) {
         __syncthreads();
         const int c = s_cnt;
@@ -764,20 +717,7 @@ merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int
         }
         const long long limit = s_limit;
         const int64_t e = e0 + threadIdx.x;
-        uint64_t key = KEY_INF;
-        if (e < total) {
-            if (lists) {
-                int lo = 0, hi = parts;  // largest part with s_pre[part] <= e
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (s_pre[mid] <= static_cast<int>(e)) lo = mid; else hi = mid;
-                }
-                key = __ldcg(in + ((static_cast<int64_t>(lo) * src.groups + gr) * src.nq_cta + ql) * src.cap + (e - s_pre[lo]));
-            } else {
-                const int64_t part = e / k, slot = e - part * k;
-                key = in[(part * nq + q) * k + slot];
-            }
-        }
+        const uint64_t key = e < total ? fetch(e) : KEY_INF;
         const bool keep = key != KEY_INF && static_cast<long long>(key >> 32) <= limit;
         const unsigned m = __ballot_sync(0xffffffffu, keep);
         int base = 0;
@@ -788,14 +728,99 @@ merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int
     __syncthreads();
     const int c = s_cnt;
     sort_prefix(c);
-    uint64_t *dst = out + q * k;
     for (int i = threadIdx.x; i < k; i += nt) dst[i] = i < c ? buf[i] : KEY_INF;
+}
+
+// Block-wide: s_pre[i] = sum of len(j) for j < i, i = 0 .. parts (lists of different lengths, flat entry index ->
+// (list, slot) by binary search).  The lengths are fetched by all threads at once (one L2 round trip instead of one per 32
+// lists), then warp 0 scans them in shared memory.  Ends without a barrier: the caller synchronises.
+template <class Len>
+__device__ void prefix_lengths(int *s_pre, int parts, Len len) {
+    for (int part = threadIdx.x; part < parts; part += blockDim.x) s_pre[part] = len(part);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        int run = 0;
+        for (int p0 = 0; p0 < parts; p0 += 32) {
+            const int part = p0 + lane;
+            const int c = part < parts ? s_pre[part] : 0;
+            int inc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += v;
+            }
+            if (part < parts) s_pre[part] = run + inc - c;
+            run += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) s_pre[parts] = run;
+    }
+}
+__device__ __forceinline__ int find_part(const int *s_pre, int parts, int e) {  // largest part with s_pre[part] <= e
+    int lo = 0, hi = parts;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_pre[mid] <= e) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// With `src.counts` the partial results are the scan CTAs' candidate lists where they lie (single-wave plans of the queue
+// kernel: CTA part * groups + group holds, for each of its nq_cta queries, src.counts[...] <= cap unsorted keys): the rows
+// have different lengths, entry e of the query maps to (part, slot) through a prefix sum of the lengths.
+struct ListSrc {
+    const int *counts = nullptr;  // [parts * groups][nq_cta]
+    int nq_cta = 0, cap = 0, groups = 0;
+};
+__global__ void __launch_bounds__(512)
+merge_bounded_kernel(const uint64_t *__restrict__ in, int parts, int64_t nq, int k, int B, const int32_t *__restrict__ bound,
+                     const int32_t *__restrict__ qconst, uint64_t *__restrict__ out, const ListSrc src = ListSrc()) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t *buf = reinterpret_cast<uint64_t *>(smem_raw);
+    __shared__ long long s_rows_limit;
+    __shared__ int s_pre[257];  // list mode: entries of the query in parts < i (parts <= 256)
+    const int64_t q = blockIdx.x;
+    const int nt = blockDim.x;
+    const bool lists = src.counts != nullptr;
+    const int gr = lists ? static_cast<int>(q / src.nq_cta) : 0, ql = lists ? static_cast<int>(q - static_cast<int64_t>(gr) * src.nq_cta) : 0;
+    if (lists) {
+        prefix_lengths(s_pre, parts, [&](int part) { return src.counts[(static_cast<int64_t>(part) * src.groups + gr) * src.nq_cta + ql]; });
+        __syncthreads();
+    }
+    // largest distance that can still be in the top k
+    long long limit = bound ? static_cast<long long>(qconst[q]) - static_cast<long long>(bound[q]) : -1;
+    if (!bound) {
+        // Sorted rows without a shared threshold (last level of a tree merge): the m-th keys of all rows, m = ceil(k / parts),
+        // bound the answer -- parts * m >= k keys are no larger than the largest of them.
+        if (threadIdx.x == 0) s_rows_limit = -1;
+        __syncthreads();
+        const int m = (k + parts - 1) / parts;
+        long long mine = -1;
+        for (int part = threadIdx.x; part < parts; part += nt) {
+            const uint64_t key = in[(static_cast<int64_t>(part) * nq + q) * k + (m - 1)];
+            const long long d = key == KEY_INF ? 0x7FFFFFFFFFFFFFFFll : static_cast<long long>(key >> 32);
+            mine = d > mine ? d : mine;
+        }
+        atomicMax(&s_rows_limit, mine);
+        __syncthreads();
+        limit = s_rows_limit;
+    }
+    const int64_t total = lists ? s_pre[parts] : static_cast<int64_t>(parts) * k;
+    merge_bounded_block(buf, B, k, total, limit, [&](int64_t e) -> uint64_t {
+        if (lists) {
+            const int part = find_part(s_pre, parts, static_cast<int>(e));
+            return __ldcg(in + ((static_cast<int64_t>(part) * src.groups + gr) * src.nq_cta + ql) * src.cap + (e - s_pre[part]));
+        }
+        const int64_t part = e / k, slot = e - part * k;
+        return in[(part * nq + q) * k + slot];
+    }, out + q * k);
 }
 
 }  // namespace
 #include "xfbq_mma.cuh"
 #include "xfbq_umma.cuh"
 #include "xfbq_select.cuh"
+#include "xfbq_coop.cuh"
 namespace {
 
 __global__ void unpack_keys_kernel(const uint64_t *__restrict__ keys, int64_t count,
@@ -1204,6 +1229,135 @@ int run_mma_scan(const MmaShape &sh, const MmaPlan &pl, unsigned char *ws, const
                         sh.cap > mma::SORT_CAP_MAX);  // large lists are emitted unsorted
 }
 
+
+// ----------------------------------------------------------------------------------------------
+// Single-launch small-batch search (kernel in xfbq_coop.cuh): <= 16 queries, codes that fit a nibble, dim <= 512.
+// ----------------------------------------------------------------------------------------------
+struct CoopPlan {
+    bool ok = false;
+    int C = 1, cap = 0, RR = 0, grid = 0, seed_shift = 0, seed_offset = 0, hist_shift = 0, B = 0;
+    int64_t stages = 0, seed_stride = 1;
+    size_t smem = 0, off_qop = 0, off_qconst = 0, off_shist = 0, off_theta = 0, off_chist = 0, off_counts = 0, off_lists = 0, bytes = 0;
+};
+
+typedef void (*CoopKernel)(const coop::Params);
+CoopKernel pick_coop_kernel(int C) {
+    switch (C) {
+        case 1: return coop::search_kernel<1>;
+        case 2: return coop::search_kernel<2>;
+        case 3: return coop::search_kernel<3>;
+        case 4: return coop::search_kernel<4>;
+    }
+    return nullptr;
+}
+
+int make_coop_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bool have_nibbles, CoopPlan *plan) {
+    CoopPlan pl;
+    *plan = pl;
+    const int C = static_cast<int>(chunks128(dim));
+    const char *eng = getenv("XFBQ_ENGINE");
+    if (eng && *eng && strcmp(eng, "imma") != 0) return XFBQ_OK;  // part of the mma.sync engine
+    if (!have_nibbles || wd > 4 || wq > 7 || C < 1 || C > 4 || k > 1024 || nq < 1 || nq > 16 || n < 1 || env_int("XFBQ_FORCE_GENERIC", 0) ||
+        env_int("XFBQ_COOP", 1) == 0 || env_int("XFBQ_SAMPLE", -1) == 0)
+        return XFBQ_OK;
+    DeviceInfo info;
+    if (int rc = device_info(&info)) return rc;
+    static thread_local int coop_ok = -1;
+    if (coop_ok < 0) {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        coop_ok = (cudaDeviceGetAttribute(&v, cudaDevAttrCooperativeLaunch, dev) == cudaSuccess && v) ? 1 : 0;
+    }
+    if (!coop_ok) return XFBQ_OK;
+    pl.C = C;
+    pl.grid = info.sms > 148 ? 148 : info.sms;
+    if (env_int("XFBQ_GRID", 0) > 0 && env_int("XFBQ_GRID", 0) < pl.grid) pl.grid = env_int("XFBQ_GRID", 0);
+    const int NT = C <= 2 ? 2 : 1, TILE = 8 * NT;
+    const int64_t n_pad = bundles_of(n) * 32;
+    const int64_t sample_tiles = static_cast<int64_t>(pl.grid) * coop::WARPS * coop::SEED_TILES;
+    const int64_t n_tiles = n_pad / TILE;
+    if (n_tiles < 8 * sample_tiles || sample_tiles * TILE < 4 * static_cast<int64_t>(k)) return XFBQ_OK;  // small databases: the multi-launch path
+    pl.seed_stride = n_tiles / sample_tiles;
+    int cap = 64;
+    while (cap < 2 * k) cap <<= 1;
+    pl.cap = cap;
+    const int stage_docs = coop::WARPS * TILE;
+    pl.stages = (n_pad + stage_docs - 1) / stage_docs;
+    if (pl.stages < pl.grid) return XFBQ_OK;
+    const int raw_stage = stage_docs * 64 * C;
+    int B = 8192;
+    while (B < 4 * k) B <<= 1;
+    const size_t budget = static_cast<size_t>(info.smem_optin) - 14 * 1024;  // static shared memory of the kernel (prefix sums, merge state)
+    int RR = env_int("XFBQ_RAW_STAGES", 5);
+    while (RR > 2 && mma::smem_layout(raw_stage, 0, RR, 0, cap, coop::WARPS).total > budget) --RR;
+    if (mma::smem_layout(raw_stage, 0, RR, 0, cap, coop::WARPS).total > budget) return XFBQ_OK;
+    while (B > 1024 && static_cast<size_t>(B) * 8 > static_cast<size_t>(RR) * raw_stage) B >>= 1;  // the merge buffer reuses the raw ring
+    if (B < k + coop::WARPS * 32) return XFBQ_OK;
+    pl.RR = RR; pl.B = B;
+    pl.smem = mma::smem_layout(raw_stage, 0, RR, 0, cap, coop::WARPS).total;
+    // sample histogram: SEED_BINS bins over the whole score range [-R, R]
+    const int64_t R = xfbq_distance_upper_bound(dim, wd, wq);
+    int shift = 0;
+    while (((2 * R) >> shift) >= coop::SEED_BINS) ++shift;
+    pl.seed_shift = shift; pl.seed_offset = static_cast<int>(R);
+    int hs = 0;
+    while ((static_cast<int64_t>(coop::CAND_BINS) << hs) < R / 56) ++hs;
+    pl.hist_shift = env_int("XFBQ_UMMA_HIST_SHIFT", hs);
+    size_t off = 0;
+    pl.off_qop = off; off = align256(off + static_cast<size_t>(4 * C) * 32 * 16);
+    pl.off_qconst = off; off = align256(off + 16 * 4);
+    pl.off_shist = off; off = align256(off + static_cast<size_t>(16) * coop::SEED_BINS * 4);
+    pl.off_theta = off; off = align256(off + 3 * 16 * 4);  // theta_g, theta0, row_bad
+    pl.off_chist = off; off = align256(off + static_cast<size_t>(16) * coop::CAND_BINS * 4);
+    pl.off_counts = off; off = align256(off + static_cast<size_t>(pl.grid) * coop::WARPS * 16 * 4);
+    pl.off_lists = off; off = align256(off + static_cast<size_t>(pl.grid) * coop::WARPS * 16 * cap * 8);
+    pl.bytes = off;
+    pl.ok = true;
+    *plan = pl;
+    return XFBQ_OK;
+}
+
+struct FloatQueries {  // float queries for the fused path (quantized inside the kernel), or all zero
+    const void *x = nullptr;
+    int f64 = 0;
+    int64_t ld = 0;
+    double scale = 1.0;
+    uint64_t *nonfinite = nullptr;
+};
+
+int run_coop(const CoopPlan &cp, unsigned char *ws, const void *nib, int64_t n, int64_t dim, int wd, const uint32_t *q, int64_t nq, int wq,
+             int k, int64_t row_offset, uint64_t *keys_out, cudaStream_t st, const FloatQueries &fq = FloatQueries()) {
+    CoopKernel kern = pick_coop_kernel(cp.C);
+    if (!kern) return fail(XFBQ_E_UNSUPPORTED, "no single-launch kernel for C=%d", cp.C);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cp.smem));
+    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "single-launch search smem opt-in (%zu bytes): %s", cp.smem, cudaGetErrorString(e));
+    coop::Params p;
+    p.nib = nib;
+    p.n = n; p.n_pad = bundles_of(n) * 32; p.row_offset = row_offset;
+    p.q = q; p.nq = static_cast<int>(nq); p.wq = wq; p.wd = wd; p.dim = static_cast<int>(dim);
+    p.xq = fq.x; p.xq_f64 = fq.f64; p.ldq = fq.ld; p.scale = fq.scale;
+    p.nonfinite = reinterpret_cast<unsigned long long *>(fq.nonfinite);
+    p.row_bad = reinterpret_cast<int *>(ws + cp.off_theta) + 32;
+    p.qop = reinterpret_cast<uint32_t *>(ws + cp.off_qop);
+    p.qconst = reinterpret_cast<int32_t *>(ws + cp.off_qconst);
+    p.shist = reinterpret_cast<uint32_t *>(ws + cp.off_shist);
+    p.theta_g = reinterpret_cast<int32_t *>(ws + cp.off_theta);
+    p.theta0 = p.theta_g + 16;
+    p.chist = reinterpret_cast<uint32_t *>(ws + cp.off_chist);
+    p.lists = reinterpret_cast<uint64_t *>(ws + cp.off_lists);
+    p.counts = reinterpret_cast<int *>(ws + cp.off_counts);
+    p.keys_out = keys_out;
+    p.stages = cp.stages; p.seed_tile_stride = cp.seed_stride;
+    p.k = k; p.cap = cp.cap; p.RR = cp.RR;
+    p.seed_shift = cp.seed_shift; p.seed_offset = cp.seed_offset; p.hist_shift = cp.hist_shift; p.merge_B = cp.B;
+    p.prof = g_prof;
+    void *args[] = {&p};
+    if (g_timing) timing_begin(st);
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kern), dim3(static_cast<unsigned>(cp.grid)), dim3(coop::WARPS * 32), args, cp.smem, st);
+    if (g_timing) timing_end(st);
+    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "coop::search_kernel: %s", cudaGetErrorString(e));
+    return check_launch("coop::search_kernel");
+}
 
 // ----------------------------------------------------------------------------------------------
 // tcgen05 engine planning (kernel in xfbq_umma.cuh).
@@ -1946,6 +2100,47 @@ XFBQ_API int xfbq_refine_f32(const float *rows, int64_t n, int64_t dim, int64_t 
     return refine_impl<float>(rows, n, dim, ld, gathered, ids, count, q, k, sims_out, ids_out, ws, ws_bytes, stream);
 }
 
+namespace {
+int search_small_impl(const void *db, const void *nib, int64_t n, int64_t dim, int wd, const void *queries, int f64, int64_t nq, int64_t ld,
+                      double scale, int wq, int k, int64_t row_offset, uint64_t *keys_out, uint64_t *nonfinite, void *workspace,
+                      int64_t workspace_bytes, void *stream) {
+    if (!width_ok(wd) || !width_ok(wq)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d/%d", wd, wq);
+    if (!(scale > 0.0)) return fail(XFBQ_E_INVALID, "scale must be positive, got %g", scale);
+    if (n < 1 || dim < 1 || nq < 1 || ld < dim) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld nq=%lld ld=%lld", (long long)n, (long long)dim, (long long)nq, (long long)ld);
+    if (k < 1) return fail(XFBQ_E_INVALID, "k must be >= 1, got %d", k);
+    if (row_offset < 0 || row_offset + n > (1ll << 32)) return fail(XFBQ_E_UNSUPPORTED, "row ids must fit 32 bits");
+    if (!db || !nib || !queries || !keys_out || !nonfinite || !workspace) return fail(XFBQ_E_INVALID, "null pointer");
+    CoopPlan cp;
+    if (int rc = make_coop_plan(n, dim, wd, nq, wq, k, true, &cp)) return rc;
+    if (!cp.ok) return fail(XFBQ_E_UNSUPPORTED, "no single-launch search for this shape (xfbq_search_small_workspace_bytes returns 0)");
+    if (workspace_bytes < static_cast<int64_t>(cp.bytes))
+        return fail(XFBQ_E_INVALID, "workspace too small: need %zu bytes, got %lld", cp.bytes, (long long)workspace_bytes);
+    FloatQueries fq;
+    fq.x = queries; fq.f64 = f64; fq.ld = ld; fq.scale = scale; fq.nonfinite = nonfinite;
+    return run_coop(cp, static_cast<unsigned char *>(workspace), nib, n, dim, wd, nullptr, nq, wq, k, row_offset, keys_out,
+                    static_cast<cudaStream_t>(stream), fq);
+}
+}  // namespace
+
+XFBQ_API int64_t xfbq_search_small_workspace_bytes(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k) {
+    if (!width_ok(wd) || !width_ok(wq) || n < 1 || dim < 1 || nq < 1 || k < 1 || k > XFBQ_MAX_K) return 0;
+    CoopPlan cp;
+    if (make_coop_plan(n, dim, wd, nq, wq, k, true, &cp) || !cp.ok) return 0;
+    return static_cast<int64_t>(cp.bytes);
+}
+
+XFBQ_API int xfbq_search_small_f32(const void *db, const void *nib, int64_t n, int64_t dim, int wd, const float *queries, int64_t nq, int64_t ld,
+                                   double scale, int wq, int k, int64_t row_offset, uint64_t *keys_out, uint64_t *nonfinite, void *workspace,
+                                   int64_t workspace_bytes, void *stream) {
+    return search_small_impl(db, nib, n, dim, wd, queries, 0, nq, ld, scale, wq, k, row_offset, keys_out, nonfinite, workspace, workspace_bytes, stream);
+}
+
+XFBQ_API int xfbq_search_small_f64(const void *db, const void *nib, int64_t n, int64_t dim, int wd, const double *queries, int64_t nq, int64_t ld,
+                                   double scale, int wq, int k, int64_t row_offset, uint64_t *keys_out, uint64_t *nonfinite, void *workspace,
+                                   int64_t workspace_bytes, void *stream) {
+    return search_small_impl(db, nib, n, dim, wd, queries, 1, nq, ld, scale, wq, k, row_offset, keys_out, nonfinite, workspace, workspace_bytes, stream);
+}
+
 XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, int have_nibbles) {
     if (!width_ok(wd) || !width_ok(wq) || n < 0 || dim < 1 || nq < 0 || k < 1 || k > XFBQ_MAX_K) {
         fail(XFBQ_E_INVALID, "bad scan shape");
@@ -1955,6 +2150,9 @@ XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64
     UmmaPlan up;
     if (make_umma_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &up)) return -1;
     if (up.ok) return static_cast<int64_t>(up.bytes);
+    CoopPlan cp;
+    if (make_coop_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &cp)) return -1;
+    if (cp.ok) return static_cast<int64_t>(cp.bytes);
     MmaPlan mp;
     if (make_mma_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &mp)) return -1;
     if (mp.ok) return static_cast<int64_t>(mp.bytes);
@@ -1972,6 +2170,13 @@ XFBQ_API int xfbq_scan_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, 
     if (up.ok) {  // tcgen05 engine: tile = queries per CTA
         out[0] = 128 * up.main.MT; out[1] = up.main.groups; out[2] = up.main.parts; out[3] = up.main.cap;
         out[4] = 3; out[5] = static_cast<int32_t>(up.main.smem);
+        return XFBQ_OK;
+    }
+    CoopPlan cp;
+    if (int rc = make_coop_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &cp)) return rc;
+    if (cp.ok) {  // mma.sync engine, single-launch search: one 16-query tile, every warp of the grid keeps a list per query
+        out[0] = 16; out[1] = 1; out[2] = cp.grid * coop::WARPS; out[3] = cp.cap;
+        out[4] = 2; out[5] = static_cast<int32_t>(cp.smem);
         return XFBQ_OK;
     }
     MmaPlan mp;
@@ -2013,6 +2218,13 @@ XFBQ_API int xfbq_scan_topk(const void *db, const void *nib, int64_t n, int64_t 
             return fail(XFBQ_E_INVALID, "workspace too small: need %zu bytes, got %lld", up.bytes, (long long)workspace_bytes);
         return run_umma(up, static_cast<unsigned char *>(workspace), static_cast<const unsigned char *>(nib) + nibble_region_bytes(n, dim, wd),
                         n, dim, wd, q, nq, wq, k, row_offset, keys_out, st);
+    }
+    CoopPlan cp;
+    if (int rc = make_coop_plan(n, dim, wd, nq, wq, k, nib != nullptr, &cp)) return rc;
+    if (cp.ok) {
+        if (!workspace || workspace_bytes < static_cast<int64_t>(cp.bytes))
+            return fail(XFBQ_E_INVALID, "workspace too small: need %zu bytes, got %lld", cp.bytes, (long long)workspace_bytes);
+        return run_coop(cp, static_cast<unsigned char *>(workspace), nib, n, dim, wd, q, nq, wq, k, row_offset, keys_out, st);
     }
     MmaPlan mp;
     if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, nib != nullptr, &mp)) return rc;

@@ -58,6 +58,50 @@ class SearchResult:
     stage_seconds: dict | None = field(default=None, compare=False)
 
 
+_WORKSPACES = {}   # (device index, stream) -> uint8 tensor, grown on demand: scans on one stream are ordered, so they can share it
+_NONFINITE = {}    # device index -> int64[1] counter of non-finite query values seen by the fused small-batch kernel
+
+
+def _workspace(torch, dev, nbytes: int):
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    ws = _WORKSPACES.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=dev)
+        _WORKSPACES[key] = ws
+    return ws
+
+
+def _search_small_fused(index: Index, queries, k: int, row_offset: int):
+    """<= 16 float queries resident on the index's GPU: quantizer, threshold seeding, scan and merge in ONE cooperative launch
+    (xfbq_search_small_*).  Returns (keys, counter of non-finite query values) or None when the shape takes the general path."""
+    torch = _native.require_cuda()
+    L = _native.lib()
+    packed, p = index.packed, index.params
+    nq = int(queries.shape[0])
+    if not 1 <= nq <= 16 or packed.width > 4 or p.query_bits > 7 or packed.dim > 512 or k > 1024:
+        return None
+    dev = packed.codes.device
+    ws_bytes = int(L.xfbq_search_small_workspace_bytes(packed.count, packed.dim, packed.width, nq, p.query_bits, k))
+    if ws_bytes <= 0:
+        return None
+    if queries.dtype not in (torch.float32, torch.float64):
+        queries = queries.to(torch.float64)
+    if queries.stride(-1) != 1 or queries.device != dev:
+        queries = queries.to(dev).contiguous()
+    nib = packed.nibbles
+    counter = _NONFINITE.get(dev.index)
+    if counter is None:
+        counter = _NONFINITE[dev.index] = torch.zeros(1, dtype=torch.int64, device=dev)
+    keys = torch.empty((nq, k), dtype=torch.int64, device=dev)
+    ws = _workspace(torch, dev, ws_bytes)
+    fn = L.xfbq_search_small_f32 if queries.dtype == torch.float32 else L.xfbq_search_small_f64
+    ld = queries.stride(0) if nq > 1 else packed.dim
+    _native.check(fn(packed.codes.data_ptr(), nib.data_ptr(), packed.count, packed.dim, packed.width, queries.data_ptr(), nq, ld,
+                     float(p.scale), p.query_bits, k, int(row_offset), keys.data_ptr(), counter.data_ptr(), ws.data_ptr(), ws.numel(),
+                     _stream_ptr(torch)))
+    return keys, counter
+
+
 def scan_topk_device(packed: PackedMatrix, qwords, nq: int, query_bits: int, k: int, row_offset: int = 0):
     """Launch the fused scan+top-K on device-resident query words (query layout).
     Returns an int64 CUDA tensor [nq, k] holding the uint64 keys bit-for-bit
@@ -92,18 +136,17 @@ def scan_topk_device(packed: PackedMatrix, qwords, nq: int, query_bits: int, k: 
                                                        1 if nib is not None else 0))
             if ws_bytes < 0:
                 _native.check(_native.E_INVALID)
-            ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
+            ws = _workspace(torch, dev, max(ws_bytes, 16))
             qptr = qwords.data_ptr() + q0 * words_per_query * 4
             if SCAN_EVENTS is not None:
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 ev[0].record()
             _native.check(L.xfbq_scan_topk(packed.codes.data_ptr(), nib_ptr, packed.count, packed.dim, packed.width,
                                            qptr, qn, query_bits, k, int(row_offset),
-                                           keys.data_ptr() + q0 * k * 8, ws.data_ptr(), ws_bytes, st))
+                                           keys.data_ptr() + q0 * k * 8, ws.data_ptr(), ws.numel(), st))
             if SCAN_EVENTS is not None:
                 ev[1].record()
                 SCAN_EVENTS.append(ev)
-            # ws is stream-ordered: the caching allocator reuses it only on this stream
     return keys
 
 
@@ -126,9 +169,14 @@ def _check_queries(index: Index, queries):
         raise DimensionMismatchError(f"query dim {queries.shape[1]} != index dim {index.params.dim}")
 
 
-def search_device(index: Index, queries, k: int, row_offset: int = 0):
+def search_device(index: Index, queries, k: int, row_offset: int = 0, check: bool = True):
     """Batched search returning device tensors (keys int64 [nq, min(k, n)]).
-    `queries`: host array or CUDA tensor (nq, dim), float32/float64."""
+    `queries`: host array or CUDA tensor (nq, dim), float32/float64.
+
+    Non-finite queries raise InvalidInputError like the reference (quant.py:142-143).  Reading the quantizer's counter is a
+    stream synchronisation; `check=False` skips it for asynchronous pipelines of small device-resident batches (the fused
+    single-launch path): a query holding a non-finite value then comes back as empty keys (all ones) and
+    `pending_nonfinite()` reports it at the caller's next synchronisation point."""
     if k < 1:
         raise InvalidInputError(f"k must be >= 1, got {k}")
     if not _is_torch(queries):
@@ -139,10 +187,24 @@ def search_device(index: Index, queries, k: int, row_offset: int = 0):
     p = index.params
     kk = min(int(k), index.n)
     torch = _native.require_cuda()
-    with torch.cuda.device(index.packed.codes.device):
+    dev = index.packed.codes.device
+    with torch.cuda.device(dev):
         if kk == 0 or queries.shape[0] == 0:
-            return torch.empty((queries.shape[0], kk), dtype=torch.int64, device=index.packed.codes.device)
-        if _is_torch(queries) and queries.is_cuda:
+            return torch.empty((queries.shape[0], kk), dtype=torch.int64, device=dev)
+        on_device = _is_torch(queries) and queries.is_cuda
+        if queries.shape[0] <= 16:
+            # small batches: one cooperative launch from the float queries (host queries are copied first)
+            qt = queries
+            if not on_device:
+                qt = torch.from_numpy(np.ascontiguousarray(queries)) if not _is_torch(queries) else queries
+                qt = qt.to(dev, non_blocking=qt.is_pinned())
+            fused = _search_small_fused(index, qt, kk, row_offset)
+            if fused is not None:
+                keys, counter = fused
+                if check or not on_device:
+                    raise_pending_nonfinite(dev)
+                return keys
+        if on_device:
             # device-resident queries: the counter is read right after the quantizer, the scan runs asynchronously
             # (back-to-back searches overlap their launches with the previous scan: 358 vs 396 us per single query)
             qwords = quantize_queries(queries, p.query_bits, p.scale)
@@ -155,6 +217,23 @@ def search_device(index: Index, queries, k: int, row_offset: int = 0):
         if int(bad.item()):
             raise InvalidInputError("cannot quantize non-finite values")
         return keys
+
+
+def pending_nonfinite(device=None) -> int:
+    """Non-finite query values the fused small-batch searches on `device` have met since the last check (synchronises)."""
+    torch = _native.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    counter = _NONFINITE.get(dev.index if dev.index is not None else torch.cuda.current_device())
+    return int(counter.item()) if counter is not None else 0
+
+
+def raise_pending_nonfinite(device=None) -> None:
+    """Raise InvalidInputError (and clear the counter) if a fused small-batch search on `device` met a non-finite query."""
+    if pending_nonfinite(device):
+        torch = _native.require_cuda()
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        _NONFINITE[dev.index if dev.index is not None else torch.cuda.current_device()].zero_()
+        raise InvalidInputError("cannot quantize non-finite values")
 
 
 def search(index: Index, queries, k: int):

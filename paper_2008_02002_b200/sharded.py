@@ -65,7 +65,9 @@ def choose_query_shards(world: int, n: int, dim: int, doc_bits: int, nq_hint: in
 
 def _cuda_scan(index: Index, queries, k: int, row_offset: int):
     from .search import search_device
-    return search_device(index, queries, k, row_offset=row_offset)
+    # device-resident queries stay asynchronous (search_keys is the pipeline entry point): a non-finite query comes back as
+    # empty keys and search.pending_nonfinite() reports it; ShardedIndex.search() -- host results -- raises
+    return search_device(index, queries, k, row_offset=row_offset, check=False)
 
 
 def _cuda_merge(stacked, k: int):
@@ -155,7 +157,8 @@ class ShardedIndex:
         if not keys.is_cuda:  # CPU hooks (tests/test_sharded_gloo.py): unpack on the host
             kn = keys.contiguous().numpy().view(np.uint64)
             return (kn >> np.uint64(32)).astype(np.int64), (kn & np.uint64(0xFFFFFFFF)).astype(np.int64)
-        from .search import to_host_arrays, unpack_keys_device
+        from .search import raise_pending_nonfinite, to_host_arrays, unpack_keys_device
         d, i = unpack_keys_device(keys.contiguous())  # empty slots come back as -1
         d, i = to_host_arrays(d, i)
+        raise_pending_nonfinite(keys.device)
         return d, i
