@@ -53,6 +53,10 @@ def test_sass_has_the_expected_instructions():
     assert "sm_100a" in sass
     for mnemonic in ("POPC", "LOP3", "LDG.E.128", "VOTE"):
         assert mnemonic in sass, mnemonic
+    # the Blackwell-native path: tcgen05.mma kind::i8 (UTCIMMA), tensor-memory loads / stores (LDTM / STTM), TMA bulk copies
+    # (UBLKCP), tcgen05.commit (UTCBAR), mbarrier waits (SYNCS), mma.sync int8 for small batches (IMMA.16832)
+    for mnemonic in ("UTCIMMA", "LDTM", "STTM", "UBLKCP", "UTCBAR", "SYNCS.PHASECHK", "IMMA.16832.S8.U8"):
+        assert mnemonic in sass, mnemonic
 
 
 def test_argument_errors_match_reference_classes():
