@@ -19,7 +19,7 @@ for line in sass.splitlines():
         cur = m.group(1)
         per[cur] = collections.Counter()
         continue
-    m = re.search(r"/\*[0-9a-f]{4}\*/\s+(?:@!?U?P\d\s+)?([A-Z0-9_.]+)", line)
+    m = re.search(r"/\*[0-9a-f]{4,6}\*/\s+(?:@!?U?P\d\s+)?([A-Z0-9_.]+)", line)
     if m and cur:
         op = m.group(1)
         per[cur]["_total"] += 1
