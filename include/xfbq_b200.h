@@ -105,6 +105,18 @@ int xfbq_bundles_to_planes(const void *db_dev, int64_t n, int64_t dim, int width
  *                   by one cp.async.bulk per tile (streamed by the tcgen05 engine: >= 32 queries).
  * The tile region starts at the nibble region's size rounded up to 1024 bytes.
  */
+/* The two layouts can also be built and passed separately (a batch server needs only the tiles: 2x the packed size for 4-bit
+ * codes; a low-latency server only the nibbles: 1x): */
+#define XFBQ_LAYOUT_NIBBLES 2
+#define XFBQ_LAYOUT_TILES 4
+int64_t xfbq_nibble_region_bytes(int64_t n, int64_t dim, int width);  /* 0 when the mma.sync engine does not take the shape */
+int64_t xfbq_tile_region_bytes(int64_t n, int64_t dim);               /* 0 for dim > 1024 */
+int xfbq_build_nibbles(const void *db_dev, int64_t n, int64_t dim, int width, void *nibbles_out_dev, void *stream);
+int xfbq_build_tiles(const void *db_dev, int64_t n, int64_t dim, int width, void *tiles_out_dev, void *stream);
+/* Which layout the preferred plan of a scan reads: XFBQ_LAYOUT_TILES (tcgen05 engine), XFBQ_LAYOUT_NIBBLES (mma.sync engine /
+ * single-launch search) or 0 (XOR/POPC kernels on the bit planes). */
+int xfbq_scan_layouts(int64_t n, int64_t dim, int doc_bits, int64_t nq, int query_bits, int k);
+/* Both in one buffer, [nibble layout][byte tiles] (ABI revision 1): */
 int64_t xfbq_derived_bytes(int64_t n, int64_t dim, int width);  /* width > 4: byte tiles only (no nibble region) */
 int xfbq_build_derived(const void *db_dev, int64_t n, int64_t dim, int width, void *derived_out_dev, void *stream);
 /* the same for width <= 4 (kept for callers of ABI revision 1) */
@@ -182,6 +194,11 @@ int xfbq_scan_topk(const void *db_dev, const void *nibbles_dev, int64_t n, int64
                    const uint32_t *q_dev, int64_t nq, int query_bits, int k, int64_t row_offset,
                    uint64_t *keys_out_dev, void *workspace_dev, int64_t workspace_bytes,
                    void *stream);
+/* The same with the two derived layouts passed separately (either may be NULL; the `have_nibbles` argument of
+ * xfbq_scan_workspace_bytes / xfbq_scan_plan is then XFBQ_LAYOUT_NIBBLES | XFBQ_LAYOUT_TILES as available; 1 = both). */
+int xfbq_scan_topk_layouts(const void *db_dev, const void *nibbles_dev, const void *tiles_dev, int64_t n, int64_t dim, int doc_bits,
+                           const uint32_t *q_dev, int64_t nq, int query_bits, int k, int64_t row_offset,
+                           uint64_t *keys_out_dev, void *workspace_dev, int64_t workspace_bytes, void *stream);
 
 /*
  * Single-launch search for small batches (1 <= nq <= 16, doc_bits <= 4, query_bits <= 7, dim <= 512, k <= 1024, databases of

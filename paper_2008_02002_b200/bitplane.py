@@ -167,24 +167,46 @@ class PackedMatrix:
             self._planes = host
         return self._planes
 
-    @property
-    def nibbles(self):
-        """Derived layouts of the codes for the tensor-core scans, built on the GPU on first use and cached: the nibble
-        layout (doc_bits <= 4: mma.sync engine, <= 16 queries) followed by the byte tiles (any width: tcgen05 engine);
-        None when the dimension has no tensor path (dim > 1024)."""
-        if self._count == 0 or self._dim > 1024:
-            return None
-        cached = getattr(self, "_nibbles", None)
+    def _layout(self, attr: str, size_fn: str, build_fn: str, size_args):
+        cached = getattr(self, attr, None)
         if cached is None:
             torch = _native.require_cuda()
             L = _native.lib()
+            nbytes = int(getattr(L, size_fn)(*size_args))
+            if nbytes == 0 or self._count == 0:
+                return None
             with torch.cuda.device(self._codes.device):
-                cached = torch.empty(int(L.xfbq_derived_bytes(self._count, self._dim, self._width)), dtype=torch.uint8,
-                                     device=self._codes.device)
-                _native.check(L.xfbq_build_derived(self._codes.data_ptr(), self._count, self._dim, self._width,
+                cached = torch.empty(nbytes, dtype=torch.uint8, device=self._codes.device)
+                _native.check(getattr(L, build_fn)(self._codes.data_ptr(), self._count, self._dim, self._width,
                                                    cached.data_ptr(), _stream_ptr(torch)))
-            self._nibbles = cached
+            setattr(self, attr, cached)
         return cached
+
+    @property
+    def nibble_layout(self):
+        """Derived row-major 4-bit copy of the codes (doc_bits <= 4, dim <= 512): what the mma.sync engine and the
+        single-launch small-batch search stream (<= 16 queries, HBM-bound).  Built on the GPU on first use, cached; the
+        same size as the packed codes for 4-bit codes.  None for shapes that engine does not take."""
+        return self._layout("_nibbles", "xfbq_nibble_region_bytes", "xfbq_build_nibbles", (self._count, self._dim, self._width))
+
+    @property
+    def tile_layout(self):
+        """Derived byte tiles (one code per byte, the shared-memory image of a tcgen05 B operand; dim <= 1024): what the
+        tcgen05 engine streams (>= 17 queries).  Built on first use, cached; twice the packed size for 4-bit codes."""
+        return self._layout("_tiles", "xfbq_tile_region_bytes", "xfbq_build_tiles", (self._count, self._dim))
+
+    @property
+    def derived_nbytes(self) -> dict:
+        """Bytes of the derived layouts built so far (a server that only answers large batches never builds the nibbles,
+        one that only answers single queries never builds the tiles)."""
+        return {name: int(t.numel()) if t is not None else 0
+                for name, t in (("nibbles", getattr(self, "_nibbles", None)), ("tiles", getattr(self, "_tiles", None)))}
+
+    def release_layout(self, name: str) -> None:
+        """Free a derived layout ("nibbles" or "tiles"); it is rebuilt if a later search needs it."""
+        if name not in ("nibbles", "tiles"):
+            raise InvalidInputError("layout must be 'nibbles' or 'tiles'")
+        setattr(self, "_" + name, None)
 
     def row(self, k: int) -> PackedVector:
         return PackedVector(np.ascontiguousarray(self.planes[:, :, k]), self._dim)

@@ -1145,7 +1145,7 @@ int run_counted_seed(unsigned char *ws, const void *tiles, int64_t n, int64_t di
                      int k, int64_t sample, bool prep, size_t off_qimg, size_t off_qconst, size_t off_par, size_t off_hist,
                      int32_t *tau, cudaStream_t st);
 
-int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bool have_nibbles, MmaPlan *plan) {
+int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bool have_nibbles, MmaPlan *plan, bool have_tiles = true) {
     MmaPlan pl;
     const int C = static_cast<int>(chunks128(dim));
     const char *eng = getenv("XFBQ_ENGINE");
@@ -1172,7 +1172,7 @@ int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, boo
     // of the sample scan floods from an open threshold -- so only small batches use it.)
     if (sample < 0) sample = pl.main.groups == 1 ? (nq <= 4 ? 32768 : 65536) : 131072;
     if (sample > 0 && (n < 16 * sample || sample < 4 * k)) sample = 0;
-    pl.count = sample > 0 && env_int("XFBQ_SEED_HIST", 1) != 0;
+    pl.count = sample > 0 && have_tiles && env_int("XFBQ_SEED_HIST", 1) != 0;  // the counting seed reads byte tiles
     if (pl.count && sample > umma::SEED_MAX_SAMPLE(C)) sample = umma::SEED_MAX_SAMPLE(C);
     pl.sample = sample;
     if (sample && !pl.count) mma_shape(sample, wd, C, nq, k, info, &pl.pre);
@@ -1901,30 +1901,44 @@ inline int64_t tile_count(int64_t n) { return (n + umma::STAGE_DOCS - 1) / umma:
 inline bool tiles_supported(int64_t dim) { const int64_t C = chunks128(dim); return C >= 1 && C <= 8; }
 
 XFBQ_API int64_t xfbq_derived_bytes(int64_t n, int64_t dim, int width) {
-    return nibble_region_bytes(n, dim, width) + (tiles_supported(dim) ? tile_count(n) * umma::STAGE_DOCS * tile_geom(dim).CT * 128 : 0);
+    return nibble_region_bytes(n, dim, width) + xfbq_tile_region_bytes(n, dim);
 }
 XFBQ_API int64_t xfbq_nibble_bytes(int64_t n, int64_t dim) { return xfbq_derived_bytes(n, dim, 4); }
 
-XFBQ_API int xfbq_build_derived(const void *db, int64_t n, int64_t dim, int width, void *out, void *stream) {
+XFBQ_API int64_t xfbq_nibble_region_bytes(int64_t n, int64_t dim, int width) { return nibble_region_bytes(n, dim, width); }
+XFBQ_API int64_t xfbq_tile_region_bytes(int64_t n, int64_t dim) {
+    return tiles_supported(dim) ? tile_count(n) * umma::STAGE_DOCS * tile_geom(dim).CT * 128 : 0;
+}
+
+XFBQ_API int xfbq_build_nibbles(const void *db, int64_t n, int64_t dim, int width, void *out, void *stream) {
     if (!width_ok(width)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d", width);
     if (n < 0 || dim < 1) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld", (long long)n, (long long)dim);
-    if (n == 0) return XFBQ_OK;
+    if (n == 0 || nibble_region_bytes(n, dim, width) == 0) return XFBQ_OK;
     if (!db || !out) return fail(XFBQ_E_INVALID, "null pointer");
     const int C = static_cast<int>(chunks128(dim));
+    const int64_t n_pad = bundles_of(n) * 32, total = n_pad * 4 * C;
+    mma::planes_to_nibbles_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint32_t *>(db), n_pad, width, C, static_cast<uint4 *>(out));
+    return check_launch("planes_to_nibbles_kernel");
+}
+
+XFBQ_API int xfbq_build_tiles(const void *db, int64_t n, int64_t dim, int width, void *out, void *stream) {
+    if (!width_ok(width)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d", width);
+    if (n < 0 || dim < 1) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld", (long long)n, (long long)dim);
+    if (n == 0 || !tiles_supported(dim)) return XFBQ_OK;
+    if (!db || !out) return fail(XFBQ_E_INVALID, "null pointer");
+    const int C = static_cast<int>(chunks128(dim)), CT = tile_geom(dim).CT;
     const int64_t n_pad = bundles_of(n) * 32;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (nibble_region_bytes(n, dim, width) > 0) {
-        const int64_t total = n_pad * 4 * C;
-        mma::planes_to_nibbles_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
-            static_cast<const uint32_t *>(db), n_pad, width, C, static_cast<uint4 *>(out));
-        if (int rc = check_launch("planes_to_nibbles_kernel")) return rc;
-    }
-    if (!tiles_supported(dim)) return XFBQ_OK;
-    const int CT = tile_geom(dim).CT;
     const int64_t tiles = tile_count(n), groups = tiles * umma::STAGE_DOCS * 4 * CT;
-    umma::planes_to_tiles_kernel<<<static_cast<unsigned>((groups + 255) / 256), 256, 0, st>>>(
-        static_cast<const uint32_t *>(db), n_pad, tiles, width, C, CT, static_cast<unsigned char *>(out) + nibble_region_bytes(n, dim, width));
+    umma::planes_to_tiles_kernel<<<static_cast<unsigned>((groups + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint32_t *>(db), n_pad, tiles, width, C, CT, static_cast<unsigned char *>(out));
     return check_launch("planes_to_tiles_kernel");
+}
+
+XFBQ_API int xfbq_build_derived(const void *db, int64_t n, int64_t dim, int width, void *out, void *stream) {
+    if (int rc = xfbq_build_nibbles(db, n, dim, width, out, stream)) return rc;
+    if (n <= 0 || dim < 1 || !out) return XFBQ_OK;
+    return xfbq_build_tiles(db, n, dim, width, static_cast<unsigned char *>(out) + nibble_region_bytes(n, dim, width), stream);
 }
 
 XFBQ_API int xfbq_planes_to_nibbles(const void *db, int64_t n, int64_t dim, int width, void *nib_out, void *stream) {
@@ -2141,6 +2155,24 @@ XFBQ_API int xfbq_search_small_f64(const void *db, const void *nib, int64_t n, i
     return search_small_impl(db, nib, n, dim, wd, queries, 1, nq, ld, scale, wq, k, row_offset, keys_out, nonfinite, workspace, workspace_bytes, stream);
 }
 
+namespace {
+// `layouts` argument of the planning calls: 0 = no derived layout, XFBQ_LAYOUT_NIBBLES | XFBQ_LAYOUT_TILES, or 1 = both
+// (the single derived buffer of ABI revision 1)
+inline bool flag_nib(int layouts) { return (layouts & 1) || (layouts & XFBQ_LAYOUT_NIBBLES); }
+inline bool flag_tiles(int layouts) { return (layouts & 1) || (layouts & XFBQ_LAYOUT_TILES); }
+}  // namespace
+
+XFBQ_API int xfbq_scan_layouts(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k) {
+    if (!width_ok(wd) || !width_ok(wq) || n < 1 || dim < 1 || nq < 1 || k < 1 || k > XFBQ_MAX_K) return 0;
+    UmmaPlan up;
+    if (make_umma_plan(n, dim, wd, nq, wq, k, true, &up) == XFBQ_OK && up.ok) return XFBQ_LAYOUT_TILES;
+    CoopPlan cp;
+    if (make_coop_plan(n, dim, wd, nq, wq, k, true, &cp) == XFBQ_OK && cp.ok) return XFBQ_LAYOUT_NIBBLES;
+    MmaPlan mp;
+    if (make_mma_plan(n, dim, wd, nq, wq, k, true, &mp) == XFBQ_OK && mp.ok) return XFBQ_LAYOUT_NIBBLES;
+    return 0;
+}
+
 XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, int have_nibbles) {
     if (!width_ok(wd) || !width_ok(wq) || n < 0 || dim < 1 || nq < 0 || k < 1 || k > XFBQ_MAX_K) {
         fail(XFBQ_E_INVALID, "bad scan shape");
@@ -2148,13 +2180,13 @@ XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64
     }
     if (n == 0 || nq == 0) return 0;
     UmmaPlan up;
-    if (make_umma_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &up)) return -1;
+    if (make_umma_plan(n, dim, wd, nq, wq, k, flag_tiles(have_nibbles), &up)) return -1;
     if (up.ok) return static_cast<int64_t>(up.bytes);
     CoopPlan cp;
-    if (make_coop_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &cp)) return -1;
+    if (make_coop_plan(n, dim, wd, nq, wq, k, flag_nib(have_nibbles), &cp)) return -1;
     if (cp.ok) return static_cast<int64_t>(cp.bytes);
     MmaPlan mp;
-    if (make_mma_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &mp)) return -1;
+    if (make_mma_plan(n, dim, wd, nq, wq, k, flag_nib(have_nibbles), &mp, flag_tiles(have_nibbles))) return -1;
     if (mp.ok) return static_cast<int64_t>(mp.bytes);
     ScanPlan pl;
     if (make_plan(n, dim, wd, nq, wq, k, &pl)) return -1;
@@ -2166,21 +2198,21 @@ XFBQ_API int xfbq_scan_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, 
     if (!width_ok(wd) || !width_ok(wq) || n < 1 || dim < 1 || nq < 1 || k < 1 || k > XFBQ_MAX_K || !out)
         return fail(XFBQ_E_INVALID, "bad scan shape");
     UmmaPlan up;
-    if (int rc = make_umma_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &up)) return rc;
+    if (int rc = make_umma_plan(n, dim, wd, nq, wq, k, flag_tiles(have_nibbles), &up)) return rc;
     if (up.ok) {  // tcgen05 engine: tile = queries per CTA
         out[0] = 128 * up.main.MT; out[1] = up.main.groups; out[2] = up.main.parts; out[3] = up.main.cap;
         out[4] = 3; out[5] = static_cast<int32_t>(up.main.smem);
         return XFBQ_OK;
     }
     CoopPlan cp;
-    if (int rc = make_coop_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &cp)) return rc;
+    if (int rc = make_coop_plan(n, dim, wd, nq, wq, k, flag_nib(have_nibbles), &cp)) return rc;
     if (cp.ok) {  // mma.sync engine, single-launch search: one 16-query tile, every warp of the grid keeps a list per query
         out[0] = 16; out[1] = 1; out[2] = cp.grid * coop::WARPS; out[3] = cp.cap;
         out[4] = 2; out[5] = static_cast<int32_t>(cp.smem);
         return XFBQ_OK;
     }
     MmaPlan mp;
-    if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, have_nibbles != 0, &mp)) return rc;
+    if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, flag_nib(have_nibbles), &mp, flag_tiles(have_nibbles))) return rc;
     if (mp.ok) {  // integer-MMA engine: tile = queries per CTA
         out[0] = mp.main.QW * mp.main.QPW; out[1] = mp.main.groups; out[2] = mp.main.parts; out[3] = mp.main.cap;
         out[4] = 2; out[5] = static_cast<int32_t>(mp.main.smem);
@@ -2193,9 +2225,21 @@ XFBQ_API int xfbq_scan_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, 
     return XFBQ_OK;
 }
 
-XFBQ_API int xfbq_scan_topk(const void *db, const void *nib, int64_t n, int64_t dim, int wd, const uint32_t *q, int64_t nq,
+XFBQ_API int xfbq_scan_topk(const void *db, const void *derived, int64_t n, int64_t dim, int wd, const uint32_t *q, int64_t nq,
                             int wq, int k, int64_t row_offset, uint64_t *keys_out, void *workspace,
                             int64_t workspace_bytes, void *stream) {
+    // ABI revision 1: one derived buffer [nibble layout][byte tiles]
+    const void *nib = nullptr, *tiles = nullptr;
+    if (derived && n > 0 && dim >= 1 && width_ok(wd)) {
+        if (nibble_region_bytes(n, dim, wd) > 0) nib = derived;
+        if (tiles_supported(dim)) tiles = static_cast<const unsigned char *>(derived) + nibble_region_bytes(n, dim, wd);
+    }
+    return xfbq_scan_topk_layouts(db, nib, tiles, n, dim, wd, q, nq, wq, k, row_offset, keys_out, workspace, workspace_bytes, stream);
+}
+
+XFBQ_API int xfbq_scan_topk_layouts(const void *db, const void *nib, const void *tiles, int64_t n, int64_t dim, int wd, const uint32_t *q,
+                                    int64_t nq, int wq, int k, int64_t row_offset, uint64_t *keys_out, void *workspace,
+                                    int64_t workspace_bytes, void *stream) {
     if (!width_ok(wd) || !width_ok(wq)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d/%d", wd, wq);
     if (n < 0 || dim < 1 || nq < 0) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld nq=%lld", (long long)n, (long long)dim, (long long)nq);
     if (k < 1) return fail(XFBQ_E_INVALID, "k must be >= 1, got %d", k);
@@ -2212,12 +2256,11 @@ XFBQ_API int xfbq_scan_topk(const void *db, const void *nib, int64_t n, int64_t 
     }
     if (!db || !q) return fail(XFBQ_E_INVALID, "null pointer");
     UmmaPlan up;
-    if (int rc = make_umma_plan(n, dim, wd, nq, wq, k, nib != nullptr, &up)) return rc;
+    if (int rc = make_umma_plan(n, dim, wd, nq, wq, k, tiles != nullptr, &up)) return rc;
     if (up.ok) {
         if (!workspace || workspace_bytes < static_cast<int64_t>(up.bytes))
             return fail(XFBQ_E_INVALID, "workspace too small: need %zu bytes, got %lld", up.bytes, (long long)workspace_bytes);
-        return run_umma(up, static_cast<unsigned char *>(workspace), static_cast<const unsigned char *>(nib) + nibble_region_bytes(n, dim, wd),
-                        n, dim, wd, q, nq, wq, k, row_offset, keys_out, st);
+        return run_umma(up, static_cast<unsigned char *>(workspace), tiles, n, dim, wd, q, nq, wq, k, row_offset, keys_out, st);
     }
     CoopPlan cp;
     if (int rc = make_coop_plan(n, dim, wd, nq, wq, k, nib != nullptr, &cp)) return rc;
@@ -2227,7 +2270,7 @@ XFBQ_API int xfbq_scan_topk(const void *db, const void *nib, int64_t n, int64_t 
         return run_coop(cp, static_cast<unsigned char *>(workspace), nib, n, dim, wd, q, nq, wq, k, row_offset, keys_out, st);
     }
     MmaPlan mp;
-    if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, nib != nullptr, &mp)) return rc;
+    if (int rc = make_mma_plan(n, dim, wd, nq, wq, k, nib != nullptr, &mp, tiles != nullptr)) return rc;
     if (mp.ok) {
         if (!workspace || workspace_bytes < static_cast<int64_t>(mp.bytes))
             return fail(XFBQ_E_INVALID, "workspace too small: need %zu bytes, got %lld", mp.bytes, (long long)workspace_bytes);
@@ -2241,7 +2284,7 @@ XFBQ_API int xfbq_scan_topk(const void *db, const void *nib, int64_t n, int64_t 
         const int32_t *tau_init = nullptr;
         if (mp.sample && mp.count) {
             int32_t *tau = reinterpret_cast<int32_t *>(ws + mp.off_tau);
-            if (int rc = run_counted_seed(ws, static_cast<const unsigned char *>(nib) + nibble_region_bytes(n, dim), n, dim, wd, q, nq, wq, k, mp.sample,
+            if (int rc = run_counted_seed(ws, tiles, n, dim, wd, q, nq, wq, k, mp.sample,
                                           true, mp.off_uqimg, mp.off_uqconst, mp.off_seedpar, mp.off_seedhist, tau, st)) return rc;
             tau_init = tau;
         } else if (mp.sample) {

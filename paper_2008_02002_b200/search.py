@@ -88,7 +88,9 @@ def _search_small_fused(index: Index, queries, k: int, row_offset: int):
         queries = queries.to(torch.float64)
     if queries.stride(-1) != 1 or queries.device != dev:
         queries = queries.to(dev).contiguous()
-    nib = packed.nibbles
+    nib = packed.nibble_layout
+    if nib is None:
+        return None
     counter = _NONFINITE.get(dev.index)
     if counter is None:
         counter = _NONFINITE[dev.index] = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -127,13 +129,15 @@ def scan_topk_device(packed: PackedMatrix, qwords, nq: int, query_bits: int, k: 
                                                      qwords.data_ptr() + qi * words_per_query * 4, query_bits, d.data_ptr(), st))
                 keys[qi] = torch.sort((d << 32) | ids).values[:k]
             return keys
-        # derived layouts only where a tensor engine will read them (dim <= 1024): other shapes take the POPC kernels
-        nib = packed.nibbles if query_bits <= 7 and k <= 1024 and C <= 8 else None
-        nib_ptr = nib.data_ptr() if nib is not None else None
         for q0 in range(0, nq, _QUERY_BATCH):
             qn = min(_QUERY_BATCH, nq - q0)
-            ws_bytes = int(L.xfbq_scan_workspace_bytes(packed.count, packed.dim, packed.width, qn, query_bits, k,
-                                                       1 if nib is not None else 0))
+            # the derived layout the preferred plan reads is built on first use (tiles: tcgen05 engine; nibbles: mma.sync
+            # engine); one that already exists is passed along too (the mma.sync path seeds its thresholds from tiles)
+            want = int(L.xfbq_scan_layouts(packed.count, packed.dim, packed.width, qn, query_bits, k))
+            nib = packed.nibble_layout if want & 2 else getattr(packed, "_nibbles", None)
+            tiles = packed.tile_layout if want & 4 else getattr(packed, "_tiles", None)
+            have = (2 if nib is not None else 0) | (4 if tiles is not None else 0)
+            ws_bytes = int(L.xfbq_scan_workspace_bytes(packed.count, packed.dim, packed.width, qn, query_bits, k, have))
             if ws_bytes < 0:
                 _native.check(_native.E_INVALID)
             ws = _workspace(torch, dev, max(ws_bytes, 16))
@@ -141,9 +145,10 @@ def scan_topk_device(packed: PackedMatrix, qwords, nq: int, query_bits: int, k: 
             if SCAN_EVENTS is not None:
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 ev[0].record()
-            _native.check(L.xfbq_scan_topk(packed.codes.data_ptr(), nib_ptr, packed.count, packed.dim, packed.width,
-                                           qptr, qn, query_bits, k, int(row_offset),
-                                           keys.data_ptr() + q0 * k * 8, ws.data_ptr(), ws.numel(), st))
+            _native.check(L.xfbq_scan_topk_layouts(packed.codes.data_ptr(), nib.data_ptr() if nib is not None else None,
+                                                   tiles.data_ptr() if tiles is not None else None, packed.count, packed.dim,
+                                                   packed.width, qptr, qn, query_bits, k, int(row_offset),
+                                                   keys.data_ptr() + q0 * k * 8, ws.data_ptr(), ws.numel(), st))
             if SCAN_EVENTS is not None:
                 ev[1].record()
                 SCAN_EVENTS.append(ev)

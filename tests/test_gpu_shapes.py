@@ -116,3 +116,38 @@ def test_dims_513_to_1024_on_two_part_tiles(dim, wd, monkeypatch):
             assert np.array_equal(ids, want_i[:nq]), (dim, wd, env, nq)
         for key in env:
             monkeypatch.delenv(key)
+
+
+def test_derived_layouts_are_built_on_demand_and_legacy_buffer_still_works():
+    """A batch server never builds the nibble layout, a single-query server never the byte tiles; releasing one frees it
+    until the next search that needs it.  The one-buffer form of ABI revision 1 (xfbq_build_derived + xfbq_scan_topk)
+    gives the same keys."""
+    import torch
+    n, dim, k = 80_000, 256, 20
+    docs = xo.synthetic_unit_rows(n, dim, 1234)
+    queries = xo.synthetic_unit_rows(64, dim, 1235)
+    scale = xo.estimate_scale(docs[:20_000], 0.98)
+    idx = xb.build_index(docs, xb.QuantParams(dim=dim, scale=scale, doc_bits=4, query_bits=4), keep_originals=False)
+    pm = idx.packed
+    assert pm.derived_nbytes == {"nibbles": 0, "tiles": 0}
+    s64, i64 = xb.search(idx, queries, k)
+    assert pm.derived_nbytes["nibbles"] == 0 and pm.derived_nbytes["tiles"] == 2 * pm.nbytes    # tcgen05 engine: tiles only
+    s3, i3 = xb.search(idx, queries[:3], k)
+    assert pm.derived_nbytes["nibbles"] == pm.nbytes                                              # mma.sync engine
+    assert np.array_equal(s3, s64[:3]) and np.array_equal(i3, i64[:3])
+    pm.release_layout("tiles")
+    assert pm.derived_nbytes["tiles"] == 0
+    s3b, i3b = xb.search(idx, queries[:3], k)                                                      # list-keeping seed without tiles
+    assert np.array_equal(s3b, s3) and np.array_equal(i3b, i3) and pm.derived_nbytes["tiles"] == 0
+    # ABI revision 1: one derived buffer
+    L = xb._native.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    derived = torch.empty(int(L.xfbq_derived_bytes(n, dim, 4)), dtype=torch.uint8, device="cuda")
+    xb._native.check(L.xfbq_build_derived(pm.codes.data_ptr(), n, dim, 4, derived.data_ptr(), st))
+    qwords = xb.quantize_queries(queries, 4, scale)
+    for nq in (64, 3):
+        ws = torch.empty(max(int(L.xfbq_scan_workspace_bytes(n, dim, 4, nq, 4, k, 1)), 16), dtype=torch.uint8, device="cuda")
+        keys = torch.empty((nq, k), dtype=torch.int64, device="cuda")
+        xb._native.check(L.xfbq_scan_topk(pm.codes.data_ptr(), derived.data_ptr(), n, dim, 4, qwords.data_ptr(), nq, 4, k, 0,
+                                          keys.data_ptr(), ws.data_ptr(), ws.numel(), st))
+        assert np.array_equal((keys.cpu().numpy() >> 32), s64[:nq]) and np.array_equal(keys.cpu().numpy() & 0xFFFFFFFF, i64[:nq])

@@ -14,7 +14,7 @@ params = xb.QuantParams(dim=dim, scale=scale, doc_bits=4, query_bits=4)
 docs = bench.gen_rows_gpu(torch, 0, n, n, dim)
 index = xb.build_index(docs, params, keep_originals=False)
 del docs
-nib = index.packed.nibbles
+nib = index.packed.nibble_layout
 q = torch.from_numpy(bench.gen_queries(64, dim)).cuda()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
