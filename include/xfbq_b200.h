@@ -169,6 +169,19 @@ int xfbq_refine_f32(const float *rows_dev, int64_t n, int64_t dim, int64_t ld, i
                     void *workspace_dev, int64_t workspace_bytes, void *stream);
 
 /*
+ * The stand-alone histogram / gather stage of the reference (search.py:70-126), for callers that hold a distance array
+ * (int64 on the device): DistanceHistogram.from_distances = xfbq_distance_histogram (*out_of_range_dev counts values outside
+ * [0, bins)), kth_smallest = xfbq_histogram_kth (smallest t with >= k distances <= t), gather_candidates = xfbq_gather_le_count
+ * (the number of rows with d <= threshold lands in workspace word [ceil(n / 65536)]) + xfbq_gather_le_ids (their ids,
+ * ascending).  k_select itself never materialises the array (xfbq_scan_topk + xfbq_collect_candidates).
+ */
+int xfbq_distance_histogram(const int64_t *dist_dev, int64_t n, int64_t bins, uint64_t *hist_dev, uint64_t *out_of_range_dev, void *stream);
+int xfbq_histogram_kth(const uint64_t *hist_dev, int64_t bins, int64_t k, int64_t *kth_out_dev, void *stream);
+int64_t xfbq_gather_workspace_bytes(int64_t n);
+int xfbq_gather_le_count(const int64_t *dist_dev, int64_t n, int64_t threshold, void *workspace_dev, int64_t workspace_bytes, void *stream);
+int xfbq_gather_le_ids(const int64_t *dist_dev, int64_t n, int64_t threshold, const void *workspace_dev, int64_t *ids_out_dev, void *stream);
+
+/*
  * Fused scan + top-K: for each of nq queries the k smallest keys
  * (distance << 32 | row_offset + row) over the n documents, ascending, written
  * to keys_out_dev[nq][k] (slots beyond min(k, n) hold UINT64_MAX).  No score

@@ -2114,6 +2114,66 @@ XFBQ_API int xfbq_refine_f32(const float *rows, int64_t n, int64_t dim, int64_t 
     return refine_impl<float>(rows, n, dim, ld, gathered, ids, count, q, k, sims_out, ids_out, ws, ws_bytes, stream);
 }
 
+XFBQ_API int xfbq_distance_histogram(const int64_t *dist, int64_t n, int64_t bins, uint64_t *hist, uint64_t *out_of_range, void *stream) {
+    if (n < 0 || bins < 1) return fail(XFBQ_E_INVALID, "bad shape n=%lld bins=%lld", (long long)n, (long long)bins);
+    if (!hist || !out_of_range) return fail(XFBQ_E_INVALID, "null pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(hist, 0, static_cast<size_t>(bins) * 8, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(out_of_range, 0, 8, st);
+    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
+    if (n == 0) return XFBQ_OK;
+    if (!dist) return fail(XFBQ_E_INVALID, "null pointer");
+    DeviceInfo info;
+    if (int rc = device_info(&info)) return rc;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > static_cast<int64_t>(info.sms) * 8) blocks = static_cast<int64_t>(info.sms) * 8;
+    sel::dist_histogram_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(dist, n, bins, reinterpret_cast<unsigned long long *>(hist),
+                                                                             reinterpret_cast<unsigned long long *>(out_of_range));
+    return check_launch("sel::dist_histogram_kernel");
+}
+
+XFBQ_API int xfbq_histogram_kth(const uint64_t *hist, int64_t bins, int64_t k, int64_t *kth_out, void *stream) {
+    if (bins < 1 || k < 1) return fail(XFBQ_E_INVALID, "bad arguments bins=%lld k=%lld", (long long)bins, (long long)k);
+    if (!hist || !kth_out) return fail(XFBQ_E_INVALID, "null pointer");
+    sel::hist_kth_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const unsigned long long *>(hist), bins,
+                                                                           static_cast<unsigned long long>(k), reinterpret_cast<long long *>(kth_out));
+    return check_launch("sel::hist_kth_kernel");
+}
+
+XFBQ_API int64_t xfbq_gather_workspace_bytes(int64_t n) {
+    if (n < 0) return -1;
+    return static_cast<int64_t>(align256((static_cast<size_t>((n + 65535) / 65536) + 2) * 8));
+}
+
+XFBQ_API int xfbq_gather_le_count(const int64_t *dist, int64_t n, int64_t threshold, void *workspace, int64_t workspace_bytes, void *stream) {
+    if (n < 0) return fail(XFBQ_E_INVALID, "negative n");
+    if (!workspace || workspace_bytes < xfbq_gather_workspace_bytes(n)) return fail(XFBQ_E_INVALID, "workspace too small");
+    const int blocks = static_cast<int>((n + 65535) / 65536);
+    unsigned long long *counts = static_cast<unsigned long long *>(workspace);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (blocks == 0) {
+        cudaError_t e = cudaMemsetAsync(counts, 0, 16, st);
+        if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
+        return XFBQ_OK;
+    }
+    if (!dist) return fail(XFBQ_E_INVALID, "null pointer");
+    sel::count_le_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(dist, n, threshold, 65536, counts);
+    if (int rc = check_launch("sel::count_le_kernel")) return rc;
+    sel::exclusive_scan_kernel<<<1, 1024, 0, st>>>(counts, blocks);   // counts[blocks] = total
+    return check_launch("sel::exclusive_scan_kernel");
+}
+
+XFBQ_API int xfbq_gather_le_ids(const int64_t *dist, int64_t n, int64_t threshold, const void *workspace, int64_t *ids_out, void *stream) {
+    if (n < 0) return fail(XFBQ_E_INVALID, "negative n");
+    if (n == 0) return XFBQ_OK;
+    if (!dist || !workspace || !ids_out) return fail(XFBQ_E_INVALID, "null pointer");
+    const int blocks = static_cast<int>((n + 65535) / 65536);
+    sel::gather_le_kernel<<<static_cast<unsigned>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        dist, n, threshold, 65536, static_cast<const unsigned long long *>(workspace), ids_out);
+    return check_launch("sel::gather_le_kernel");
+}
+
+
 namespace {
 int search_small_impl(const void *db, const void *nib, int64_t n, int64_t dim, int wd, const void *queries, int f64, int64_t nq, int64_t ld,
                       double scale, int wq, int k, int64_t row_offset, uint64_t *keys_out, uint64_t *nonfinite, void *workspace,

@@ -282,4 +282,101 @@ __global__ void __launch_bounds__(256) rank_final_kernel(const RankPair *__restr
     }
 }
 
+
+// ------------------------------------------------------------------------------ stand-alone histogram / gather
+// histogram_kth_distance and gather_candidates of the reference (search.py:70-126) take a DISTANCE ARRAY; k_select here
+// never materialises one (the fused scan's k-th key is the threshold), these kernels serve the stand-alone functions.
+__global__ void __launch_bounds__(256) dist_histogram_kernel(const int64_t *__restrict__ d, int64_t n, int64_t bins,
+                                                             unsigned long long *__restrict__ hist, unsigned long long *__restrict__ over) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    unsigned long long bad = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int64_t v = d[i];
+        if (v < 0 || v >= bins) ++bad; else atomicAdd(hist + v, 1ull);
+    }
+    if (bad) atomicAdd(over, bad);
+}
+
+// One block: smallest value t with at least k distances <= t (search.py:92-98: searchsorted(cumsum(bins), k, 'left')).
+__global__ void __launch_bounds__(1024) hist_kth_kernel(const unsigned long long *__restrict__ hist, int64_t bins, unsigned long long k,
+                                                        long long *__restrict__ out) {
+    __shared__ unsigned long long s_part[1024];
+    const int64_t per = (bins + blockDim.x - 1) / blockDim.x;
+    const int64_t lo = threadIdx.x * per, hi = min(bins, lo + per);
+    unsigned long long sum = 0;
+    for (int64_t b = lo; b < hi; ++b) sum += hist[b];
+    s_part[threadIdx.x] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long run = 0;
+        long long ans = bins;  // k > total: past the last bin (the caller clamps k to the total first)
+        for (int t = 0; t < static_cast<int>(blockDim.x); ++t) {
+            if (run + s_part[t] >= k) {
+                for (int64_t b = t * per; b < min(bins, (t + 1) * per); ++b) {
+                    run += hist[b];
+                    if (run >= k) { ans = b; break; }
+                }
+                break;
+            }
+            run += s_part[t];
+        }
+        *out = ans;
+    }
+}
+
+// ids with d <= threshold in ascending id order: per-block counts, then (after a host-side / device prefix) ordered writes.
+__global__ void __launch_bounds__(256) count_le_kernel(const int64_t *__restrict__ d, int64_t n, int64_t thr, int64_t per_block,
+                                                       unsigned long long *__restrict__ block_counts) {
+    __shared__ unsigned long long s;
+    if (threadIdx.x == 0) s = 0;
+    __syncthreads();
+    const int64_t lo = static_cast<int64_t>(blockIdx.x) * per_block, hi = min(n, lo + per_block);
+    unsigned long long c = 0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) c += d[i] <= thr ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s, c);
+    __syncthreads();
+    if (threadIdx.x == 0) block_counts[blockIdx.x] = s;
+}
+__global__ void __launch_bounds__(1024) exclusive_scan_kernel(unsigned long long *__restrict__ v, int n) {  // one block, in place; v[n] = total
+    __shared__ unsigned long long s_part[1024];
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int lo = threadIdx.x * per, hi = min(n, lo + per);
+    unsigned long long sum = 0;
+    for (int i = lo; i < hi; ++i) sum += v[i];
+    s_part[threadIdx.x] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long run = 0;
+        for (int t = 0; t < static_cast<int>(blockDim.x); ++t) { const unsigned long long c = s_part[t]; s_part[t] = run; run += c; }
+        v[n] = run;
+    }
+    __syncthreads();
+    unsigned long long run = s_part[threadIdx.x];
+    for (int i = lo; i < hi; ++i) { const unsigned long long c = v[i]; v[i] = run; run += c; }
+}
+__global__ void __launch_bounds__(256) gather_le_kernel(const int64_t *__restrict__ d, int64_t n, int64_t thr, int64_t per_block,
+                                                        const unsigned long long *__restrict__ block_offsets, int64_t *__restrict__ ids) {
+    __shared__ unsigned long long s_base;
+    const int64_t lo = static_cast<int64_t>(blockIdx.x) * per_block, hi = min(n, lo + per_block);
+    if (threadIdx.x == 0) s_base = block_offsets[blockIdx.x];
+    __shared__ int s_warp[8];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t i0 = lo; i0 < hi; i0 += blockDim.x) {   // block-ordered compaction, 256 rows per round
+        const int64_t i = i0 + threadIdx.x;
+        const bool hit = i < hi && d[i] <= thr;
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (lane == 0) s_warp[warp] = __popc(m);
+        __syncthreads();
+        int before = 0, total = 0;
+        for (int w = 0; w < 8; ++w) { if (w < warp) before += s_warp[w]; total += s_warp[w]; }
+        if (hit) ids[s_base + before + __popc(m & ((1u << lane) - 1u))] = i;
+        __syncthreads();
+        if (threadIdx.x == 0) s_base += total;
+        __syncthreads();
+    }
+}
+
 }  // namespace sel

@@ -20,6 +20,16 @@ def distance_upper_bound(dim: int, width_x: int, width_y: int) -> int:
     return int(dim) * scalar_product_upper_bound(width_x, width_y)
 
 
+def packed_distance(x: PackedVector, y: PackedVector) -> int:
+    """distance.py:32-41: pairwise XOR/popcount distance; widths may differ, dims must match.  One-row use of the
+    distance kernel (the definition twin of batch_distances)."""
+    if x.dim != y.dim:
+        raise DimensionMismatchError(f"dim mismatch: {x.dim} vs {y.dim}")
+    if x.dim == 0:
+        return 0
+    return int(batch_distances(PackedMatrix(np.ascontiguousarray(x.planes[:, :, None]), x.dim), y)[0])
+
+
 def batch_distances(matrix: PackedMatrix, query: PackedVector, out: np.ndarray | None = None) -> np.ndarray:
     """distance.py:44-62: uint64[n] distances from one packed query to every row, computed by
     the CUDA distance kernel and copied to the host (or into the caller's `out`)."""

@@ -365,3 +365,119 @@ def k_select(index: Index, request: SearchRequest, collect_timing: bool = False)
         timings["refine"] = t4 - t3
     return SearchResult(hits=hits, candidate_count=candidate_count, threshold_distance=threshold,
                         approximate=approximate, stage_seconds=timings)
+
+
+# ------------------------------------------------------------------------------------------------------------------
+# Stand-alone stages of the reference pipeline (search.py:70-185), for callers that use them directly.  k_select above
+# fuses them: it never builds a distance array, a histogram or an id list of the whole database.
+def _device_int64(distances):
+    """Distance array (numpy uint64/int64 or CUDA int64 tensor) -> CUDA int64 tensor."""
+    torch = _native.require_cuda()
+    if _is_torch(distances):
+        t = distances if distances.is_cuda else distances.cuda()
+        return t.to(torch.int64).contiguous().reshape(-1)
+    a = np.asarray(distances)
+    if a.dtype == np.uint64:
+        a = a.view(np.int64)
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64).reshape(-1)).cuda()
+
+
+@dataclass(frozen=True)
+class DistanceHistogram:
+    """search.py:68-98: frequency of every integer distance value in 0..upper_bound (bins: host int64 array)."""
+
+    bins: np.ndarray
+
+    @classmethod
+    def from_distances(cls, distances, upper_bound: int) -> "DistanceHistogram":
+        torch = _native.require_cuda()
+        L = _native.lib()
+        d = _device_int64(distances)
+        if d.numel() == 0:
+            raise InvalidInputError("cannot histogram an empty distance array")
+        nbins = int(upper_bound) + 1
+        with torch.cuda.device(d.device):
+            hist = torch.empty(nbins, dtype=torch.int64, device=d.device)
+            over = torch.empty(1, dtype=torch.int64, device=d.device)
+            _native.check(L.xfbq_distance_histogram(d.data_ptr(), d.numel(), nbins, hist.data_ptr(), over.data_ptr(), _stream_ptr(torch)))
+            if int(over.item()):
+                raise InvalidInputError(f"distance {int(d.max())} exceeds upper bound {upper_bound}")
+            return cls(bins=hist.cpu().numpy())
+
+    @property
+    def total(self) -> int:
+        return int(self.bins.sum())
+
+    def kth_smallest(self, k: int) -> int:
+        """Smallest distance value t with at least k distances <= t."""
+        if k < 1:
+            raise InvalidInputError(f"k must be >= 1, got {k}")
+        torch = _native.require_cuda()
+        L = _native.lib()
+        k = min(int(k), self.total)
+        hist = torch.from_numpy(np.ascontiguousarray(self.bins, dtype=np.int64)).cuda()
+        out = torch.empty(1, dtype=torch.int64, device=hist.device)
+        _native.check(L.xfbq_histogram_kth(hist.data_ptr(), hist.numel(), max(k, 1), out.data_ptr(), _stream_ptr(torch)))
+        return int(out.item())
+
+
+def histogram_kth_distance(distances, k: int, extra: int = 0, upper_bound: int | None = None) -> int:
+    """search.py:101-117: k-th smallest distance by histogram, plus `extra`."""
+    d = _device_int64(distances)
+    if d.numel() == 0:
+        raise InvalidInputError("cannot select from an empty distance array")
+    if extra < 0:
+        raise InvalidInputError(f"extra must be >= 0, got {extra}")
+    if upper_bound is None:
+        upper_bound = int(d.max())
+    return DistanceHistogram.from_distances(d, upper_bound).kth_smallest(k) + int(extra)
+
+
+def gather_candidates(distances, threshold: int) -> np.ndarray:
+    """search.py:120-126: ids with distance <= threshold, ascending (ordered compaction on the GPU)."""
+    torch = _native.require_cuda()
+    L = _native.lib()
+    d = _device_int64(distances)
+    if d.numel() == 0 or threshold < 0:
+        return np.empty(0, dtype=np.int64)
+    n = d.numel()
+    with torch.cuda.device(d.device):
+        ws = torch.empty(int(L.xfbq_gather_workspace_bytes(n)) // 8, dtype=torch.int64, device=d.device)
+        st = _stream_ptr(torch)
+        _native.check(L.xfbq_gather_le_count(d.data_ptr(), n, int(threshold), ws.data_ptr(), ws.numel() * 8, st))
+        count = int(ws[(n + 65535) // 65536].item())
+        ids = torch.empty(count, dtype=torch.int64, device=d.device)
+        if count:
+            _native.check(L.xfbq_gather_le_ids(d.data_ptr(), n, int(threshold), ws.data_ptr(), ids.data_ptr(), st))
+        return ids.cpu().numpy()
+
+
+def refine(index: Index, query, candidates, k: int, distances=None):
+    """search.py:134-172: re-rank candidate rows; returns (hits, approximate).  With originals: float64 dot products of the
+    float32 rows (xfbq_refine_f32); without: similarities decoded from quantized distances, flagged approximate."""
+    torch = _native.require_cuda()
+    cand = np.asarray(candidates, dtype=np.int64)
+    if cand.size == 0:
+        return [], index.originals is None
+    q = np.ascontiguousarray(query, dtype=np.float64)
+    p = index.params
+    if index.originals is not None:
+        hits = _refine_device(index, q, torch.from_numpy(cand).to(index.packed.codes.device), k)
+        return hits, False
+    if distances is None:
+        from .distance import batch_distances_device
+        cand_d = batch_distances_device(index.packed, quantize_vector(q, p.query_bits, p.scale))[torch.from_numpy(cand).to(index.packed.codes.device)].cpu().numpy()
+    else:
+        cand_d = np.asarray(distances)[cand]
+    sims = decode_inner_product_values(cand_d, p.dim, p.doc_bits, p.query_bits)
+    sims /= p.scale * p.scale
+    order = np.lexsort((cand, -sims))[:k]                               # search.py:129-131 on <= candidate-count values
+    return [(int(cand[i]), float(sims[i])) for i in order], True
+
+
+def suggest_extra_distance(index: Index, fraction: float) -> int:
+    """search.py:175-185."""
+    if not 0.0 <= fraction <= 1.0:
+        raise InvalidInputError(f"fraction must be in [0, 1], got {fraction}")
+    p = index.params
+    return round(fraction * distance_upper_bound(p.dim, p.query_bits, p.doc_bits))

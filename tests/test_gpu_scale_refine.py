@@ -126,3 +126,48 @@ def test_k_above_max_k_and_full_range_extra():
     assert np.allclose([h[1] for h in res.hits], want_sims, rtol=1e-12)
     res = xb.k_select(idx, xb.SearchRequest(query=q[0].astype(np.float64), k=5000, extra_distance=0))
     assert len(res.hits) == 5000
+
+
+def test_standalone_histogram_gather_refine_and_packed_distance():
+    """The stand-alone stages of the reference pipeline (search.py:70-185, distance.py:32-41) on GPU kernels, against numpy
+    restatements of the reference lines (pkg/tests/test_search.py:45-70, test_distance.py:30-35,114-124)."""
+    import torch
+    rng = np.random.Generator(np.random.PCG64(3))
+    d = rng.integers(0, 5000, size=300_001).astype(np.uint64)
+    ub = 6000
+    h = xb.DistanceHistogram.from_distances(d, ub)
+    assert np.array_equal(h.bins, np.bincount(d.astype(np.int64), minlength=ub + 1)) and h.total == d.size
+    srt = np.sort(d)
+    for k in (1, 2, 100, 4321, d.size, d.size + 5):
+        assert h.kth_smallest(k) == int(srt[min(k, d.size) - 1])
+        assert xb.histogram_kth_distance(d, k, extra=7) == int(srt[min(k, d.size) - 1]) + 7
+    assert xb.histogram_kth_distance(torch.from_numpy(d.astype(np.int64)).cuda(), 10, upper_bound=ub) == int(srt[9])
+    with pytest.raises(xb.InvalidInputError):
+        xb.DistanceHistogram.from_distances(d, 100)
+    with pytest.raises(xb.InvalidInputError):
+        xb.histogram_kth_distance(np.zeros(0, dtype=np.uint64), 1)
+    for thr in (0, 17, 2500, 4999, 10**9):
+        assert np.array_equal(xb.gather_candidates(d, thr), np.flatnonzero(d <= thr))
+    assert xb.gather_candidates(d, -1).size == 0
+    # packed_distance: worked values 55 / 40 (test_distance.py:30-35) and equality with batch_distances rows
+    x = xb.pack_matrix(np.array([[0b010, 0b010]], dtype=np.uint8), 3).row(0)
+    y = xb.pack_matrix(np.array([[0b010, 0b111]], dtype=np.uint8), 3).row(0)
+    assert xb.packed_distance(x, y) == 55 and xb.packed_distance(x, x) == 40
+    docs = xo.synthetic_unit_rows(500, 200, 9)
+    idx = xb.build_index(docs, xb.QuantParams(dim=200, scale=4.0, doc_bits=3, query_bits=4))
+    pq = xb.quantize_vector(docs[3].astype(np.float64), 4, 4.0)
+    full = xb.batch_distances(idx.packed, pq)
+    assert [xb.packed_distance(idx.packed.row(r), pq) for r in (0, 3, 499)] == [int(full[r]) for r in (0, 3, 499)]
+    # refine: both branches, and suggest_extra_distance
+    cand = np.flatnonzero(full <= np.sort(full)[40])
+    hits, approx = xb.refine(idx, docs[3].astype(np.float64), cand, 10)
+    want_ids, want_sims = _reference_refine(docs, docs[3].astype(np.float64), cand, 10)
+    assert not approx and [h[0] for h in hits] == want_ids.tolist() and np.allclose([h[1] for h in hits], want_sims, rtol=1e-12)
+    idx2 = xb.Index(params=idx.params, packed=idx.packed, originals=None)
+    hits2, approx2 = xb.refine(idx2, docs[3].astype(np.float64), cand, 10, distances=full)
+    sims = xb.decode_inner_product_values(full[cand], 200, 3, 4) / 16.0
+    order = np.lexsort((cand, -sims))[:10]
+    assert approx2 and hits2 == [(int(cand[i]), float(sims[i])) for i in order]
+    hits3, _ = xb.refine(idx2, docs[3].astype(np.float64), cand, 10)
+    assert hits3 == hits2
+    assert xb.suggest_extra_distance(idx, 0.05) == round(0.05 * xb.distance_upper_bound(200, 4, 3))
