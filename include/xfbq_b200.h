@@ -168,6 +168,12 @@ int xfbq_refine_f32(const float *rows_dev, int64_t n, int64_t dim, int64_t ld, i
                     int64_t count, const double *q_dev, int k, double *sims_out_dev, int64_t *ids_out_dev,
                     void *workspace_dev, int64_t workspace_bytes, void *stream);
 
+/* The same gather from the nibble layout (doc_bits <= 4, query_bits <= 7, dim <= 512): the exact integer form of the distance on
+ * dp4a, HBM-bound instead of POPC-bound; identical counts and ids. */
+int xfbq_collect_candidates_nibbles(const void *nibbles_dev, int64_t n, int64_t dim, int doc_bits, const uint32_t *q_dev,
+                                    int query_bits, int64_t threshold, int64_t *ids_out_dev, int64_t cap,
+                                    uint64_t *count_out_dev, void *stream);
+
 /*
  * The stand-alone histogram / gather stage of the reference (search.py:70-126), for callers that hold a distance array
  * (int64 on the device): DistanceHistogram.from_distances = xfbq_distance_histogram (*out_of_range_dev counts values outside
@@ -231,6 +237,18 @@ int xfbq_search_small_f32(const void *db_dev, const void *nibbles_dev, int64_t n
 int xfbq_search_small_f64(const void *db_dev, const void *nibbles_dev, int64_t n, int64_t dim, int doc_bits, const double *queries_dev,
                           int64_t nq, int64_t ld, double scale, int query_bits, int k, int64_t row_offset, uint64_t *keys_out_dev,
                           uint64_t *nonfinite_dev, void *workspace_dev, int64_t workspace_bytes, void *stream);
+
+/*
+ * k_select in one launch (search.py:188-232 up to the re-rank): the search above plus the histogram / gather stage -- per query
+ * the number of rows with distance <= (k-th distance + extra_distance) in cand_count_out_dev[nq] and, when cand_ids_out_dev is
+ * not NULL, the first min(count, cand_cap) of their row ids (unordered) in cand_ids_out_dev[nq][cand_cap].  The scan keeps every
+ * such row in its candidate lists unless a list overflowed and was cut: then *inexact_out_dev != 0 and the caller runs
+ * xfbq_collect_candidates* instead (large extra_distance, heavy ties).  float64 queries (SearchRequest.query is float64).
+ */
+int xfbq_kselect_small_f64(const void *db_dev, const void *nibbles_dev, int64_t n, int64_t dim, int doc_bits, const double *queries_dev,
+                           int64_t nq, int64_t ld, double scale, int query_bits, int k, int64_t extra_distance, int64_t row_offset,
+                           uint64_t *keys_out_dev, uint64_t *cand_count_out_dev, int64_t *cand_ids_out_dev, int64_t cand_cap,
+                           int *inexact_out_dev, uint64_t *nonfinite_dev, void *workspace_dev, int64_t workspace_bytes, void *stream);
 
 /*
  * Merge `parts` partial results keys_in_dev[parts][nq][k] (each row ascending,

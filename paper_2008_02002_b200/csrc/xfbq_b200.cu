@@ -1323,6 +1323,12 @@ struct FloatQueries {  // float queries for the fused path (quantized inside the
     int64_t ld = 0;
     double scale = 1.0;
     uint64_t *nonfinite = nullptr;
+    // k_select outputs (xfbq_kselect_small_*): candidates within `extra` of the k-th distance
+    int extra = 0;
+    uint64_t *cand_count = nullptr;
+    int64_t *cand_ids = nullptr;
+    int64_t cand_cap = 0;
+    int *inexact = nullptr;
 };
 
 int run_coop(const CoopPlan &cp, unsigned char *ws, const void *nib, int64_t n, int64_t dim, int wd, const uint32_t *q, int64_t nq, int wq,
@@ -1338,6 +1344,9 @@ int run_coop(const CoopPlan &cp, unsigned char *ws, const void *nib, int64_t n, 
     p.xq = fq.x; p.xq_f64 = fq.f64; p.ldq = fq.ld; p.scale = fq.scale;
     p.nonfinite = reinterpret_cast<unsigned long long *>(fq.nonfinite);
     p.row_bad = reinterpret_cast<int *>(ws + cp.off_theta) + 32;
+    p.extra = fq.extra;
+    p.cand_count = reinterpret_cast<unsigned long long *>(fq.cand_count);
+    p.cand_ids = fq.cand_ids; p.cand_cap = fq.cand_cap; p.inexact = fq.inexact;
     p.qop = reinterpret_cast<uint32_t *>(ws + cp.off_qop);
     p.qconst = reinterpret_cast<int32_t *>(ws + cp.off_qconst);
     p.shist = reinterpret_cast<uint32_t *>(ws + cp.off_shist);
@@ -2114,6 +2123,34 @@ XFBQ_API int xfbq_refine_f32(const float *rows, int64_t n, int64_t dim, int64_t 
     return refine_impl<float>(rows, n, dim, ld, gathered, ids, count, q, k, sims_out, ids_out, ws, ws_bytes, stream);
 }
 
+XFBQ_API int xfbq_collect_candidates_nibbles(const void *nib, int64_t n, int64_t dim, int wd, const uint32_t *q, int wq,
+                                             int64_t threshold, int64_t *ids_out, int64_t cap, uint64_t *count_out, void *stream) {
+    if (!width_ok(wd) || !width_ok(wq)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d/%d", wd, wq);
+    if (n < 0 || dim < 1 || cap < 0) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld cap=%lld", (long long)n, (long long)dim, (long long)cap);
+    const int C = static_cast<int>(chunks128(dim));
+    if (wd > 4 || wq > 7 || C > 4) return fail(XFBQ_E_UNSUPPORTED, "no nibble layout for doc_bits=%d query_bits=%d dim=%lld", wd, wq, (long long)dim);
+    if (!count_out) return fail(XFBQ_E_INVALID, "null pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(count_out, 0, 8, st);
+    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
+    if (n == 0 || threshold < 0) return XFBQ_OK;
+    if (!nib || !q) return fail(XFBQ_E_INVALID, "null pointer");
+    DeviceInfo info;
+    if (int rc = device_info(&info)) return rc;
+    int64_t blocks = (n + 255) / 256;
+    const int64_t max_blocks = static_cast<int64_t>(info.sms) * 8;
+    if (blocks > max_blocks) blocks = max_blocks;
+    const uint32_t thr = threshold > 0xFFFFFFFFll ? 0xFFFFFFFFu : static_cast<uint32_t>(threshold);
+    typedef void (*Kern)(const uint4 *, int64_t, int, int, const uint32_t *, int, uint32_t, int64_t *, int64_t, unsigned long long *);
+    static const Kern kernels[4] = {sel::collect_candidates_nib_warp_kernel<1>, sel::collect_candidates_nib_warp_kernel<2>,
+                                    sel::collect_candidates_nib_kernel<3>, sel::collect_candidates_nib_warp_kernel<4>};
+    blocks = (bundles_of(n) + 7) / 8;   // a warp per bundle of 32 documents
+    if (blocks > max_blocks) blocks = max_blocks;
+    kernels[C - 1]<<<static_cast<unsigned>(blocks), 256, 0, st>>>(static_cast<const uint4 *>(nib), n, static_cast<int>(dim), wd, q, wq, thr, ids_out,
+                                                                  ids_out ? cap : 0, reinterpret_cast<unsigned long long *>(count_out));
+    return check_launch("sel::collect_candidates_nib_kernel");
+}
+
 XFBQ_API int xfbq_distance_histogram(const int64_t *dist, int64_t n, int64_t bins, uint64_t *hist, uint64_t *out_of_range, void *stream) {
     if (n < 0 || bins < 1) return fail(XFBQ_E_INVALID, "bad shape n=%lld bins=%lld", (long long)n, (long long)bins);
     if (!hist || !out_of_range) return fail(XFBQ_E_INVALID, "null pointer");
@@ -2177,7 +2214,10 @@ XFBQ_API int xfbq_gather_le_ids(const int64_t *dist, int64_t n, int64_t threshol
 namespace {
 int search_small_impl(const void *db, const void *nib, int64_t n, int64_t dim, int wd, const void *queries, int f64, int64_t nq, int64_t ld,
                       double scale, int wq, int k, int64_t row_offset, uint64_t *keys_out, uint64_t *nonfinite, void *workspace,
-                      int64_t workspace_bytes, void *stream) {
+                      int64_t workspace_bytes, void *stream, int64_t extra = 0, uint64_t *cand_count = nullptr, int64_t *cand_ids = nullptr,
+                      int64_t cand_cap = 0, int *inexact = nullptr) {
+    if (extra < 0 || extra >= (1ll << 30)) return fail(XFBQ_E_INVALID, "extra distance out of range");
+    if (cand_count && !inexact) return fail(XFBQ_E_INVALID, "null pointer");
     if (!width_ok(wd) || !width_ok(wq)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d/%d", wd, wq);
     if (!(scale > 0.0)) return fail(XFBQ_E_INVALID, "scale must be positive, got %g", scale);
     if (n < 1 || dim < 1 || nq < 1 || ld < dim) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld nq=%lld ld=%lld", (long long)n, (long long)dim, (long long)nq, (long long)ld);
@@ -2191,6 +2231,7 @@ int search_small_impl(const void *db, const void *nib, int64_t n, int64_t dim, i
         return fail(XFBQ_E_INVALID, "workspace too small: need %zu bytes, got %lld", cp.bytes, (long long)workspace_bytes);
     FloatQueries fq;
     fq.x = queries; fq.f64 = f64; fq.ld = ld; fq.scale = scale; fq.nonfinite = nonfinite;
+    fq.extra = static_cast<int>(extra); fq.cand_count = cand_count; fq.cand_ids = cand_ids; fq.cand_cap = cand_cap; fq.inexact = inexact;
     return run_coop(cp, static_cast<unsigned char *>(workspace), nib, n, dim, wd, nullptr, nq, wq, k, row_offset, keys_out,
                     static_cast<cudaStream_t>(stream), fq);
 }
@@ -2231,6 +2272,15 @@ XFBQ_API int xfbq_scan_layouts(int64_t n, int64_t dim, int wd, int64_t nq, int w
     MmaPlan mp;
     if (make_mma_plan(n, dim, wd, nq, wq, k, true, &mp) == XFBQ_OK && mp.ok) return XFBQ_LAYOUT_NIBBLES;
     return 0;
+}
+
+XFBQ_API int xfbq_kselect_small_f64(const void *db, const void *nib, int64_t n, int64_t dim, int wd, const double *queries, int64_t nq, int64_t ld,
+                                    double scale, int wq, int k, int64_t extra_distance, int64_t row_offset, uint64_t *keys_out,
+                                    uint64_t *cand_count_out, int64_t *cand_ids_out, int64_t cand_cap, int *inexact_out, uint64_t *nonfinite,
+                                    void *workspace, int64_t workspace_bytes, void *stream) {
+    if (!cand_count_out) return fail(XFBQ_E_INVALID, "null pointer");
+    return search_small_impl(db, nib, n, dim, wd, queries, 1, nq, ld, scale, wq, k, row_offset, keys_out, nonfinite, workspace, workspace_bytes, stream,
+                             extra_distance, cand_count_out, cand_ids_out, cand_cap, inexact_out);
 }
 
 XFBQ_API int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, int have_nibbles) {

@@ -63,6 +63,14 @@ struct Params {
     int seed_shift, seed_offset;  // bin = (acc + seed_offset) >> seed_shift
     int hist_shift;               // candidate bins of width 1 << hist_shift
     int merge_B;                  // keys of the final merge buffer (power of two)
+    // k_select in the same launch (search.py:206-216): the scan prunes `extra` score units below the thresholds, so the lists
+    // hold every row with distance <= (k-th distance + extra); the merge counts them per query (and lists their ids) unless a
+    // list had to be cut during the scan (*inexact != 0: the caller falls back to the separate gather pass)
+    int extra;
+    unsigned long long *cand_count;   // [nq] or nullptr (feature off)
+    int64_t *cand_ids;                // [nq][cand_cap] or nullptr
+    int64_t cand_cap;
+    int *inexact;                     // [1]
     unsigned long long *prof;     // optional [8 + 2 * grid] phase time stamps (ns, xfbq_debug_profile), else nullptr
 };
 __device__ __forceinline__ unsigned long long now_ns() {
@@ -180,6 +188,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) search_kernel(const Params p) {
         for (int64_t i = gtid; i < 16 * SEED_BINS; i += gthreads) p.shist[i] = 0u;
         for (int64_t i = gtid; i < 16 * CAND_BINS; i += gthreads) p.chist[i] = 0u;
         if (gtid < 16) { p.theta_g[gtid] = TAU_OPEN; p.theta0[gtid] = TAU_OPEN; }
+        if (gtid == 0 && p.inexact) *p.inexact = 0;
         for (int row = blockIdx.x; row < 16; row += gridDim.x)
             if (warp == 0) prep_row(p, row, C, lane);
     }
@@ -322,7 +331,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) search_kernel(const Params p) {
     __syncwarp();
     cnt_s[lane] = 0;
     __syncwarp();
-    int negtau0 = -__shfl_sync(0xffffffffu, my_tau, g), negtau1 = -__shfl_sync(0xffffffffu, my_tau, g + 8);
+    // a row passes a score when acc >= tau - extra (extra > 0 only for k_select's candidate slack); rows without a query never pass
+    auto prune_of = [&](int tau) { return row_valid ? max(TAU_OPEN, tau - p.extra) : 1; };
+    int negtau0 = -__shfl_sync(0xffffffffu, prune_of(my_tau), g), negtau1 = -__shfl_sync(0xffffffffu, prune_of(my_tau), g + 8);
+
     const int dq0 = __shfl_sync(0xffffffffu, my_dq, g), dq1 = __shfl_sync(0xffffffffu, my_dq, g + 8);
     const int th00 = __shfl_sync(0xffffffffu, my_th0, g), th01 = __shfl_sync(0xffffffffu, my_th0, g + 8);
 
@@ -363,9 +375,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1) search_kernel(const Params p) {
                 need &= need - 1;
                 const int nv = small_lists ? mma::compact_row_sorted(lists + ql * p.cap, scratch, &cnt_s[ql], p.k, ql, lane, my_dq, &my_tau)
                                            : mma::compact_row(lists + ql * p.cap, hist, &cnt_s[ql], p.k, ql, lane, my_dq, &my_tau);
-                if (g == ql) negtau0 = nv;
-                if (g + 8 == ql) negtau1 = nv;
-                if (lane == ql) atomicMax(p.theta_g + ql, -nv);
+                negtau0 = -__shfl_sync(0xffffffffu, prune_of(my_tau), g);
+                negtau1 = -__shfl_sync(0xffffffffu, prune_of(my_tau), g + 8);
+                if (lane == ql) {
+                    atomicMax(p.theta_g + ql, -nv);
+                    if (p.inexact) *p.inexact = 1;   // the list was cut to its k best: it no longer holds every candidate
+                }
             }
         }
     };
@@ -398,8 +413,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) search_kernel(const Params p) {
             const int tnew = max(my_tau, tg_next);
             if (__any_sync(0xffffffffu, tnew != my_tau)) {
                 my_tau = tnew;
-                negtau0 = -__shfl_sync(0xffffffffu, my_tau, g);
-                negtau1 = -__shfl_sync(0xffffffffu, my_tau, g + 8);
+                negtau0 = -__shfl_sync(0xffffffffu, prune_of(my_tau), g);
+                negtau1 = -__shfl_sync(0xffffffffu, prune_of(my_tau), g + 8);
             }
         }
         // One warp of the CTA per 16 stages (per 64 once the thresholds have settled) turns one query's candidate histogram
@@ -467,6 +482,31 @@ __global__ void __launch_bounds__(WARPS * 32, 1) search_kernel(const Params p) {
             const int part = find_part(s_pre, parts, static_cast<int>(e));
             return __ldcg(p.lists + (static_cast<int64_t>(part) * 16 + r) * p.cap + (e - s_pre[part]));
         }, p.keys_out + static_cast<int64_t>(r) * p.k);
+        if (p.cand_count) {  // every list entry within `extra` of the k-th distance (the k best keys have just been written)
+            __syncthreads();
+            const int total = s_pre[parts];
+            const int valid = total < p.k ? total : p.k;
+            const long long thr = valid > 0 ? static_cast<long long>(__ldcg(p.keys_out + static_cast<int64_t>(r) * p.k + valid - 1) >> 32) + p.extra : -1;
+            if (threadIdx.x == 0) p.cand_count[r] = 0ull;
+            __syncthreads();
+            for (int e0 = 0; e0 < total; e0 += blockDim.x) {
+                const int e = e0 + threadIdx.x;
+                uint64_t key = KEY_INF;
+                if (e < total) {
+                    const int part = find_part(s_pre, parts, e);
+                    key = __ldcg(p.lists + (static_cast<int64_t>(part) * 16 + r) * p.cap + (e - s_pre[part]));
+                }
+                const bool hit = key != KEY_INF && static_cast<long long>(key >> 32) <= thr;
+                const unsigned m = __ballot_sync(0xffffffffu, hit);
+                if (m) {
+                    unsigned long long base = 0;
+                    if (lane == 0) base = atomicAdd(p.cand_count + r, static_cast<unsigned long long>(__popc(m)));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    const int64_t pos = static_cast<int64_t>(base) + __popc(m & ((1u << lane) - 1u));
+                    if (hit && p.cand_ids && pos < p.cand_cap) p.cand_ids[static_cast<int64_t>(r) * p.cand_cap + pos] = static_cast<int64_t>(key & 0xFFFFFFFFull);
+                }
+            }
+        }
         if (p.prof && r == 0 && threadIdx.x == 0) { p.prof[5] = now_ns(); p.prof[6] = static_cast<unsigned long long>(s_pre[parts]); }
     }
 }

@@ -59,21 +59,32 @@ def batch_distances_device(matrix: PackedMatrix, query: PackedVector):
     return d
 
 
-def collect_candidates_device(matrix: PackedMatrix, query: PackedVector, threshold: int, want_ids: bool, cap: int = 1 << 16):
+def collect_candidates_device(matrix: PackedMatrix, query, threshold: int, want_ids: bool, cap: int = 1 << 16, query_bits: int | None = None):
     """Number of rows with distance <= threshold and (want_ids) their row ids as a device int64 tensor, unordered:
     the histogram/gather stage of k_select (search.py:206-216) in one pass over the codes, without the distance
-    array.  The id buffer grows to the count when `cap` was too small (second pass)."""
+    array.  `query`: a PackedVector, or device query words (query layout, with `query_bits`).  The pass runs on the nibble
+    layout when the index has built it (dp4a, HBM-bound), else on the bit planes (XOR/POPC).  The id buffer grows to the
+    count when `cap` was too small (second pass)."""
     torch = _native.require_cuda()
     L = _native.lib()
     dev = matrix.codes.device
     with torch.cuda.device(dev):
-        q = query.device_words()
+        if isinstance(query, PackedVector):
+            q, wq = query.device_words(), query.width
+        else:
+            q, wq = query, int(query_bits)
+        nib = getattr(matrix, "_nibbles", None) if wq <= 7 else None
         count_dev = torch.empty(1, dtype=torch.int64, device=dev)
         while True:
             ids = torch.empty(cap if want_ids else 0, dtype=torch.int64, device=dev)
-            _native.check(L.xfbq_collect_candidates(matrix.codes.data_ptr(), matrix.count, matrix.dim, matrix.width,
-                                                    q.data_ptr(), query.width, int(threshold),
-                                                    ids.data_ptr() if want_ids else None, cap, count_dev.data_ptr(), _stream_ptr(torch)))
+            if nib is not None:
+                _native.check(L.xfbq_collect_candidates_nibbles(nib.data_ptr(), matrix.count, matrix.dim, matrix.width, q.data_ptr(), wq,
+                                                                int(threshold), ids.data_ptr() if want_ids else None, cap,
+                                                                count_dev.data_ptr(), _stream_ptr(torch)))
+            else:
+                _native.check(L.xfbq_collect_candidates(matrix.codes.data_ptr(), matrix.count, matrix.dim, matrix.width,
+                                                        q.data_ptr(), wq, int(threshold),
+                                                        ids.data_ptr() if want_ids else None, cap, count_dev.data_ptr(), _stream_ptr(torch)))
             count = int(count_dev.item())
             if not want_ids or count <= cap:
                 return count, (ids[:count] if want_ids else None)

@@ -104,6 +104,42 @@ def _search_small_fused(index: Index, queries, k: int, row_offset: int):
     return keys, counter
 
 
+def _kselect_small_fused(index: Index, query: np.ndarray, k: int, extra: int, want_ids: bool, cap: int):
+    """k_select's quantize + scan + top-k + histogram/gather stage as ONE cooperative launch (xfbq_kselect_small_f64).
+    Returns (keys int64[k] on the host, candidate count, device ids or None), or None when the shape takes the general path or a
+    candidate list had to be cut during the scan (large extra_distance, heavy ties): the caller then runs the separate passes."""
+    torch = _native.require_cuda()
+    L = _native.lib()
+    packed, p = index.packed, index.params
+    if packed.width > 4 or p.query_bits > 7 or packed.dim > 512 or k > 1024 or extra >= (1 << 30):
+        return None
+    dev = packed.codes.device
+    ws_bytes = int(L.xfbq_search_small_workspace_bytes(packed.count, packed.dim, packed.width, 1, p.query_bits, k))
+    if ws_bytes <= 0:
+        return None
+    nib = packed.nibble_layout
+    if nib is None:
+        return None
+    with torch.cuda.device(dev):
+        counter = _NONFINITE.get(dev.index)
+        if counter is None:
+            counter = _NONFINITE[dev.index] = torch.zeros(1, dtype=torch.int64, device=dev)
+        q_dev = torch.from_numpy(np.ascontiguousarray(query, dtype=np.float64)[None, :]).to(dev)
+        keys = torch.empty(k + 2, dtype=torch.int64, device=dev)        # k keys, candidate count, inexact flag: one D2H copy
+        ids = torch.empty(cap if want_ids else 0, dtype=torch.int64, device=dev)
+        ws = _workspace(torch, dev, ws_bytes)
+        _native.check(L.xfbq_kselect_small_f64(packed.codes.data_ptr(), nib.data_ptr(), packed.count, packed.dim, packed.width,
+                                               q_dev.data_ptr(), 1, packed.dim, float(p.scale), p.query_bits, k, int(extra), 0,
+                                               keys.data_ptr(), keys.data_ptr() + 8 * k, ids.data_ptr() if want_ids else None, cap,
+                                               keys.data_ptr() + 8 * (k + 1), counter.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(torch)))
+        (host,) = to_host_arrays(keys)
+        raise_pending_nonfinite(dev)
+    count, inexact = int(host[k]), int(host[k + 1]) & 0xFFFFFFFF
+    if inexact or (want_ids and count > cap):
+        return None
+    return host[:k], count, (ids[:count] if want_ids else None)
+
+
 def scan_topk_device(packed: PackedMatrix, qwords, nq: int, query_bits: int, k: int, row_offset: int = 0):
     """Launch the fused scan+top-K on device-resident query words (query layout).
     Returns an int64 CUDA tensor [nq, k] holding the uint64 keys bit-for-bit
@@ -335,17 +371,33 @@ def k_select(index: Index, request: SearchRequest, collect_timing: bool = False)
     upper = distance_upper_bound(p.dim, p.doc_bits, p.query_bits)
 
     t0 = time.perf_counter()
-    packed_query = quantize_vector(request.query, p.query_bits, p.scale)
-    qwords = packed_query.device_words()
-    sync(); t1 = time.perf_counter()
-    keys = scan_topk_device(index.packed, qwords.view(torch.int32), 1, p.query_bits, kk)
-    top_d, top_i = to_host_arrays(*(t[0] for t in unpack_keys_device(keys)))
-    sync(); t2 = time.perf_counter()
-    # the k-th smallest distance IS the reference's histogram threshold (search.py:206-213); the gather is one
-    # more pass over the codes (no distance array): count, and row ids when they are re-ranked
-    threshold = int(top_d[kk - 1]) + int(request.extra_distance)
-    candidate_count, cand = collect_candidates_device(index.packed, packed_query, min(threshold, upper),
-                                                      want_ids=index.originals is not None, cap=max(1 << 16, 4 * kk))
+    dev = index.packed.codes.device
+    want_ids = index.originals is not None
+    extra = min(int(request.extra_distance), upper)
+    fused = _kselect_small_fused(index, request.query, kk, extra, want_ids, cap=max(1 << 16, 4 * kk))
+    if fused is not None:
+        # one cooperative launch did the whole of search.py:206-214: quantize, distances + top-k, threshold, candidate gather
+        host_keys, candidate_count, cand = fused
+        kn = host_keys.view(np.uint64)
+        top_d, top_i = (kn >> np.uint64(32)).astype(np.int64), (kn & np.uint64(0xFFFFFFFF)).astype(np.int64)
+        threshold = int(top_d[kk - 1]) + int(request.extra_distance)
+        t1, t2 = t0, time.perf_counter()   # the fused launch is booked under "distances"
+    else:
+        # the query never round-trips through the host: upload the floats, quantize on the device (counter read after the scan)
+        with torch.cuda.device(dev):
+            q_dev = torch.from_numpy(request.query[None, :]).to(dev)
+            qwords, bad = quantize_queries(q_dev, p.query_bits, p.scale, defer_check=True)
+        sync(); t1 = time.perf_counter()
+        keys = scan_topk_device(index.packed, qwords, 1, p.query_bits, kk)
+        top_d, top_i = to_host_arrays(*(t[0] for t in unpack_keys_device(keys)))
+        if int(bad.item()):
+            raise InvalidInputError("cannot quantize non-finite values")
+        sync(); t2 = time.perf_counter()
+        # the k-th smallest distance IS the reference's histogram threshold (search.py:206-213); the gather is one
+        # more pass over the codes (no distance array): count, and row ids when they are re-ranked
+        threshold = int(top_d[kk - 1]) + int(request.extra_distance)
+        candidate_count, cand = collect_candidates_device(index.packed, qwords, min(threshold, upper), want_ids=want_ids,
+                                                          cap=max(1 << 16, 4 * kk), query_bits=p.query_bits)
     sync(); t3 = time.perf_counter()
     if index.originals is None:
         sims = decode_inner_product_values(top_d, p.dim, p.doc_bits, p.query_bits)
