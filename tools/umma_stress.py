@@ -11,10 +11,8 @@ os.environ["XFBQ_ENGINE"] = "umma"
 bad = 0
 for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 60):
     n = int(rng.choice([1, 2, 31, 33, 127, 128, 129, 200, 1000, 4097, 20000]))
-    dim = int(rng.choice([1, 7, 64, 100, 128, 129, 200, 256, 300, 512]))
-    if 256 < dim <= 384:
-        dim = 300  # C == 3 is not a tensor-engine shape: falls back, still must be exact
-    wd = int(rng.integers(1, 5))
+    dim = int(rng.choice([1, 7, 64, 100, 128, 129, 200, 256, 300, 384, 512, 513, 700, 1024]))
+    wd = int(rng.integers(1, 9))
     nq = int(rng.choice([17, 40, 128, 129, 256, 257, 700]))
     k = int(rng.choice([1, 5, 100, 1000]))
     docs = xo.synthetic_unit_rows(n, dim, 100 + it)
