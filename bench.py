@@ -339,7 +339,7 @@ def run_ours(a):
     scan_events, xsearch.SCAN_EVENTS = xsearch.SCAN_EVENTS, None
     ms_step = max_over_ranks(e0.elapsed_time(e1) / a.steps)
     scan_ms = [s.elapsed_time(e) for s, e in scan_events]
-    scan_ms_avg = sum(scan_ms) / len(scan_ms)          # whole xfbq_scan_topk call (prep + sample + scan + merge)
+    scan_ms_avg = sum(scan_ms) / max(len(scan_ms), 1)  # whole xfbq_scan_topk call (prep + sample + scan + merge)
     kernel_ms, kernel_launches = _native.scan_ms_mean()  # the dominant kernel alone: mean over the launches of the timed region
     kernel_ms = max_over_ranks(kernel_ms)
     _native.set_timing(False)

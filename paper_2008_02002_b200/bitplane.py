@@ -75,13 +75,13 @@ class PackedVector:
     def nbytes(self) -> int:
         return self.planes.nbytes
 
-    def device_words(self):
-        """Query layout uint32 [1][width][4C] on the current CUDA device."""
+    def device_words(self, device=None):
+        """Query layout uint32 [1][width][4C] on `device` (default: the current CUDA device)."""
         torch = _native.require_cuda()
         C = (self.dim + 127) // 128
         host = np.zeros((self.width, 2 * C), dtype=np.uint64)
         host[:, : self.planes.shape[1]] = self.planes
-        return torch.from_numpy(host.view(np.int64).reshape(1, -1)).cuda()
+        return torch.from_numpy(host.view(np.int64).reshape(1, -1)).to(device if device is not None else "cuda")
 
 
 class PackedMatrix:
@@ -117,9 +117,9 @@ class PackedMatrix:
         torch = _native.require_cuda()
         L = _native.lib()
         self._codes = torch.empty(max(int(L.xfbq_db_bytes(self._count, self._dim, self._width)), 16),
-                                  dtype=torch.uint8, device="cuda")
+                                  dtype=torch.uint8, device=torch.device("cuda", torch.cuda.current_device()))
         if self._count:
-            dev = torch.from_numpy(planes.view(np.int64)).cuda()
+            dev = torch.from_numpy(planes.view(np.int64)).to(self._codes.device)
             _native.check(L.xfbq_planes_to_bundles(dev.data_ptr(), self._count, self._dim, self._width,
                                                    self._codes.data_ptr(), _stream_ptr(torch)))
             torch.cuda.current_stream().synchronize()
@@ -258,12 +258,19 @@ def quantize_to_device(values, width: int, scale: float, queries: bool, defer_ch
         n, dim = values.shape
     if dim < 1:
         raise InvalidInputError("dim must be >= 1")
+    # everything lives on the input's device (a CUDA tensor on a non-current device is quantized where it is)
+    dev = values.device if on_device else torch.device("cuda", torch.cuda.current_device())
+    with torch.cuda.device(dev):
+        return _quantize_on(torch, L, dev, values, n, dim, width, scale, queries, on_device, defer_check)
+
+
+def _quantize_on(torch, L, dev, values, n, dim, width, scale, queries, on_device, defer_check):
     st = _stream_ptr(torch)
-    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    bad = torch.zeros(1, dtype=torch.int64, device=dev)
     if queries:
-        out = torch.empty(max(int(L.xfbq_query_bytes(n, dim, width)), 16) // 4, dtype=torch.int32, device="cuda")
+        out = torch.empty(max(int(L.xfbq_query_bytes(n, dim, width)), 16) // 4, dtype=torch.int32, device=dev)
     else:
-        out = torch.empty(max(int(L.xfbq_db_bytes(n, dim, width)), 16), dtype=torch.uint8, device="cuda")
+        out = torch.empty(max(int(L.xfbq_db_bytes(n, dim, width)), 16), dtype=torch.uint8, device=dev)
     row_bytes_out = int(L.xfbq_query_bytes(1, dim, width)) if queries else None
 
     def run(chunk, row0):
@@ -283,7 +290,7 @@ def quantize_to_device(values, width: int, scale: float, queries: bool, defer_ch
             run(values, 0)
     else:
         for row0 in range(0, n, _ROW_CHUNK):
-            chunk = torch.from_numpy(values[row0:row0 + _ROW_CHUNK]).cuda()
+            chunk = torch.from_numpy(values[row0:row0 + _ROW_CHUNK]).to(dev)
             run(chunk, row0)
             del chunk
     if defer_check:

@@ -14,7 +14,14 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <unistd.h>
+
 #include <atomic>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+extern char **environ;
 
 #include "../../include/xfbq_b200.h"
 
@@ -852,8 +859,36 @@ ScanKernel pick_kernel(int wd, int wq, int C) {
     return nullptr;
 }
 
+// Plan overrides come from XFBQ_* environment variables.  They are read ONCE, at the first planning call
+// of the process, into a snapshot: no getenv on the call path (it is not safe against a concurrent setenv) and a plan cannot
+// change between xfbq_scan_workspace_bytes and xfbq_scan_topk.  XFBQ_ENV_LIVE=1 (set before the first call: the test-suite,
+// the experiment tools) re-reads the environment on every call instead, so tests can switch plans in-process.
+struct EnvSnapshot {
+    bool live = false;
+    std::unordered_map<std::string, std::string> kv;
+};
+const EnvSnapshot &env_snapshot() {
+    static EnvSnapshot snap;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char *live = getenv("XFBQ_ENV_LIVE");
+        snap.live = live && *live && strcmp(live, "0") != 0;
+        for (char **e = environ; e && *e; ++e) {
+            if (strncmp(*e, "XFBQ_", 5) != 0) continue;
+            const char *eq = strchr(*e, '=');
+            if (eq) snap.kv.emplace(std::string(*e, eq - *e), std::string(eq + 1));
+        }
+    });
+    return snap;
+}
+const char *env_get(const char *name) {
+    const EnvSnapshot &snap = env_snapshot();
+    if (snap.live) return getenv(name);
+    auto it = snap.kv.find(name);
+    return it == snap.kv.end() ? nullptr : it->second.c_str();
+}
 int env_int(const char *name, int dflt) {
-    const char *v = getenv(name);
+    const char *v = env_get(name);
     if (!v || !*v) return dflt;
     return atoi(v);
 }
@@ -1148,7 +1183,7 @@ int run_counted_seed(unsigned char *ws, const void *tiles, int64_t n, int64_t di
 int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bool have_nibbles, MmaPlan *plan, bool have_tiles = true) {
     MmaPlan pl;
     const int C = static_cast<int>(chunks128(dim));
-    const char *eng = getenv("XFBQ_ENGINE");
+    const char *eng = env_get("XFBQ_ENGINE");
     const bool forced_popc = eng && strcmp(eng, "popc") == 0;
     if (!have_nibbles || forced_popc || wd > 4 || wq > 7 || C < 1 || C > 4 || k > 1024 || nq < 1 || n < 1 ||
         env_int("XFBQ_FORCE_GENERIC", 0)) {
@@ -1255,7 +1290,7 @@ int make_coop_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     CoopPlan pl;
     *plan = pl;
     const int C = static_cast<int>(chunks128(dim));
-    const char *eng = getenv("XFBQ_ENGINE");
+    const char *eng = env_get("XFBQ_ENGINE");
     if (eng && *eng && strcmp(eng, "imma") != 0) return XFBQ_OK;  // part of the mma.sync engine
     if (!have_nibbles || wd > 4 || wq > 7 || C < 1 || C > 4 || k > 1024 || nq < 1 || nq > 16 || n < 1 || env_int("XFBQ_FORCE_GENERIC", 0) ||
         env_int("XFBQ_COOP", 1) == 0 || env_int("XFBQ_SAMPLE", -1) == 0)
@@ -1517,7 +1552,7 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     *plan = pl;
     const TileGeom tg = tile_geom(dim);
     const int C = tg.Cp, KP = tg.KP;
-    const char *eng = getenv("XFBQ_ENGINE");
+    const char *eng = env_get("XFBQ_ENGINE");
     if (eng && *eng && strcmp(eng, "umma") != 0) return XFBQ_OK;  // another engine was asked for
     const bool forced = eng && strcmp(eng, "umma") == 0;
     if (!have_nibbles || wq > 7 || tg.CP < 1 || tg.CP > 8 || k > 1024 || n < 1 || env_int("XFBQ_FORCE_GENERIC", 0))  // any document width: the B operand is u8
@@ -1629,8 +1664,12 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
     p.seed_hist = sh.count ? reinterpret_cast<uint32_t *>(ws + pl.off_seedhist) : nullptr;
     p.list_counts = direct ? reinterpret_cast<int *>(ws + pl.off_counts) : nullptr;
     p.prof = (&sh == &pl.main) ? g_prof : nullptr;
-    p.pace = env_int("XFBQ_UMMA_PACE", 48);
+    p.pace = 48;
+#ifdef XFBQ_DEBUG_KNOBS  // timing experiments only (results are NOT valid under them): compiled out of the shipped library
     p.debug = env_int("XFBQ_UMMA_DEBUG", 0);
+#else
+    p.debug = 0;
+#endif
     if (sh.slots > 1 && !sh.queue && !sh.count) {  // slots a group does not use stay KEY_INF (the queue kernel writes every slice)
         e = cudaMemsetAsync(p.out, 0xFF, sh.parts_bytes, st);
         if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
@@ -1733,7 +1772,9 @@ int run_umma(const UmmaPlan &up, unsigned char *ws, const void *nib, int64_t n, 
             while ((static_cast<int64_t>(umma::HIST_BINS) << shift) < ub / 56) ++shift;
             g_hist_shift = env_int("XFBQ_UMMA_HIST_SHIFT", shift);
         }
+#ifdef XFBQ_DEBUG_KNOBS
         if (env_int("XFBQ_DEBUG_TAU_NEVER", 0)) cudaMemsetAsync(tau, 0x40, static_cast<size_t>(nq) * 4, st);  // timing experiments only: nothing passes
+#endif
     }
     return run_umma_scan(up.main, up, ws, nib, n, C, nq, k, row_offset, tau_init, keys_out, st);
 }

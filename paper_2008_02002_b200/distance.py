@@ -52,7 +52,7 @@ def batch_distances_device(matrix: PackedMatrix, query: PackedVector):
     torch = _native.require_cuda()
     L = _native.lib()
     with torch.cuda.device(matrix.codes.device):
-        q = query.device_words()
+        q = query.device_words(matrix.codes.device)
         d = torch.empty(matrix.count, dtype=torch.int64, device=matrix.codes.device)
         _native.check(L.xfbq_batch_distances(matrix.codes.data_ptr(), matrix.count, matrix.dim, matrix.width,
                                              q.data_ptr(), query.width, d.data_ptr(), _stream_ptr(torch)))
@@ -70,7 +70,7 @@ def collect_candidates_device(matrix: PackedMatrix, query, threshold: int, want_
     dev = matrix.codes.device
     with torch.cuda.device(dev):
         if isinstance(query, PackedVector):
-            q, wq = query.device_words(), query.width
+            q, wq = query.device_words(dev), query.width
         else:
             q, wq = query, int(query_bits)
         nib = getattr(matrix, "_nibbles", None) if wq <= 7 else None

@@ -98,9 +98,15 @@ def _search_small_fused(index: Index, queries, k: int, row_offset: int):
     ws = _workspace(torch, dev, ws_bytes)
     fn = L.xfbq_search_small_f32 if queries.dtype == torch.float32 else L.xfbq_search_small_f64
     ld = queries.stride(0) if nq > 1 else packed.dim
+    if SCAN_EVENTS is not None:
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
     _native.check(fn(packed.codes.data_ptr(), nib.data_ptr(), packed.count, packed.dim, packed.width, queries.data_ptr(), nq, ld,
                      float(p.scale), p.query_bits, k, int(row_offset), keys.data_ptr(), counter.data_ptr(), ws.data_ptr(), ws.numel(),
                      _stream_ptr(torch)))
+    if SCAN_EVENTS is not None:
+        ev[1].record()
+        SCAN_EVENTS.append(ev)
     return keys, counter
 
 

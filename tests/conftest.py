@@ -4,6 +4,11 @@ from pathlib import Path
 
 import pytest
 
+import os
+
+# the library snapshots its XFBQ_* plan overrides at first use; the tests switch plans in-process (monkeypatch.setenv)
+os.environ.setdefault("XFBQ_ENV_LIVE", "1")
+
 ROOT = Path(__file__).resolve().parent.parent
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))

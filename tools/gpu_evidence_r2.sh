@@ -33,4 +33,9 @@ done
 for v in 0 1 4 5; do compute-sanitizer --tool racecheck tools/bin/sanitizer_probe $v 2>&1 | grep -E "variant|RACECHECK SUMMARY"; done > gpurun_out/racecheck_probe_r2.log 2>&1
 for v in 2 3; do compute-sanitizer --tool synccheck tools/bin/sanitizer_probe $v 2>&1 | grep -E "variant|ERROR SUMMARY|Barrier error" | sort | uniq -c; done > gpurun_out/synccheck_probe_r2.log 2>&1
 timeout 900 python tools/umma_stress.py 1 60 > gpurun_out/umma_stress_r2.log 2>&1; echo "stress rc=$?"
-ls -la gpurun_out | tail -40
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_r2.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu_r2.log
+rm -f gpurun_out/*.ncu-rep gpurun_out/src_*.csv   # only the exported summaries travel back (64 MiB limit)
+for f in gpurun_out/memcheck_*_r2.log gpurun_out/racecheck_*_r2.log gpurun_out/synccheck_*_r2.log; do   # keep heads + summaries of the sanitizer logs
+  if [ -f "$f" ] && [ $(stat -c %s "$f") -gt 200000 ]; then (head -150 "$f"; echo "[... $(wc -l < "$f") lines in all ...]"; grep -E "SUMMARY|match|k_select|small batch" "$f" | tail -12) > "$f.tmp" && mv "$f.tmp" "$f"; fi
+done
+du -sh gpurun_out; ls -la gpurun_out | tail -45

@@ -1,4 +1,5 @@
 import os, sys
+os.environ.setdefault('XFBQ_ENV_LIVE', '1')
 from pathlib import Path
 import numpy as np
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))

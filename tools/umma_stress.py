@@ -1,5 +1,6 @@
 """Randomised small-shape stress of the tcgen05 engine against the CPU oracle (tiny n, k up to n, ragged dims)."""
 import os, sys
+os.environ.setdefault('XFBQ_ENV_LIVE', '1')
 from pathlib import Path
 import numpy as np
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
