@@ -2,7 +2,7 @@
 
 Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
 ``--impl reference`` legs may import this module.  Nothing under
-``paper_2008_02002_b200/`` imports it (tests/test_layout_rules.py enforces that).
+``paper_2008_02002_b200/`` imports it (tests/test_abi.py::test_product_never_imports_oracle enforces that).
 
 Two independent restatements of the reference algorithm live here:
 

@@ -82,6 +82,12 @@ def test_config3_glove_shaped_1p2m_200_4bit_top10_10k_queries():
     _check_config(n=1_200_000, dim=200, wd=4, wq=4, k=10, nq=10_000, n_check=256, seed=3000)
 
 
+def test_config4_deep_shaped_10m_256_4bit_top100_10k_queries():
+    """The headline workload itself at full size against the CPU oracle (every row's codes; 48 strided queries of the 10k-query
+    production batch; single queries and an 8-query batch through the single-launch path)."""
+    _check_config(n=10_000_000, dim=256, wd=4, wq=4, k=100, nq=10_000, n_check=48, seed=4000)
+
+
 def test_config5_shard_2p5m_512_4bit_top1000_batched_and_single_query():
     """One GPU's part of config 5 (100M x 512 over 8 GPUs = 12.5M rows each; 2.5M rows here keep the CPU side at
     seconds): top-1000, a 1 024-query batch (tcgen05 engine, k = 1000 lists) and single queries."""
