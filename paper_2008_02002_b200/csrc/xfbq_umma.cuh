@@ -135,7 +135,10 @@ __device__ __forceinline__ bool elect_one() {  // one lane of a converged warp
 }
 // bar.sync is the .aligned barrier: every thread of a warp must arrive converged.  Role branches end in lane-dependent code
 // (`if (lane == 0)`, `if (valid)`), and reconvergence after those is not guaranteed without a warp barrier (synccheck).
-__device__ __forceinline__ void cta_sync() {
+// The barrier lives in ONE out-of-line function: every role of a kernel then arrives at the same bar.sync instruction, which
+// is what compute-sanitizer's synccheck expects of a CTA-wide barrier (it reports arrivals from different call sites as
+// "divergent threads").  Barriers are per work item, not per stage, so the call costs nothing measurable.
+__device__ __noinline__ void cta_sync() {
     __syncwarp();
     asm volatile("bar.sync 0;" ::: "memory");
 }
