@@ -12,9 +12,10 @@ query batch: quantize queries -> fused XOR/POPC scan + top-K over the (sharded) 
 
 Prints ONE JSON line (rank 0).  `value` = whole-job QPS with inputs resident in HBM, `e2e` = QPS
 through the public API with host query buffers (H2D + D2H inside the timed region), `roofline`
-= the scan kernel against the measured HBM peak, `cpu_baseline` = the CPU port timed on this
-box's cores on a bounded sample.  Multi-GPU: the database is row-sharded (total fixed ->
-"strong" scaling), one all-gather of [nq, k] keys + a merge kernel per step.
+= the dominant kernel against the measured tcgen05 int8 rate, `roofline_hbm` = the single-launch small-batch search
+against the measured HBM peak, `cpu_baseline` = the CPU port timed on this box's cores on a bounded sample.
+Multi-GPU: an R x Q grid of row shards x query blocks (sharded.py; `--layout`), the total workload fixed ->
+"strong" scaling, one all-gather of the key blocks (+ a merge kernel when R > 1) per step.
 """
 from __future__ import annotations
 
