@@ -1272,7 +1272,8 @@ struct CoopPlan {
     bool ok = false;
     int C = 1, cap = 0, RR = 0, grid = 0, seed_shift = 0, seed_offset = 0, hist_shift = 0, B = 0;
     int64_t stages = 0, seed_stride = 1;
-    size_t smem = 0, off_qop = 0, off_qconst = 0, off_shist = 0, off_theta = 0, off_chist = 0, off_counts = 0, off_lists = 0, bytes = 0;
+    size_t smem = 0, off_qop = 0, off_qconst = 0, off_shist = 0, off_theta = 0, off_chist = 0, off_counts = 0, off_final = 0, off_lists = 0, bytes = 0;
+    int final_cap = 0;
 };
 
 typedef void (*CoopKernel)(const coop::Params);
@@ -1345,6 +1346,8 @@ int make_coop_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     pl.off_theta = off; off = align256(off + 3 * 16 * 4);  // theta_g, theta0, row_bad
     pl.off_chist = off; off = align256(off + static_cast<size_t>(16) * coop::CAND_BINS * 4);
     pl.off_counts = off; off = align256(off + static_cast<size_t>(pl.grid) * coop::WARPS * 16 * 4);
+    pl.final_cap = pl.B - coop::WARPS * 32;   // what one sort of the merge buffer takes
+    pl.off_final = off; off = align256(off + 16 * 4 + static_cast<size_t>(16) * pl.final_cap * 8);
     pl.off_lists = off; off = align256(off + static_cast<size_t>(pl.grid) * coop::WARPS * 16 * cap * 8);
     pl.bytes = off;
     pl.ok = true;
@@ -1390,6 +1393,9 @@ int run_coop(const CoopPlan &cp, unsigned char *ws, const void *nib, int64_t n, 
     p.chist = reinterpret_cast<uint32_t *>(ws + cp.off_chist);
     p.lists = reinterpret_cast<uint64_t *>(ws + cp.off_lists);
     p.counts = reinterpret_cast<int *>(ws + cp.off_counts);
+    p.final_cnt = reinterpret_cast<unsigned *>(ws + cp.off_final);
+    p.final_list = reinterpret_cast<uint64_t *>(ws + cp.off_final + 64);
+    p.final_cap = cp.final_cap;
     p.keys_out = keys_out;
     p.stages = cp.stages; p.seed_tile_stride = cp.seed_stride;
     p.k = k; p.cap = cp.cap; p.RR = cp.RR;

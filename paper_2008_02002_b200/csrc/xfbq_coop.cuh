@@ -55,7 +55,10 @@ struct Params {
     int32_t *theta0;           // [16] seeded thresholds: origin of the candidate histogram
     uint32_t *chist;           // [16][CAND_BINS]
     uint64_t *lists;           // [grid * WARPS][16][cap]
-    int *counts;               // [grid * WARPS][16]
+    int *counts;               // [16][grid * WARPS] list lengths (row-major by query: coalesced for the merging CTA)
+    uint64_t *final_list;      // [16][final_cap] list entries the FINAL thresholds still admit, forwarded by every warp after the scan
+    unsigned *final_cnt;       // [16] their number (may exceed final_cap: then the merging CTA reads the lists themselves)
+    int final_cap;
     uint64_t *keys_out;        // [nq][k]
     int64_t stages;            // stages of WARPS * TILE documents
     int64_t seed_tile_stride;  // sample tile i of the grid is tile i * seed_tile_stride of the database
@@ -189,6 +192,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) search_kernel(const Params p) {
         for (int64_t i = gtid; i < 16 * CAND_BINS; i += gthreads) p.chist[i] = 0u;
         if (gtid < 16) { p.theta_g[gtid] = TAU_OPEN; p.theta0[gtid] = TAU_OPEN; }
         if (gtid == 0 && p.inexact) *p.inexact = 0;
+        if (gtid < 16) p.final_cnt[gtid] = 0u;
         for (int row = blockIdx.x; row < 16; row += gridDim.x)
             if (warp == 0) prep_row(p, row, C, lane);
     }
@@ -442,6 +446,32 @@ __global__ void __launch_bounds__(WARPS * 32, 1) search_kernel(const Params p) {
     __threadfence();
     grid.sync();
     stamp(4);
+    // ---- 5a: the thresholds are final now; every warp forwards the entries of its own lists that they still admit (about k per
+    // query in all, against ~20 k entries at k = 1000) to one compact list per query, so that the merging CTA sorts a handful
+    // of keys instead of walking 2 368 lists (merge 85 -> see profiles, 12.5M x 512, k = 1000)
+    {
+        const int tgf = row_valid ? __ldcg(p.theta_g + lane) : TAU_OPEN;
+        for (int r = 0; r < p.nq; ++r) {
+            const int cnt = cnt_s[r];
+            const int tg = __shfl_sync(0xffffffffu, tgf, r), dq = __shfl_sync(0xffffffffu, my_dq, r);
+            const long long limit = tg > TAU_OPEN ? static_cast<long long>(dq) - tg + p.extra : 0x7FFFFFFFll;
+            for (int e0 = 0; e0 < cnt; e0 += 32) {
+                const int e = e0 + lane;
+                const uint64_t key = e < cnt ? __ldcg(lists + r * p.cap + e) : KEY_INF;
+                const bool keep = key != KEY_INF && static_cast<long long>(key >> 32) <= limit;
+                const unsigned m = __ballot_sync(0xffffffffu, keep);
+                if (m) {
+                    unsigned base = 0;
+                    if (lane == 0) base = atomicAdd(p.final_cnt + r, static_cast<unsigned>(__popc(m)));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    const unsigned pos = base + __popc(m & ((1u << lane) - 1u));
+                    if (keep && pos < static_cast<unsigned>(p.final_cap)) p.final_list[static_cast<int64_t>(r) * p.final_cap + pos] = key;
+                }
+            }
+        }
+    }
+    __threadfence();
+    grid.sync();
     for (int r = blockIdx.x; r < p.nq; r += gridDim.x) {
         const int parts = static_cast<int>(gridDim.x) * WARPS;
         __syncthreads();
@@ -449,6 +479,36 @@ __global__ void __launch_bounds__(WARPS * 32, 1) search_kernel(const Params p) {
             for (int i = threadIdx.x; i < p.k; i += blockDim.x) p.keys_out[static_cast<int64_t>(r) * p.k + i] = KEY_INF;
             continue;
         }
+        const unsigned nfin = __ldcg(p.final_cnt + r);
+        if (nfin <= static_cast<unsigned>(p.final_cap) && static_cast<int>(nfin) + static_cast<int>(blockDim.x) <= p.merge_B) {
+            // ---- 5b: sort the compact list, write the k best; k_select's candidates are counted from it as well
+            const uint64_t *fl = p.final_list + static_cast<int64_t>(r) * p.final_cap;
+            merge_bounded_block(reinterpret_cast<uint64_t *>(smem_raw), p.merge_B, p.k, static_cast<int64_t>(nfin), 0x7FFFFFFFll,
+                                [&](int64_t e) -> uint64_t { return __ldcg(fl + e); }, p.keys_out + static_cast<int64_t>(r) * p.k);
+            if (p.cand_count) {
+                __syncthreads();
+                const int valid = static_cast<int>(nfin) < p.k ? static_cast<int>(nfin) : p.k;
+                const long long thr = valid > 0 ? static_cast<long long>(__ldcg(p.keys_out + static_cast<int64_t>(r) * p.k + valid - 1) >> 32) + p.extra : -1;
+                if (threadIdx.x == 0) p.cand_count[r] = 0ull;
+                __syncthreads();
+                for (unsigned e0 = 0; e0 < nfin; e0 += blockDim.x) {
+                    const unsigned e = e0 + threadIdx.x;
+                    const uint64_t key = e < nfin ? __ldcg(fl + e) : KEY_INF;
+                    const bool hit = key != KEY_INF && static_cast<long long>(key >> 32) <= thr;
+                    const unsigned m = __ballot_sync(0xffffffffu, hit);
+                    if (m) {
+                        unsigned long long base = 0;
+                        if (lane == 0) base = atomicAdd(p.cand_count + r, static_cast<unsigned long long>(__popc(m)));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        const int64_t pos = static_cast<int64_t>(base) + __popc(m & ((1u << lane) - 1u));
+                        if (hit && p.cand_ids && pos < p.cand_cap) p.cand_ids[static_cast<int64_t>(r) * p.cand_cap + pos] = static_cast<int64_t>(key & 0xFFFFFFFFull);
+                    }
+                }
+            }
+            if (p.prof && r == 0 && threadIdx.x == 0) { p.prof[5] = now_ns(); p.prof[6] = static_cast<unsigned long long>(nfin); }
+            continue;
+        }
+        // ---- fallback (more admitted entries than the compact list holds: heavy ties): walk the lists themselves
         {   // s_pre[i] = entries in lists < i: thread t sums its run of PER lists, a block scan over the 512 partial sums follows
             constexpr int PER = (148 * WARPS + WARPS * 32 - 1) / (WARPS * 32);
             int len[PER], sum = 0;
