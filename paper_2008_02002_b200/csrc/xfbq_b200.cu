@@ -161,16 +161,22 @@ quantize_pack_kernel(const T *__restrict__ x, int64_t n, int dim, int64_t ld, do
 
 
 // Fast quantizer for float32 rows (16-byte aligned, dim % 4 == 0).  Same result as quantize_one for every
-// input, with float64 touched only near a code boundary:
-//   yz = x * fl32(scale * 2^(w-1) * 2^16)  carries a relative error <= 2^-23 against the exact product, i.e.
-//   < 2.1 units of 2^-16 for |y| < 2^(w-1) + 2 <= 130; so when the 16 fraction bits of floor(yz) lie in
-//   [4, 65531] the float64 value the reference computes, floor((double(x) * scale) * 2^(w-1)), has the same
-//   integer part (quant.py:146).  yz is first clamped to +-(2^(w-1) + 1.5) * 2^16: saturating values land on
-//   fraction 0x8000, pass the test and are clipped like quant.py:147 does.  Anything else -- about 1 element
-//   in 10^4, plus every non-finite value -- is flagged in a per-lane bit mask and redone in float64 after the
-//   branch-free main loop.  x == 0 is exact (t = 0) and never flagged.
-// A lane owns 32 consecutive dimensions of one document (8 LDG.128 in flight), builds its word of every bit
-// plane in registers, and the warp's stores of one plane are 128 contiguous bytes of the bundle layout.
+// input, with float64 touched only near a code boundary.  The clip range [-1/scale, 1/scale) is mapped onto the
+// whole int32 range, one code = 2^(32-w) integers:
+//   Z = cvt.rmi.s32.f32( fma(x, fl32(scale * 2^31), 1024) )        (the conversion saturates: quant.py:147's clip for free)
+//   code = top w bits of (Z xor 0x7FFFFFFF)                          (= 2^(w-1) - 1 - (Z >> (32-w)), quant.py:148)
+// fl32(scale * 2^31) and the fused multiply-add each carry a relative error <= 2^-24, i.e. together < 257 integers for
+// in-range values, so when the low 32-w bits of Z lie in [2048, 2^(32-w)) the exact product lies strictly inside the
+// same code step, and so does the float64 value the reference floors (quant.py:146; its own rounding is 2^-22 of an
+// integer).  Values beyond the range saturate to the end codes like the reference's clip; the lower end is lifted to
+// INT_MIN + 2048 so that it does not look like a boundary.  Everything else -- a value within 2^-21 of the range from a
+// code boundary (x = 0 sits exactly on one: its code is right, float multiplication keeps zero exact), about 1 element in
+// 10^5 (4-bit) to 10^4 (8-bit) -- is caught by a per-8-elements minimum of the masked low bits and re-examined after the
+// branch-free loop; the truly ambiguous ones are redone in float64.  Non-finite inputs poison a running fma(x, 0, acc)
+// and take the same route (quant.py:142-143).  Per element: 2 FFMA, F2I, VIMNMX, LOP3, half a VIMNMX3, SHF (codes wider
+// than 4 bits: two more shifts).
+// A lane owns 32 dimensions of one document (8 LDG.128 in flight; which ones: see the load mapping in the kernel), builds
+// their bits of every plane in registers, and the warp's stores of one plane are 128 contiguous bytes of the bundle layout.
 // 4x4 bit-block transpose of four 32-bit words (delta swaps; its own inverse): plane words <-> nibble words
 __device__ __forceinline__ void transpose_4x4_blocks(uint32_t &p0, uint32_t &p1, uint32_t &p2, uint32_t &p3) {
     uint32_t t;
@@ -180,18 +186,34 @@ __device__ __forceinline__ void transpose_4x4_blocks(uint32_t &p0, uint32_t &p1,
     t = ((p1 >> 2) ^ p3) & 0x33333333u; p3 ^= t; p1 ^= t << 2;
 }
 
+constexpr int QF_WIN = 1024;  // half width of the boundary window, in int32 units of the mapped range
+
+template <int WIDTH>
+__device__ __forceinline__ int quant_fast_z(float e, float s32) {
+    return max(__float2int_rd(fmaf(e, s32, static_cast<float>(QF_WIN))), INT_MIN + 2 * QF_WIN);
+}
+
 template <int WIDTH>
 __global__ void __launch_bounds__(256)
 quantize_pack_f32_fast_kernel(const float *__restrict__ x, int64_t n, int dim, int64_t ld, double scale,
                               int C, uint32_t *__restrict__ out, unsigned long long *__restrict__ nonfinite) {
     const int lane = threadIdx.x & 31;
     const int d = lane >> 2, t = lane & 3;
-    constexpr int ihalf = 1 << (WIDTH - 1);
-    const double half = static_cast<double>(ihalf);
-    const float sz = static_cast<float>(scale * half * 65536.0);
-    constexpr float satc = (static_cast<float>(ihalf) + 1.5f) * 65536.0f;
+    constexpr int SH = 32 - WIDTH;
+    constexpr int MASK = static_cast<int>(((1u << SH) - 1u) & ~(2u * QF_WIN - 1u));  // low bits of a step, minus the window
+    const double half = static_cast<double>(1 << (WIDTH - 1));
+    const float s32 = static_cast<float>(scale * 2147483648.0);
     const int64_t nb = (n + 31) >> 5;
     const int64_t units = nb * C * 4;  // (bundle, chunk, group of 8 documents)
+    // Load mapping.  A warp takes 8 documents x 128 dimensions; the four lanes of a document share each 128-byte line:
+    // load j = 2 t' + h of lane t fetches dimensions 32 t' + 8 t + 4 h .. + 3, so one load instruction touches 8 lines
+    // (one per document), not 32 -- the L1 looks up one line per cycle, and with a lane owning 32 CONSECUTIVE
+    // dimensions (32 lines per instruction, 16 bytes each) the kernel sat at 16 B/clk/SM = 4.4 TB/s whatever the ALU
+    // work.  A lane's element 4 j + q is then bit 8 t + (4 h + q) of plane word t': byte t' of the lane's plane word
+    // belongs to output word t', at byte position t -- a 4 x 4 byte transpose among the four lanes, two rounds of one
+    // shuffle and one byte permute per plane, and lane t ends up with output word t.
+    const uint32_t sel1 = (t & 1) ? 0x3715u : 0x6240u;  // round 1 (partner t ^ 1): [even source, odd source] x [dest parity of t, + 2]
+    const uint32_t sel2 = (t & 2) ? 0x3276u : 0x5410u;  // round 2 (partner t ^ 2): sources 0..3 of this lane's own word
     unsigned long long bad = 0;
     for (int64_t u = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; u < units;
          u += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
@@ -200,50 +222,77 @@ quantize_pack_f32_fast_kernel(const float *__restrict__ x, int64_t n, int dim, i
         const int c = static_cast<int>(bc % C);
         const int64_t b = bc / C;
         const int64_t doc = b * 32 + s8 * 8 + d;
-        const int k0 = c * 128 + t * 32;
-        const float *src = x + doc * ld + k0;
-        // dimensions k0 .. k0 + 31 that exist (dim % 4 == 0: whole float4s), none for a padding document
-        const int nvalid = doc < n ? min(max(dim - k0, 0), 32) : 0;
-        const uint32_t valid = nvalid >= 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
+        const float *src = x + doc * ld + c * 128 + 8 * t;
+        // dimensions of this chunk that exist (dim % 4 == 0: whole float4s), none for a padding document
+        const int nvc = doc < n ? min(max(dim - c * 128, 0), 128) - 8 * t : 0;
         float4 v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = 4 * j < nvalid ? __ldg(reinterpret_cast<const float4 *>(src + 4 * j)) : make_float4(0.f, 0.f, 0.f, 0.f);
-        constexpr bool NIBBLES = WIDTH <= 4;  // codes fit a nibble: pack them first, transpose to bit planes once per 32
-        uint32_t w[NIBBLES ? 4 : WIDTH];
-#pragma unroll
-        for (int i = 0; i < (NIBBLES ? 4 : WIDTH); ++i) w[i] = 0u;
-        uint32_t redo = 0u;
+        uint32_t valid = 0u;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
+            const int off = 32 * (j >> 1) + 4 * (j & 1);
+            const bool ok = off < nvc;
+            v[j] = ok ? __ldg(reinterpret_cast<const float4 *>(src + off)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            valid |= ok ? 0xFu << (4 * j) : 0u;
+        }
+        // Codes are collected as nibbles (word q: nibble j = element 4j + q) and turned into bit planes by one 4 x 4
+        // bit-block transpose per 32 elements; codes wider than 4 bits as two nibbles (the top 8 bits of Z).
+        constexpr bool WIDE = WIDTH > 4;
+        uint32_t w[4] = {0u, 0u, 0u, 0u}, wl[4] = {0u, 0u, 0u, 0u};
+        int m[4] = {MASK, MASK, MASK, MASK};  // per 8 elements: minimum of the masked low bits (0 = somebody is near a boundary)
+        float poison = 0.0f;                  // NaN once any element is not finite
+#pragma unroll
+        for (int j = 7; j >= 0; --j) {        // nibbles are shifted in from the bottom: last one first
             const float e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+            int z[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const float yz = fminf(fmaxf(e[q] * sz, -satc), satc);
-                const int z = __float2int_rd(yz);
-                const bool inexact = ((static_cast<unsigned>(z) & 0xFFFFu) - 4u > 65527u && e[q] != 0.0f) || !(fabsf(e[q]) <= 3.402823466e38f);
-                redo = __funnelshift_r(redo, inexact ? 1u : 0u, 1);
-                const unsigned code = static_cast<unsigned>(ihalf - 1 - min(max(z >> 16, -ihalf), ihalf - 1));  // quant.py:147-148
-                if (NIBBLES) {
-                    w[q] = __funnelshift_r(w[q], code, 4);  // word q: nibble j = code of element 4j + q
-                } else {
+                z[q] = quant_fast_z<WIDTH>(e[q], s32);
+                poison = fmaf(e[q], 0.0f, poison);
+                w[q] = __funnelshift_l(static_cast<uint32_t>(z[q]), w[q], 4);            // bits 31..28 of Z
+                if (WIDE) wl[q] = __funnelshift_l(static_cast<uint32_t>(z[q]) << 4, wl[q], 4);  // bits 27..24
+            }
+            m[j >> 1] = min(min(m[j >> 1], z[0] & MASK), z[1] & MASK);
+            m[j >> 1] = min(min(m[j >> 1], z[2] & MASK), z[3] & MASK);
+        }
+        uint32_t p[WIDTH];  // p[i] = bit plane i of the lane's 32 elements
 #pragma unroll
-                    for (int i = 0; i < WIDTH; ++i) w[i] = __funnelshift_r(w[i], code >> i, 1);  // after 32 elements bit p = element p
+        for (int q = 0; q < 4; ++q) { w[q] ^= 0x77777777u; wl[q] = ~wl[q]; }  // the code is the top WIDTH bits of Z xor 0x7FFFFFFF (quant.py:147-148)
+        transpose_4x4_blocks(w[0], w[1], w[2], w[3]);   // -> w[i] = bit 28 + i of every Z
+        if (WIDE) transpose_4x4_blocks(wl[0], wl[1], wl[2], wl[3]);   // -> wl[i] = bit 24 + i
+#pragma unroll
+        for (int i = 0; i < WIDTH; ++i) {   // code bit i = bit 32 - WIDTH + i of Z
+            const int zb = 32 - WIDTH + i;
+            p[i] = zb >= 28 ? w[zb - 28] : wl[zb >= 24 ? zb - 24 : 0];
+        }
+        uint32_t groups = 0u;
+        const bool poisoned = !(poison == poison);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) if ((m[g] == 0 || poisoned) && 32 * g < nvc) groups |= 1u << g;
+        while (groups) {  // rare: look at the group's elements again; exact float64 path for the ambiguous ones (re-read through L1)
+            const int g = __ffs(groups) - 1;
+            groups &= groups - 1;
+            for (int r = 0; r < 8; ++r) {
+                const int pos = 8 * g + r;
+                if (!((valid >> pos) & 1u)) break;
+                const float e = src[32 * g + r];
+                const int z = quant_fast_z<WIDTH>(e, s32);
+                if (((z & MASK) == 0 && e != 0.0f) || !(fabsf(e) <= 3.402823466e38f)) {
+                    const unsigned code = quantize_one<float>(e, scale, half, bad);
+#pragma unroll
+                    for (int i = 0; i < WIDTH; ++i) p[i] = (p[i] & ~(1u << pos)) | (((code >> i) & 1u) << pos);
                 }
             }
         }
-        if (NIBBLES) transpose_4x4_blocks(w[0], w[1], w[2], w[3]);  // -> w[i] = bit plane i
-        redo &= valid;
-        while (redo) {  // rare: exact float64 path for the flagged elements (re-read through L1)
-            const int pos = __ffs(redo) - 1;
-            redo &= redo - 1;
-            const unsigned code = quantize_one<float>(src[pos], scale, half, bad);
-#pragma unroll
-            for (int i = 0; i < WIDTH; ++i) w[i] = (w[i] & ~(1u << pos)) | (((code >> i) & 1u) << pos);
-        }
+        __syncwarp();
         // bundle layout: 16-byte word ((b * width + i) * C + c) * 32 + doc-in-bundle, 32-bit word t
         const int64_t lane_word = static_cast<int64_t>(s8 * 8 + d) * 4 + t;
 #pragma unroll
-        for (int i = 0; i < WIDTH; ++i) out[(((b * WIDTH + i) * C + c) * 32) * 4 + lane_word] = w[i] & valid;
+        for (int i = 0; i < WIDTH; ++i) {
+            const uint32_t mine = p[i] & valid;
+            const uint32_t x1 = __byte_perm(mine, __shfl_xor_sync(0xffffffffu, mine, 1), sel1);
+            const uint32_t x2 = __byte_perm(x1, __shfl_xor_sync(0xffffffffu, x1, 2), sel2);
+            out[(((b * WIDTH + i) * C + c) * 32) * 4 + lane_word] = x2;
+        }
     }
     if (bad) atomicAdd(nonfinite, bad);
 }
@@ -1800,7 +1849,7 @@ int quantize_pack_impl(const T *x, int64_t n, int64_t dim, int64_t ld, double sc
     if (int rc = device_info(&info)) return rc;
     const int64_t nb = bundles_of(n);
     if (sizeof(T) == 4 && dim % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
-        scale * static_cast<double>(1 << (width - 1)) * 65536.0 <= 1e30 && env_int("XFBQ_QUANT_SLOW", 0) == 0) {
+        scale * 2147483648.0 <= 1e30 && scale * 2147483648.0 >= 1e-30 && env_int("XFBQ_QUANT_SLOW", 0) == 0) {
         const int64_t units = nb * chunks128(dim) * 4;
         int64_t fblocks = (units + 7) / 8;
         const int64_t fmax = static_cast<int64_t>(info.sms) * 16;

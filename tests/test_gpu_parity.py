@@ -267,8 +267,8 @@ def test_small_batches_counted_seed(extra, n, dim, wd, nq, k, monkeypatch):
 @pytest.mark.parametrize("width", [1, 2, 3, 4, 5, 6, 7, 8])
 def test_fast_float32_quantizer_on_code_boundaries(width, monkeypatch):
     """The float32-first quantizer (exact float64 redo near code boundaries) against the CPU oracle and the
-    all-float64 kernel: values on, one ulp and two ulps around every code boundary, saturation edges,
-    denormals, +-0, huge values, plus random data; dims that leave a ragged last float4 group of a lane."""
+    all-float64 kernel: values on and up to 40 ulps around every code boundary, saturation edges, denormals, +-0,
+    huge values, zero-heavy rows, plus random data; dims that leave a ragged last float4 group of a lane."""
     import torch
     rng = np.random.default_rng(100 + width)
     for scale in (1.0, 0.7310585786300049, 3.3333333333333335, 12.345, 1e-3):
@@ -278,7 +278,14 @@ def test_fast_float32_quantizer_on_code_boundaries(width, monkeypatch):
         dn = np.nextafter(g32, np.float32(-np.inf))
         special = np.array([0.0, -0.0, 1e-45, -1e-45, 1e-38, -1e-38, 3e38, -3e38, 1.0, -1.0, 0.5, -0.5], dtype=np.float32)
         rnd = rng.uniform(-2, 2, size=6000).astype(np.float32) / np.float32(scale)
-        vals = np.concatenate([g32, up, dn, np.nextafter(up, np.float32(np.inf)), np.nextafter(dn, np.float32(-np.inf)), special, rnd])
+        # every float32 within 40 ulps of a boundary: the fast path's window (+-1024 of 2^32 integers over the clip range) is
+        # 8-16 ulps wide at the outer boundaries, so both its edges and its inside are covered
+        bits = g32.view(np.int32)[None, :] + np.arange(-40, 41, dtype=np.int32)[:, None]
+        sweep = bits.astype(np.int32).view(np.float32).ravel()
+        sweep = sweep[np.isfinite(sweep)]
+        sparse = rnd[:2000] * (rng.random(2000) < 0.3)   # zero-heavy rows: x = 0 sits exactly on a boundary
+        vals = np.concatenate([g32, up, dn, np.nextafter(up, np.float32(np.inf)), np.nextafter(dn, np.float32(-np.inf)), special, rnd,
+                               sweep, sparse.astype(np.float32)])
         dim = 200                                   # ragged: the fourth lane of a row holds 8 of its 32 dims
         vals = np.concatenate([vals, np.zeros((-len(vals)) % dim, np.float32)]).reshape(-1, dim).astype(np.float32)
         want = xo.c_quantize_matrix(vals, width, scale)
@@ -292,6 +299,11 @@ def test_fast_float32_quantizer_on_code_boundaries(width, monkeypatch):
         xb.quantize_matrix(torch.tensor([[1.0, float("inf"), 0.0, 0.0]], device="cuda"), width, 1.0)
     with pytest.raises(xb.InvalidInputError):
         xb.quantize_matrix(torch.tensor([[float("nan"), 0.0, 0.0, 0.0]], device="cuda"), width, 1.0)
+    for bad in (float("inf"), float("-inf"), float("nan")):   # anywhere in a row, among ordinary values
+        rows = rng.uniform(-1, 1, size=(70, 256)).astype(np.float32)
+        rows[33, 157] = bad
+        with pytest.raises(xb.InvalidInputError):
+            xb.quantize_matrix(torch.from_numpy(rows).cuda(), width, 1.0)
 
 
 def test_concurrent_searches_are_deterministic():
