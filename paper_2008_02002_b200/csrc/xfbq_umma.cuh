@@ -1135,13 +1135,15 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
     } else if (warp == Q_MMA_WARP) {
         // ================================ MMA issuer ================================
         const uint32_t b_lo0 = desc_lo(smem_u32(sB));
-        const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+        if (tmem != 0u) __trap();  // the CTA owns all 512 columns: the allocation starts at lane 0, column 0 (addresses below rely on it)
+        constexpr uint32_t tm = 0u;
         while (sg.next()) {
             cta_sync();
             fence_after();
             Ring rb{static_cast<int>((s_run * KP) % NS), ((s_run * KP) / NS) & 1u};
             const uint32_t u0 = s_run * MT;
             Ring ac{static_cast<int>(u0 % AB), ((u0 / AB) & 1u) ^ 1u};
+            if constexpr (KP > 1) {
             for (int i = 0; i < sg.cnt; ++i) {
                 if constexpr (KP > 1) {  // one accumulator per tile, fed by KP operand stages
                     const uint32_t buf = ac.idx;
@@ -1168,33 +1170,76 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                         rb.advance(NS);
                     }
                     ac.advance(AB);
-                    continue;
                 }
-                if (prof) mbar_wait_prof(&b_full[rb.idx], rb.phase, true, w0); else mbar_wait_tight(&b_full[rb.idx], rb.phase);
-                fence_after();
+            }
+            } else {
+            // One tile = MT groups of KSTEPS MMAs.  Whatever the issuing warp executes between the last tcgen05.mma of a group
+            // and the first of the next is NOT hidden behind the MMAs it has queued (tools/umma_probe.cu tests 10-12: in a steady
+            // stream the tensor pipe accepts an MMA only about when it can start it, so a dependent chain between two groups adds
+            // its full length to every group), but what sits between two MMAs of the SAME group is free as long as it fits one
+            // MMA time (64 clk).  So the barrier waits of the NEXT group are placed in the middle of the current one, the second half
+            // of a group and the first half of the next are issued from one elected block, and every operand of the MMAs is computed from warp-uniform values only
+            // (tensor memory starts at column 0: checked after the allocation), which keeps them in uniform registers -- the
+            // R2UR moves of the first version were the longest part of the gap.
+            auto wait_operand = [&](const Ring &r) { if (prof) mbar_wait_prof(&b_full[r.idx], r.phase, true, w0); else mbar_wait_tight(&b_full[r.idx], r.phase); };
+            auto wait_acc = [&](const Ring &r) { if (prof) mbar_wait_prof(&acc_empty[r.idx], r.phase, true, w1); else mbar_wait_tight(&acc_empty[r.idx], r.phase); };
+            auto mmas = [&](uint32_t d, uint32_t ta0, uint32_t b_lo, int ks0, int ks1) {
+#pragma unroll
+                for (int ks = 0; ks < KSTEPS; ++ks)
+                    if (ks >= ks0 && ks < ks1) {
+                        const uint32_t bo = ((ks >> 2) * (STAGE_DOCS * 128) + (ks & 3) * 32) >> 4;
+                        if (ks == 0) umma_i8<false>(d, ta0 + ks * 8, b_lo + bo);
+                        else umma_i8<true>(d, ta0 + ks * 8, b_lo + bo);
+                    }
+            };
+            constexpr int H = KSTEPS / 2;
+            // Rotated loop: an elected block issues the second half of one group, its commit(s) and the first half of the NEXT
+            // group back to back, so every group boundary lies inside a block; the gaps between blocks (barrier polls, elect,
+            // uniform-register set-up) fall between two MMAs of the same group.
+            if (sg.cnt > 0) {
+                wait_operand(rb); wait_acc(ac); fence_after();
+                if (elect_one()) mmas(static_cast<uint32_t>(ac.idx) * STAGE_DOCS, ACOL0, b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4), 0, H);
+                __syncwarp();
+            }
+            for (int i = 0; i < sg.cnt; ++i) {
                 const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4);
-#pragma unroll
-                for (int mt = 0; mt < MT; ++mt) {
-                    const uint32_t buf = ac.idx;
-                    if (prof) mbar_wait_prof(&acc_empty[buf], ac.phase, true, w1); else mbar_wait_tight(&acc_empty[buf], ac.phase);
+                const uint32_t d0 = static_cast<uint32_t>(ac.idx) * STAGE_DOCS;
+                uint64_t *stage_done = &b_empty[rb.idx];
+                uint64_t *acc0_done = &acc_full[ac.idx];
+                const bool more = i + 1 < sg.cnt;
+                ac.advance(AB);
+                rb.advance(NS);
+                if constexpr (MT == 2) {
+                    const uint32_t d1 = static_cast<uint32_t>(ac.idx) * STAGE_DOCS;
+                    uint64_t *acc1_done = &acc_full[ac.idx];
+                    wait_acc(ac);      // the second query tile's accumulator
                     fence_after();
+                    ac.advance(AB);
                     if (elect_one()) {
-                        const uint32_t d = tm + buf * STAGE_DOCS;
-#pragma unroll
-                        for (int ks = 0; ks < KSTEPS; ++ks) {
-                            const uint32_t ta = tm + ACOL0 + mt * A_COLS + ks * 8;
-                            const uint32_t bo = ((ks >> 2) * (STAGE_DOCS * 128) + (ks & 3) * 32) >> 4;
-                            if (ks == 0) umma_i8<false>(d, ta, b_lo + bo);
-                            else umma_i8<true>(d, ta, b_lo + bo);
-                        }
-                        umma_commit(&acc_full[buf]);
+                        mmas(d0, ACOL0, b_lo, H, KSTEPS);
+                        umma_commit(acc0_done);
+                        mmas(d1, ACOL0 + A_COLS, b_lo, 0, H);
                     }
                     __syncwarp();
-                    ac.advance(AB);
+                    if (more) { wait_operand(rb); wait_acc(ac); fence_after(); }   // the next tile
+                    if (elect_one()) {
+                        mmas(d1, ACOL0 + A_COLS, b_lo, H, KSTEPS);
+                        umma_commit(acc1_done);
+                        umma_commit(stage_done);
+                        if (more) mmas(static_cast<uint32_t>(ac.idx) * STAGE_DOCS, ACOL0, b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4), 0, H);
+                    }
+                    __syncwarp();
+                } else {
+                    if (more) { wait_operand(rb); wait_acc(ac); fence_after(); }
+                    if (elect_one()) {
+                        mmas(d0, ACOL0, b_lo, H, KSTEPS);
+                        umma_commit(acc0_done);
+                        umma_commit(stage_done);
+                        if (more) mmas(static_cast<uint32_t>(ac.idx) * STAGE_DOCS, ACOL0, b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4), 0, H);
+                    }
+                    __syncwarp();
                 }
-                if (elect_one()) umma_commit(&b_empty[rb.idx]);
-                __syncwarp();
-                rb.advance(NS);
+            }
             }
             s_run += static_cast<uint32_t>(sg.cnt);
             cta_sync();  // lists final

@@ -250,6 +250,418 @@ __global__ void __launch_bounds__(288, 1) rate_kernel(int iters_mma, int iters_l
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+
+// ---------------------------------------------------------------- test 7: the scan kernel's issue pattern
+// Groups of `gm` MMAs (M = 128, N = 128, K = 32, A in tensor memory) into `nacc` rotating 128-column accumulators.
+// flags: 1 = tcgen05.commit after every group; 2 = the first MMA of a group overwrites (accumulate = 0);
+// 4 = before issuing group g wait for the commit of group g - lag (an ideal, zero-work drain: the accumulator is free
+// the moment its MMAs are done); 8 = a second warp waits for every commit and arrives on an "empty" barrier the issuer
+// waits for instead (one hand-off hop, as in the real kernel with nothing to drain).
+__global__ void __launch_bounds__(288, 1) pipe_kernel(int groups, int gm, int nacc, int lag, int flags, long long *clk, int *err) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char *sB = smem;  // 128 rows x 256 B (two K blocks)
+    __shared__ uint64_t full[8], empty[8];
+    __shared__ uint32_t tmem_base_s;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 128 * 256; i += blockDim.x) smem[i] = static_cast<unsigned char>((i * 2654435761u) >> 13) & 15;
+    fence_async_smem();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 8; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) tmem_alloc(&tmem_base_s, 512);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const uint32_t a_col = nacc * 128 <= 384 ? 384 : 0;  // four accumulators: the operand overlaps one (timing only)
+    if (warp == 8) {
+        if (lane == 0) {
+            const uint32_t idesc = make_idesc(128, 128, true, (flags & 64) != 0);
+            const uint64_t bd0 = make_desc(smem_u32(sB));
+            const int bmask = (flags & 16) ? 0 : 1, amask = (flags & 32) ? 3 : 7;  // 16: one K block of B; 32: four column groups of A
+            const uint32_t a0 = tmem + a_col;
+            const bool first_overwrites = (flags & 2) != 0;
+            const long long t0 = clock64();
+            int buf = -1;
+            for (int g = 0; g < groups; ++g) {
+                buf = buf + 1 == nacc ? 0 : buf + 1;
+                if ((flags & 4) && g >= lag) {
+                    const int gw = g - lag;  // its commit went to full[gw % nacc], use number gw / nacc
+                    if (flags & 8) { if (!mbar_wait_bounded(&empty[gw % nacc], (gw / nacc) & 1)) { atomicExch(err, 3); break; } }
+                    else if (!mbar_wait_bounded(&full[gw % nacc], (gw / nacc) & 1)) { atomicExch(err, 3); break; }
+                    fence_after();
+                }
+                const uint32_t d = tmem + buf * 128;
+                for (int k0 = 0; k0 < gm; k0 += 8) {
+#pragma unroll
+                    for (int ks = 0; ks < 8; ++ks)
+                        umma_i8_ts(d, a0 + (ks & amask) * 8, bd0 + ((((ks >> 2) & bmask) * (128 * 128) + (ks & 3) * 32) >> 4), idesc,
+                                   (first_overwrites && k0 == 0 && ks == 0) ? 0u : 1u);
+                }
+                if (flags & 1) umma_commit(&full[buf]);
+            }
+            umma_commit(&full[7]);
+            if (!mbar_wait_bounded(&full[7], 0)) atomicExch(err, 2);
+            clk[blockIdx.x] = clock64() - t0;
+        }
+        __syncwarp();
+    } else if (warp == 0 && (flags & 8)) {
+        for (int g = 0; g < groups; ++g) {  // the hop: every lane polls, lane 0 hands the accumulator back
+            if (!mbar_wait_bounded(&full[g % nacc], (g / nacc) & 1)) { atomicExch(err, 4); break; }
+            fence_after();
+            fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[g % nacc])) : "memory");
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------- test 8: the same with the scan kernel's issue idiom
+// (whole warp walks the pipeline, one elected lane issues; 32-bit descriptor words, constant high word; waits with the
+// retry loop inside the asm block).  flags as in test 7.
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
+__device__ __forceinline__ void mbar_wait_tight(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@p bra DONE_%=;\n\tbra WAIT_%=;\n\tDONE_%=:\n\t}"
+        ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+constexpr uint32_t P_DESC_HI = (1024u >> 4) | (1u << 14) | (2u << 29);
+template <bool ACC>
+__device__ __forceinline__ void umma_i8_ts32(uint32_t d_tmem, uint32_t a_tmem, uint32_t b_lo, uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b64 db;\n\tsetp.ne.b32 p, %4, 0;\n\tmov.b64 db, {%2, %5};\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], db, %3, p;\n\t}"
+        ::"r"(d_tmem), "r"(a_tmem), "r"(b_lo), "r"(idesc), "n"(ACC ? 1 : 0), "r"(P_DESC_HI) : "memory");
+}
+template <int GM, int NACC>
+__global__ void __launch_bounds__(512, 1) pipe2_kernel(int groups, int lag, int flags, int hop_warps, long long *clk, int *err, int delay = 0) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char *sB = smem;  // 128 rows x 256 B (two K blocks)
+    __shared__ uint64_t full[8], empty[8], bfull[4], bempty[4];
+    __shared__ uint32_t tmem_base_s;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 3 * 128 * 256; i += blockDim.x) smem[i] = static_cast<unsigned char>((i * 2654435761u) >> 13) & 15;
+    fence_async_smem();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 4; ++i) { mbar_init(&bfull[i], 1); mbar_init(&bempty[i], 1); }
+        for (int i = 0; i < 8; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], hop_warps > 0 ? hop_warps : 1); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) tmem_alloc(&tmem_base_s, 512);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base_s;
+    constexpr uint32_t A_COL = NACC * 128 <= 384 ? 384 : 0;
+    const uint32_t idesc = make_idesc(128, 128, true, false);
+    if (warp == 12) {
+        const uint32_t b_lo = ((smem_u32(sB) >> 4) & 0x3FFFu) | (1u << 16);
+        const long long t0 = clock64();
+        long long waited = 0;
+        int buf = 0; uint32_t ph = 0;          // accumulator ring
+        int wbuf = 0; uint32_t wph = 0;        // the group waited for (lag groups behind)
+        int slot = 0; uint32_t sph = 0;        // operand ring (flags 512 / 1024): one slot per two groups
+        for (int g = 0; g < groups; ++g) {
+            if ((flags & 1024) && !(g & 1)) { mbar_wait_tight(&bfull[slot], sph); fence_after(); }
+            if ((flags & 4) && g >= lag) {
+                const long long w0 = clock64();
+                mbar_wait_tight((flags & 8) ? &empty[wbuf] : &full[wbuf], wph);
+                waited += clock64() - w0;
+                fence_after();
+                if (++wbuf == NACC) { wbuf = 0; wph ^= 1u; }
+            }
+            const uint32_t a_g = ((flags & 256) && (g & 1)) ? 64u : 0u;
+            const uint32_t b_g = (flags & 1536) ? b_lo + static_cast<uint32_t>(slot) * ((128 * 256) >> 4) : b_lo;
+            if (elect_one()) {
+                const uint32_t d = tmem + buf * 128;
+#pragma unroll
+                for (int ks = 0; ks < GM; ++ks) {
+                    const uint32_t ta = tmem + A_COL + a_g + (ks & 7) * 8;
+                    const uint32_t bo = ((((ks >> 2) & 1) * (128 * 128)) + (ks & 3) * 32) >> 4;
+                    if (ks == 0 && (flags & 2)) umma_i8_ts32<false>(d, ta, b_g + bo, idesc);
+                    else umma_i8_ts32<true>(d, ta, b_g + bo, idesc);
+                }
+                if (flags & 1) umma_commit(&full[buf]);
+            }
+            __syncwarp();
+            if (delay) {  // a dependent chain between two groups: is the issuer's path hidden behind queued MMAs?
+                uint32_t x = static_cast<uint32_t>(g);
+                for (int i = 0; i < delay; ++i) asm volatile("mad.lo.u32 %0, %0, 3, 1;" : "+r"(x));
+                if (x == 0x7fffffffu) err[2] = 1;
+            }
+            if (++buf == NACC) { buf = 0; ph ^= 1u; }
+            if ((flags & 1536) && (g & 1)) {
+                if (flags & 1024) { if (elect_one()) umma_commit(&bempty[slot]); __syncwarp(); }
+                if (++slot == 3) { slot = 0; sph ^= 1u; }
+            }
+        }
+        if (elect_one()) umma_commit(&full[7]);
+        __syncwarp();
+        mbar_wait_tight(&full[7], 0);
+        if (lane == 0) { clk[blockIdx.x] = clock64() - t0; clk[gridDim.x + blockIdx.x] = waited; }
+        (void)ph;
+    } else if (warp == 13 && (flags & 1024)) {
+        if (lane == 0) {
+            int slot = 0; uint32_t sph = 1;   // "empty" waits start on the completed phase
+            for (int st = 0; st < groups / 2; ++st) {
+                mbar_wait_tight(&bempty[slot], sph);
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bfull[slot])) : "memory");
+                if (++slot == 3) { slot = 0; sph ^= 1u; }
+            }
+        }
+        __syncwarp();
+    } else if (warp < hop_warps && (flags & 8)) {
+        int buf = 0; uint32_t ph = 0;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        uint32_t sinkv = 0;
+        for (int g = 0; g < groups; ++g) {  // the hop: every lane polls, [reads its share of the accumulator], lane 0 hands it back
+            mbar_wait_tight(&full[buf], ph);
+            fence_after();
+            if (flags & 128) {
+                uint32_t v[32];
+                tmem_ld32(lane_base + buf * 128 + ((warp >> 2) & 1) * 64, v);
+                tmem_ld32(lane_base + buf * 128 + ((warp >> 2) & 1) * 64 + 32, v);
+                tmem_ld_wait();
+                sinkv ^= v[0];
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[buf])) : "memory");
+            if (++buf == NACC) { buf = 0; ph ^= 1u; }
+        }
+        if (sinkv == 0x12345u) err[1] = 1;
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------- test 9: how far ahead of the tensor pipe can the issuer run?
+// From an idle pipe, one elected lane issues K MMAs (128 x 128 x 32, A in tensor memory) back to back and reads the clock after the
+// last one was ACCEPTED (not completed): the time stays flat up to the depth of the instruction queue, then grows by one MMA time each.
+template <int K>
+__global__ void __launch_bounds__(128, 1) queue_kernel(long long *clk, int *err) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base_s;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 128 * 256; i += blockDim.x) smem[i] = static_cast<unsigned char>((i * 2654435761u) >> 13) & 15;
+    fence_async_smem();
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+    if (warp == 0) tmem_alloc(&tmem_base_s, 512);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const uint32_t idesc = make_idesc(128, 128, true, false);
+    if (warp == 1) {
+        const uint32_t b_lo = ((smem_u32(smem) >> 4) & 0x3FFFu) | (1u << 16);
+        long long best_issue = 1ll << 60, best_total = 0;
+        for (int rep = 0; rep < 8; ++rep) {
+            long long t0 = 0, t1 = 0;
+            if (elect_one()) {
+                t0 = clock64();
+#pragma unroll
+                for (int ks = 0; ks < K; ++ks)
+                    umma_i8_ts32<true>(tmem + (ks >> 3) * 128, tmem + 384 + (ks & 7) * 8, b_lo + (((((ks >> 2) & 1) * (128 * 128)) + (ks & 3) * 32) >> 4), idesc);
+                t1 = clock64();
+                umma_commit(&bar);
+            }
+            __syncwarp();
+            mbar_wait_tight(&bar, rep & 1);
+            const long long t2 = clock64();
+            t0 = __shfl_sync(0xffffffffu, t0, __ffs(__ballot_sync(0xffffffffu, t0 != 0)) - 1);
+            t1 = __shfl_sync(0xffffffffu, t1, __ffs(__ballot_sync(0xffffffffu, t1 != 0)) - 1);
+            if (t1 - t0 < best_issue) { best_issue = t1 - t0; best_total = t2 - t0; }
+        }
+        if (lane == 0) { clk[blockIdx.x * 2] = best_issue; clk[blockIdx.x * 2 + 1] = best_total; }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+    (void)err;
+}
+
+// ---------------------------------------------------------------- test 11: do queued MMAs execute while the issuing warp computes?
+// Warp 1 issues 8 MMAs + commit, then runs a dependent integer chain of `delay` iterations and reads the clock; warp 2 polls the
+// commit barrier and reads the clock when the MMAs are done.  Both relative to the same start (a CTA barrier).
+__global__ void __launch_bounds__(128, 1) overlap_kernel(int delay, long long *clk, int *err) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base_s;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 128 * 256; i += blockDim.x) smem[i] = static_cast<unsigned char>((i * 2654435761u) >> 13) & 15;
+    fence_async_smem();
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+    if (warp == 0) tmem_alloc(&tmem_base_s, 512);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const uint32_t idesc = make_idesc(128, 128, true, false);
+    for (int rep = 0; rep < 4; ++rep) {
+        __syncthreads();
+        const long long t0 = clock64();
+        if (warp == 1) {
+            const uint32_t b_lo = ((smem_u32(smem) >> 4) & 0x3FFFu) | (1u << 16);
+            if (elect_one()) {
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks)
+                    umma_i8_ts32<true>(tmem, tmem + 384 + (ks & 7) * 8, b_lo + (((((ks >> 2) & 1) * (128 * 128)) + (ks & 3) * 32) >> 4), idesc);
+                umma_commit(&bar);
+            }
+            __syncwarp();
+            const long long t1 = clock64();
+            uint32_t x = static_cast<uint32_t>(rep);
+            for (int i = 0; i < delay; ++i) asm volatile("mad.lo.u32 %0, %0, 3, 1;" : "+r"(x));
+            const long long t2 = clock64();
+            if (x == 0x7fffffffu) err[2] = 1;
+            if (lane == 0) { clk[0] = t1 - t0; clk[1] = t2 - t0; }
+        } else if (warp == 2) {
+            mbar_wait_tight(&bar, rep & 1);
+            const long long t3 = clock64();
+            if (lane == 0) clk[2] = t3 - t0;
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------- test 12: two issuing warps, alternate groups
+// Warps 12 and 13 issue the even / odd groups (8 MMAs + commit each) into rotating accumulators; before group g a warp waits
+// for the commit of group g - 2 (flags & 4) -- and, to keep the two streams in step, for nothing else.  A dependent chain of
+// `delay` iterations follows every group, as in test 10: with one warp it is fully exposed, with two it should hide.
+template <int NACC>
+__global__ void __launch_bounds__(512, 1) pipe3_kernel(int groups, int flags, int delay, int issuers, long long *clk, int *err) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ uint64_t full[8];
+    __shared__ uint32_t tmem_base_s;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 128 * 256; i += blockDim.x) smem[i] = static_cast<unsigned char>((i * 2654435761u) >> 13) & 15;
+    fence_async_smem();
+    if (threadIdx.x == 0) { for (int i = 0; i < 8; ++i) mbar_init(&full[i], 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+    if (warp == 0) tmem_alloc(&tmem_base_s, 512);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const uint32_t idesc = make_idesc(128, 128, true, false);
+    if (warp >= 12 && warp < 12 + issuers) {
+        const int me = warp - 12;
+        const uint32_t b_lo = ((smem_u32(smem) >> 4) & 0x3FFFu) | (1u << 16);
+        const long long t0 = clock64();
+        for (int g = me; g < groups; g += issuers) {
+            const int buf = g % NACC;
+            if ((flags & 4) && g >= 2) { const int gw = g - 2; mbar_wait_tight(&full[gw % NACC], (gw / NACC) & 1); fence_after(); }
+            if (elect_one()) {
+                const uint32_t d = tmem + buf * 128;
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint32_t bo = ((((ks >> 2) & 1) * (128 * 128)) + (ks & 3) * 32) >> 4;
+                    if (ks == 0) umma_i8_ts32<false>(d, tmem + 384 + (g & 1) * 64 + ks * 8, b_lo + bo, idesc);
+                    else umma_i8_ts32<true>(d, tmem + 384 + (g & 1) * 64 + ks * 8, b_lo + bo, idesc);
+                }
+                umma_commit(&full[buf]);
+            }
+            __syncwarp();
+            if (delay) {
+                uint32_t x = static_cast<uint32_t>(g);
+                for (int i = 0; i < delay; ++i) asm volatile("mad.lo.u32 %0, %0, 3, 1;" : "+r"(x));
+                if (x == 0x7fffffffu) err[2] = 1;
+            }
+        }
+        if (elect_one()) umma_commit(&full[6 + me]);
+        __syncwarp();
+        mbar_wait_tight(&full[6 + me], 0);
+        if (lane == 0) clk[blockIdx.x * 2 + me] = clock64() - t0;
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------- test 13: are two concurrently issued MMA chains independent?
+// Warps 1 and 2 each issue 8 MMAs (K = 256) of their own query tile (A0 / A1 in tensor memory) against the same documents into
+// their own accumulator, at the same time (mode 0) or one after the other (mode 1); both accumulators are checked against the CPU.
+__global__ void __launch_bounds__(128, 1) two_chain_kernel(const int8_t *A, const int8_t *B, int32_t *D, int mode, int *err) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char *sB = smem;       // 128 x 256
+    __shared__ uint64_t bar[2];
+    __shared__ uint32_t tmem_base_s;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 128 * 256; i += blockDim.x) sB[sw128_offset(i / 256, i % 256, 128)] = static_cast<unsigned char>(B[i]);
+    fence_async_smem();
+    if (threadIdx.x == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+    if (warp == 0) tmem_alloc(&tmem_base_s, 512);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base_s;
+    {
+        const int m = warp * 32 + lane;
+        for (int tile = 0; tile < 2; ++tile) {
+            const uint32_t *arow = reinterpret_cast<const uint32_t *>(A + (tile * 128 + m) * 256);
+            for (int c0 = 0; c0 < 64; c0 += 8) {
+                uint32_t v[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] = arow[c0 + j];
+                tmem_st8(tmem + 256 + tile * 64 + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+            }
+        }
+        tmem_st_wait();
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t idesc = make_idesc(128, 128, true, false);
+    for (int rep = 0; rep < 64; ++rep) {
+        __syncthreads();
+        if (warp == 1 || warp == 2) {
+            const int me = warp - 1;
+            if (mode == 1 && me == 1) { mbar_wait_tight(&bar[0], rep & 1); fence_after(); }
+            const uint32_t b_lo = ((smem_u32(sB) >> 4) & 0x3FFFu) | (1u << 16);
+            if (elect_one()) {
+#pragma unroll
+                for (int ks = 0; ks < 8; ++ks) {
+                    const uint32_t bo = ((((ks >> 2) & 1) * (128 * 128)) + (ks & 3) * 32) >> 4;
+                    if (ks == 0) umma_i8_ts32<false>(tmem + me * 128, tmem + 256 + me * 64 + ks * 8, b_lo + bo, idesc);
+                    else umma_i8_ts32<true>(tmem + me * 128, tmem + 256 + me * 64 + ks * 8, b_lo + bo, idesc);
+                }
+                umma_commit(&bar[me]);
+            }
+            __syncwarp();
+        }
+        mbar_wait_tight(&bar[0], rep & 1);
+        mbar_wait_tight(&bar[1], rep & 1);
+        fence_after();
+        // check against the first repetition's result (kept in registers), report differences
+        for (int acc = 0; acc < 2; ++acc)
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem + acc * 128 + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    int32_t *dst = D + ((acc * 128 + warp * 32 + lane) * 128 + c0 + j);
+                    if (rep == 0) *dst = static_cast<int32_t>(v[j]);
+                    else if (*dst != static_cast<int32_t>(v[j])) atomicAdd(err + 1, 1);
+                }
+            }
+        fence_before();
+    }
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 int main(int argc, char **argv) {
     int which = argc > 1 ? atoi(argv[1]) : 0;
     int *err;
@@ -358,5 +770,149 @@ int main(int argc, char **argv) {
     if (which == 0 || which == 3) { if (run_rate(256, 0, 1, 4)) return 1; if (run_rate(256, 0, 1, 8)) return 1; }
     if (which == 0 || which == 4) { if (run_rate(256, 1, 1, 4)) return 1; if (run_rate(256, 1, 1, 8)) return 1; if (run_rate(128, 1, 1, 8)) return 1; }
     if (which == 0 || which == 6) { if (run_rate(128, 1, 0, 0, true)) return 1; if (run_rate(128, 1, 1, 8, true)) return 1; }
+    if (which == 0 || which == 7) {
+        const int smem = 128 * 256;
+        CK(cudaFuncSetAttribute(pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        struct Cfg { int gm, nacc, lag, flags; };
+        const Cfg cfgs[] = {{8, 3, 0, 16}, {8, 3, 0, 32}, {8, 3, 0, 64}, {8, 3, 0, 112}, {8, 2, 0, 112}, {8, 1, 0, 112}, {8, 1, 0, 0}, {8, 3, 0, 0}, {8, 3, 0, 1}, {8, 3, 0, 2}, {8, 3, 0, 3}, {8, 3, 2, 7}, {8, 3, 1, 7}, {8, 3, 2, 15}, {8, 4, 3, 7}, {8, 4, 3, 15},
+                            {16, 3, 2, 7}, {16, 3, 2, 15}, {8, 2, 1, 7}, {8, 2, 1, 15}};
+        for (const Cfg &c : cfgs) {
+            const int groups = 4096;
+            CK(cudaMemset(mma_clk, 0, sms * 8));
+            pipe_kernel<<<sms, 288, smem>>>(groups, c.gm, c.nacc, c.lag, c.flags, mma_clk, err);
+            CK(cudaDeviceSynchronize());
+            int herr = 0;
+            CK(cudaMemcpy(&herr, err, 4, cudaMemcpyDeviceToHost));
+            std::vector<long long> mc(sms);
+            CK(cudaMemcpy(mc.data(), mma_clk, sms * 8, cudaMemcpyDeviceToHost));
+            long long mmax = 0;
+            for (auto v : mc) if (v > mmax) mmax = v;
+            printf("{\"test\": \"pipe\", \"mmas_per_group\": %d, \"accumulators\": %d, \"lag\": %d, \"flags\": %d, \"timeout\": %d, "
+                   "\"clk_per_group\": %.1f, \"clk_per_mma\": %.2f}\n", c.gm, c.nacc, c.lag, c.flags, herr, double(mmax) / groups, double(mmax) / groups / c.gm);
+            fflush(stdout);
+            CK(cudaMemset(err, 0, 4));
+        }
+    }
+    if (which == 0 || which == 8) {
+        const int smem = 3 * 128 * 256;
+        struct Cfg { int gm, nacc, lag, flags, hop; };
+        const Cfg cfgs[] = {{8, 3, 0, 3, 0}, {8, 3, 2, 7, 0}, {8, 3, 2, 143, 8}, {8, 3, 2, 143 + 256, 8}, {8, 3, 2, 143 + 512, 8}, {8, 3, 2, 143 + 768, 8}, {8, 3, 2, 143 + 1024, 8}, {8, 3, 2, 143 + 1024 + 256, 8}, {8, 3, 3, 143 + 1024 + 256, 8}, {8, 3, 1, 143, 8},
+                            {8, 4, 3, 7, 0}, {8, 4, 3, 15, 8}, {8, 4, 2, 15, 8}, {16, 3, 2, 7, 0}, {16, 3, 2, 15, 8}, {16, 3, 2, 143, 8}, {8, 2, 1, 7, 0}, {8, 2, 1, 15, 8}};
+        for (const Cfg &c : cfgs) {
+            const int groups = 4096;
+            CK(cudaMemset(mma_clk, 0, sms * 8));
+            long long *clk2; CK(cudaMalloc(&clk2, sms * 16)); CK(cudaMemset(clk2, 0, sms * 16));
+#define RUN_PIPE2(GM, NACC) do { CK(cudaFuncSetAttribute(pipe2_kernel<GM, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+            pipe2_kernel<GM, NACC><<<sms, 512, smem>>>(groups, c.lag, c.flags, c.hop, clk2, err); } while (0)
+            if (c.gm == 8 && c.nacc == 3) RUN_PIPE2(8, 3); else if (c.gm == 8 && c.nacc == 4) RUN_PIPE2(8, 4);
+            else if (c.gm == 8 && c.nacc == 2) RUN_PIPE2(8, 2); else RUN_PIPE2(16, 3);
+            CK(cudaDeviceSynchronize());
+            int herr = 0;
+            CK(cudaMemcpy(&herr, err, 4, cudaMemcpyDeviceToHost));
+            std::vector<long long> mc(2 * sms);
+            CK(cudaMemcpy(mc.data(), clk2, sms * 16, cudaMemcpyDeviceToHost));
+            CK(cudaFree(clk2));
+            long long mmax = 0, wmax = 0;
+            for (int i = 0; i < sms; ++i) { if (mc[i] > mmax) mmax = mc[i]; if (mc[sms + i] > wmax) wmax = mc[sms + i]; }
+            printf("{\"test\": \"pipe2\", \"mmas_per_group\": %d, \"accumulators\": %d, \"lag\": %d, \"flags\": %d, \"hop_warps\": %d, \"timeout\": %d, "
+                   "\"clk_per_group\": %.1f, \"clk_per_mma\": %.2f, \"issuer_wait_clk_per_group\": %.1f}\n", c.gm, c.nacc, c.lag, c.flags, c.hop, herr,
+                   double(mmax) / groups, double(mmax) / groups / c.gm, double(wmax) / groups);
+            fflush(stdout);
+            CK(cudaMemset(err, 0, 4));
+        }
+    }
+    if (which == 0 || which == 9) {
+        const int smem = 128 * 256;
+        long long *clk2; CK(cudaMalloc(&clk2, 16)); 
+        long long h[2];
+#define RUN_Q(K) do { CK(cudaFuncSetAttribute(queue_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); CK(cudaMemset(clk2, 0, 16)); \
+        queue_kernel<K><<<1, 128, smem>>>(clk2, err); CK(cudaDeviceSynchronize()); CK(cudaMemcpy(h, clk2, 16, cudaMemcpyDeviceToHost)); \
+        printf("{\"test\": \"issue_queue\", \"mmas\": %d, \"clk_until_last_accepted\": %lld, \"clk_until_complete\": %lld}\n", K, h[0], h[1]); fflush(stdout); } while (0)
+        RUN_Q(1); RUN_Q(2); RUN_Q(3); RUN_Q(4); RUN_Q(5); RUN_Q(6); RUN_Q(8); RUN_Q(10); RUN_Q(12); RUN_Q(16); RUN_Q(24);
+        CK(cudaFree(clk2));
+    }
+    if (which == 10) {
+        const int smem = 3 * 128 * 256;
+        const int groups = 4096;
+        long long *clk2; CK(cudaMalloc(&clk2, sms * 16));
+        CK(cudaFuncSetAttribute(pipe2_kernel<8, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        for (int flags : {0, 2, 1, 3, 143}) for (int delay : {0, 4, 32, 128}) {
+            CK(cudaMemset(clk2, 0, sms * 16));
+            pipe2_kernel<8, 3><<<sms, 512, smem>>>(groups, 2, flags, 8, clk2, err, delay);
+            CK(cudaDeviceSynchronize());
+            std::vector<long long> mc(2 * sms);
+            CK(cudaMemcpy(mc.data(), clk2, sms * 16, cudaMemcpyDeviceToHost));
+            long long mmax = 0;
+            for (int i = 0; i < sms; ++i) if (mc[i] > mmax) mmax = mc[i];
+            printf("{\"test\": \"pipe2_delay\", \"flags\": %d, \"delay_iters\": %d, \"clk_per_group\": %.1f}\n", flags, delay, double(mmax) / groups);
+            fflush(stdout);
+        }
+        CK(cudaFree(clk2));
+    }
+    if (which == 11) {
+        const int smem = 128 * 256;
+        long long *clk2; CK(cudaMalloc(&clk2, 32));
+        long long h[3];
+        CK(cudaFuncSetAttribute(overlap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        for (int delay : {0, 32, 128, 512}) {
+            CK(cudaMemset(clk2, 0, 32));
+            overlap_kernel<<<1, 128, smem>>>(delay, clk2, err);
+            CK(cudaDeviceSynchronize());
+            CK(cudaMemcpy(h, clk2, 24, cudaMemcpyDeviceToHost));
+            printf("{\"test\": \"overlap\", \"delay_iters\": %d, \"issued_at\": %lld, \"issuer_chain_done_at\": %lld, \"mmas_complete_at\": %lld}\n", delay, h[0], h[1], h[2]);
+            fflush(stdout);
+        }
+        CK(cudaFree(clk2));
+    }
+    if (which == 12) {
+        const int smem = 128 * 256;
+        const int groups = 4096;
+        long long *clk2; CK(cudaMalloc(&clk2, sms * 16));
+        CK(cudaFuncSetAttribute(pipe3_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        for (int issuers : {1, 2}) for (int flags : {0, 4}) for (int delay : {0, 4, 32, 64, 128}) {
+            CK(cudaMemset(clk2, 0, sms * 16));
+            pipe3_kernel<3><<<sms, 512, smem>>>(groups, flags, delay, issuers, clk2, err);
+            CK(cudaDeviceSynchronize());
+            std::vector<long long> mc(2 * sms);
+            CK(cudaMemcpy(mc.data(), clk2, sms * 16, cudaMemcpyDeviceToHost));
+            long long mmax = 0;
+            for (int i = 0; i < 2 * sms; ++i) if (mc[i] > mmax) mmax = mc[i];
+            int herr = 0; CK(cudaMemcpy(&herr, err, 4, cudaMemcpyDeviceToHost));
+            printf("{\"test\": \"pipe3\", \"issuers\": %d, \"flags\": %d, \"delay_iters\": %d, \"err\": %d, \"clk_per_group\": %.1f}\n", issuers, flags, delay, herr, double(mmax) / groups);
+            fflush(stdout);
+        }
+        CK(cudaFree(clk2));
+    }
+    if (which == 13) {
+        std::vector<int8_t> A(256 * 256), B(128 * 256);
+        srand(777);
+        for (auto &a : A) a = static_cast<int8_t>(2 * (rand() % 16) - 15);
+        for (auto &b : B) b = static_cast<int8_t>(rand() % 16);
+        int8_t *dA, *dB; int32_t *dD; int *err2;
+        CK(cudaMalloc(&dA, A.size())); CK(cudaMalloc(&dB, B.size())); CK(cudaMalloc(&dD, 256 * 128 * 4)); CK(cudaMalloc(&err2, 16));
+        CK(cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice));
+        const int smem = 128 * 256;
+        CK(cudaFuncSetAttribute(two_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        for (int mode = 0; mode < 2; ++mode) {
+            CK(cudaMemset(dD, 0xCC, 256 * 128 * 4)); CK(cudaMemset(err2, 0, 16));
+            two_chain_kernel<<<1, 128, smem>>>(dA, dB, dD, mode, err2);
+            CK(cudaDeviceSynchronize());
+            int herr[4];
+            CK(cudaMemcpy(herr, err2, 16, cudaMemcpyDeviceToHost));
+            std::vector<int32_t> D(256 * 128);
+            CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
+            long long bad = 0;
+            for (int m = 0; m < 256; ++m)
+                for (int n = 0; n < 128; ++n) {
+                    int32_t acc = 0;
+                    for (int k = 0; k < 256; ++k) acc += static_cast<int32_t>(A[m * 256 + k]) * static_cast<int32_t>(static_cast<uint8_t>(B[n * 256 + k]));
+                    if (acc != D[m * 128 + n]) ++bad;
+                }
+            printf("{\"test\": \"two_chains\", \"mode\": \"%s\", \"mismatches_vs_cpu_first_rep\": %lld, \"changes_in_later_reps\": %d}\n",
+                   mode ? "one after the other" : "concurrent", bad, herr[1]);
+            fflush(stdout);
+        }
+    }
     return 0;
 }
