@@ -1074,7 +1074,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                         }
                         if (prof) w3 += clock64() - tw;
                     }
-                    if (hit) {
+                    if (p.debug & 64) { head = t0; }  // timing experiments: evaluate the filter, park nothing
+                    else if (hit) {
                         const int t = t0 + __popc(hm & ((1u << lane) - 1u));
                         uint32_t *row = ring + (t & (RING_ROWS - 1)) * STASH_WORDS;
 #pragma unroll
@@ -1082,7 +1083,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                             *reinterpret_cast<uint4 *>(row + 4 * c) = make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
                         row[32] = qloc;
                         row[33] = doc0;
-                        st_release(reinterpret_cast<int *>(row + 34), t + 1);  // publishes the row
+                        if (p.debug & 16) *reinterpret_cast<volatile int *>(row + 34) = t + 1;  // timing experiments: no release fence
+                        else st_release(reinterpret_cast<int *>(row + 34), t + 1);  // publishes the row
                     }
                 }
             };
@@ -1195,7 +1197,16 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             constexpr int H = KSTEPS / 2;
             // Rotated loop: an elected block issues the second half of one group, its commit(s) and the first half of the NEXT
             // group back to back, so every group boundary lies inside a block; the gaps between blocks (barrier polls, elect,
-            // uniform-register set-up) fall between two MMAs of the same group.
+            // uniform-register set-up) fall between two MMAs of the same group.  The next group's barriers are only PROBED in
+            // the middle of a group: when its accumulator or operand tile is not there yet (short rings, the HBM-bound batch
+            // sizes) the current group is finished and committed first -- holding its second half back would delay the
+            // release of its own operand stage -- and the next group starts from its own block after a blocking wait.
+            auto ready = [&](uint64_t *bar, uint32_t parity) {   // warp-uniform: every lane reads the same barrier
+                uint32_t ok;
+                asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                             : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+                return __all_sync(0xffffffffu, ok != 0);
+            };
             if (sg.cnt > 0) {
                 wait_operand(rb); wait_acc(ac); fence_after();
                 if (elect_one()) mmas(static_cast<uint32_t>(ac.idx) * STAGE_DOCS, ACOL0, b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4), 0, H);
@@ -1209,35 +1220,52 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                 const bool more = i + 1 < sg.cnt;
                 ac.advance(AB);
                 rb.advance(NS);
+                uint32_t d1 = 0;
+                uint64_t *acc1_done = nullptr;
                 if constexpr (MT == 2) {
-                    const uint32_t d1 = static_cast<uint32_t>(ac.idx) * STAGE_DOCS;
-                    uint64_t *acc1_done = &acc_full[ac.idx];
-                    wait_acc(ac);      // the second query tile's accumulator
-                    fence_after();
-                    ac.advance(AB);
-                    if (elect_one()) {
-                        mmas(d0, ACOL0, b_lo, H, KSTEPS);
-                        umma_commit(acc0_done);
-                        mmas(d1, ACOL0 + A_COLS, b_lo, 0, H);
+                    d1 = static_cast<uint32_t>(ac.idx) * STAGE_DOCS;
+                    acc1_done = &acc_full[ac.idx];
+                    if (ready(&acc_empty[ac.idx], ac.phase)) {   // the second query tile's accumulator is free: one block
+                        fence_after();
+                        if (elect_one()) {
+                            mmas(d0, ACOL0, b_lo, H, KSTEPS);
+                            umma_commit(acc0_done);
+                            mmas(d1, ACOL0 + A_COLS, b_lo, 0, H);
+                        }
+                        __syncwarp();
+                    } else {
+                        if (elect_one()) { mmas(d0, ACOL0, b_lo, H, KSTEPS); umma_commit(acc0_done); }
+                        __syncwarp();
+                        wait_acc(ac);
+                        fence_after();
+                        if (elect_one()) mmas(d1, ACOL0 + A_COLS, b_lo, 0, H);
+                        __syncwarp();
                     }
-                    __syncwarp();
-                    if (more) { wait_operand(rb); wait_acc(ac); fence_after(); }   // the next tile
+                    ac.advance(AB);
+                }
+                // second half of the tile's last group, the commits, and -- when it can start -- the first half of the next tile
+                const uint32_t dl = MT == 2 ? d1 : d0;
+                const uint32_t al = MT == 2 ? ACOL0 + A_COLS : ACOL0;
+                uint64_t *accl_done = MT == 2 ? acc1_done : acc0_done;
+                const uint32_t dn = static_cast<uint32_t>(ac.idx) * STAGE_DOCS;
+                const uint32_t bn = b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4);
+                if (more && ready(&b_full[rb.idx], rb.phase) && ready(&acc_empty[ac.idx], ac.phase)) {
+                    fence_after();
                     if (elect_one()) {
-                        mmas(d1, ACOL0 + A_COLS, b_lo, H, KSTEPS);
-                        umma_commit(acc1_done);
+                        mmas(dl, al, b_lo, H, KSTEPS);
+                        umma_commit(accl_done);
                         umma_commit(stage_done);
-                        if (more) mmas(static_cast<uint32_t>(ac.idx) * STAGE_DOCS, ACOL0, b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4), 0, H);
+                        mmas(dn, ACOL0, bn, 0, H);
                     }
                     __syncwarp();
                 } else {
-                    if (more) { wait_operand(rb); wait_acc(ac); fence_after(); }
-                    if (elect_one()) {
-                        mmas(d0, ACOL0, b_lo, H, KSTEPS);
-                        umma_commit(acc0_done);
-                        umma_commit(stage_done);
-                        if (more) mmas(static_cast<uint32_t>(ac.idx) * STAGE_DOCS, ACOL0, b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4), 0, H);
-                    }
+                    if (elect_one()) { mmas(dl, al, b_lo, H, KSTEPS); umma_commit(accl_done); umma_commit(stage_done); }
                     __syncwarp();
+                    if (more) {
+                        wait_operand(rb); wait_acc(ac); fence_after();
+                        if (elect_one()) mmas(dn, ACOL0, bn, 0, H);
+                        __syncwarp();
+                    }
                 }
             }
             }
@@ -1346,7 +1374,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                         if (pend) atomicExch(&claim_s[q], lane);
                         __syncwarp();
                         const bool go = pend && claim_s[q] == lane;
-                        if (go) {
+                        if (go && (p.debug & 8)) pend = false;  // timing experiments: parked rows are dropped unread
+                        else if (go) {
                             const int th = theta_s[q], dqe = dq_s[q];
                             uint32_t below = 0;  // bit j: score j < threshold
 #pragma unroll
