@@ -430,7 +430,7 @@ def run_ours(a):
 
     hbm_peak, bf16_peak, peak_src = peaks()
     traffic = None  # DRAM bytes of the dominant kernel per launch, from the committed ncu --set full capture of this workload
-    traffic_file = "ncu_full_umma_queue_r2.csv" if (ROOT / "profiles" / "ncu_full_umma_queue_r2.csv").exists() else "ncu_full_umma_queue_r1_v13.csv"
+    traffic_file = next((f for f in ("ncu_full_umma_queue_r2b.csv", "ncu_full_umma_queue_r2.csv") if (ROOT / "profiles" / f).exists()), "ncu_full_umma_queue_r1_v13.csv")
     if (a.n, a.dim, a.nq, a.k, a.doc_bits, world) == (10_000_000, 256, 10000, 100, 4, 1):
         try:
             import csv

@@ -1194,8 +1194,9 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                         else umma_i8<true>(d, ta0 + ks * 8, b_lo + bo);
                     }
             };
-            constexpr int H = KSTEPS / 2;
-            // Rotated loop: an elected block issues the second half of one group, its commit(s) and the first half of the NEXT
+            constexpr int H = KSTEPS - 1;   // MMAs of a group issued from the earlier block: the later the probe for the next group's
+                                            // accumulator, the more time its drain has had (H = 4 / 6 / 7 of 8: 1 152 / 1 143 / 1 120 clk per tile)
+            // Rotated loop: an elected block issues the last MMA of one group, its commit(s) and the first MMAs of the NEXT
             // group back to back, so every group boundary lies inside a block; the gaps between blocks (barrier polls, elect,
             // uniform-register set-up) fall between two MMAs of the same group.  The next group's barriers are only PROBED in
             // the middle of a group: when its accumulator or operand tile is not there yet (short rings, the HBM-bound batch
