@@ -482,6 +482,10 @@ def run_ours(a):
                                     "dense bf16 burst (" + peak_src + ") is peak_2x_measured_bf16, which this kernel exceeds, so the "
                                     "stricter hardware rate is the denominator",
                      "launch_ms": round(kernel_ms, 3), "launches_averaged": int(kernel_launches), "macs_per_launch": int(macs_per_launch),
+                     # information only: the board's power cap holds the SM clock below 1965 MHz under this kernel; the same work against the
+                     # pipe's rate at the clock sampled during the timed region (ncu at the capped clock: 87.9 % of the int8 path)
+                     "frac_at_sampled_clock": (round(tops / (hw_int8_peak * clocks["sm_mhz"] / 1965.0), 4)
+                                               if clocks and clocks.get("sm_mhz") else None),
                      "legacy_imma_pipe_peak_TOPs": 1163.7, "frac_of_legacy_imma_pipe": round(tops / 1163.7, 4),
                      "note": "tcgen05.mma kind::i8 measured at 8188 MAC/clk/SM (tools/umma_probe.cu) = 4.76 POP/s at 1965 MHz; "
                              "mma.sync int8 (IMMA.16832) pipe peak is 4096 op/clk/SM (ncu) = 1164 TOP/s"},
@@ -501,8 +505,13 @@ def run_ours(a):
         "device_bytes": {"packed_codes": int(index.packed.device_nbytes), **index.packed.derived_nbytes,
                          "algorithmic": int(db_bytes_local),
                          "ratio_to_algorithmic": round((index.packed.device_nbytes + sum(index.packed.derived_nbytes.values())) / db_bytes_local, 2),
+                         "ratio_batch_server": round(index.packed.derived_nbytes.get("tiles", 0) / db_bytes_local, 2),
+                         "ratio_single_query_server": round(index.packed.derived_nbytes.get("nibbles", 0) / db_bytes_local, 2),
                          "note": "derived layouts are built on first use: byte tiles (2x for 4-bit codes) by batches of >= 17 queries, the nibble "
-                                 "layout (1x) by smaller ones; this run exercised both"},
+                                 "layout (1x) by smaller ones; this run exercised both and kept the packed codes.  PackedMatrix.release_codes() frees "
+                                 "the packed codes while a layout holds the same information (rebuilt on the GPU when something reads bit planes): a "
+                                 "server that only answers large batches then holds ratio_batch_server x the algorithmic bytes, one that only answers "
+                                 "single queries ratio_single_query_server x"},
         "build": {"rows_per_s": round((hi - lo) / build_s, 1), "seconds": round(build_s, 3),
                   "quantize_kernel_ms": round(quant_ms, 3),
                   "quantize_read_GBps": round((hi - lo) * a.dim * 4 / (quant_ms * 1e-3) / 1e9, 1)},

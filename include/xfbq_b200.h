@@ -113,6 +113,13 @@ int64_t xfbq_nibble_region_bytes(int64_t n, int64_t dim, int width);  /* 0 when 
 int64_t xfbq_tile_region_bytes(int64_t n, int64_t dim);               /* 0 for dim > 1024 */
 int xfbq_build_nibbles(const void *db_dev, int64_t n, int64_t dim, int width, void *nibbles_out_dev, void *stream);
 int xfbq_build_tiles(const void *db_dev, int64_t n, int64_t dim, int width, void *tiles_out_dev, void *stream);
+/* The inverse conversions: rebuild the packed codes (bundle layout, xfbq_db_bytes) from a derived layout, so that a server may
+ * free them while it only scans (a batch server then holds the tiles alone, 2x the packed size for 4-bit codes; a single-query
+ * server the nibbles alone, 1x) and get them back for the entry points that read bit planes (the reference's PackedMatrix.planes,
+ * bitplane.py:79-122; batch_distances, distance.py:44-62; the index files, index.py:191-255).  Padding documents come back as
+ * zeros, as the quantizer writes them. */
+int xfbq_restore_codes_from_nibbles(const void *nibbles_dev, int64_t n, int64_t dim, int width, void *db_out_dev, void *stream);
+int xfbq_restore_codes_from_tiles(const void *tiles_dev, int64_t n, int64_t dim, int width, void *db_out_dev, void *stream);
 /* Which layout the preferred plan of a scan reads: XFBQ_LAYOUT_TILES (tcgen05 engine), XFBQ_LAYOUT_NIBBLES (mma.sync engine /
  * single-launch search) or 0 (XOR/POPC kernels on the bit planes). */
 int xfbq_scan_layouts(int64_t n, int64_t dim, int doc_bits, int64_t nq, int query_bits, int k);
@@ -214,7 +221,9 @@ int xfbq_scan_topk(const void *db_dev, const void *nibbles_dev, int64_t n, int64
                    uint64_t *keys_out_dev, void *workspace_dev, int64_t workspace_bytes,
                    void *stream);
 /* The same with the two derived layouts passed separately (either may be NULL; the `have_nibbles` argument of
- * xfbq_scan_workspace_bytes / xfbq_scan_plan is then XFBQ_LAYOUT_NIBBLES | XFBQ_LAYOUT_TILES as available; 1 = both). */
+ * xfbq_scan_workspace_bytes / xfbq_scan_plan is then XFBQ_LAYOUT_NIBBLES | XFBQ_LAYOUT_TILES as available; 1 = both).
+ * `db_dev` may be NULL when xfbq_scan_layouts() names a derived layout for the shape and that layout is passed: only the XOR/POPC
+ * kernels read the packed codes (see xfbq_restore_codes_from_*).  The same holds for xfbq_search_small_* / xfbq_kselect_small_f64. */
 int xfbq_scan_topk_layouts(const void *db_dev, const void *nibbles_dev, const void *tiles_dev, int64_t n, int64_t dim, int doc_bits,
                            const uint32_t *q_dev, int64_t nq, int query_bits, int k, int64_t row_offset,
                            uint64_t *keys_out_dev, void *workspace_dev, int64_t workspace_bytes, void *stream);

@@ -32,7 +32,7 @@ SYMBOLS = [
     "xfbq_distance_upper_bound", "xfbq_quantize_pack_f32", "xfbq_quantize_pack_f64",
     "xfbq_quantize_queries_f32", "xfbq_quantize_queries_f64", "xfbq_planes_to_bundles",
     "xfbq_bundles_to_planes", "xfbq_nibble_bytes", "xfbq_planes_to_nibbles", "xfbq_derived_bytes", "xfbq_build_derived",
-    "xfbq_nibble_region_bytes", "xfbq_tile_region_bytes", "xfbq_build_nibbles", "xfbq_build_tiles", "xfbq_scan_layouts", "xfbq_scan_topk_layouts", "xfbq_batch_distances", "xfbq_collect_candidates", "xfbq_collect_candidates_nibbles",
+    "xfbq_nibble_region_bytes", "xfbq_tile_region_bytes", "xfbq_build_nibbles", "xfbq_build_tiles", "xfbq_restore_codes_from_nibbles", "xfbq_restore_codes_from_tiles", "xfbq_scan_layouts", "xfbq_scan_topk_layouts", "xfbq_batch_distances", "xfbq_collect_candidates", "xfbq_collect_candidates_nibbles",
     "xfbq_select_workspace_bytes", "xfbq_abs_order_stats_f32", "xfbq_abs_order_stats_f64", "xfbq_refine_workspace_bytes", "xfbq_refine_f32",
     "xfbq_distance_histogram", "xfbq_histogram_kth", "xfbq_gather_workspace_bytes", "xfbq_gather_le_count", "xfbq_gather_le_ids",
     "xfbq_search_small_workspace_bytes", "xfbq_search_small_f32", "xfbq_search_small_f64", "xfbq_kselect_small_f64",
@@ -118,6 +118,8 @@ def lib():
         "xfbq_nibble_region_bytes": (i64, [i64, i64, i32]),
         "xfbq_tile_region_bytes": (i64, [i64, i64]),
         "xfbq_build_nibbles": (i32, [vp, i64, i64, i32, vp, vp]),
+        "xfbq_restore_codes_from_nibbles": (i32, [vp, i64, i64, i32, vp, vp]),
+        "xfbq_restore_codes_from_tiles": (i32, [vp, i64, i64, i32, vp, vp]),
         "xfbq_build_tiles": (i32, [vp, i64, i64, i32, vp, vp]),
         "xfbq_scan_layouts": (i32, [i64, i64, i32, i64, i32, i32]),
         "xfbq_scan_topk_layouts": (i32, [vp, vp, vp, i64, i64, i32, vp, i64, i32, i32, i64, vp, vp, i64, vp]),

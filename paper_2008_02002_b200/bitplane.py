@@ -144,12 +144,48 @@ class PackedMatrix:
 
     @property
     def device_nbytes(self) -> int:
-        return int(self._codes.numel())
+        """Bytes of the packed codes resident in HBM (0 after :meth:`release_codes`)."""
+        return int(self._codes.numel()) if self._codes is not None else 0
 
     @property
     def codes(self):
-        """torch.uint8 device buffer holding the bundle layout."""
+        """torch.uint8 device buffer holding the bundle layout.  After :meth:`release_codes` it is rebuilt here, on the GPU,
+        from the nibble layout (``xfbq_restore_codes_from_nibbles``) or the byte tiles (``xfbq_restore_codes_from_tiles``)."""
+        if self._codes is None:
+            torch = _native.require_cuda()
+            L = _native.lib()
+            src, fn = ((self._nibbles, L.xfbq_restore_codes_from_nibbles) if getattr(self, "_nibbles", None) is not None
+                       else (getattr(self, "_tiles", None), L.xfbq_restore_codes_from_tiles))
+            if src is None:  # release_layout() refuses to drop the last copy, so this cannot happen through the API
+                raise NativeLibraryError("the packed codes were released and no derived layout is left to rebuild them from")
+            with torch.cuda.device(src.device):
+                codes = torch.zeros(max(int(L.xfbq_db_bytes(self._count, self._dim, self._width)), 16), dtype=torch.uint8, device=src.device)
+                _native.check(fn(src.data_ptr(), self._count, self._dim, self._width, codes.data_ptr(), _stream_ptr(torch)))
+            self._codes = codes
         return self._codes
+
+    @property
+    def device(self):
+        """The GPU the codes live on (never rebuilds anything)."""
+        for t in (self._codes, getattr(self, "_nibbles", None), getattr(self, "_tiles", None)):
+            if t is not None:
+                return t.device
+        raise NativeLibraryError("no device buffer")
+
+    @property
+    def codes_ptr(self):
+        """Device pointer of the packed codes, or None after :meth:`release_codes` (the scans that read a derived layout take a
+        null pointer for them; nothing is rebuilt here)."""
+        return self._codes.data_ptr() if self._codes is not None else None
+
+    def release_codes(self) -> None:
+        """Free the packed codes (the bundle layout) while a derived layout holds the same information: a server that only
+        answers large batches then keeps the byte tiles alone (2x the packed size for 4-bit codes), one that only answers
+        single queries the nibbles alone (1x).  Anything that reads bit planes (``planes``, ``batch_distances``, ``save_index``,
+        the XOR/POPC kernels, building the other derived layout) rebuilds them on the GPU first."""
+        if getattr(self, "_nibbles", None) is None and getattr(self, "_tiles", None) is None:
+            raise InvalidInputError("no derived layout to rebuild the codes from: build nibble_layout or tile_layout first")
+        self._codes = None
 
     @property
     def planes(self) -> np.ndarray:
@@ -157,10 +193,11 @@ class PackedMatrix:
             torch = _native.require_cuda()
             L = _native.lib()
             W64 = words_needed(self._dim)
-            with torch.cuda.device(self._codes.device):
-                out = torch.zeros((self._width, W64, self._count), dtype=torch.int64, device=self._codes.device)
+            codes = self.codes
+            with torch.cuda.device(codes.device):
+                out = torch.zeros((self._width, W64, self._count), dtype=torch.int64, device=codes.device)
                 if self._count:
-                    _native.check(L.xfbq_bundles_to_planes(self._codes.data_ptr(), self._count, self._dim,
+                    _native.check(L.xfbq_bundles_to_planes(codes.data_ptr(), self._count, self._dim,
                                                            self._width, out.data_ptr(), _stream_ptr(torch)))
                 host = out.cpu().numpy().view(np.uint64)
             host.setflags(write=False)
@@ -175,9 +212,10 @@ class PackedMatrix:
             nbytes = int(getattr(L, size_fn)(*size_args))
             if nbytes == 0 or self._count == 0:
                 return None
-            with torch.cuda.device(self._codes.device):
-                cached = torch.empty(nbytes, dtype=torch.uint8, device=self._codes.device)
-                _native.check(getattr(L, build_fn)(self._codes.data_ptr(), self._count, self._dim, self._width,
+            codes = self.codes
+            with torch.cuda.device(codes.device):
+                cached = torch.empty(nbytes, dtype=torch.uint8, device=codes.device)
+                _native.check(getattr(L, build_fn)(codes.data_ptr(), self._count, self._dim, self._width,
                                                    cached.data_ptr(), _stream_ptr(torch)))
             setattr(self, attr, cached)
         return cached
@@ -206,6 +244,9 @@ class PackedMatrix:
         """Free a derived layout ("nibbles" or "tiles"); it is rebuilt if a later search needs it."""
         if name not in ("nibbles", "tiles"):
             raise InvalidInputError("layout must be 'nibbles' or 'tiles'")
+        other = "_tiles" if name == "nibbles" else "_nibbles"
+        if self._codes is None and getattr(self, other, None) is None:
+            raise InvalidInputError("this layout is the only copy of the codes left (release_codes() was called): rebuild the codes first")
         setattr(self, "_" + name, None)
 
     def row(self, k: int) -> PackedVector:

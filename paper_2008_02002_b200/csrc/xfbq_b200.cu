@@ -2042,6 +2042,32 @@ XFBQ_API int xfbq_build_tiles(const void *db, int64_t n, int64_t dim, int width,
     return check_launch("planes_to_tiles_kernel");
 }
 
+XFBQ_API int xfbq_restore_codes_from_nibbles(const void *nibbles, int64_t n, int64_t dim, int width, void *db_out, void *stream) {
+    if (width < 1 || width > 4) return fail(XFBQ_E_UNSUPPORTED, "nibble layout holds codes of at most 4 bits, got %d", width);
+    if (n < 0 || dim < 1) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld", (long long)n, (long long)dim);
+    if (n == 0) return XFBQ_OK;
+    if (nibble_region_bytes(n, dim, width) == 0) return fail(XFBQ_E_UNSUPPORTED, "no nibble layout for dim=%lld", (long long)dim);
+    if (!nibbles || !db_out) return fail(XFBQ_E_INVALID, "null pointer");
+    const int C = static_cast<int>(chunks128(dim));
+    const int64_t n_pad = bundles_of(n) * 32, total = n_pad * 4 * C;
+    mma::nibbles_to_planes_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint4 *>(nibbles), n_pad, width, C, static_cast<uint32_t *>(db_out));
+    return check_launch("nibbles_to_planes_kernel");
+}
+
+XFBQ_API int xfbq_restore_codes_from_tiles(const void *tiles, int64_t n, int64_t dim, int width, void *db_out, void *stream) {
+    if (!width_ok(width)) return fail(XFBQ_E_INVALID, "bit width must be in 1..8, got %d", width);
+    if (n < 0 || dim < 1) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld", (long long)n, (long long)dim);
+    if (n == 0) return XFBQ_OK;
+    if (!tiles_supported(dim)) return fail(XFBQ_E_UNSUPPORTED, "no tile layout for dim=%lld", (long long)dim);
+    if (!tiles || !db_out) return fail(XFBQ_E_INVALID, "null pointer");
+    const int C = static_cast<int>(chunks128(dim)), CT = tile_geom(dim).CT;
+    const int64_t n_pad = bundles_of(n) * 32, total = n_pad * 4 * C;
+    umma::tiles_to_planes_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const unsigned char *>(tiles), n_pad, width, C, CT, static_cast<uint32_t *>(db_out));
+    return check_launch("tiles_to_planes_kernel");
+}
+
 XFBQ_API int xfbq_build_derived(const void *db, int64_t n, int64_t dim, int width, void *out, void *stream) {
     if (int rc = xfbq_build_nibbles(db, n, dim, width, out, stream)) return rc;
     if (n <= 0 || dim < 1 || !out) return XFBQ_OK;
@@ -2321,7 +2347,8 @@ int search_small_impl(const void *db, const void *nib, int64_t n, int64_t dim, i
     if (n < 1 || dim < 1 || nq < 1 || ld < dim) return fail(XFBQ_E_INVALID, "bad shape n=%lld dim=%lld nq=%lld ld=%lld", (long long)n, (long long)dim, (long long)nq, (long long)ld);
     if (k < 1) return fail(XFBQ_E_INVALID, "k must be >= 1, got %d", k);
     if (row_offset < 0 || row_offset + n > (1ll << 32)) return fail(XFBQ_E_UNSUPPORTED, "row ids must fit 32 bits");
-    if (!db || !nib || !queries || !keys_out || !nonfinite || !workspace) return fail(XFBQ_E_INVALID, "null pointer");
+    (void)db;  // the single-launch search reads the nibble layout only: the packed codes may have been released (null)
+    if (!nib || !queries || !keys_out || !nonfinite || !workspace) return fail(XFBQ_E_INVALID, "null pointer");
     CoopPlan cp;
     if (int rc = make_coop_plan(n, dim, wd, nq, wq, k, true, &cp)) return rc;
     if (!cp.ok) return fail(XFBQ_E_UNSUPPORTED, "no single-launch search for this shape (xfbq_search_small_workspace_bytes returns 0)");
@@ -2462,7 +2489,7 @@ XFBQ_API int xfbq_scan_topk_layouts(const void *db, const void *nib, const void 
         if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
         return XFBQ_OK;
     }
-    if (!db || !q) return fail(XFBQ_E_INVALID, "null pointer");
+    if (!q) return fail(XFBQ_E_INVALID, "null pointer");
     UmmaPlan up;
     if (int rc = make_umma_plan(n, dim, wd, nq, wq, k, tiles != nullptr, &up)) return rc;
     if (up.ok) {
@@ -2505,6 +2532,7 @@ XFBQ_API int xfbq_scan_topk_layouts(const void *db, const void *nib, const void 
         }
         return run_mma_scan(mp.main, mp, ws, nib, n, C, nq, k, row_offset, tau_init, keys_out, st);
     }
+    if (!db) return fail(XFBQ_E_INVALID, "this shape scans the bit planes (XOR/POPC kernels): the packed codes are required");
     ScanPlan pl;
     if (int rc = make_plan(n, dim, wd, nq, wq, k, &pl)) return rc;
     const int64_t need = pl.splits <= 1 ? 0 : static_cast<int64_t>(pl.splits + merge_scratch_parts(pl.splits, k, nq)) * nq * k * 8;

@@ -123,6 +123,22 @@ planes_to_nibbles_kernel(const uint32_t *__restrict__ db, int64_t n_pad, int wd,
     out[(b * 32 + dl) * G + grp] = planes_to_nibbles(p[0], p[1], p[2], p[3]);
 }
 
+// nibble layout -> bundle layout (bit planes): the 4x4 bit-block transpose is its own inverse.  Lets a server that only answers
+// single queries keep the nibbles alone (1x the packed size) and rebuild the packed codes when something needs them.
+__global__ void __launch_bounds__(256)
+nibbles_to_planes_kernel(const uint4 *__restrict__ nib, int64_t n_pad, int wd, int C, uint32_t *__restrict__ db) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int G = 4 * C;
+    if (e >= n_pad * G) return;
+    const int64_t b = e / (32 * G);
+    const int rem = static_cast<int>(e - b * (32 * G));
+    const int grp = rem >> 5, dl = rem & 31;
+    const uint4 w = nib[(b * 32 + dl) * G + grp];
+    const uint4 p = planes_to_nibbles(w.x, w.y, w.z, w.w);
+    const uint32_t pl[4] = {p.x, p.y, p.z, p.w};
+    for (int i = 0; i < wd; ++i) db[((((b * wd + i) * C + (grp >> 2)) * 32 + dl) << 2) + (grp & 3)] = pl[i];
+}
+
 // D = A(s8, 16x32 row) * B(u8, 32x8 col) + C
 __device__ __forceinline__ void imma(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1,
                                      int c0, int c1, int c2, int c3) {

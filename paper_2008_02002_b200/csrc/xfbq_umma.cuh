@@ -255,6 +255,32 @@ planes_to_tiles_kernel(const uint32_t *__restrict__ db, int64_t n_pad, int64_t n
     *reinterpret_cast<uint4 *>(rowp + (((2 * gg + 1) ^ (r & 7)) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
 }
 
+// byte tiles -> bundle layout (bit planes): the inverse of planes_to_tiles_kernel, one thread per (document, group of 32 dims).
+// Lets a server that only answers large batches keep the tiles alone and rebuild the packed codes when something needs them.
+__global__ void __launch_bounds__(256)
+tiles_to_planes_kernel(const unsigned char *__restrict__ tiles, int64_t n_pad, int wd, int CP, int C, uint32_t *__restrict__ db) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int G = 4 * CP;  // groups of the bundle layout; the tile may hold padded chunks beyond them
+    if (e >= n_pad * G) return;
+    const int64_t doc = e / G;
+    const int g = static_cast<int>(e - doc * G);
+    const int64_t tile = doc / STAGE_DOCS;
+    const int r = static_cast<int>(doc - tile * STAGE_DOCS);
+    const int kb = g >> 2, gg = g & 3;
+    const unsigned char *rowp = tiles + tile * (static_cast<int64_t>(STAGE_DOCS) * 128 * C) + kb * (STAGE_DOCS * 128) + (r >> 3) * 1024 + (r & 7) * 128;
+    const uint4 lo = *reinterpret_cast<const uint4 *>(rowp + (((2 * gg) ^ (r & 7)) << 4));
+    const uint4 hi = *reinterpret_cast<const uint4 *>(rowp + (((2 * gg + 1) ^ (r & 7)) << 4));
+    const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};  // w[2 e + hi]: bytes j = codes of dims e + 4 hi + 8 j
+    const int64_t b = doc >> 5;
+    const int l = static_cast<int>(doc & 31);
+    for (int i = 0; i < wd; ++i) {
+        uint32_t pw = 0u;
+#pragma unroll
+        for (int x = 0; x < 8; ++x) pw |= ((w[x] >> i) & 0x01010101u) << ((x >> 1) + 4 * (x & 1));
+        db[((((b * wd + i) * CP + kb) * 32 + l) << 2) + gg] = pw;
+    }
+}
+
 // mbarrier wait (every lane polls: measured far faster than one polling lane + warp barrier) that adds the
 // cycles spent waiting to `acc` when profiling is on
 __device__ __forceinline__ void mbar_wait_prof(uint64_t *bar, uint32_t parity, bool prof, long long &acc) {

@@ -51,9 +51,9 @@ def batch_distances_device(matrix: PackedMatrix, query: PackedVector):
     """Device-resident int64[n] distances (same values)."""
     torch = _native.require_cuda()
     L = _native.lib()
-    with torch.cuda.device(matrix.codes.device):
-        q = query.device_words(matrix.codes.device)
-        d = torch.empty(matrix.count, dtype=torch.int64, device=matrix.codes.device)
+    with torch.cuda.device(matrix.device):
+        q = query.device_words(matrix.device)
+        d = torch.empty(matrix.count, dtype=torch.int64, device=matrix.device)
         _native.check(L.xfbq_batch_distances(matrix.codes.data_ptr(), matrix.count, matrix.dim, matrix.width,
                                              q.data_ptr(), query.width, d.data_ptr(), _stream_ptr(torch)))
     return d
@@ -67,7 +67,7 @@ def collect_candidates_device(matrix: PackedMatrix, query, threshold: int, want_
     count when `cap` was too small (second pass)."""
     torch = _native.require_cuda()
     L = _native.lib()
-    dev = matrix.codes.device
+    dev = matrix.device
     with torch.cuda.device(dev):
         if isinstance(query, PackedVector):
             q, wq = query.device_words(dev), query.width

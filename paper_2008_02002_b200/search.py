@@ -80,7 +80,7 @@ def _search_small_fused(index: Index, queries, k: int, row_offset: int):
     nq = int(queries.shape[0])
     if not 1 <= nq <= 16 or packed.width > 4 or p.query_bits > 7 or packed.dim > 512 or k > 1024:
         return None
-    dev = packed.codes.device
+    dev = packed.device
     ws_bytes = int(L.xfbq_search_small_workspace_bytes(packed.count, packed.dim, packed.width, nq, p.query_bits, k))
     if ws_bytes <= 0:
         return None
@@ -101,7 +101,7 @@ def _search_small_fused(index: Index, queries, k: int, row_offset: int):
     if SCAN_EVENTS is not None:
         ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
         ev[0].record()
-    _native.check(fn(packed.codes.data_ptr(), nib.data_ptr(), packed.count, packed.dim, packed.width, queries.data_ptr(), nq, ld,
+    _native.check(fn(packed.codes_ptr, nib.data_ptr(), packed.count, packed.dim, packed.width, queries.data_ptr(), nq, ld,
                      float(p.scale), p.query_bits, k, int(row_offset), keys.data_ptr(), counter.data_ptr(), ws.data_ptr(), ws.numel(),
                      _stream_ptr(torch)))
     if SCAN_EVENTS is not None:
@@ -119,7 +119,7 @@ def _kselect_small_fused(index: Index, query: np.ndarray, k: int, extra: int, wa
     packed, p = index.packed, index.params
     if packed.width > 4 or p.query_bits > 7 or packed.dim > 512 or k > 1024 or extra >= (1 << 30):
         return None
-    dev = packed.codes.device
+    dev = packed.device
     ws_bytes = int(L.xfbq_search_small_workspace_bytes(packed.count, packed.dim, packed.width, 1, p.query_bits, k))
     if ws_bytes <= 0:
         return None
@@ -134,7 +134,7 @@ def _kselect_small_fused(index: Index, query: np.ndarray, k: int, extra: int, wa
         keys = torch.empty(k + 2, dtype=torch.int64, device=dev)        # k keys, candidate count, inexact flag: one D2H copy
         ids = torch.empty(cap if want_ids else 0, dtype=torch.int64, device=dev)
         ws = _workspace(torch, dev, ws_bytes)
-        _native.check(L.xfbq_kselect_small_f64(packed.codes.data_ptr(), nib.data_ptr(), packed.count, packed.dim, packed.width,
+        _native.check(L.xfbq_kselect_small_f64(packed.codes_ptr, nib.data_ptr(), packed.count, packed.dim, packed.width,
                                                q_dev.data_ptr(), 1, packed.dim, float(p.scale), p.query_bits, k, int(extra), 0,
                                                keys.data_ptr(), keys.data_ptr() + 8 * k, ids.data_ptr() if want_ids else None, cap,
                                                keys.data_ptr() + 8 * (k + 1), counter.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(torch)))
@@ -152,7 +152,7 @@ def scan_topk_device(packed: PackedMatrix, qwords, nq: int, query_bits: int, k: 
     (distance << 32 | row_offset + row; 0xFFFF... for empty slots)."""
     torch = _native.require_cuda()
     L = _native.lib()
-    dev = packed.codes.device
+    dev = packed.device
     with torch.cuda.device(dev):
         keys = torch.empty((nq, k), dtype=torch.int64, device=dev)
         if nq == 0:
@@ -187,7 +187,8 @@ def scan_topk_device(packed: PackedMatrix, qwords, nq: int, query_bits: int, k: 
             if SCAN_EVENTS is not None:
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 ev[0].record()
-            _native.check(L.xfbq_scan_topk_layouts(packed.codes.data_ptr(), nib.data_ptr() if nib is not None else None,
+            # the XOR/POPC kernels (want == 0) read the packed codes: rebuilt here if they were released; the other plans do not
+            _native.check(L.xfbq_scan_topk_layouts(packed.codes.data_ptr() if want == 0 else packed.codes_ptr, nib.data_ptr() if nib is not None else None,
                                                    tiles.data_ptr() if tiles is not None else None, packed.count, packed.dim,
                                                    packed.width, qptr, qn, query_bits, k, int(row_offset),
                                                    keys.data_ptr() + q0 * k * 8, ws.data_ptr(), ws.numel(), st))
@@ -234,7 +235,7 @@ def search_device(index: Index, queries, k: int, row_offset: int = 0, check: boo
     p = index.params
     kk = min(int(k), index.n)
     torch = _native.require_cuda()
-    dev = index.packed.codes.device
+    dev = index.packed.device
     with torch.cuda.device(dev):
         if kk == 0 or queries.shape[0] == 0:
             return torch.empty((queries.shape[0], kk), dtype=torch.int64, device=dev)
@@ -319,7 +320,7 @@ def _refine_device(index: Index, query: np.ndarray, cand, k: int):
     host (count rows, a memory move) and only those rows are uploaded -- the whole matrix (10 GB at 10M x 256) never is."""
     torch = _native.require_cuda()
     L = _native.lib()
-    dev = index.packed.codes.device
+    dev = index.packed.device
     count = int(cand.numel())
     kk = min(int(k), count)
     if kk == 0:
@@ -377,7 +378,7 @@ def k_select(index: Index, request: SearchRequest, collect_timing: bool = False)
     upper = distance_upper_bound(p.dim, p.doc_bits, p.query_bits)
 
     t0 = time.perf_counter()
-    dev = index.packed.codes.device
+    dev = index.packed.device
     want_ids = index.originals is not None
     extra = min(int(request.extra_distance), upper)
     fused = _kselect_small_fused(index, request.query, kk, extra, want_ids, cap=max(1 << 16, 4 * kk))
@@ -520,11 +521,11 @@ def refine(index: Index, query, candidates, k: int, distances=None):
     q = np.ascontiguousarray(query, dtype=np.float64)
     p = index.params
     if index.originals is not None:
-        hits = _refine_device(index, q, torch.from_numpy(cand).to(index.packed.codes.device), k)
+        hits = _refine_device(index, q, torch.from_numpy(cand).to(index.packed.device), k)
         return hits, False
     if distances is None:
         from .distance import batch_distances_device
-        cand_d = batch_distances_device(index.packed, quantize_vector(q, p.query_bits, p.scale))[torch.from_numpy(cand).to(index.packed.codes.device)].cpu().numpy()
+        cand_d = batch_distances_device(index.packed, quantize_vector(q, p.query_bits, p.scale))[torch.from_numpy(cand).to(index.packed.device)].cpu().numpy()
     else:
         cand_d = np.asarray(distances)[cand]
     sims = decode_inner_product_values(cand_d, p.dim, p.doc_bits, p.query_bits)

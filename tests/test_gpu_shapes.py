@@ -151,3 +151,52 @@ def test_derived_layouts_are_built_on_demand_and_legacy_buffer_still_works():
         xb._native.check(L.xfbq_scan_topk(pm.codes.data_ptr(), derived.data_ptr(), n, dim, 4, qwords.data_ptr(), nq, 4, k, 0,
                                           keys.data_ptr(), ws.data_ptr(), ws.numel(), st))
         assert np.array_equal((keys.cpu().numpy() >> 32), s64[:nq]) and np.array_equal(keys.cpu().numpy() & 0xFFFFFFFF, i64[:nq])
+
+
+@pytest.mark.parametrize("n,dim,wd", [(70_001, 256, 4), (50_000, 200, 3), (40_000, 768, 4), (30_000, 128, 7)])
+def test_release_codes_and_rebuild_from_derived_layouts(n, dim, wd, monkeypatch):
+    """The packed codes may be freed while a derived layout holds the same information (a batch server keeps the byte tiles
+    alone, a single-query server the nibbles alone): searches that read the layout run without them, and everything that
+    reads bit planes gets them back bit for bit (xfbq_restore_codes_from_tiles / _nibbles)."""
+    docs = xo.synthetic_unit_rows(n, dim, 31)
+    queries = xo.synthetic_unit_rows(40, dim, 32)
+    scale = xo.estimate_scale(docs[:20_000], 0.98)
+    idx = xb.build_index(docs, xb.QuantParams(dim=dim, scale=scale, doc_bits=wd, query_bits=4), keep_originals=False)
+    packed = idx.packed
+    planes = xo.c_quantize_matrix(docs, wd, scale)
+    qp = xo.c_quantize_matrix(queries.astype(np.float64), 4, scale).transpose(2, 0, 1)
+    want_d, want_i = xo.c_search(planes, qp, 10)
+    codes0 = packed.codes.clone()
+    with pytest.raises(xb.InvalidInputError):
+        packed.release_codes()                       # nothing to rebuild them from yet
+    monkeypatch.setenv("XFBQ_ENGINE", "umma")
+    s, i = xb.search(idx, queries, 10)               # builds the byte tiles
+    assert np.array_equal(i, want_i) and packed.derived_nbytes["tiles"] > 0
+    packed.release_codes()
+    assert packed.device_nbytes == 0 and packed.codes_ptr is None
+    s, i = xb.search(idx, queries, 10)               # tiles only: no packed codes in HBM
+    assert np.array_equal(s.astype(np.uint64), want_d) and np.array_equal(i, want_i)
+    assert packed.codes_ptr is None
+    monkeypatch.delenv("XFBQ_ENGINE")
+    with pytest.raises(xb.InvalidInputError):
+        packed.release_layout("tiles")               # the only copy left
+    assert torch_equal(packed.codes, codes0)         # rebuilt from the tiles
+    packed._planes = None
+    assert np.array_equal(packed.planes, planes)
+    if wd <= 4 and dim <= 512:
+        assert packed.nibble_layout is not None
+        packed.release_layout("tiles")
+        packed.release_codes()
+        s1, i1 = xb.search(idx, queries[:3], 10)     # nibbles only (single-launch search or the mma.sync plan)
+        assert np.array_equal(i1, want_i[:3]) and np.array_equal(s1.astype(np.uint64), want_d[:3])
+        assert torch_equal(packed.codes, codes0)     # rebuilt from the nibbles
+    monkeypatch.setenv("XFBQ_ENGINE", "popc")        # the XOR/POPC kernels read the packed codes: rebuilt on demand
+    packed.tile_layout
+    packed.release_codes()
+    s2, i2 = xb.search(idx, queries[:5], 10)
+    assert np.array_equal(i2, want_i[:5]) and np.array_equal(s2.astype(np.uint64), want_d[:5])
+
+
+def torch_equal(a, b):
+    import torch
+    return bool(torch.equal(a, b))

@@ -44,6 +44,7 @@ def test_ties_on_every_engine(distinct, monkeypatch):
         routes = [
             {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1"},                                  # counted seed + queue kernel + bounded merge
             {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_UMMA_SLICES": "9"},        # several document slices per group
+            {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_UMMA_STAGES": "2"},        # two-tile operand ring: the issuer's "next group not ready" path
             {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_MERGE_BUF": "2048" if k > 512 else "1024"},  # merge overflow path
             {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_UMMA_HIST": "0"},          # no candidate histogram
             {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SEED_HIST": "0"},          # list-keeping sample scan
