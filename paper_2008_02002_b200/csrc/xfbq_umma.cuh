@@ -1240,6 +1240,9 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                 __syncwarp();
             }
             for (int i = 0; i < sg.cnt; ++i) {
+                uint32_t tz;   // a zero neither compiler can see through or hoist: tensor-memory addresses below are `tz + constant`, so ptxas moves ONE
+                               // register to the uniform datapath per block and adds the constants there instead of eight R2UR
+                asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(tz) : "r"(smem_u32(tmem_slot)));  // the allocation's base: 0 (checked above)
                 const uint32_t b_lo = b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4);
                 const uint32_t d0 = static_cast<uint32_t>(ac.idx) * STAGE_DOCS;
                 uint64_t *stage_done = &b_empty[rb.idx];
@@ -1255,24 +1258,24 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                     if (ready(&acc_empty[ac.idx], ac.phase)) {   // the second query tile's accumulator is free: one block
                         fence_after();
                         if (elect_one()) {
-                            mmas(d0, ACOL0, b_lo, H, KSTEPS);
+                            mmas(d0, tz + ACOL0, b_lo, H, KSTEPS);
                             umma_commit(acc0_done);
-                            mmas(d1, ACOL0 + A_COLS, b_lo, 0, H);
+                            mmas(d1, tz + ACOL0 + A_COLS, b_lo, 0, H);
                         }
                         __syncwarp();
                     } else {
-                        if (elect_one()) { mmas(d0, ACOL0, b_lo, H, KSTEPS); umma_commit(acc0_done); }
+                        if (elect_one()) { mmas(d0, tz + ACOL0, b_lo, H, KSTEPS); umma_commit(acc0_done); }
                         __syncwarp();
                         wait_acc(ac);
                         fence_after();
-                        if (elect_one()) mmas(d1, ACOL0 + A_COLS, b_lo, 0, H);
+                        if (elect_one()) mmas(d1, tz + ACOL0 + A_COLS, b_lo, 0, H);
                         __syncwarp();
                     }
                     ac.advance(AB);
                 }
                 // second half of the tile's last group, the commits, and -- when it can start -- the first half of the next tile
                 const uint32_t dl = MT == 2 ? d1 : d0;
-                const uint32_t al = MT == 2 ? ACOL0 + A_COLS : ACOL0;
+                const uint32_t al = tz + (MT == 2 ? ACOL0 + A_COLS : ACOL0);
                 uint64_t *accl_done = MT == 2 ? acc1_done : acc0_done;
                 const uint32_t dn = static_cast<uint32_t>(ac.idx) * STAGE_DOCS;
                 const uint32_t bn = b_lo0 + static_cast<uint32_t>(rb.idx) * (B_STAGE >> 4);
@@ -1282,7 +1285,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                         mmas(dl, al, b_lo, H, KSTEPS);
                         umma_commit(accl_done);
                         umma_commit(stage_done);
-                        mmas(dn, ACOL0, bn, 0, H);
+                        mmas(dn, tz + ACOL0, bn, 0, H);
                     }
                     __syncwarp();
                 } else {
@@ -1290,7 +1293,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                     __syncwarp();
                     if (more) {
                         wait_operand(rb); wait_acc(ac); fence_after();
-                        if (elect_one()) mmas(dn, ACOL0, bn, 0, H);
+                        if (elect_one()) mmas(dn, tz + ACOL0, bn, 0, H);
                         __syncwarp();
                     }
                 }
