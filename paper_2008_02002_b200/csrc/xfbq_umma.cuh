@@ -1264,6 +1264,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                         }
                         __syncwarp();
                     } else {
+                        ++w2;   // profiling: the second query tile's accumulator was not free at the probe
                         if (elect_one()) { mmas(d0, tz + ACOL0, b_lo, H, KSTEPS); umma_commit(acc0_done); }
                         __syncwarp();
                         wait_acc(ac);
@@ -1289,6 +1290,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                     }
                     __syncwarp();
                 } else {
+                    if (more) w2 += 1 << 16;   // profiling: the next tile's operand or accumulator was not there at the probe
                     if (elect_one()) { mmas(dl, al, b_lo, H, KSTEPS); umma_commit(accl_done); umma_commit(stage_done); }
                     __syncwarp();
                     if (more) {
@@ -1303,7 +1305,11 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
             cta_sync();  // lists final
             cta_sync();  // lists emitted
         }
-        if (prof && lane == 0) { p.prof[blockIdx.x * 8 + 2] = w0; p.prof[blockIdx.x * 8 + 3] = w1; }
+        if (prof && lane == 0) {
+            p.prof[blockIdx.x * 8 + 2] = w0; p.prof[blockIdx.x * 8 + 3] = w1;
+            p.prof[gridDim.x * 8 + blockIdx.x * 4 + 0] = static_cast<unsigned>(w2) & 0xFFFFu;   // probes that failed: second query tile ...
+            p.prof[gridDim.x * 8 + blockIdx.x * 4 + 1] = static_cast<unsigned>(w2) >> 16;        // ... next document tile
+        }
     } else if (warp == Q_TMA_WARP) {
         // ================================ loader ================================
         const unsigned char *db = reinterpret_cast<const unsigned char *>(p.db);

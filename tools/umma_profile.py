@@ -45,6 +45,7 @@ for i, nm in enumerate(names):
     else:
         print(f"  {nm:34s} {c[:, i].mean() / 1e6:9.2f} Mclk  {c[:, i].mean() / tot * 100:5.1f}%  min {c[:, i].min() / tot * 100:5.1f}% max {c[:, i].max() / tot * 100:5.1f}%")
 print(f"  epi warp0 compactions {x[:, 2].mean():.0f}")
+print(f"  issuer probes that failed (per CTA): second query tile {x[:, 0].mean():.0f}, next document tile {x[:, 1].mean():.0f} of {st:.0f} tiles (16-bit counters)")
 if len(sys.argv) > 5:
     print("per CTA: stages, total Mclk, clk/stage, mma wait acc_empty %, mma wait b_full %, drain w0 wait acc_full %, ring-full %")
     for b in range(148):
