@@ -1227,7 +1227,7 @@ void mma_shape(int64_t n, int wd, int C, int64_t nq, int k, const DeviceInfo &in
 // Thresholds by counting (defined with the tcgen05 planning below; shared by both tensor engines).
 int run_counted_seed(unsigned char *ws, const void *tiles, int64_t n, int64_t dim, int wd, const uint32_t *q, int64_t nq, int wq,
                      int k, int64_t sample, bool prep, size_t off_qimg, size_t off_qconst, size_t off_par, size_t off_hist,
-                     int32_t *tau, cudaStream_t st);
+                     int32_t *tau, cudaStream_t st, int32_t *theta0 = nullptr, uint32_t *ghist = nullptr);
 
 int make_mma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bool have_nibbles, MmaPlan *plan, bool have_tiles = true) {
     MmaPlan pl;
@@ -1765,7 +1765,7 @@ int run_umma_scan(const UmmaShape &sh, const UmmaPlan &pl, unsigned char *ws, co
 // count reaches k.  tau[q] is in the accumulator domain both tensor engines use (Dq - distance).
 int run_counted_seed(unsigned char *ws, const void *tiles, int64_t n, int64_t dim, int wd, const uint32_t *q, int64_t nq, int wq,
                      int k, int64_t sample, bool prep, size_t off_qimg, size_t off_qconst, size_t off_par, size_t off_hist,
-                     int32_t *tau, cudaStream_t st) {
+                     int32_t *tau, cudaStream_t st, int32_t *theta0, uint32_t *ghist) {
     const TileGeom tg = tile_geom(dim);
     const int C = tg.Cp;
     DeviceInfo info;
@@ -1787,14 +1787,12 @@ int run_counted_seed(unsigned char *ws, const void *tiles, int64_t n, int64_t di
     }
     int2 *par = reinterpret_cast<int2 *>(ws + off_par);
     uint32_t *hist = reinterpret_cast<uint32_t *>(ws + off_hist);
-    cudaError_t e = cudaMemsetAsync(hist, 0, static_cast<size_t>(nq) * umma::SEED_BINS * 4, st);
-    if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "memset: %s", cudaGetErrorString(e));
     umma::seed_stats_kernel<<<static_cast<unsigned>(nq), 128, 0, st>>>(static_cast<const unsigned char *>(tiles), qimg, nq, tg.CT, pl.pre.stages, pl.pre.tile_stride,
                                                                     static_cast<float>(normal_quantile(static_cast<double>(k) / static_cast<double>(sample))),
-                                                                    0.25f * env_int("XFBQ_SEED_BELOW4", 8), par);
+                                                                    0.25f * env_int("XFBQ_SEED_BELOW4", 8), par, hist);
     if (int rc = check_launch("umma::seed_stats_kernel")) return rc;
     if (int rc = run_umma_scan(pl.pre, pl, ws, tiles, sample, C, nq, k, 0, nullptr, nullptr, st)) return rc;
-    umma::seed_bounds_kernel<<<static_cast<unsigned>((nq * 32 + 255) / 256), 256, 0, st>>>(hist, par, nq, k, tau);
+    umma::seed_bounds_kernel<<<static_cast<unsigned>((nq * 32 + 255) / 256), 256, 0, st>>>(hist, par, nq, k, tau, theta0, ghist);
     return check_launch("umma::seed_bounds_kernel");
 }
 
@@ -1810,19 +1808,23 @@ int run_umma(const UmmaPlan &up, unsigned char *ws, const void *nib, int64_t n, 
     if (up.sample) {
         uint64_t *prekeys = reinterpret_cast<uint64_t *>(ws + up.off_prekeys);
         int32_t *tau = reinterpret_cast<int32_t *>(ws + up.off_tau);
-        if (up.pre.count) {
+        const bool hist_main = up.off_ghist > up.off_theta0;  // global candidate histogram of the main scan, bins measured from the seeded thresholds
+        if (up.pre.count) {   // the bounds kernel also copies the thresholds and clears the main scan's histogram
             if (int rc = run_counted_seed(ws, nib, n, dim, wd, q, nq, wq, k, up.sample, false, up.off_qimg, up.off_qconst, up.off_seedpar,
-                                          up.off_seedhist, tau, st)) return rc;
+                                          up.off_seedhist, tau, st, hist_main ? reinterpret_cast<int32_t *>(ws + up.off_theta0) : nullptr,
+                                          hist_main ? reinterpret_cast<uint32_t *>(ws + up.off_ghist) : nullptr)) return rc;
         } else {
             if (int rc = run_umma_scan(up.pre, up, ws, nib, up.sample, C, nq, k, row_offset, nullptr, prekeys, st)) return rc;
             mma::tau_from_keys_kernel<<<static_cast<unsigned>((nq + 255) / 256), 256, 0, st>>>(prekeys, qconst, nq, k, tau);
             if (int rc = check_launch("tau_from_keys_kernel")) return rc;
         }
         tau_init = tau;
-        if (up.off_ghist > up.off_theta0) {  // global candidate histogram of the main scan, bins measured from the seeded thresholds
-            cudaError_t e = cudaMemcpyAsync(ws + up.off_theta0, tau, static_cast<size_t>(nq) * 4, cudaMemcpyDeviceToDevice, st);
-            if (e == cudaSuccess) e = cudaMemsetAsync(ws + up.off_ghist, 0, static_cast<size_t>(nq) * umma::HIST_BINS * 4, st);
-            if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "histogram setup: %s", cudaGetErrorString(e));
+        if (hist_main) {
+            if (!up.pre.count) {
+                cudaError_t e = cudaMemcpyAsync(ws + up.off_theta0, tau, static_cast<size_t>(nq) * 4, cudaMemcpyDeviceToDevice, st);
+                if (e == cudaSuccess) e = cudaMemsetAsync(ws + up.off_ghist, 0, static_cast<size_t>(nq) * umma::HIST_BINS * 4, st);
+                if (e != cudaSuccess) return fail(XFBQ_E_CUDA, "histogram setup: %s", cudaGetErrorString(e));
+            }
             // scores of interest lie within ~1/64 of the distance range below the seed: 256 bins of width 2^shift cover it
             const int64_t ub = xfbq_distance_upper_bound(dim, wd, wq);
             int shift = 0;

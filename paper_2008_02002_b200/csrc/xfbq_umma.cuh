@@ -834,9 +834,11 @@ __device__ __forceinline__ int dp4a_su(uint32_t a_s8x4, uint32_t b_u8x4, int c) 
     return d;
 }
 __global__ void __launch_bounds__(128) seed_stats_kernel(const unsigned char *__restrict__ tiles, const unsigned char *__restrict__ qimg,
-                                                         int64_t nq, int C, int64_t sample_tiles, int64_t tile_stride, float z, float below, int2 *__restrict__ par) {
+                                                         int64_t nq, int C, int64_t sample_tiles, int64_t tile_stride, float z, float below, int2 *__restrict__ par,
+                                                         uint32_t *__restrict__ seed_hist) {
     const int64_t q = blockIdx.x;
     const int r = threadIdx.x;
+    if (r < SEED_BINS) seed_hist[q * SEED_BINS + r] = 0u;  // the counting scan that follows adds to it (one stream operation less than a memset)
     const int64_t t = (static_cast<int64_t>(r) * sample_tiles / 128) * tile_stride;
     const unsigned char *tile = tiles + t * (static_cast<int64_t>(STAGE_DOCS) * 128 * C);
     const uint4 *qrow = reinterpret_cast<const uint4 *>(qimg + q * (128 * C));
@@ -875,10 +877,16 @@ __global__ void __launch_bounds__(128) seed_stats_kernel(const unsigned char *__
 // suffix count reaches k proves that k real documents score at least origin + d_b, d_b = the smallest offset
 // that maps to bin b.  TAU_OPEN when the frame missed (fewer than k sample scores at or above the origin).
 __global__ void __launch_bounds__(256) seed_bounds_kernel(const uint32_t *__restrict__ hist, const int2 *__restrict__ par,
-                                                          int64_t nq, int k, int32_t *__restrict__ tau) {
+                                                          int64_t nq, int k, int32_t *__restrict__ tau,
+                                                          int32_t *__restrict__ theta0, uint32_t *__restrict__ ghist) {
     const int64_t q = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (q >= nq) return;
+    if (ghist) {  // the main scan's candidate histogram of this query starts empty (instead of a memset + a copy of the thresholds)
+        uint4 *row = reinterpret_cast<uint4 *>(ghist + q * HIST_BINS) + 2 * lane;
+        row[0] = make_uint4(0u, 0u, 0u, 0u);
+        row[1] = make_uint4(0u, 0u, 0u, 0u);
+    }
     const uint2 c = *reinterpret_cast<const uint2 *>(hist + q * SEED_BINS + 2 * lane);  // bins 2 lane, 2 lane + 1
     const uint32_t s = c.x + c.y;
     uint32_t suf = s;
@@ -902,6 +910,7 @@ __global__ void __launch_bounds__(256) seed_bounds_kernel(const uint32_t *__rest
             out = pr.x / 2 + static_cast<int32_t>(d_b);
         }
         tau[q] = out;
+        if (theta0) theta0[q] = out;
     }
 }
 
