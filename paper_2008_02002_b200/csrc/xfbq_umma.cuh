@@ -1087,8 +1087,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
 
             // 32 scores of one query row: 3-input max tree, one compare, one vote; a row whose maximum passes is
             // parked for the resolver (its scores, its query, its first document, a ticket)
-            auto filter = [&](const int (&v)[32], int theta, int qloc, uint32_t doc0) {
-                const int m = max(max(max8(v), max8(v + 8)), max(max8(v + 16), max8(v + 24)));
+            auto max32 = [](const int (&v)[32]) { return max(max(max8(v), max8(v + 8)), max(max8(v + 16), max8(v + 24))); };
+            auto filter = [&](const int (&v)[32], int m, int theta, int qloc, uint32_t doc0) {   // m = max32(v)
                 const bool hit = m >= theta;
                 const unsigned hm = __ballot_sync(0xffffffffu, hit);
                 if (hm) {
@@ -1139,6 +1139,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                     const uint32_t doc0 = (static_cast<uint32_t>(sg.sd0) + rel / MT) * STAGE_DOCS + half * 64;
                     const uint32_t taddr = lane_base + buf * STAGE_DOCS + half * 64;
                     const int theta = theta_s[qloc];
+                    asm volatile("" ::"r"(taddr), "r"(doc0), "r"(theta));   // computed BEFORE the wait: between the barrier and the tensor-memory read only the read itself
                     if (prof) mbar_wait_prof(&acc_full[buf], (u / AB) & 1u, true, w0); else mbar_wait_tight(&acc_full[buf], (u / AB) & 1u);
                     fence_after();
                     int v[2][32];
@@ -1148,9 +1149,12 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                     fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&acc_empty[buf]);
-                    if (!(p.debug & 4)) {
-                        filter(v[0], theta, qloc, doc0);
-                        filter(v[1], theta, qloc, doc0 + 32);
+                    if (!(p.debug & 4)) {   // one vote for the 64 columns: the common case (nothing passes) costs two max trees, a compare and a vote
+                        const int m0 = max32(v[0]), m1 = max32(v[1]);
+                        if (__any_sync(0xffffffffu, max(m0, m1) >= theta)) {
+                            filter(v[0], m0, theta, qloc, doc0);
+                            filter(v[1], m1, theta, qloc, doc0 + 32);
+                        }
                     }
                 }
             }
