@@ -1028,7 +1028,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
     const uint32_t tmem = *tmem_slot;
     uint32_t s_run = 0;
     const bool prof = p.prof != nullptr;
-    long long w0 = 0, w1 = 0, w3 = 0;
+    long long w0 = 0, w1 = 0, w3 = 0, w5 = 0;
     int w2 = 0;
     const long long t_begin = prof ? clock64() : 0;
     uint64_t *group_lists = p.lists + static_cast<int64_t>(blockIdx.x) * NQ_CTA * static_cast<int64_t>(p.cap);
@@ -1093,6 +1093,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                 const unsigned hm = __ballot_sync(0xffffffffu, hit);
                 if (hm) {
                     ++w1;
+                    const long long th0 = prof ? clock64() : 0;
                     const int n = __popc(hm);
                     const int t0 = head;
                     head += n;
@@ -1121,6 +1122,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
                         if (p.debug & 16) *reinterpret_cast<volatile int *>(row + 34) = t + 1;  // timing experiments: no release fence
                         else st_release(reinterpret_cast<int *>(row + 34), t + 1);  // publishes the row
                     }
+                    __syncwarp();
+                    if (prof) w5 += clock64() - th0;
                 }
             };
 
@@ -1172,6 +1175,12 @@ __global__ void __launch_bounds__(Q_THREADS, 1) scan_queue_kernel(const Params p
         if (prof && threadIdx.x == 0) {
             unsigned long long *o = p.prof + blockIdx.x * 8;
             o[0] = w0; o[1] = w1; o[5] = w3; o[6] = clock64() - t_begin; o[7] = s_run;
+        }
+        if (prof && lane == 0) {   // every drain warp's time waiting for an accumulator / for room in its ring
+            p.prof[gridDim.x * 12 + blockIdx.x * 12 + warp] = w0;
+            p.prof[gridDim.x * 24 + blockIdx.x * 12 + warp] = w3;
+            p.prof[gridDim.x * 36 + blockIdx.x * 24 + warp] = w5;        // time inside the park path ...
+            p.prof[gridDim.x * 36 + blockIdx.x * 24 + 12 + warp] = w1;   // ... of this many chunks
         }
     } else if (warp == Q_MMA_WARP) {
         // ================================ MMA issuer ================================

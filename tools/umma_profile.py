@@ -24,7 +24,7 @@ idx = xb.build_index(docs, xb.QuantParams(dim=dim, scale=scale, doc_bits=4, quer
 del docs
 for _ in range(2):
     xb.search(idx, q, k)
-prof = torch.zeros((148 * 12,), dtype=torch.int64, device="cuda")
+prof = torch.zeros((148 * 60,), dtype=torch.int64, device="cuda")
 _native.check(_native.lib().xfbq_debug_profile(prof.data_ptr()))
 _native.set_timing(True)
 xb.search(idx, q, k)
@@ -33,7 +33,10 @@ _native.set_timing(False)
 _native.check(_native.lib().xfbq_debug_profile(0))
 allc = prof.cpu().numpy().astype(np.float64)
 c = allc[:148 * 8].reshape(148, 8)
-x = allc[148 * 8:].reshape(148, 4)
+x = allc[148 * 8:148 * 12].reshape(148, 4)
+per_warp = allc[148 * 12:148 * 24].reshape(148, 12)
+ring_full = allc[148 * 24:148 * 36].reshape(148, 12)
+park = allc[148 * 36:].reshape(148, 2, 12)
 tot = c[:, 6].mean()
 st = c[:, 7].mean()
 print(f"kernel {ms:.3f} ms; per CTA: {tot / 1e6:.2f} Mclk, {st:.0f} stages, {tot / st:.0f} clk/stage")
@@ -46,6 +49,9 @@ for i, nm in enumerate(names):
         print(f"  {nm:34s} {c[:, i].mean() / 1e6:9.2f} Mclk  {c[:, i].mean() / tot * 100:5.1f}%  min {c[:, i].min() / tot * 100:5.1f}% max {c[:, i].max() / tot * 100:5.1f}%")
 print(f"  epi warp0 compactions {x[:, 2].mean():.0f}")
 print(f"  issuer probes that failed (per CTA): second query tile {x[:, 0].mean():.0f}, next document tile {x[:, 1].mean():.0f} of {st:.0f} tiles (16-bit counters)")
+print("  drain warps waiting for an accumulator, % of the kernel (warp = 4 * set + lane quarter): " + " ".join(f"{v / tot * 100:.0f}" for v in per_warp.mean(axis=0)))
+print("  drain warps waiting for room in their ring, clk per tile: " + " ".join(f"{v / st:.1f}" for v in ring_full.mean(axis=0)) + f"  (sum {ring_full.mean(axis=0).sum() / st:.1f})")
+print(f"  park path: {park[:, 1, :].sum() / 148 / st:.2f} chunks per tile park a row, {park[:, 0, :].sum() / max(park[:, 1, :].sum(), 1):.0f} clk each (ring waits included)")
 if len(sys.argv) > 5:
     print("per CTA: stages, total Mclk, clk/stage, mma wait acc_empty %, mma wait b_full %, drain w0 wait acc_full %, ring-full %")
     for b in range(148):
