@@ -10,6 +10,8 @@ reaches HBM.  Keys are (distance << 32 | row id), so ties resolve to the lower r
 """
 from __future__ import annotations
 
+import threading
+
 import time
 from dataclasses import dataclass, field
 
@@ -58,12 +60,13 @@ class SearchResult:
     stage_seconds: dict | None = field(default=None, compare=False)
 
 
-_WORKSPACES = {}   # (device index, stream) -> uint8 tensor, grown on demand: scans on one stream are ordered, so they can share it
+_WORKSPACES = {}   # (device index, stream, host thread) -> uint8 tensor, grown on demand: the scans ONE thread enqueues on a stream are ordered and
+                   # can share it; two host threads on the same stream interleave their launches, so each thread has its own
 _NONFINITE = {}    # device index -> int64[1] counter of non-finite query values seen by the fused small-batch kernel
 
 
 def _workspace(torch, dev, nbytes: int):
-    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream, threading.get_ident())
     ws = _WORKSPACES.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=dev)

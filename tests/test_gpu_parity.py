@@ -314,23 +314,24 @@ def test_concurrent_searches_are_deterministic():
     z = c["z"]
     params = xb.QuantParams(dim=c["dim"], scale=c["scale"], doc_bits=c["wd"], query_bits=c["wq"])
     idx = xb.build_index(c["docs"], params, keep_originals=False)
-    batch = xo.synthetic_unit_rows(96, c["dim"], 4242)          # tcgen05 engine
-    serial_batch = xb.search(idx, batch, 50)
+    batches = [xo.synthetic_unit_rows(96, c["dim"], 4242 + j) for j in range(3)]   # tcgen05 engine; DIFFERENT queries per batch:
+    serial_batch = [xb.search(idx, b, 50) for b in batches]                          # threads that shared a workspace would mix them up
     serial_single = [xb.k_select(idx, xb.SearchRequest(query=q, k=c["k"])) for q in c["queries"][:8]]
 
     def work(i):
         if i % 2:
-            return xb.search(idx, batch, 50)
+            return xb.search(idx, batches[(i // 2) % 3], 50)
         return xb.k_select(idx, xb.SearchRequest(query=c["queries"][(i // 2) % 8], k=c["k"]))
 
-    with ThreadPoolExecutor(max_workers=6) as pool:
-        results = list(pool.map(work, range(48)))
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        results = list(pool.map(work, range(96)))
     for i, r in enumerate(results):
         if i % 2:
-            assert np.array_equal(r[0], serial_batch[0]) and np.array_equal(r[1], serial_batch[1])
+            want = serial_batch[(i // 2) % 3]
+            assert np.array_equal(r[0], want[0]) and np.array_equal(r[1], want[1]), i
         else:
             want = serial_single[(i // 2) % 8]
-            assert r.hits == want.hits and r.threshold_distance == want.threshold_distance
+            assert r.hits == want.hits and r.threshold_distance == want.threshold_distance, i
     assert [h[0] for h in serial_single[0].hits] == z["ids"][0].tolist()
 
 
