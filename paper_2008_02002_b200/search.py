@@ -62,7 +62,11 @@ class SearchResult:
 
 _WORKSPACES = {}   # (device index, stream, host thread) -> uint8 tensor, grown on demand: the scans ONE thread enqueues on a stream are ordered and
                    # can share it; two host threads on the same stream interleave their launches, so each thread has its own
-_NONFINITE = {}    # device index -> int64[1] counter of non-finite query values seen by the fused small-batch kernel
+_NONFINITE = {}    # (device index, host thread) -> int64[1] counter of non-finite query values seen by that thread's fused small-batch searches
+
+
+def _nf_key(torch, dev):
+    return (dev.index if dev.index is not None else torch.cuda.current_device(), threading.get_ident())
 
 
 def _workspace(torch, dev, nbytes: int):
@@ -94,9 +98,9 @@ def _search_small_fused(index: Index, queries, k: int, row_offset: int):
     nib = packed.nibble_layout
     if nib is None:
         return None
-    counter = _NONFINITE.get(dev.index)
+    counter = _NONFINITE.get(_nf_key(torch, dev))
     if counter is None:
-        counter = _NONFINITE[dev.index] = torch.zeros(1, dtype=torch.int64, device=dev)
+        counter = _NONFINITE[_nf_key(torch, dev)] = torch.zeros(1, dtype=torch.int64, device=dev)
     keys = torch.empty((nq, k), dtype=torch.int64, device=dev)
     ws = _workspace(torch, dev, ws_bytes)
     fn = L.xfbq_search_small_f32 if queries.dtype == torch.float32 else L.xfbq_search_small_f64
@@ -130,9 +134,9 @@ def _kselect_small_fused(index: Index, query: np.ndarray, k: int, extra: int, wa
     if nib is None:
         return None
     with torch.cuda.device(dev):
-        counter = _NONFINITE.get(dev.index)
+        counter = _NONFINITE.get(_nf_key(torch, dev))
         if counter is None:
-            counter = _NONFINITE[dev.index] = torch.zeros(1, dtype=torch.int64, device=dev)
+            counter = _NONFINITE[_nf_key(torch, dev)] = torch.zeros(1, dtype=torch.int64, device=dev)
         q_dev = torch.from_numpy(np.ascontiguousarray(query, dtype=np.float64)[None, :]).to(dev)
         keys = torch.empty(k + 2, dtype=torch.int64, device=dev)        # k keys, candidate count, inexact flag: one D2H copy
         ids = torch.empty(cap if want_ids else 0, dtype=torch.int64, device=dev)
@@ -271,10 +275,10 @@ def search_device(index: Index, queries, k: int, row_offset: int = 0, check: boo
 
 
 def pending_nonfinite(device=None) -> int:
-    """Non-finite query values the fused small-batch searches on `device` have met since the last check (synchronises)."""
+    """Non-finite query values the calling thread's fused small-batch searches on `device` have met since the last check (synchronises)."""
     torch = _native.require_cuda()
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    counter = _NONFINITE.get(dev.index if dev.index is not None else torch.cuda.current_device())
+    counter = _NONFINITE.get(_nf_key(torch, dev))
     return int(counter.item()) if counter is not None else 0
 
 
@@ -283,7 +287,7 @@ def raise_pending_nonfinite(device=None) -> None:
     if pending_nonfinite(device):
         torch = _native.require_cuda()
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        _NONFINITE[dev.index if dev.index is not None else torch.cuda.current_device()].zero_()
+        _NONFINITE[_nf_key(torch, dev)].zero_()
         raise InvalidInputError("cannot quantize non-finite values")
 
 
