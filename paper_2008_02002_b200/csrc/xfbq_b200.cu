@@ -1565,7 +1565,15 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
         // Work items = document slices x query groups, dealt to the CTAs round-robin (umma::Items).  Pick the
         // slice count that fills whole waves of CTAs; slices stay long enough to amortise the per-item list
         // start-up and emission.
-        const int64_t min_stages = env_int("XFBQ_UMMA_MIN_SLICE", 512);
+        int64_t min_stages = env_int("XFBQ_UMMA_MIN_SLICE", 512);
+        // Few query groups over a mid-size database: slices of 512 tiles would leave SMs without work (one group over 4M rows:
+        // 61 slices on 148 SMs, the scan at 4.6 TB/s instead of > 7).  Filling the first wave matters more than the per-slice
+        // list work there: slices may shrink to what one wave needs, down to 128 tiles.
+        const int64_t fill_S = (grid + sh.groups - 1) / sh.groups;
+        if (sh.stages / min_stages < fill_S && env_int("XFBQ_UMMA_FILL", 1) != 0) {
+            const int64_t relaxed = sh.stages / fill_S > 128 ? sh.stages / fill_S : 128;
+            if (relaxed < min_stages) min_stages = relaxed;
+        }
         int best = 1;
         double best_score = -1.0;
         for (int S = 1; S <= 256; ++S) {
@@ -1615,9 +1623,10 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     if (!have_nibbles || wq > 7 || tg.CP < 1 || tg.CP > 8 || k > 1024 || n < 1 || env_int("XFBQ_FORCE_GENERIC", 0))  // any document width: the B operand is u8
         return XFBQ_OK;
     // where the mma.sync engine cannot go (codes wider than a nibble, more than 512 dims) this engine also takes the small
-    // batches: from two queries on it beats the POPC kernels (1 POPC per code byte and query)
+    // batches, single queries included: the POPC kernels pay 1 POPC per code byte and query (one query over 8M x 768:
+    // 3.60 ms there, 0.97 ms here; 4M x 1024: 2.39 / 1.06; 1M x 768: 0.56 / 0.42 -- profiles/wide_single_r2c.log)
     const bool no_imma = wd > 4 || tg.CP > 4;
-    if (!forced && nq < env_int("XFBQ_UMMA_MIN_NQ", no_imma ? 2 : 17)) return XFBQ_OK;  // <= 16 queries: the mma.sync scans (HBM-bound on the nibble layout; a 24-query batch took 0.72 ms there, 0.55 ms here)
+    if (!forced && nq < env_int("XFBQ_UMMA_MIN_NQ", no_imma ? 1 : 17)) return XFBQ_OK;  // <= 16 queries: the mma.sync scans (HBM-bound on the nibble layout; a 24-query batch took 0.72 ms there, 0.55 ms here)
     if (nq < 1) return XFBQ_OK;
     if (merge_group_max(k) == 0 || nq > 65535) return XFBQ_OK;  // lists are emitted unsorted: needs the tree merge
     DeviceInfo info;
