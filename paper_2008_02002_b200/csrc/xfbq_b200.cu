@@ -1568,10 +1568,12 @@ void umma_shape(int64_t n, int C, int64_t nq, int k, int MT, const DeviceInfo &i
         int64_t min_stages = env_int("XFBQ_UMMA_MIN_SLICE", 512);
         // Few query groups over a mid-size database: slices of 512 tiles would leave SMs without work (one group over 4M rows:
         // 61 slices on 148 SMs, the scan at 4.6 TB/s instead of > 7).  Filling the first wave matters more than the per-slice
-        // list work there: slices may shrink to what one wave needs, down to 128 tiles.
+        // list work there: slices may shrink to what one wave needs, down to 32 tiles (4 096 documents; 1M x 256, 256 queries:
+        // 61 slices 0.304 ms, 148 slices 0.251).
         const int64_t fill_S = (grid + sh.groups - 1) / sh.groups;
         if (sh.stages / min_stages < fill_S && env_int("XFBQ_UMMA_FILL", 1) != 0) {
-            const int64_t relaxed = sh.stages / fill_S > 128 ? sh.stages / fill_S : 128;
+            const int64_t floor_stages = env_int("XFBQ_UMMA_FILL_FLOOR", 32);
+            const int64_t relaxed = sh.stages / fill_S > floor_stages ? sh.stages / fill_S : floor_stages;
             if (relaxed < min_stages) min_stages = relaxed;
         }
         int best = 1;
@@ -1636,13 +1638,21 @@ int make_umma_plan(int64_t n, int64_t dim, int wd, int64_t nq, int wq, int k, bo
     // most 4 CTAs per query group balance its cost -- it starts from open lists -- against the rows the main
     // scan's resolvers then have to handle).
     int64_t sample = env_int("XFBQ_SAMPLE", -1);
-    if (sample < 0) { sample = 16384; while (sample < 64 * static_cast<int64_t>(k)) sample <<= 1; }
+    if (sample < 0) {
+        sample = 16384;
+        while (sample < 64 * static_cast<int64_t>(k)) sample <<= 1;
+        // small databases: a smaller sample still seeds the thresholds (and with them the queue kernel) as long as it holds 64 k documents
+        if (env_int("XFBQ_SAMPLE_SHRINK", 1))
+            while (sample > 4096 && n < 8 * sample && (sample >> 1) >= 64 * static_cast<int64_t>(k)) sample >>= 1;
+    }
     if (sample > 0 && (n < 8 * sample || sample < 4 * k)) sample = 0;
     // Without seeded thresholds every score passes at first: list work dominates and the kernel whose eight
     // epilogue warps own their lists beats the two resolvers of the queue kernel (100k x 128, 100 queries: 4x).
-    // The same holds for small problems with few query groups (1M x 128, 1000 queries: 2.5x): the lists stay hot.
+    // With seeded thresholds the queue kernel wins at every size that was measured (profiles/queue_min_ab2_r2d.log: 150k-1M
+    // rows, 32-1 024 queries, 1.6-9x; the list-keeping kernel was the choice below 2M rows until the counted seed, the
+    // bounded merge and the first-wave fill of the slice planner existed).
     const int64_t groups = (nq + 128 * MT - 1) / (128 * MT);
-    const bool big = n >= env_int("XFBQ_UMMA_QUEUE_MIN_N", 2000000) || groups >= 16;
+    const bool big = n >= env_int("XFBQ_UMMA_QUEUE_MIN_N", 1) || groups >= 16;
     umma_shape(n, C, nq, k, MT, info, &pl.main, false, sample > 0 && big, false, KP);
     if (pl.main.NS == 0) return XFBQ_OK;
     pl.sample = sample;

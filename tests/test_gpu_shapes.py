@@ -30,8 +30,8 @@ def test_dims_on_tensor_engines(dim, wd, monkeypatch):
     qp = xo.c_quantize_matrix(queries.astype(np.float64), wq, scale).transpose(2, 0, 1)
     want_d, want_i = xo.c_search(planes, qp, k)
     assert _engine(n, dim, wd, 200, wq, k) == 3 and _engine(n, dim, wd, 5, wq, k) == 2   # tcgen05 / mma.sync by default
-    for env in ({}, {"XFBQ_ENGINE": "umma"}, {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SAMPLE": "4096"},
-                {"XFBQ_ENGINE": "imma"}):
+    for env in ({}, {"XFBQ_ENGINE": "umma"}, {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE": "0"},
+                {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SAMPLE": "4096"}, {"XFBQ_ENGINE": "imma"}):
         for key, val in env.items():
             monkeypatch.setenv(key, val)
         for nq in (200, 5, 1):
@@ -58,7 +58,8 @@ def test_wide_codes_on_the_tcgen05_engine(wd, wq, dim, monkeypatch):
     qp = xo.c_quantize_matrix(queries.astype(np.float64), wq, scale).transpose(2, 0, 1)
     want_d, want_i = xo.c_search(planes, qp, k)
     assert _engine(n, dim, wd, 150, wq, k) == 3
-    for env in ({}, {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SAMPLE": "4096"}, {"XFBQ_ENGINE": "popc"}):
+    for env in ({}, {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE": "0"}, {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SAMPLE": "4096"},
+                {"XFBQ_ENGINE": "popc"}):
         for key, val in env.items():
             monkeypatch.setenv(key, val)
         scores, ids = xb.search(idx, queries, k)
@@ -106,7 +107,7 @@ def test_dims_513_to_1024_on_two_part_tiles(dim, wd, monkeypatch):
     qp = xo.c_quantize_matrix(queries.astype(np.float64), wq, scale).transpose(2, 0, 1)
     want_d, want_i = xo.c_search(planes, qp, k)
     assert _engine(n, dim, wd, 160, wq, k) == 3 and _engine(n, dim, wd, 2, wq, k) == 3 and _engine(n, dim, wd, 1, wq, k) == 3
-    for env in ({}, {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SAMPLE": "4096"},
+    for env in ({}, {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE": "0"}, {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SAMPLE": "4096"},
                 {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SAMPLE": "4096", "XFBQ_UMMA_SLICES": "3"}):
         for key, val in env.items():
             monkeypatch.setenv(key, val)

@@ -49,7 +49,8 @@ def test_ties_on_every_engine(distinct, monkeypatch):
             {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_UMMA_HIST": "0"},          # no candidate histogram
             {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SEED_HIST": "0"},          # list-keeping sample scan
             {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE_MIN_N": "1", "XFBQ_SAMPLE": "0"},             # open thresholds
-            {"XFBQ_ENGINE": "umma"},                                                                  # list-owning epilogue kernel
+            {"XFBQ_ENGINE": "umma", "XFBQ_UMMA_QUEUE": "0"},                                          # list-owning epilogue kernel
+            {"XFBQ_ENGINE": "umma"},                                                                  # the default plan of the tcgen05 engine
             {"XFBQ_ENGINE": "imma"},
             {"XFBQ_ENGINE": "popc"},
         ]

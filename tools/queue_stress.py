@@ -11,9 +11,10 @@ from oracle import xfbq_oracle as xo
 rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 os.environ["XFBQ_ENGINE"] = "umma"
 os.environ["XFBQ_UMMA_QUEUE_MIN_N"] = "1"
+DEFAULT_PLANS = os.environ.get("QS_DEFAULT_PLANS", "0") == "1"   # no plan overrides: the planner's own sample, slices and ring depth
 bad = 0
 for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 40):
-    n = int(rng.choice([20_000, 33_333, 70_001, 150_000, 400_000]))
+    n = int(rng.choice([20_000, 33_333, 70_001, 150_000, 400_000] + ([40_000, 100_000, 250_000, 900_000] if DEFAULT_PLANS else [])))
     dim = int(rng.choice([64, 128, 200, 256, 300, 384, 512, 700, 1024]))
     wd = int(rng.integers(1, 9))
     nq = int(rng.choice([17, 100, 128, 129, 256, 257, 520, 700]))
@@ -24,6 +25,8 @@ for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 40):
         del env["XFBQ_UMMA_SLICES"]
     for key in ("XFBQ_UMMA_SLICES", "XFBQ_UMMA_STAGES", "XFBQ_SAMPLE"):
         os.environ.pop(key, None)
+    if DEFAULT_PLANS:
+        env = {}
     os.environ.update(env)
     docs = xo.synthetic_unit_rows(n, dim, 300 + it)
     queries = xo.synthetic_unit_rows(nq, dim, 400 + it)
