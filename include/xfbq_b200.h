@@ -100,9 +100,10 @@ int xfbq_bundles_to_planes(const void *db_dev, int64_t n, int64_t dim, int width
  *   [nibble layout] row-major 4-bit codes, 64*C bytes per document (documents rounded up to 32), one
  *                   16-byte word per group of 32 dims whose 32-bit word e holds in nibble m the code of
  *                   dimension 4m + e (streamed by the mma.sync engine: <= 16 queries, HBM-bound);
- *   [byte tiles]    (C in {1, 2, 4}) tiles of 128 documents x 128*C bytes, one code per byte, K-major with
- *                   the 128-byte swizzle: the exact shared-memory image of a tcgen05.mma B operand, copied
- *                   by one cp.async.bulk per tile (streamed by the tcgen05 engine: >= 32 queries).
+ *   [byte tiles]    (any doc_bits 1..8, dim <= 1024) tiles of 128 documents x 128*C bytes, one code per byte,
+ *                   K-major with the 128-byte swizzle: the exact shared-memory image of a tcgen05.mma B operand,
+ *                   copied by one cp.async.bulk per tile (streamed by the tcgen05 engine: >= 17 queries, and every
+ *                   batch size where the mma.sync engine does not go: doc_bits > 4 or dim > 512).
  * The tile region starts at the nibble region's size rounded up to 1024 bytes.
  */
 /* The two layouts can also be built and passed separately (a batch server needs only the tiles: 2x the packed size for 4-bit
@@ -203,10 +204,10 @@ int xfbq_gather_le_ids(const int64_t *dist_dev, int64_t n, int64_t threshold, co
  * workspace_dev must hold xfbq_scan_workspace_bytes(...) bytes.
  * 1 <= k <= XFBQ_MAX_K;  row_offset + n <= 2^32.
  * nibbles_dev: optional derived layouts of the codes (xfbq_planes_to_nibbles).
- * When given (doc_bits <= 4, query_bits <= 7, dim <= 256 or 385..512, k <= 1024) the scan runs on the
- * integer tensor path -- tcgen05.mma kind::i8 with accumulators in tensor memory for >= 32 queries,
- * mma.sync (IMMA) below -- with identical results; when NULL, or outside those shapes, the XOR/POPC
- * kernels scan the bit planes.  XFBQ_ENGINE=umma|imma|popc forces one engine.
+ * When given (query_bits <= 7, dim <= 1024, k <= 1024) the scan runs on the integer tensor path -- tcgen05.mma
+ * kind::i8 with accumulators in tensor memory for >= 17 queries (any batch size when doc_bits > 4 or dim > 512),
+ * mma.sync (IMMA) below (doc_bits <= 4, dim <= 512) -- with identical results; when NULL, or outside those
+ * shapes, the XOR/POPC kernels scan the bit planes.  XFBQ_ENGINE=umma|imma|popc forces one engine.
  */
 int64_t xfbq_scan_workspace_bytes(int64_t n, int64_t dim, int doc_bits, int64_t nq,
                                   int query_bits, int k, int have_nibbles);
